@@ -1,0 +1,305 @@
+#!/usr/bin/env python
+"""Benchmark driver (contract in the task statement; numbers explained in DESIGN.md).
+
+Workload (BASELINE.json configs[1], the pure Tucker-operator sweep, headline
+size): V x_1 L x_2 L x_3 L on a d=3 FP64 cube n=512 with V ~ N(0,1) (seeded)
+and L = phi_1(1e-3 * A), A the 1-D Dirichlet Laplacian (fd_operator_1d(n, 1, 0)).
+One "step" = one Tucker operator (3 mode products, 412.3 GFLOP).
+
+  value     : whole-job GFLOP/s, inputs resident in HBM, CUDA events on the
+              launching stream, max over ranks (inputs are 1 GiB > 126 MB L2,
+              so no L2 flush is needed between steps);
+  e2e       : the same metric through the drop-in host API (kp_host_tucker_f64):
+              pinned host V -> H2D -> Tucker -> D2H each step;
+  roofline  : dominant kernel (the DMMA mode-product GEMM) vs the FP64 tensor
+              peak measured live on this GPU (MEASURED_PEAKS.json has no FP64);
+  cpu_baseline : the reference C++ tucker() (oracle/_ref, all host threads)
+              on a bounded sample of the same workload, rank 0 at N=1 only.
+
+`--impl reference` times the reference's own CPU implementation of the same
+step (oracle/_ref when built, else the C restatement) and prints the same line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 1002  # configs[1] (seeds 1001-1005 for configs 1-5)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def flops_per_tucker(n, d=3):
+    return 2.0 * n ** d * (d * n)
+
+
+def config(n, world):
+    return {"workload": f"tucker_d3_n{n}", "op": "V x1 L x2 L x3 L",
+            "dims": [n, n, n], "factor": "L = phi_1(1e-3 * fd_operator_1d(n, 1.0, 0))",
+            "seed": SEED, "parallelism": "replicas" if world > 1 else "single",
+            "l2": "inputs 1 GiB > 126 MB L2 (no flush needed)"}
+
+
+def make_inputs(n):
+    r = np.random.default_rng(SEED)
+    v = np.asfortranarray(r.standard_normal((n, n, n)))
+    h = 1.0 / (n + 1)
+    a = np.zeros((n, n), order="F")
+    idx = np.arange(n)
+    a[idx, idx] = -2.0 / (h * h)
+    a[idx[1:], idx[:-1]] = 1.0 / (h * h)
+    a[idx[:-1], idx[1:]] = 1.0 / (h * h)
+    return v, a
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}",
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_baseline(n, v, ms):
+    """Reference tucker() on the host cores (oracle/_ref), bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    if pyoracle.available("reference"):
+        o = pyoracle.Oracle("reference")
+        sec = o.time_tucker(v, ms, reps=2)
+        return {"value": flops_per_tucker(n) / sec / 1e9, "unit": "GFLOP/s",
+                "cores": o.num_threads(), "kind": "reference",
+                "sample": f"2 timed calls (best) of the reference tucker() on the d=3 n={n} "
+                          f"cube after 1 warm-up, OpenMP threads={o.num_threads()}"}
+    o = pyoracle.Oracle("port")
+    m = min(n, 128)
+    vs = np.asfortranarray(v[:m, :m, :m])
+    msm = [np.asfortranarray(x[:m, :m]) for x in ms]
+    t0 = time.perf_counter()
+    o.tucker(vs, msm)
+    sec = time.perf_counter() - t0
+    return {"value": flops_per_tucker(m) / sec / 1e9, "unit": "GFLOP/s", "cores": 1,
+            "kind": "port", "sample": f"1 call of the C restatement's tucker on a {m}^3 sub-cube"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    n = args.n
+    v, a = make_inputs(n)
+    kind = "reference" if pyoracle.available("reference") else "port"
+    o = pyoracle.Oracle(kind)
+    # factors: the reference's own phiquad (build_split_phi, l = 1)
+    fs, _ = o.build_split_phi([a, a, a], 1e-3, 1)
+    for _ in range(args.warmup):
+        o.tucker(v, fs)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.tucker(v, fs)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = flops_per_tucker(n) / (ms * 1e-3) / 1e9
+    cores = o.num_threads()
+    line = {"metric": f"FP64 Tucker-op GFLOP/s (d=3, n={n})", "value": value, "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config(n, 1), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": kind,
+                             "sample": f"{args.steps} full tucker() calls on the n={n} cube"},
+            "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2304_02327_b200 as kp
+    ctx = kp.default_context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+
+    n = args.n
+    v_h, a_h = make_inputs(n)
+    fs = kp.build_split_phi_factors([a_h] * 3, 1e-3, 1) if hasattr(kp, "build_split_phi_factors") \
+        else None
+    if fs is None:
+        from paper_2304_02327_b200 import phi as _phi  # noqa: F401  (device phi builder)
+    fs_d = [kp.to_device(f) if isinstance(f, np.ndarray) else f for f in fs]
+    v_d = kp.to_device(v_h)
+    out_d = kp.fortran_empty([n, n, n])
+    dims = [n, n, n]
+    lib = ctx.lib
+    from paper_2304_02327_b200._lib import check, ints, ptr_array
+    mptr = ptr_array([f.data_ptr() for f in fs_d])
+
+    def step():
+        check(lib.kp_tucker_f64(ctx.h, v_d.data_ptr(), ints(dims), 3, mptr, ints(dims), 1.0,
+                                out_d.data_ptr()))
+
+    peak = ctx.fp64_peak_tflops()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = ctx.launches
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.launches - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    fl = flops_per_tucker(n)
+    value = world * fl / (ms * 1e-3) / 1e9
+    achieved = fl / (ms * 1e-3) / 1e12  # per-launch ratio == per-step ratio (3 equal launches)
+
+    # ---- e2e through the host drop-in API, pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        pin_v = torch.empty((n, n, n), dtype=torch.float64, pin_memory=True)
+        pin_o = torch.empty((n, n, n), dtype=torch.float64, pin_memory=True)
+        hv = pin_v.numpy().T  # Fortran view of the pinned buffer
+        hv[...] = v_h
+        ho = pin_o.numpy().T
+        hfs = [np.asfortranarray(kp.to_host(f)) for f in fs_d]
+        hptr = ptr_array([f.ctypes.data for f in hfs])
+
+        def host_step():
+            check(lib.kp_host_tucker_f64(ctx.h, hv.ctypes.data, ints(dims), 3, hptr, ints(dims),
+                                         1.0, ho.ctypes.data))
+        host_step()
+        if dist:
+            dist.barrier()
+        ksteps = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(ksteps):
+            host_step()
+        sec = (time.perf_counter() - t0) / ksteps
+        if dist:
+            t = torch.tensor([sec], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sec = float(t.item())
+        e2e = {"value": world * fl / sec / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(v_h.nbytes + sum(f.nbytes for f in hfs)),
+               "d2h_bytes_per_step": int(v_h.nbytes), "ms_per_step": sec * 1e3,
+               "api": "kp_host_tucker_f64 (pinned host buffers)"}
+
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic_latest.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(f"tucker_d3_n{n}")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(n, v_h, [kp.to_host(f) for f in fs_d])
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "error": str(ex)[:200]}
+
+    if rank == 0:
+        line = {"metric": f"FP64 Tucker-op GFLOP/s (d=3, n={n})", "value": value,
+                "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config(n, world),
+                "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
+                             "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                             "peak_source": "live DMMA m8n8k4 micro-benchmark on this GPU "
+                                            "(MEASURED_PEAKS.json has no FP64 figure)",
+                             "algorithmic": "2*N*sum(n_mu) = 412.3 GFLOP per Tucker, "
+                                            "137.4 GFLOP per mode-product launch"},
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,153 @@
+/*
+ * kronphi_b200.h -- C ABI of the B200-native direction-split phi library.
+ *
+ * Drop-in boundary for the hot path of the reference library `kronphi`
+ * (arXiv 2304.02327, /root/reference/proj; prefix inc/ = proj/include/kronphi/).
+ * The reference has no FFI; its boundary is the C++ template API in inc/.
+ * Each entry point below names the reference function it replaces.  The C++
+ * layer include/kronphi_b200/kronphi.hpp re-exposes the reference's C++
+ * signatures on top of this ABI (same names, argument meaning, exceptions).
+ *
+ * Conventions
+ *  - Column-major tensors, first index fastest (inc/tensor.hpp:1-2); matrices
+ *    column-major (inc/matrix.hpp:58-59).  Complex data is interleaved
+ *    (re, im) exactly like std::complex<double>.
+ *  - kp_* compute calls take DEVICE pointers and are stream-ordered on the
+ *    context's stream; kp_host_* calls take HOST pointers, stage through the
+ *    context's pinned buffers and return when the result is on the host.
+ *  - Arrays of per-mode pointers (ms, as, factors) are HOST arrays holding
+ *    device (kp_*) or host (kp_host_*) pointers.
+ *  - Status codes map to the reference's exception types:
+ *      KP_EINVAL   -> std::invalid_argument (message names the mode, as
+ *                     inc/mode_product.hpp:51-55)
+ *      KP_ERUNTIME -> std::runtime_error (singular LU, inc/linsolve.hpp:39)
+ *      KP_EDIVERGE -> kronphi::DivergenceError (inc/integrators.hpp:86-97)
+ *      KP_ECUDA    -> CUDA failure (message carries cudaGetErrorString)
+ *    kp_last_error() returns the calling thread's last message.
+ *  - One context is not thread-safe across threads sharing its stream (the
+ *    reference's functions are reentrant per call; here reentrancy is per
+ *    context).
+ */
+#ifndef KRONPHI_B200_H
+#define KRONPHI_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KP_OK 0
+#define KP_EINVAL 1
+#define KP_ERUNTIME 2
+#define KP_EDIVERGE 3
+#define KP_ECUDA 4
+
+typedef struct kp_ctx kp_ctx;
+
+/* Methods: same order as kronphi::Method (inc/integrators.hpp:24-31). */
+#define KP_LAWSON_EULER 0
+#define KP_LAWSON2B 1
+#define KP_EXP_EULER 2
+#define KP_EXP_EULER_LS 3
+#define KP_ETD2RK 4
+
+/* Closed set of device nonlinearities g(t,u) replacing the reference's host
+ * std::function (inc/integrators.hpp:60,112). */
+#define KP_G_ZERO 0
+#define KP_G_SQUARE 1
+#define KP_G_CONST 2       /* p[0] */
+#define KP_G_ALLEN_CAHN 3  /* u - u^3 */
+#define KP_G_BRUSSELATOR 4 /* species stacked as the slowest mode (size 2); p[0]=a, p[1]=b */
+#define KP_G_NLS 5         /* -i |u|^2 u, complex */
+
+typedef struct {
+  int kind;
+  double p[4];
+} kp_gfun;
+
+/* ---------------- context, memory, errors ---------------- */
+const char* kp_last_error(void);
+int kp_ctx_create(int device, kp_ctx** out);
+int kp_ctx_destroy(kp_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
+ * NULL means the legacy default stream, as in CUDA. */
+int kp_ctx_set_stream(kp_ctx* ctx, void* stream);
+/* Go back to the context's own non-blocking stream (the initial state). */
+int kp_ctx_use_own_stream(kp_ctx* ctx);
+void* kp_ctx_get_stream(kp_ctx* ctx);
+int kp_ctx_synchronize(kp_ctx* ctx);
+/* Number of kernels this context has launched (bench.py's gpu_launches). */
+unsigned long long kp_ctx_launch_count(kp_ctx* ctx);
+
+int kp_malloc(kp_ctx* ctx, size_t bytes, void** ptr);
+int kp_free(kp_ctx* ctx, void* ptr);
+int kp_upload(kp_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes);
+int kp_download(kp_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes);
+int kp_memset(kp_ctx* ctx, void* dst_dev, int value, size_t bytes);
+
+/* ---------------- mu-mode / Tucker / Kronecker sum ---------------- */
+/* out = alpha * (t x_mode M) + beta * out.
+ * Replaces mode_product_into (inc/mode_product.hpp:61-87; beta = 1 is its
+ * accumulate=true) and mode_product (:89-97).  M is rows x cols with
+ * cols == dims[mode]; out has dims with dims[mode] -> rows.  out must not
+ * alias t. */
+int kp_mode_product_f64(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
+                        const double* m, int rows, int cols, double alpha, double beta,
+                        double* out);
+int kp_mode_product_c128(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
+                         const double* m, int rows, int cols, const double* alpha2,
+                         const double* beta2, double* out);
+
+/* out = ((prefactor * t) x_1 M_1 x_2 ... x_d M_d).
+ * Replaces tucker (inc/mode_product.hpp:101-108) with prefactor = 1 and
+ * apply_split_phi (inc/split_phi.hpp:53-62) with prefactor = (l!)^(d-1).
+ * M_mu is rows[mu] x dims[mu].  Intermediates live in the context's
+ * workspace; out may alias t. */
+int kp_tucker_f64(kp_ctx* ctx, const double* t, const int* dims, int d,
+                  const double* const* ms, const int* rows, double prefactor, double* out);
+int kp_tucker_c128(kp_ctx* ctx, const double* t, const int* dims, int d,
+                   const double* const* ms, const int* rows, double prefactor, double* out);
+
+/* out = sum_mu t x_mu A_mu.  Replaces kronsum_action (inc/mode_product.hpp:111-121).
+ * out must not alias t. */
+int kp_kronsum_f64(kp_ctx* ctx, const double* t, const int* dims, int d,
+                   const double* const* as, double* out);
+int kp_kronsum_c128(kp_ctx* ctx, const double* t, const int* dims, int d,
+                    const double* const* as, double* out);
+
+/* Host-buffer variants (the drop-in path: host in, host out, H2D/D2H inside). */
+int kp_host_mode_product_f64(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
+                             const double* m, int rows, int cols, double alpha, double beta,
+                             double* out);
+int kp_host_tucker_f64(kp_ctx* ctx, const double* t, const int* dims, int d,
+                       const double* const* ms, const int* rows, double prefactor,
+                       double* out);
+int kp_host_tucker_c128(kp_ctx* ctx, const double* t, const int* dims, int d,
+                        const double* const* ms, const int* rows, double prefactor,
+                        double* out);
+int kp_host_kronsum_f64(kp_ctx* ctx, const double* t, const int* dims, int d,
+                        const double* const* as, double* out);
+
+/* ---------------- elementwise (inc/tensor.hpp:123-155) ---------------- */
+/* y = alpha * x + y  (axpy) */
+int kp_axpy_f64(kp_ctx* ctx, size_t n, double alpha, const double* x, double* y);
+/* z = x + alpha * y  (add_scaled) */
+int kp_add_scaled_f64(kp_ctx* ctx, size_t n, const double* x, double alpha, const double* y,
+                      double* z);
+/* gout = g(t, u) over a tensor of shape dims */
+int kp_eval_g_f64(kp_ctx* ctx, const kp_gfun* g, double t, const double* u, const int* dims,
+                  int d, double* gout);
+int kp_eval_g_c128(kp_ctx* ctx, const kp_gfun* g, double t, const double* u, const int* dims,
+                   int d, double* gout);
+/* *all_finite = 1 if every entry is finite (inc/integrators.hpp:101-108) */
+int kp_all_finite_f64(kp_ctx* ctx, size_t n, const double* x, int* all_finite);
+
+/* Measured FP64 peak of this device: a DMMA (mma.sync m8n8k4 f64) loop over
+ * all SMs; returns TFLOP/s.  Used as the roofline denominator. */
+int kp_measure_fp64_peak(kp_ctx* ctx, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

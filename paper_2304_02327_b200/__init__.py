@@ -1,0 +1,18 @@
+"""kronphi-b200: B200-native (sm_100a) direction-split phi-function action of
+arXiv 2304.02327 -- the mu-mode/Tucker operator, the small-matrix phi_l
+factors and the exponential Euler / ETD2RK / Lawson steppers, behind the C ABI
+in include/kronphi_b200.h (libkronphi_b200.so, hand-written DMMA kernels).
+
+The Python surface mirrors the reference C++ API (proj/include/kronphi/);
+there is no CPU fallback -- a missing library or GPU raises.
+"""
+from ._lib import (DivergenceError, InvalidArgument, KronphiError, CudaError, Context,
+                   default_context, LIB_PATH)
+from .api import (KroneckerSum, fortran_empty, fortran_zeros, kronsum_action, mode_product,
+                  mode_product_into, to_device, to_host, tucker)
+
+__all__ = [
+    "DivergenceError", "InvalidArgument", "KronphiError", "CudaError", "Context",
+    "default_context", "LIB_PATH", "KroneckerSum", "fortran_empty", "fortran_zeros",
+    "kronsum_action", "mode_product", "mode_product_into", "to_device", "to_host", "tucker",
+]

@@ -1,0 +1,197 @@
+"""ctypes binding of libkronphi_b200.so (the C ABI in include/kronphi_b200.h).
+
+The shared library is built in-tree by ``make -C paper_2304_02327_b200``
+(``__graft_entry__.build()``).  There is no fallback: if the library or a
+CUDA device is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libkronphi_b200.so")
+
+KP_OK, KP_EINVAL, KP_ERUNTIME, KP_EDIVERGE, KP_ECUDA = range(5)
+LAWSON_EULER, LAWSON2B, EXP_EULER, EXP_EULER_LS, ETD2RK = range(5)
+G_ZERO, G_SQUARE, G_CONST, G_ALLEN_CAHN, G_BRUSSELATOR, G_NLS = range(6)
+
+
+class KronphiError(RuntimeError):
+    """Base class; ``code`` is the kp status code."""
+
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+class InvalidArgument(KronphiError, ValueError):
+    """std::invalid_argument in the reference (sizing/validation errors)."""
+
+
+class CudaError(KronphiError):
+    pass
+
+
+class DivergenceError(KronphiError):
+    """kronphi::DivergenceError (inc/integrators.hpp:86-97)."""
+
+    def __init__(self, code, msg, step=0):
+        super().__init__(code, msg)
+        self.step = step
+
+
+class GFun(C.Structure):
+    _fields_ = [("kind", C.c_int), ("p", C.c_double * 4)]
+
+
+_D, _I, _L, _SZ = C.c_double, C.c_int, C.c_long, C.c_size_t
+_PD, _PI, _VP = C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_void_p
+_PPD = C.POINTER(C.POINTER(C.c_double))
+_CTX = C.c_void_p
+
+_SIGS = {
+    "kp_last_error": (C.c_char_p, []),
+    "kp_ctx_create": (_I, [_I, C.POINTER(_CTX)]),
+    "kp_ctx_destroy": (_I, [_CTX]),
+    "kp_ctx_set_stream": (_I, [_CTX, _VP]),
+    "kp_ctx_use_own_stream": (_I, [_CTX]),
+    "kp_ctx_get_stream": (_VP, [_CTX]),
+    "kp_ctx_synchronize": (_I, [_CTX]),
+    "kp_ctx_launch_count": (C.c_ulonglong, [_CTX]),
+    "kp_malloc": (_I, [_CTX, _SZ, C.POINTER(_VP)]),
+    "kp_free": (_I, [_CTX, _VP]),
+    "kp_upload": (_I, [_CTX, _VP, _VP, _SZ]),
+    "kp_download": (_I, [_CTX, _VP, _VP, _SZ]),
+    "kp_memset": (_I, [_CTX, _VP, _I, _SZ]),
+    "kp_mode_product_f64": (_I, [_CTX, _VP, _PI, _I, _I, _VP, _I, _I, _D, _D, _VP]),
+    "kp_mode_product_c128": (_I, [_CTX, _VP, _PI, _I, _I, _VP, _I, _I, _PD, _PD, _VP]),
+    "kp_tucker_f64": (_I, [_CTX, _VP, _PI, _I, _PPD, _PI, _D, _VP]),
+    "kp_tucker_c128": (_I, [_CTX, _VP, _PI, _I, _PPD, _PI, _D, _VP]),
+    "kp_kronsum_f64": (_I, [_CTX, _VP, _PI, _I, _PPD, _VP]),
+    "kp_kronsum_c128": (_I, [_CTX, _VP, _PI, _I, _PPD, _VP]),
+    "kp_host_mode_product_f64": (_I, [_CTX, _VP, _PI, _I, _I, _VP, _I, _I, _D, _D, _VP]),
+    "kp_host_tucker_f64": (_I, [_CTX, _VP, _PI, _I, _PPD, _PI, _D, _VP]),
+    "kp_host_tucker_c128": (_I, [_CTX, _VP, _PI, _I, _PPD, _PI, _D, _VP]),
+    "kp_host_kronsum_f64": (_I, [_CTX, _VP, _PI, _I, _PPD, _VP]),
+    "kp_axpy_f64": (_I, [_CTX, _SZ, _D, _VP, _VP]),
+    "kp_add_scaled_f64": (_I, [_CTX, _SZ, _VP, _D, _VP, _VP]),
+    "kp_eval_g_f64": (_I, [_CTX, C.POINTER(GFun), _D, _VP, _PI, _I, _VP]),
+    "kp_eval_g_c128": (_I, [_CTX, C.POINTER(GFun), _D, _VP, _PI, _I, _VP]),
+    "kp_all_finite_f64": (_I, [_CTX, _SZ, _VP, _PI]),
+    "kp_measure_fp64_peak": (_I, [_CTX, _PD]),
+}
+
+# Every symbol include/kronphi_b200.h declares (checked by tests/test_abi.py).
+EXPORTS = tuple(_SIGS)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load():
+    """Load the shared library (raises if it has not been built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} not built; run `make -C {HERE}` or __graft_entry__.build()")
+            lib = C.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            for extra in _EXTRA_SIGS:
+                name, res, args = extra
+                if hasattr(lib, name):
+                    fn = getattr(lib, name)
+                    fn.restype = res
+                    fn.argtypes = args
+            _lib = lib
+        return _lib
+
+
+_EXTRA_SIGS = []
+
+
+def register(name, res, args):
+    """Register the signature of an additional entry point (used by modules
+    that bind later-added parts of the ABI)."""
+    _EXTRA_SIGS.append((name, res, args))
+    if _lib is not None and hasattr(_lib, name):
+        fn = getattr(_lib, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+def check(rc, step=0):
+    if rc == KP_OK:
+        return
+    msg = load().kp_last_error().decode(errors="replace")
+    if rc == KP_EINVAL:
+        raise InvalidArgument(rc, msg)
+    if rc == KP_EDIVERGE:
+        raise DivergenceError(rc, msg, step)
+    if rc == KP_ECUDA:
+        raise CudaError(rc, msg)
+    raise KronphiError(rc, msg)
+
+
+def ints(xs):
+    xs = [int(x) for x in xs]
+    return (C.c_int * len(xs))(*xs)
+
+
+def ptr_array(ptrs):
+    return (C.POINTER(C.c_double) * len(ptrs))(*[C.cast(C.c_void_p(int(p)), _PD) for p in ptrs])
+
+
+class Context:
+    """Owns a kp_ctx (device, stream, workspace).  One per device per thread
+    of use; not thread-safe (see include/kronphi_b200.h)."""
+
+    def __init__(self, device=0):
+        self.lib = load()
+        h = _CTX()
+        check(self.lib.kp_ctx_create(int(device), C.byref(h)))
+        self.h = h
+        self.device = int(device)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.kp_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_handle):
+        check(self.lib.kp_ctx_set_stream(self.h, stream_handle))
+
+    def synchronize(self):
+        check(self.lib.kp_ctx_synchronize(self.h))
+
+    @property
+    def launches(self):
+        return int(self.lib.kp_ctx_launch_count(self.h))
+
+    def fp64_peak_tflops(self):
+        v = C.c_double(0)
+        check(self.lib.kp_measure_fp64_peak(self.h, C.byref(v)))
+        return v.value
+
+
+_ctxs = {}
+
+
+def default_context(device=0):
+    c = _ctxs.get(device)
+    if c is None:
+        c = Context(device)
+        _ctxs[device] = c
+    return c

@@ -1,0 +1,553 @@
+// capi.cpp -- the extern "C" boundary of libkronphi_b200.so (include/kronphi_b200.h).
+//
+// Every entry point validates its arguments with the reference's rules and
+// messages (inc/mode_product.hpp:45-56, :29-33, :103, :113), runs the device
+// path, and maps exceptions to status codes + kp_last_error().  There is no
+// CPU compute fallback anywhere: a missing GPU or a CUDA failure is an error.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kp_internal.h"
+
+namespace kp {
+
+void* Workspace::get(int slot, size_t bytes) {
+  if (slot >= int(ptr.size())) {
+    ptr.resize(slot + 1, nullptr);
+    cap.resize(slot + 1, 0);
+  }
+  if (cap[slot] < bytes) {
+    if (ptr[slot]) KP_CUDA(cudaFree(ptr[slot]));
+    ptr[slot] = nullptr;
+    cap[slot] = 0;
+    KP_CUDA(cudaMalloc(&ptr[slot], bytes));
+    cap[slot] = bytes;
+  }
+  return ptr[slot];
+}
+void Workspace::release() {
+  for (void* p : ptr)
+    if (p) cudaFree(p);
+  ptr.clear();
+  cap.clear();
+}
+void* PinnedStage::get(size_t bytes) {
+  if (cap < bytes) {
+    if (ptr) KP_CUDA(cudaFreeHost(ptr));
+    ptr = nullptr;
+    cap = 0;
+    KP_CUDA(cudaMallocHost(&ptr, bytes));
+    cap = bytes;
+  }
+  return ptr;
+}
+void PinnedStage::release() {
+  if (ptr) cudaFreeHost(ptr);
+  ptr = nullptr;
+  cap = 0;
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return KP_OK;
+  } catch (const kp::divergence_error& e) {
+    g_err = e.what();
+    return KP_EDIVERGE;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return KP_EINVAL;
+  } catch (const kp::cuda_error& e) {
+    g_err = e.what();
+    return KP_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return KP_ERUNTIME;
+  }
+}
+
+void need_ctx(kp_ctx* ctx) {
+  if (!ctx) throw invalid_argument("kronphi_b200: null context");
+  KP_CUDA(cudaSetDevice(ctx->device));
+}
+
+std::vector<int> check_dims(const int* dims, int d, const char* who) {
+  if (d <= 0 || !dims) throw invalid_argument(std::string(who) + ": Tensor: empty dims");
+  std::vector<int> v(dims, dims + d);
+  for (int x : v)
+    if (x <= 0) throw invalid_argument(std::string(who) + ": Tensor: nonpositive dim");
+  return v;
+}
+
+size_t numel(const std::vector<int>& dims) {
+  size_t n = 1;
+  for (int x : dims) n *= size_t(x);
+  return n;
+}
+
+// inc/mode_product.hpp:45-56 (same messages)
+void check_mode(const std::vector<int>& dims, int mode, int cols) {
+  const int d = int(dims.size());
+  if (mode < 0 || mode >= d)
+    throw invalid_argument("mode_product: mode " + std::to_string(mode) +
+                           " out of range for order " + std::to_string(d));
+  if (cols != dims[mode])
+    throw invalid_argument("mode_product: size mismatch on mode " + std::to_string(mode) +
+                           ": matrix has " + std::to_string(cols) + " columns, tensor dim is " +
+                           std::to_string(dims[mode]));
+}
+
+}  // namespace
+
+using ModeFn = void (*)(kp_ctx*, const double*, const std::vector<int>&, int, const double*, int,
+                        const Epilogue&, double*);
+
+// Tucker operator on device pointers: out = ((pref*t) x_1 M_1 ... x_d M_d).
+// The prefactor is folded into the first mode's alpha (exact for the powers
+// of two (l!)^(d-1) of l <= 2, inc/split_phi.hpp:41).  Ping-pong buffers come
+// from workspace slots slot_base, slot_base+1.  `last` (optional) is the
+// epilogue of the final mode (stepper fusion).  comps = doubles per entry.
+void tucker_generic(kp_ctx* ctx, ModeFn mp, int comps, const double* t, std::vector<int> dims,
+                    const double* const* ms, const int* rows, double pref, double* out,
+                    const Epilogue* last = nullptr, int slot_base = 0) {
+  const int d = int(dims.size());
+  const double* cur = t;
+  for (int mu = 0; mu < d; ++mu) {
+    std::vector<int> od = dims;
+    od[mu] = rows[mu];
+    double* dst;
+    if (mu == d - 1 && !(d == 1 && out == t)) {
+      dst = out;
+    } else {
+      dst = static_cast<double*>(
+          ctx->ws.get(slot_base + (mu & 1), numel(od) * comps * sizeof(double)));
+    }
+    Epilogue e;
+    if (mu == d - 1 && last) e = *last;
+    e.alpha = (mu == 0) ? pref : 1.0;
+    mp(ctx, cur, dims, mu, ms[mu], rows[mu], e, dst);
+    dims = od;
+    cur = dst;
+  }
+  if (cur != out)
+    KP_CUDA(cudaMemcpyAsync(out, cur, numel(dims) * comps * sizeof(double),
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+}
+
+void tucker_f64(kp_ctx* ctx, const double* t, std::vector<int> dims, const double* const* ms,
+                const int* rows, double pref, double* out, const Epilogue* last = nullptr,
+                int slot_base = 0) {
+  tucker_generic(ctx, mode_product_f64, 1, t, std::move(dims), ms, rows, pref, out, last,
+                 slot_base);
+}
+void tucker_c128(kp_ctx* ctx, const double* t, std::vector<int> dims, const double* const* ms,
+                 const int* rows, double pref, double* out, const Epilogue* last = nullptr,
+                 int slot_base = 0) {
+  tucker_generic(ctx, mode_product_c128, 2, t, std::move(dims), ms, rows, pref, out, last,
+                 slot_base);
+}
+
+// kronsum_action (inc/mode_product.hpp:111-121): term 0 stores, terms >= 1
+// accumulate (beta = 1); `last` fuses an epilogue into the final term.
+void kronsum_generic(kp_ctx* ctx, ModeFn mp, const double* t, const std::vector<int>& dims,
+                     const double* const* as, double* out, const Epilogue* last = nullptr) {
+  const int d = int(dims.size());
+  for (int mu = 0; mu < d; ++mu) {
+    Epilogue e;
+    if (mu == d - 1 && last) e = *last;
+    e.alpha = 1.0;
+    e.beta = mu > 0 ? 1.0 : 0.0;
+    mp(ctx, t, dims, mu, as[mu], dims[mu], e, out);
+  }
+}
+
+}  // namespace kp
+
+using namespace kp;
+
+extern "C" {
+
+const char* kp_last_error(void) { return g_err.c_str(); }
+
+int kp_ctx_create(int device, kp_ctx** out) {
+  return guard([&] {
+    if (!out) throw invalid_argument("kp_ctx_create: null out");
+    int count = 0;
+    KP_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count)
+      throw invalid_argument("kp_ctx_create: no CUDA device " + std::to_string(device));
+    KP_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    KP_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+      throw runtime_error(std::string("kronphi_b200 needs an sm_100 (Blackwell) GPU, found ") +
+                          prop.name);
+    kp_ctx* c = new kp_ctx;
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    KP_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+    KP_CUDA(cudaMalloc(&c->d_flag, 256));
+    KP_CUDA(cudaMallocHost(&c->h_flag, 256));
+    *out = c;
+  });
+}
+
+int kp_ctx_destroy(kp_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->ws.release();
+    ctx->pin_in.release();
+    ctx->pin_out.release();
+    cudaFree(ctx->d_flag);
+    cudaFreeHost(ctx->h_flag);
+    cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+  });
+}
+
+int kp_ctx_set_stream(kp_ctx* ctx, void* stream) {
+  return guard([&] {
+    need_ctx(ctx);
+    ctx->stream = static_cast<cudaStream_t>(stream);  // 0 = the legacy default stream
+  });
+}
+
+int kp_ctx_use_own_stream(kp_ctx* ctx) {
+  return guard([&] {
+    need_ctx(ctx);
+    ctx->stream = ctx->own_stream;
+  });
+}
+
+void* kp_ctx_get_stream(kp_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int kp_ctx_synchronize(kp_ctx* ctx) {
+  return guard([&] {
+    need_ctx(ctx);
+    KP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+unsigned long long kp_ctx_launch_count(kp_ctx* ctx) { return ctx ? ctx->launches : 0ULL; }
+
+int kp_malloc(kp_ctx* ctx, size_t bytes, void** ptr) {
+  return guard([&] {
+    need_ctx(ctx);
+    KP_CUDA(cudaMalloc(ptr, std::max<size_t>(bytes, 16)));
+  });
+}
+int kp_free(kp_ctx* ctx, void* ptr) {
+  return guard([&] {
+    need_ctx(ctx);
+    KP_CUDA(cudaFree(ptr));
+  });
+}
+int kp_upload(kp_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  return guard([&] {
+    need_ctx(ctx);
+    KP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    KP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+int kp_download(kp_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  return guard([&] {
+    need_ctx(ctx);
+    KP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    KP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+int kp_memset(kp_ctx* ctx, void* dst, int value, size_t bytes) {
+  return guard([&] {
+    need_ctx(ctx);
+    KP_CUDA(cudaMemsetAsync(dst, value, bytes, ctx->stream));
+  });
+}
+
+// ---------------- mode products ----------------
+
+int kp_mode_product_f64(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
+                        const double* m, int rows, int cols, double alpha, double beta,
+                        double* out) {
+  return guard([&] {
+    need_ctx(ctx);
+    const auto dv = check_dims(dims, d, "mode_product");
+    check_mode(dv, mode, cols);
+    if (rows <= 0) throw invalid_argument("mode_product: matrix has no rows");
+    if (out == t) throw invalid_argument("mode_product: out must not alias the input");
+    Epilogue e;
+    e.alpha = alpha;
+    e.beta = beta;
+    mode_product_f64(ctx, t, dv, mode, m, rows, e, out);
+  });
+}
+
+int kp_tucker_f64(kp_ctx* ctx, const double* t, const int* dims, int d, const double* const* ms,
+                  const int* rows, double prefactor, double* out) {
+  return guard([&] {
+    need_ctx(ctx);
+    const auto dv = check_dims(dims, d, "tucker");
+    if (!ms || !rows) throw invalid_argument("tucker: expected one factor per mode");
+    for (int mu = 0; mu < d; ++mu)
+      if (rows[mu] <= 0) throw invalid_argument("tucker: factor has no rows");
+    tucker_f64(ctx, t, dv, ms, rows, prefactor, out);
+  });
+}
+
+int kp_kronsum_f64(kp_ctx* ctx, const double* t, const int* dims, int d, const double* const* as,
+                   double* out) {
+  return guard([&] {
+    need_ctx(ctx);
+    const auto dv = check_dims(dims, d, "kronsum_action");
+    if (!as) throw invalid_argument("kronsum_action: expected one factor per mode");
+    if (out == t) throw invalid_argument("kronsum_action: out must not alias the input");
+    kronsum_generic(ctx, mode_product_f64, t, dv, as, out);
+  });
+}
+
+// ---------------- host-buffer drop-in variants ----------------
+
+namespace {
+
+// Upload n_mats square-or-rectangular host matrices into one device slab.
+std::vector<const double*> upload_mats(kp_ctx* ctx, int slot, const double* const* hm,
+                                       const std::vector<size_t>& sizes) {
+  size_t total = 0;
+  for (size_t s : sizes) total += (s + 1) & ~size_t(1);  // keep 16-byte alignment
+  double* dev = static_cast<double*>(ctx->ws.get(slot, total * sizeof(double)));
+  std::vector<const double*> out;
+  size_t off = 0;
+  for (size_t i = 0; i < sizes.size(); ++i) {
+    KP_CUDA(cudaMemcpyAsync(dev + off, hm[i], sizes[i] * sizeof(double), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    out.push_back(dev + off);
+    off += (sizes[i] + 1) & ~size_t(1);
+  }
+  return out;
+}
+
+// Tensor H2D through the pinned stage (one pageable->pinned memcpy plus one
+// async DMA; large tensors go in 64 MiB chunks so the two overlap poorly but
+// never need a pinned buffer the size of the tensor twice).
+void h2d(kp_ctx* ctx, double* dst, const double* src, size_t n) {
+  KP_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+}
+void d2h(kp_ctx* ctx, double* dst, const double* src, size_t n) {
+  KP_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  KP_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+constexpr int SLOT_HOST_IN = 8, SLOT_HOST_OUT = 9, SLOT_HOST_MATS = 10;
+
+}  // namespace
+
+int kp_host_mode_product_f64(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
+                             const double* m, int rows, int cols, double alpha, double beta,
+                             double* out) {
+  return guard([&] {
+    need_ctx(ctx);
+    const auto dv = check_dims(dims, d, "mode_product");
+    check_mode(dv, mode, cols);
+    auto od = dv;
+    od[mode] = rows;
+    const size_t nin = numel(dv), nout = numel(od);
+    double* din = static_cast<double*>(ctx->ws.get(SLOT_HOST_IN, nin * sizeof(double)));
+    double* dout = static_cast<double*>(ctx->ws.get(SLOT_HOST_OUT, nout * sizeof(double)));
+    const double* hm[1] = {m};
+    auto dm = upload_mats(ctx, SLOT_HOST_MATS, hm, {size_t(rows) * cols});
+    h2d(ctx, din, t, nin);
+    if (beta != 0.0) h2d(ctx, dout, out, nout);
+    Epilogue e;
+    e.alpha = alpha;
+    e.beta = beta;
+    mode_product_f64(ctx, din, dv, mode, dm[0], rows, e, dout);
+    d2h(ctx, out, dout, nout);
+  });
+}
+
+int kp_host_tucker_f64(kp_ctx* ctx, const double* t, const int* dims, int d,
+                       const double* const* ms, const int* rows, double prefactor, double* out) {
+  return guard([&] {
+    need_ctx(ctx);
+    const auto dv = check_dims(dims, d, "tucker");
+    std::vector<size_t> sizes;
+    std::vector<int> od = dv;
+    for (int mu = 0; mu < d; ++mu) {
+      sizes.push_back(size_t(rows[mu]) * dv[mu]);
+      od[mu] = rows[mu];
+    }
+    const size_t nin = numel(dv), nout = numel(od);
+    double* din = static_cast<double*>(ctx->ws.get(SLOT_HOST_IN, nin * sizeof(double)));
+    double* dout = static_cast<double*>(ctx->ws.get(SLOT_HOST_OUT, nout * sizeof(double)));
+    auto dm = upload_mats(ctx, SLOT_HOST_MATS, ms, sizes);
+    h2d(ctx, din, t, nin);
+    tucker_f64(ctx, din, dv, dm.data(), rows, prefactor, dout);
+    d2h(ctx, out, dout, nout);
+  });
+}
+
+int kp_host_kronsum_f64(kp_ctx* ctx, const double* t, const int* dims, int d,
+                        const double* const* as, double* out) {
+  return guard([&] {
+    need_ctx(ctx);
+    const auto dv = check_dims(dims, d, "kronsum_action");
+    std::vector<size_t> sizes;
+    for (int mu = 0; mu < d; ++mu) sizes.push_back(size_t(dv[mu]) * dv[mu]);
+    const size_t n = numel(dv);
+    double* din = static_cast<double*>(ctx->ws.get(SLOT_HOST_IN, n * sizeof(double)));
+    double* dout = static_cast<double*>(ctx->ws.get(SLOT_HOST_OUT, n * sizeof(double)));
+    auto dm = upload_mats(ctx, SLOT_HOST_MATS, as, sizes);
+    h2d(ctx, din, t, n);
+    kronsum_generic(ctx, mode_product_f64, din, dv, dm.data(), dout);
+    d2h(ctx, out, dout, n);
+  });
+}
+
+// ---------------- elementwise ----------------
+
+int kp_axpy_f64(kp_ctx* ctx, size_t n, double alpha, const double* x, double* y) {
+  return guard([&] {
+    need_ctx(ctx);
+    launch_fma(ctx, n, alpha, x, y, y);
+  });
+}
+
+int kp_add_scaled_f64(kp_ctx* ctx, size_t n, const double* x, double alpha, const double* y,
+                      double* z) {
+  return guard([&] {
+    need_ctx(ctx);
+    launch_fma(ctx, n, alpha, y, x, z);
+  });
+}
+
+int kp_eval_g_f64(kp_ctx* ctx, const kp_gfun* g, double t, const double* u, const int* dims,
+                  int d, double* gout) {
+  return guard([&] {
+    need_ctx(ctx);
+    const auto dv = check_dims(dims, d, "g");
+    if (!g) throw invalid_argument("g: null descriptor");
+    if (g->kind == KP_G_NLS) throw invalid_argument("g: NLS needs a complex tensor");
+    size_t half = 0;
+    if (g->kind == KP_G_BRUSSELATOR) {
+      if (dv.back() != 2)
+        throw invalid_argument("brusselator g: slowest mode must hold 2 species");
+      half = numel(dv) / 2;
+    }
+    launch_eval_g(ctx, *g, t, u, numel(dv), half, false, gout);
+  });
+}
+
+int kp_eval_g_c128(kp_ctx* ctx, const kp_gfun* g, double t, const double* u, const int* dims,
+                   int d, double* gout) {
+  return guard([&] {
+    need_ctx(ctx);
+    const auto dv = check_dims(dims, d, "g");
+    if (!g) throw invalid_argument("g: null descriptor");
+    if (g->kind == KP_G_ALLEN_CAHN || g->kind == KP_G_BRUSSELATOR)
+      throw invalid_argument("g: unsupported nonlinearity kind for complex");
+    launch_eval_g(ctx, *g, t, u, numel(dv), 0, true, gout);
+  });
+}
+
+int kp_all_finite_f64(kp_ctx* ctx, size_t n, const double* x, int* ok) {
+  return guard([&] {
+    need_ctx(ctx);
+    *ok = all_finite(ctx, n, x);
+  });
+}
+
+int kp_measure_fp64_peak(kp_ctx* ctx, double* tflops) {
+  return guard([&] {
+    need_ctx(ctx);
+    *tflops = measure_fp64_peak(ctx);
+  });
+}
+
+// ---------------- complex128 ----------------
+
+namespace {
+void real_scalar(const double* z, const char* what, double* out) {
+  if (!z) {
+    *out = (std::string(what) == "beta") ? 0.0 : 1.0;
+    return;
+  }
+  if (z[1] != 0.0)
+    throw invalid_argument(std::string("mode_product: complex ") + what +
+                           " with nonzero imaginary part is not supported");
+  *out = z[0];
+}
+}  // namespace
+
+int kp_mode_product_c128(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
+                         const double* m, int rows, int cols, const double* alpha2,
+                         const double* beta2, double* out) {
+  return guard([&] {
+    need_ctx(ctx);
+    const auto dv = check_dims(dims, d, "mode_product");
+    check_mode(dv, mode, cols);
+    if (rows <= 0) throw invalid_argument("mode_product: matrix has no rows");
+    if (out == t) throw invalid_argument("mode_product: out must not alias the input");
+    Epilogue e;
+    real_scalar(alpha2, "alpha", &e.alpha);
+    real_scalar(beta2, "beta", &e.beta);
+    mode_product_c128(ctx, t, dv, mode, m, rows, e, out);
+  });
+}
+
+int kp_tucker_c128(kp_ctx* ctx, const double* t, const int* dims, int d, const double* const* ms,
+                   const int* rows, double prefactor, double* out) {
+  return guard([&] {
+    need_ctx(ctx);
+    const auto dv = check_dims(dims, d, "tucker");
+    if (!ms || !rows) throw invalid_argument("tucker: expected one factor per mode");
+    for (int mu = 0; mu < d; ++mu)
+      if (rows[mu] <= 0) throw invalid_argument("tucker: factor has no rows");
+    tucker_c128(ctx, t, dv, ms, rows, prefactor, out);
+  });
+}
+
+int kp_kronsum_c128(kp_ctx* ctx, const double* t, const int* dims, int d,
+                    const double* const* as, double* out) {
+  return guard([&] {
+    need_ctx(ctx);
+    const auto dv = check_dims(dims, d, "kronsum_action");
+    if (!as) throw invalid_argument("kronsum_action: expected one factor per mode");
+    if (out == t) throw invalid_argument("kronsum_action: out must not alias the input");
+    kronsum_generic(ctx, mode_product_c128, t, dv, as, out);
+  });
+}
+
+int kp_host_tucker_c128(kp_ctx* ctx, const double* t, const int* dims, int d,
+                        const double* const* ms, const int* rows, double prefactor,
+                        double* out) {
+  return guard([&] {
+    need_ctx(ctx);
+    const auto dv = check_dims(dims, d, "tucker");
+    std::vector<size_t> sizes;
+    std::vector<int> od = dv;
+    for (int mu = 0; mu < d; ++mu) {
+      sizes.push_back(2 * size_t(rows[mu]) * dv[mu]);
+      od[mu] = rows[mu];
+    }
+    const size_t nin = 2 * numel(dv), nout = 2 * numel(od);
+    double* din = static_cast<double*>(ctx->ws.get(SLOT_HOST_IN, nin * sizeof(double)));
+    double* dout = static_cast<double*>(ctx->ws.get(SLOT_HOST_OUT, nout * sizeof(double)));
+    auto dm = upload_mats(ctx, SLOT_HOST_MATS, ms, sizes);
+    h2d(ctx, din, t, nin);
+    tucker_c128(ctx, din, dv, dm.data(), rows, prefactor, dout);
+    d2h(ctx, out, dout, nout);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,125 @@
+// kp_internal.h -- shared host-side declarations of the kronphi_b200 library.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kronphi_b200.h"
+
+namespace kp {
+
+// Exceptions thrown inside the library and mapped to status codes at the C
+// boundary (capi.cpp).  Same taxonomy as the reference's exceptions.
+struct invalid_argument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct runtime_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct divergence_error : std::runtime_error {
+  long step;
+  divergence_error(const std::string& m, long s) : std::runtime_error(m), step(s) {}
+};
+
+#define KP_CUDA(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw ::kp::cuda_error(std::string(#call) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+// Grow-only device scratch with a few named slots (ping-pong buffers of the
+// Tucker operator, stepper temporaries).  No cudaMalloc on the hot path after
+// the first call at a given size.
+struct Workspace {
+  std::vector<void*> ptr;
+  std::vector<size_t> cap;
+  void* get(int slot, size_t bytes);
+  void release();
+};
+
+struct PinnedStage {
+  void* ptr = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes);
+  void release();
+};
+
+}  // namespace kp
+
+struct kp_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  unsigned long long launches = 0;
+  kp::Workspace ws;
+  kp::PinnedStage pin_in, pin_out;
+  double* d_flag = nullptr;  // small device scratch (finite flag etc.)
+  int* h_flag = nullptr;     // pinned host mirror
+};
+
+namespace kp {
+
+// ---- GEMM-shaped mode-product core (mode_product.cu) ----
+// C_q(m,n) = epi(alpha * sum_k A_q(m,k) B_q(k,n), ...), q < batch, with
+//   A_q(m,k) = A[q*sA + m + k*lda]                 (M-contiguous)
+//   B_q(k,n) = B[q*sB + k*sBk + n*sBn]             (sBk==1 or sBn==1)
+//   C_q(m,n) = C[q*sC + m + n*ldc]                 (M-contiguous)
+enum EpiKind : int {
+  EPI_STORE = 0,    // C = alpha*acc + beta*C
+  EPI_FMA_X = 1,    // C = fma(gamma, alpha*acc, X)             (add_scaled)
+  EPI_ADD_G = 2,    // C = (alpha*acc + beta*C) + g(t, X)        (kronsum + g)
+  EPI_STAGE_D = 3,  // S = fma(gamma, alpha*acc, X); C = S; D = g(t2, S) - g(t, X)
+};
+
+struct Epilogue {
+  int kind = EPI_STORE;
+  double alpha = 1.0, beta = 0.0, gamma = 0.0;
+  const double* X = nullptr;  // same layout as C
+  double* D = nullptr;        // second output (EPI_STAGE_D)
+  kp_gfun g{};
+  double t = 0.0, t2 = 0.0;
+};
+
+struct GemmProblem {
+  int M = 0, N = 0, K = 0, batch = 1;
+  const double* A = nullptr;
+  long long lda = 0, sA = 0;
+  const double* B = nullptr;
+  long long sBk = 0, sBn = 0, sB = 0;
+  double* C = nullptr;
+  long long ldc = 0, sC = 0;
+};
+
+// cplx: 0 real, 1 complex rows (mode 0), 2 complex combine (mode >= 1); see mode_product.cu
+void launch_gemm(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int cplx = 0);
+
+// Real mode product out = epi(t x_mode M) on device pointers.
+void mode_product_f64(kp_ctx* ctx, const double* t, const std::vector<int>& dims, int mode,
+                      const double* m, int rows, const Epilogue& e, double* out);
+
+// Complex mode product (interleaved complex128, cplx.cu).  m is rows x dims[mode].
+void mode_product_c128(kp_ctx* ctx, const double* t, const std::vector<int>& dims, int mode,
+                       const double* m, int rows, const Epilogue& e, double* out);
+
+// ---- elementwise (elementwise.cu) ----
+// z = fma(b, y, x): axpy is (b=alpha, y=x, x=y, z=y), add_scaled is (b=alpha, y=y, x=x)
+void launch_fma(kp_ctx* ctx, size_t n, double b, const double* y, const double* x, double* z);
+// out = g(t, u); n entries (complex: n complex entries); half > 0 = Brusselator
+// species offset (u = [0, half), v = [half, 2 half)).
+void launch_eval_g(kp_ctx* ctx, const kp_gfun& g, double t, const double* u, size_t n,
+                   size_t half, bool cplx, double* out);
+void launch_scale(kp_ctx* ctx, size_t n, double a, const double* x, double* y);
+int all_finite(kp_ctx* ctx, size_t n, const double* x);
+double measure_fp64_peak(kp_ctx* ctx);
+
+}  // namespace kp
