@@ -194,11 +194,9 @@ def main():
 
     n = args.n
     v_h, a_h = make_inputs(n)
-    fs = kp.build_split_phi_factors([a_h] * 3, 1e-3, 1) if hasattr(kp, "build_split_phi_factors") \
-        else None
-    if fs is None:
-        from paper_2304_02327_b200 import phi as _phi  # noqa: F401  (device phi builder)
-    fs_d = [kp.to_device(f) if isinstance(f, np.ndarray) else f for f in fs]
+    # L = phi_1(1e-3 A) built by the device phi builder (untimed setup)
+    a_d = kp.to_device(a_h)
+    fs_d = kp.build_split_phi([a_d, a_d, a_d], 1e-3, 1).factors
     v_d = kp.to_device(v_h)
     out_d = kp.fortran_empty([n, n, n])
     dims = [n, n, n]

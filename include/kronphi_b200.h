@@ -143,6 +143,61 @@ int kp_eval_g_c128(kp_ctx* ctx, const kp_gfun* g, double t, const double* u, con
 /* *all_finite = 1 if every entry is finite (inc/integrators.hpp:101-108) */
 int kp_all_finite_f64(kp_ctx* ctx, size_t n, const double* x, int* all_finite);
 
+/* ---------------- matrix functions (inc/matrix_functions.hpp) ---------------- */
+/* q-point Gauss-Legendre-Lobatto rule on [0,1] (host; src/gll_rule.cpp:35-72) */
+int kp_gll_rule(int q, double* nodes, double* weights);
+/* out = e^x, n x n (expm, inc/matrix_functions.hpp:76-95) */
+int kp_expm_f64(kp_ctx* ctx, const double* x, int n, double* out);
+int kp_expm_c128(kp_ctx* ctx, const double* x, int n, double* out);
+/* phis = [phi_0(x), ..., phi_ell_max(x)], ell_max+1 consecutive n x n
+ * matrices (phiquad, :146-199; PhiTable::phis); forced_scaling < 0 = none. */
+int kp_phiquad_f64(kp_ctx* ctx, const double* x, int n, int ell_max, int q, int forced_scaling,
+                   double* phis, int* scaling_exponent);
+int kp_phiquad_c128(kp_ctx* ctx, const double* x, int n, int ell_max, int q, int forced_scaling,
+                    double* phis, int* scaling_exponent);
+
+/* ---------------- direction splitting (inc/split_phi.hpp) ---------------- */
+/* factors[mu] = phi_ell(tau*A_mu) (expm for ell = 0), *prefactor = (ell!)^(d-1)
+ * (build_split_phi, :25-48).  Apply with kp_tucker_* (prefactor argument). */
+int kp_build_split_phi_f64(kp_ctx* ctx, const double* const* as, const int* dims, int d,
+                           double tau, int ell, int q, double* const* factors, double* prefactor);
+int kp_build_split_phi_c128(kp_ctx* ctx, const double* const* as, const int* dims, int d,
+                            double tau, int ell, int q, double* const* factors,
+                            double* prefactor);
+
+/* ---------------- steppers (inc/integrators.hpp) ---------------- */
+/* One step out = step(u).  f1/f2 as in the reference's step functions:
+ * Lawson methods f1 = exp factors; ExpEuler f1 = phi1; ExpEulerLS f1 = exp,
+ * f2 = phi1; ETD2RK f1 = phi1, f2 = phi2 (pref1/pref2 = split prefactors).
+ * Replaces lawson_euler_step, lawson2b_step, exp_euler_step,
+ * exp_euler_linear_split_step, etd2rk_step (:116-164).  out must not alias u. */
+int kp_step_f64(kp_ctx* ctx, int method, const double* u, const int* dims, int d, double t,
+                double tau, const double* const* as, const double* const* f1, double pref1,
+                const double* const* f2, double pref2, const kp_gfun* g, double* out);
+int kp_step_c128(kp_ctx* ctx, int method, const double* u, const int* dims, int d, double t,
+                 double tau, const double* const* as, const double* const* f1, double pref1,
+                 const double* const* f2, double pref2, const kp_gfun* g, double* out);
+/* integrate (:219-373, Split backend): tau = (t_final-t0)/n_steps, factors
+ * built once on the device, n_steps steps on device-resident state u (in:
+ * u0, out: final state), per-step finite check.  On divergence returns
+ * KP_EDIVERGE with *diverged_step = first non-finite step (1-based).
+ * *loop_seconds (may be NULL) = device time of the time loop. */
+int kp_integrate_f64(kp_ctx* ctx, int method, double* u, const int* dims, int d,
+                     const double* const* as, const kp_gfun* g, double t0, double t_final,
+                     long n_steps, int q, long* diverged_step, double* loop_seconds);
+int kp_integrate_c128(kp_ctx* ctx, int method, double* u, const int* dims, int d,
+                      const double* const* as, const kp_gfun* g, double t0, double t_final,
+                      long n_steps, int q, long* diverged_step, double* loop_seconds);
+/* Host-buffer drop-in: u0/as on the host, u_final written on the host. */
+int kp_host_integrate_f64(kp_ctx* ctx, int method, const double* u0, const int* dims, int d,
+                          const double* const* as, const kp_gfun* g, double t0, double t_final,
+                          long n_steps, int q, double* u_final, long* diverged_step,
+                          double* loop_seconds);
+int kp_host_integrate_c128(kp_ctx* ctx, int method, const double* u0, const int* dims, int d,
+                           const double* const* as, const kp_gfun* g, double t0, double t_final,
+                           long n_steps, int q, double* u_final, long* diverged_step,
+                           double* loop_seconds);
+
 /* Measured FP64 peak of this device: a DMMA (mma.sync m8n8k4 f64) loop over
  * all SMs; returns TFLOP/s.  Used as the roofline denominator. */
 int kp_measure_fp64_peak(kp_ctx* ctx, double* tflops);

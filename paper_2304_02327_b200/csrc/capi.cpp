@@ -55,6 +55,12 @@ namespace {
 
 thread_local std::string g_err;
 
+}  // namespace
+
+void kp_set_last_error(const std::string& m) { g_err = m; }
+
+namespace {
+
 template <typename F>
 int guard(F&& f) {
   try {

@@ -29,6 +29,8 @@ struct divergence_error : std::runtime_error {
   divergence_error(const std::string& m, long s) : std::runtime_error(m), step(s) {}
 };
 
+void kp_set_last_error(const std::string& m);
+
 #define KP_CUDA(call)                                                                    \
   do {                                                                                   \
     cudaError_t e_ = (call);                                                             \
@@ -88,6 +90,10 @@ struct Epilogue {
   double* D = nullptr;        // second output (EPI_STAGE_D)
   kp_gfun g{};
   double t = 0.0, t2 = 0.0;
+  // divergence tracking (inc/integrators.hpp:364): when set, any non-finite
+  // value written by this epilogue records atomicMin(*bad_step, *step_ctr + 1)
+  int* bad_step = nullptr;
+  const int* step_ctr = nullptr;
 };
 
 struct GemmProblem {
@@ -110,6 +116,18 @@ void mode_product_f64(kp_ctx* ctx, const double* t, const std::vector<int>& dims
 // Complex mode product (interleaved complex128, cplx.cu).  m is rows x dims[mode].
 void mode_product_c128(kp_ctx* ctx, const double* t, const std::vector<int>& dims, int mode,
                        const double* m, int rows, const Epilogue& e, double* out);
+
+// ---- matrix functions (phi.cu, gll_rule.cpp) ----
+void gll_rule_host(int q, double* nodes, double* weights);
+// expm of `batch` consecutive n x n matrices (inc/matrix_functions.hpp:76-95)
+void expm_batch(kp_ctx* ctx, const double* x, int n, int batch, double* out);
+// phiquad (inc/matrix_functions.hpp:146-199): phis = ell_max+1 consecutive
+// n x n matrices; returns the scaling exponent
+int phiquad_dev(kp_ctx* ctx, const double* x, int n, int ell_max, int q, int forced, double* phis);
+// complex128 (interleaved) versions through the real 2n x 2n representation
+void expm_batch_c128(kp_ctx* ctx, const double* x, int n, int batch, double* out);
+int phiquad_dev_c128(kp_ctx* ctx, const double* x, int n, int ell_max, int q, int forced,
+                     double* phis);
 
 // ---- elementwise (elementwise.cu) ----
 // z = fma(b, y, x): axpy is (b=alpha, y=x, x=y, z=y), add_scaled is (b=alpha, y=y, x=x)

@@ -27,6 +27,7 @@
 //     kronsum+g and the ETD2RK stage/difference, written as 16-byte stores.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "kp_g.cuh"
 #include "kp_internal.h"
@@ -128,8 +129,8 @@ struct Cfg {
 // C(2p+1,2i)) at complex offset p + i*P (ldc is then the complex row pitch
 // in doubles, 2P).
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool B_KCONTIG, int VEC,
-          int CPLX>
-__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
+          int CPLX, int MINB>
+__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
     dmma_gemm_kernel(GemmProblem p, Epilogue e, int tiles_m, int tiles_n, int n_fastest,
                      int c_vec2, long long species_half) {
   using CF = Cfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, B_KCONTIG, VEC>;
@@ -164,38 +165,59 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
   const int M = p.M, N = p.N, K = p.K;
   const int KT = (K + BK - 1) / BK;
 
+  // Per-thread copy plan, fixed for the whole tile: every thread owns the
+  // same contiguous-index offset in each of its chunks, so a stage costs one
+  // pointer bump + predicate per 16-byte copy (no divisions, no branches).
+  constexpr int A_ROW = BM / VEC;  // chunks per k row of A
+  static_assert(NT % A_ROW == 0, "A copy plan");
+  constexpr int A_KSTEP = NT / A_ROW, A_PER = BK / A_KSTEP;
+  const int a_col = (tid % A_ROW) * VEC, a_kk0 = tid / A_ROW;
+  const int a_bytes = max(0, min(VEC, M - (m0 + a_col))) * 8;
+  const double* a_src0 = Ab + m0 + a_col + (long long)a_kk0 * p.lda;
+  const int a_dst0 = a_kk0 * LDA + a_col;
+
+  constexpr int B_ROW = B_KCONTIG ? BK / VEC : BN / VEC;
+  static_assert(NT % B_ROW == 0, "B copy plan");
+  constexpr int B_STEP = NT / B_ROW;
+  constexpr int B_PER = B_KCONTIG ? BN / B_STEP : BK / B_STEP;
+  const int b_in = (tid % B_ROW) * VEC, b_out0 = tid / B_ROW;  // contiguous / strided index
+  const double* b_src0;
+  int b_dst0, b_bytes_n = 0;
+  if constexpr (B_KCONTIG) {
+    b_src0 = Bb + b_in + (long long)(n0 + b_out0) * p.sBn;
+    b_dst0 = b_out0 * LDB + b_in;
+  } else {
+    b_src0 = Bb + n0 + b_in + (long long)b_out0 * p.sBk;
+    b_dst0 = b_out0 * LDB + b_in;
+    b_bytes_n = max(0, min(VEC, N - (n0 + b_in))) * 8;
+  }
+
   auto load_stage = [&](int slot, int kt) {
     const int k0 = kt * BK;
     double* as = As + slot * CF::A_STAGE;
     double* bs = Bs + slot * CF::B_STAGE;
-    constexpr int ACH = BK * (BM / VEC);
+    const double* a_src = a_src0 + (long long)k0 * p.lda;
 #pragma unroll
-    for (int c = tid; c < ACH; c += NT) {
-      const int kk = c / (BM / VEC), col = (c % (BM / VEC)) * VEC;
-      const int gm = m0 + col, gk = k0 + kk;
-      const int valid = (gk < K) ? max(0, min(VEC, M - gm)) : 0;
-      const double* src = valid ? Ab + gm + (long long)gk * p.lda : Ab;
-      cp_async<VEC>(as + kk * LDA + col, src, valid * 8);
+    for (int i = 0; i < A_PER; ++i) {
+      const int bytes = (k0 + a_kk0 + i * A_KSTEP < K) ? a_bytes : 0;
+      cp_async<VEC>(as + a_dst0 + i * A_KSTEP * LDA,
+                    bytes ? a_src + (long long)i * A_KSTEP * p.lda : Ab, bytes);
     }
     if constexpr (B_KCONTIG) {
-      constexpr int BCH = BN * (BK / VEC);
+      const int kv = max(0, min(VEC, K - (k0 + b_in))) * 8;
 #pragma unroll
-      for (int c = tid; c < BCH; c += NT) {
-        const int nn = c / (BK / VEC), kk = (c % (BK / VEC)) * VEC;
-        const int gn = n0 + nn, gk = k0 + kk;
-        const int valid = (gn < N) ? max(0, min(VEC, K - gk)) : 0;
-        const double* src = valid ? Bb + gk + (long long)gn * p.sBn : Bb;
-        cp_async<VEC>(bs + nn * LDB + kk, src, valid * 8);
+      for (int i = 0; i < B_PER; ++i) {
+        const int bytes = (n0 + b_out0 + i * B_STEP < N) ? kv : 0;
+        cp_async<VEC>(bs + b_dst0 + i * B_STEP * LDB,
+                      bytes ? b_src0 + k0 + (long long)i * B_STEP * p.sBn : Bb, bytes);
       }
     } else {
-      constexpr int BCH = BK * (BN / VEC);
+      const double* b_src = b_src0 + (long long)k0 * p.sBk;
 #pragma unroll
-      for (int c = tid; c < BCH; c += NT) {
-        const int kk = c / (BN / VEC), col = (c % (BN / VEC)) * VEC;
-        const int gn = n0 + col, gk = k0 + kk;
-        const int valid = (gk < K) ? max(0, min(VEC, N - gn)) : 0;
-        const double* src = valid ? Bb + gn + (long long)gk * p.sBk : Bb;
-        cp_async<VEC>(bs + kk * LDB + col, src, valid * 8);
+      for (int i = 0; i < B_PER; ++i) {
+        const int bytes = (k0 + b_out0 + i * B_STEP < K) ? b_bytes_n : 0;
+        cp_async<VEC>(bs + b_dst0 + i * B_STEP * LDB,
+                      bytes ? b_src + (long long)i * B_STEP * p.sBk : Bb, bytes);
       }
     }
   };
@@ -268,6 +290,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
   // ---- epilogue ----
   double* __restrict__ Cb = p.C + q * p.sC;
   const long long cq = q * p.sC;
+  bool nonfinite = false;
   if constexpr (CPLX == 2) {
     // pairs of n tiles (2pj, 2pj+1) hold the re/im columns of one factor row
 #pragma unroll
@@ -288,9 +311,11 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
           double2 dv = make_double2(0.0, 0.0);
           const double2 rr = epi_pair_c(e, v, p.C, cq + off, &dv);
           *reinterpret_cast<double2*>(Cb + off) = rr;
+          nonfinite |= !isfinite(rr.x) || !isfinite(rr.y);
           if (e.kind == EPI_STAGE_D) *reinterpret_cast<double2*>(e.D + cq + off) = dv;
         }
     }
+    if (e.bad_step && nonfinite) atomicMin(e.bad_step, *e.step_ctr + 1);
     return;
   }
 #pragma unroll
@@ -316,13 +341,16 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
           double2 dv = make_double2(0.0, 0.0);
           const double2 rr = epi_pair_c(e, make_double2(v0, v1), p.C, cq + off, &dv);
           *reinterpret_cast<double2*>(Cb + off) = rr;
+          nonfinite |= !isfinite(rr.x) || !isfinite(rr.y);
           if (e.kind == EPI_STAGE_D) *reinterpret_cast<double2*>(e.D + cq + off) = dv;
           continue;
         }
         double d0 = 0.0, d1 = 0.0;
         const double r0 = epi_one(e, v0, p.C, cq + off, species_half, &d0);
+        nonfinite |= !isfinite(r0);
         if (two) {
           const double r1 = epi_one(e, v1, p.C, cq + off + 1, species_half, &d1);
+          nonfinite |= !isfinite(r1);
           if (c_vec2) {
             *reinterpret_cast<double2*>(Cb + off) = make_double2(r0, r1);
             if (e.kind == EPI_STAGE_D)
@@ -341,13 +369,20 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
         }
       }
   }
+  if (e.bad_step && nonfinite) atomicMin(e.bad_step, *e.step_ctr + 1);
 }
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, bool B_KCONTIG, int VEC, int CPLX>
 void launch_cfg(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, long long half) {
-  constexpr int BK = 16, STAGES = 4;
+  // 128x128 with 8 warps of 64x32: one CTA per SM, BK=32 x 3 stages.
+  // Every other tile uses 32x32 warp tiles (<= 128 registers) so that two or
+  // more CTAs share an SM and hide each other's barrier/load phases: the
+  // measured winner (tools/tucker_sweep.py, profiles/gemm_tiles_r01.txt).
+  constexpr bool BIG = (BM == 128 && BN == 128 && WARPS_M * WARPS_N == 8);
+  constexpr int BK = BIG ? 32 : 16, STAGES = BIG ? 3 : 4;
+  constexpr int MINB = BIG ? 1 : (WARPS_M * WARPS_N * 32 >= 512 ? 1 : 2);
   using CF = Cfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, B_KCONTIG, VEC>;
-  auto kern = dmma_gemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, B_KCONTIG, VEC, CPLX>;
+  auto kern = dmma_gemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, B_KCONTIG, VEC, CPLX, MINB>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     KP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -413,14 +448,22 @@ void launch_gemm(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int cplx)
   const long long tiles128 =
       (long long)((p.M + 127) / 128) * ((p.N + 127) / 128) * p.batch;
   const bool few = tiles128 < ctx->num_sms;
-  if ((bm_small && bn_small) || (few && (bm_small || bn_small)) || tiles128 * 4 < ctx->num_sms)
-    launch_layout<64, 64, 2, 2>(ctx, p, e, kcontig, vec2, cplx, half);
-  else if (bm_small || (few && p.M <= p.N))
-    launch_layout<64, 128, 2, 4>(ctx, p, e, kcontig, vec2, cplx, half);
-  else if (bn_small || few)
-    launch_layout<128, 64, 4, 2>(ctx, p, e, kcontig, vec2, cplx, half);
-  else
-    launch_layout<128, 128, 2, 4>(ctx, p, e, kcontig, vec2, cplx, half);
+  // 0: 128x128 (8 warps 64x32), 1: 128x64, 2: 64x128, 3: 64x64, 4: 128x128 (16 warps 32x32)
+  (void)few;
+  int tile = 3;
+  if (kcontig && !bm_small && tiles128 * 2 >= ctx->num_sms) tile = 1;
+  static const int forced = [] {  // benchmarking override
+    const char* v = getenv("KP_GEMM_TILE");
+    return v ? atoi(v) : -1;
+  }();
+  if (forced >= 0 && forced <= 4) tile = forced;
+  switch (tile) {
+    case 0: launch_layout<128, 128, 2, 4>(ctx, p, e, kcontig, vec2, cplx, half); break;
+    case 1: launch_layout<128, 64, 4, 2>(ctx, p, e, kcontig, vec2, cplx, half); break;
+    case 2: launch_layout<64, 128, 2, 4>(ctx, p, e, kcontig, vec2, cplx, half); break;
+    case 4: launch_layout<128, 128, 4, 4>(ctx, p, e, kcontig, vec2, cplx, half); break;
+    default: launch_layout<64, 64, 2, 2>(ctx, p, e, kcontig, vec2, cplx, half); break;
+  }
 }
 
 // out = epi(t x_mode m): the two permute-free GEMM views of

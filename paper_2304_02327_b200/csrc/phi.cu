@@ -1,0 +1,809 @@
+// phi.cu -- the small-matrix phi_l(tau A_mu) factors on the device, batched.
+//
+// Restates the reference's matrix-function layer with the same algorithms and
+// thresholds, every O(n^3) step on the DMMA GEMM (launch_gemm):
+//   expm          inc/matrix_functions.hpp:76-95  (Pade 3/5/7/9/13, theta table :20-22)
+//   pade_low/13   inc/matrix_functions.hpp:37-72  (elementwise sums in the same
+//                 order, each product/sum separately rounded like the
+//                 reference's temporaries)
+//   lu_factor     inc/linsolve.hpp:125-146 (64-wide panels, partial pivoting
+//                 over the full column, trailing update = GEMM)
+//   lu_solve      inc/linsolve.hpp:149-176
+//   phiquad       inc/matrix_functions.hpp:146-199 (GLL nodes on the host,
+//                 src/gll_rule.cpp:35-72; q-1 expms batched in one pass)
+//   phi_square_step inc/matrix_functions.hpp:121-138 (all orders from
+//                 same-scale values; phi0*phi_j as one batched GEMM)
+// Matrices of one call are processed as a batch (stride n*n) so the 11 GLL
+// nodes (and several factors) share every launch.  The data-dependent
+// branches of the reference (scaling exponent, Pade degree, singularity) read
+// small device results back to the host: a handful of 8-byte syncs per build.
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "kp_internal.h"
+
+namespace kp {
+namespace {
+
+constexpr int LU_NB = 64;  // inc/linsolve.hpp:22
+
+const double kPadeTheta[5] = {1.495585217958292e-2, 2.539398330063230e-1,
+                              9.504178996162932e-1, 2.097847961257068e0, 5.371920351148152e0};
+const std::vector<std::vector<double>>& pade_coeffs() {  // inc/matrix_functions.hpp:24-35
+  static const std::vector<std::vector<double>> b = {
+      {120., 60., 12., 1.},
+      {30240., 15120., 3360., 420., 30., 1.},
+      {17297280., 8648640., 1995840., 277200., 25200., 1512., 56., 1.},
+      {17643225600., 8821612800., 2075673600., 302702400., 30270240., 2162160., 110880.,
+       3960., 90., 1.},
+      {64764752532480000., 32382376266240000., 7771770303897600., 1187353796428800.,
+       129060195264000., 10559470521600., 670442572800., 33522128640., 1323241920.,
+       40840800., 960960., 16380., 182., 1.}};
+  return b;
+}
+
+double factorial(int k) {
+  double f = 1.0;
+  for (int i = 2; i <= k; ++i) f *= i;
+  return f;
+}
+
+unsigned grid1(kp_ctx* ctx, long long n, int threads = 256) {
+  return unsigned(std::max<long long>(1, std::min<long long>((n + threads - 1) / threads,
+                                                              ctx->num_sms * 16LL)));
+}
+
+// ---------------------------------------------------------------- kernels
+
+// out[b] = max_j sum_i |x_b(i,j)|, sums in increasing i (inc/matrix.hpp norm1)
+__global__ void norm1_kernel(const double* __restrict__ x, int n, long long stride,
+                             double* __restrict__ out) {
+  const double* xb = x + blockIdx.x * stride;
+  double best = 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double s = 0.0;
+    const double* col = xb + (long long)j * n;
+    for (int i = 0; i < n; ++i) s = __dadd_rn(s, fabs(col[i]));
+    best = fmax(best, s);
+  }
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    best = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (threadIdx.x == 0) out[blockIdx.x] = best;
+  }
+}
+
+// y_b = x * scale_b  (per-batch scalar; x shared when xstride == 0)
+__global__ void scale_batch_kernel(const double* __restrict__ x, long long xstride,
+                                   const double* __restrict__ scale, long long nn, int batch,
+                                   double* __restrict__ y) {
+  const long long total = nn * batch;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long b = t / nn, e = t - b * nn;
+    y[t] = __dmul_rn(x[b * xstride + e], scale[b]);
+  }
+}
+
+// Pade numerator/denominator sums of pade_low (inc/matrix_functions.hpp:45-50):
+// u = b1 I, v = b0 I, then for p: u += b[2p+3] pow_p, v += b[2p+2] pow_p.
+__global__ void pade_uv_kernel(const double* __restrict__ pw, int npow, long long nn, int n,
+                               int batch, double b0, double b1, const double* __restrict__ bu,
+                               const double* __restrict__ bv, double* __restrict__ u,
+                               double* __restrict__ v) {
+  const long long total = nn * batch;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long b = t / nn, e = t - b * nn;
+    const bool diag = (e % (n + 1)) == 0;
+    double uu = diag ? b1 : 0.0, vv = diag ? b0 : 0.0;
+    for (int p = 0; p < npow; ++p) {
+      const double x = pw[(long long)p * nn * batch + t];
+      uu = __dadd_rn(uu, __dmul_rn(bu[p], x));
+      vv = __dadd_rn(vv, __dmul_rn(bv[p], x));
+    }
+    u[t] = uu;
+    v[t] = vv;
+    (void)b;
+  }
+}
+
+// pade13 sums (inc/matrix_functions.hpp:63-69):
+//   w1 = c0*a6 + c1*a4 + c2*a2                    (then multiplied by a6)
+//   w2 = d0*a6 + d1*a4 + d2*a2 + d3*I             (added after the product)
+__global__ void pade13_w_kernel(const double* __restrict__ a2, const double* __restrict__ a4,
+                                const double* __restrict__ a6, long long total, int n,
+                                long long nn, double c0, double c1, double c2,
+                                double* __restrict__ w) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    w[t] = __dadd_rn(__dadd_rn(__dmul_rn(c0, a6[t]), __dmul_rn(c1, a4[t])),
+                     __dmul_rn(c2, a2[t]));
+  }
+  (void)n;
+  (void)nn;
+}
+__global__ void pade13_add_kernel(const double* __restrict__ a2, const double* __restrict__ a4,
+                                  const double* __restrict__ a6, long long total, int n,
+                                  long long nn, double d0, double d1, double d2, double d3,
+                                  double* __restrict__ w) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long e = t % nn;
+    const double eye = (e % (n + 1)) == 0 ? 1.0 : 0.0;
+    const double rhs = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(d0, a6[t]), __dmul_rn(d1, a4[t])),
+                                           __dmul_rn(d2, a2[t])),
+                                 __dmul_rn(d3, eye));
+    w[t] = __dadd_rn(w[t], rhs);
+  }
+}
+
+// lhs = v - u, rhs = v + u
+__global__ void pm_kernel(const double* __restrict__ u, double* __restrict__ v, long long total,
+                          double* __restrict__ lhs) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const double uu = u[t], vv = v[t];
+    lhs[t] = __dsub_rn(vv, uu);
+    v[t] = __dadd_rn(vv, uu);
+  }
+}
+
+// ---- LU (inc/linsolve.hpp) ----
+
+// Panel factorization of a_b(j0:n, j0:j0+nb) (lu_panel, :56-81): one CTA per
+// matrix.  Pivot = first row of maximal |a| (strict >, increasing i).
+__global__ void lu_panel_kernel(double* __restrict__ a, int n, long long stride, int j0, int nb,
+                                int* __restrict__ piv, int* __restrict__ singular) {
+  double* ab = a + blockIdx.x * stride;
+  int* pb = piv + (long long)blockIdx.x * n;
+  __shared__ double sval[32];
+  __shared__ int sidx[32];
+  __shared__ int s_p;
+  __shared__ double s_inv;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int j = j0; j < j0 + nb; ++j) {
+    double* colj = ab + (long long)j * n;
+    // argmax |a(i, j)|, i >= j; ties -> smallest i
+    double best = -1.0;
+    int bi = n;
+    for (int i = j + tid; i < n; i += nt) {
+      const double v = fabs(colj[i]);
+      if (v > best) {
+        best = v;
+        bi = i;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    if ((tid & 31) == 0) {
+      sval[tid >> 5] = best;
+      sidx[tid >> 5] = bi;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      best = tid < (nt >> 5) ? sval[tid] : -1.0;
+      bi = tid < (nt >> 5) ? sidx[tid] : n;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) {
+          best = ov;
+          bi = oi;
+        }
+      }
+      if (tid == 0) {
+        if (!(best > 0.0)) {
+          *singular = 1;
+          bi = j;
+        }
+        s_p = bi;
+        pb[j] = bi;
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    if (p != j) {
+      for (int c = j0 + tid; c < j0 + nb; c += nt) {
+        const double t = ab[j + (long long)c * n];
+        ab[j + (long long)c * n] = ab[p + (long long)c * n];
+        ab[p + (long long)c * n] = t;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) s_inv = 1.0 / colj[j];
+    __syncthreads();
+    const double inv = s_inv;
+    for (int i = j + 1 + tid; i < n; i += nt) colj[i] = __dmul_rn(colj[i], inv);
+    __syncthreads();
+    for (int c = j + 1; c < j0 + nb; ++c) {
+      double* colc = ab + (long long)c * n;
+      const double ajc = colc[j];
+      if (ajc == 0.0) continue;
+      for (int i = j + 1 + tid; i < n; i += nt) colc[i] = __fma_rn(-colj[i], ajc, colc[i]);
+    }
+    __syncthreads();
+  }
+}
+
+// Row swaps j0..j0+nb-1 applied to columns [c0, c1) (lu_apply_swaps, :85-92)
+// of a matrix with leading dimension ld (ld rows); one thread per column.
+__global__ void swaps_kernel(double* __restrict__ a, int ld, long long stride,
+                             const int* __restrict__ piv, int n, int j0, int nb, int c0, int c1) {
+  const int c = c0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= c1) return;
+  double* col = a + blockIdx.y * stride + (long long)c * ld;
+  const int* pb = piv + (long long)blockIdx.y * n;
+  for (int j = j0; j < j0 + nb; ++j) {
+    const int p = pb[j];
+    if (p != j) {
+      const double t = col[j];
+      col[j] = col[p];
+      col[p] = t;
+    }
+  }
+}
+
+// b(j0..j0+nb) <- L11^{-1} b per column (trsm_lower_unit, :96-107); L11 staged in smem
+__global__ void trsm_lower_unit_kernel(const double* __restrict__ lu, int n, long long lstride,
+                                       int j0, int nb, double* __restrict__ b, int ldb,
+                                       long long bstride, int nrhs) {
+  __shared__ double L[LU_NB * LU_NB];
+  const double* lb = lu + blockIdx.y * lstride;
+  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
+    const int i = t % nb, r = t / nb;
+    L[i + r * LU_NB] = lb[(j0 + i) + (long long)(j0 + r) * n];
+  }
+  __syncthreads();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nrhs) return;
+  double* col = b + blockIdx.y * bstride + (long long)c * ldb + j0;
+  double x[LU_NB];
+#pragma unroll
+  for (int i = 0; i < LU_NB; ++i)
+    if (i < nb) x[i] = col[i];
+#pragma unroll
+  for (int i = 1; i < LU_NB; ++i) {
+    if (i >= nb) break;
+    double s = x[i];
+#pragma unroll
+    for (int r = 0; r < LU_NB; ++r)
+      if (r < i) s = __fma_rn(-L[i + r * LU_NB], x[r], s);
+    x[i] = s;
+  }
+#pragma unroll
+  for (int i = 0; i < LU_NB; ++i)
+    if (i < nb) col[i] = x[i];
+}
+
+// trsm_upper (:109-120): back substitution with U11 and division by the diagonal
+__global__ void trsm_upper_kernel(const double* __restrict__ lu, int n, long long lstride, int j0,
+                                  int nb, double* __restrict__ b, int ldb, long long bstride,
+                                  int nrhs) {
+  __shared__ double U[LU_NB * LU_NB];
+  const double* lb = lu + blockIdx.y * lstride;
+  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
+    const int i = t % nb, r = t / nb;
+    U[i + r * LU_NB] = lb[(j0 + i) + (long long)(j0 + r) * n];
+  }
+  __syncthreads();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nrhs) return;
+  double* col = b + blockIdx.y * bstride + (long long)c * ldb + j0;
+  double x[LU_NB];
+#pragma unroll
+  for (int i = 0; i < LU_NB; ++i)
+    if (i < nb) x[i] = col[i];
+#pragma unroll
+  for (int i = LU_NB - 1; i >= 0; --i) {
+    if (i >= nb) continue;
+    double s = x[i];
+#pragma unroll
+    for (int r = 0; r < LU_NB; ++r)
+      if (r > i && r < nb) s = __fma_rn(-U[i + r * LU_NB], x[r], s);
+    x[i] = s / U[i + i * LU_NB];
+  }
+#pragma unroll
+  for (int i = 0; i < LU_NB; ++i)
+    if (i < nb) col[i] = x[i];
+}
+
+// phi_j = sum_i coeff[i] exps[i] + endpoint * I (phiquad, :179-194): each
+// term separately rounded then added, in increasing i.
+__global__ void quad_combine_kernel(const double* __restrict__ exps, int nexp, long long nn,
+                                    int n, int batch, const double* __restrict__ coeff,
+                                    double endpoint, double* __restrict__ out,
+                                    long long out_stride) {
+  const long long total = nn * batch;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long b = t / nn, e = t - b * nn;
+    double m = 0.0;  // skipped terms (theta = 0, j > 1) carry c = 0: m + 0*x == m
+    for (int i = 0; i < nexp; ++i)
+      m = __dadd_rn(m, __dmul_rn(coeff[i], exps[((long long)i * batch + b) * nn + e]));
+    if ((e % (n + 1)) == 0) m = __dadd_rn(m, endpoint);
+    out[b * out_stride + e] = m;
+  }
+}
+
+// One phi_square_step combine for order l (:130-136):
+// m = P0*P_l (given); for k=1..l: m += (1/(l-k)!) P_k; m *= 2^-l
+__global__ void square_combine_kernel(const double* __restrict__ prod, const double* __restrict__ phis,
+                                      long long nn, int batch, int ell_max, int ell,
+                                      double* __restrict__ out) {
+  const long long total = nn * batch;
+  const double sc = ldexp(1.0, -ell);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long b = t / nn, e = t - b * nn;
+    const long long base = b * (long long)(ell_max + 1) * nn + e;
+    double m = prod[base + (long long)ell * nn];
+    if (ell > 0) {
+      for (int k = 1; k <= ell; ++k) {
+        double f = 1.0;
+        for (int i = 2; i <= ell - k; ++i) f *= i;
+        m = __dadd_rn(m, __dmul_rn(1.0 / f, phis[base + (long long)k * nn]));
+      }
+      m = __dmul_rn(m, sc);
+    }
+    out[base + (long long)ell * nn] = m;
+  }
+}
+
+__global__ void all_finite_batch_kernel(const double* __restrict__ x, long long total,
+                                        int* __restrict__ flag) {
+  bool ok = true;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x)
+    ok &= isfinite(x[t]);
+  if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) *flag = 0;
+}
+
+// ------------------------------------------------------------- host side
+
+// Batched square matmul C_b = A_b B_b (A/B shared when the stride is 0).
+void matmul_batch(kp_ctx* ctx, int n, int batch, const double* A, long long sA, const double* B,
+                  long long sB, double* C, long long sC, double alpha = 1.0, double beta = 0.0) {
+  GemmProblem p;
+  p.M = n;
+  p.N = n;
+  p.K = n;
+  p.batch = batch;
+  p.A = A;
+  p.lda = n;
+  p.sA = sA;
+  p.B = B;
+  p.sBk = 1;
+  p.sBn = n;
+  p.sB = sB;
+  p.C = C;
+  p.ldc = n;
+  p.sC = sC;
+  Epilogue e;
+  e.alpha = alpha;
+  e.beta = beta;
+  launch_gemm(ctx, p, e);
+}
+
+template <typename T>
+T* slot(kp_ctx* ctx, int s, size_t count) {
+  return static_cast<T*>(ctx->ws.get(s, count * sizeof(T)));
+}
+
+// Workspace slots used by this file (others: 0..1 Tucker ping-pong,
+// 2..7 steppers, 8..12 host staging / complex factor).
+enum : int {
+  S_NORMS = 20, S_PIV, S_LHS, S_POW, S_U, S_V, S_AU, S_ARG, S_EXPS, S_TAB, S_PROD, S_COEF,
+  S_T1, S_T2, S_A2, S_A4, S_A6, S_SING
+};
+
+std::vector<double> norms1(kp_ctx* ctx, const double* x, int n, int batch) {
+  double* d = slot<double>(ctx, S_NORMS, std::max(batch, 1));
+  norm1_kernel<<<batch, 256, 0, ctx->stream>>>(x, n, (long long)n * n, d);
+  ctx->launches++;
+  KP_CUDA(cudaGetLastError());
+  std::vector<double> h(batch);
+  KP_CUDA(cudaMemcpyAsync(h.data(), d, batch * sizeof(double), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  KP_CUDA(cudaStreamSynchronize(ctx->stream));
+  return h;
+}
+
+void check_finite(kp_ctx* ctx, const double* x, long long total, const char* who) {
+  int* flag = slot<int>(ctx, S_SING, 4);
+  const int one = 1;
+  KP_CUDA(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  all_finite_batch_kernel<<<grid1(ctx, total), 256, 0, ctx->stream>>>(x, total, flag);
+  ctx->launches++;
+  int h = 1;
+  KP_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  KP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (!h) throw invalid_argument(std::string(who) + ": non-finite entries");
+}
+
+// lu_factor + lu_solve(lhs, rhs) for a batch; rhs overwritten with the solution.
+void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs) {
+  const long long nn = (long long)n * n;
+  int* piv = slot<int>(ctx, S_PIV, size_t(n) * batch);
+  int* sing = slot<int>(ctx, S_SING, 4);
+  KP_CUDA(cudaMemsetAsync(sing, 0, sizeof(int), ctx->stream));
+  const int nt = 256;
+  for (int j0 = 0; j0 < n; j0 += LU_NB) {  // lu_factor (:125-146)
+    const int nb = std::min(LU_NB, n - j0);
+    lu_panel_kernel<<<batch, 512, 0, ctx->stream>>>(lhs, n, nn, j0, nb, piv, sing);
+    ctx->launches++;
+    if (j0 > 0) {
+      swaps_kernel<<<dim3((j0 + nt - 1) / nt, batch), nt, 0, ctx->stream>>>(lhs, n, nn, piv, n, j0,
+                                                                          nb, 0, j0);
+      ctx->launches++;
+    }
+    const int rest = n - j0 - nb;
+    if (rest > 0) {
+      swaps_kernel<<<dim3((rest + nt - 1) / nt, batch), nt, 0, ctx->stream>>>(
+          lhs, n, nn, piv, n, j0, nb, j0 + nb, n);
+      trsm_lower_unit_kernel<<<dim3((rest + 127) / 128, batch), 128, 0, ctx->stream>>>(
+          lhs, n, nn, j0, nb, lhs + (long long)(j0 + nb) * n, n, nn, rest);
+      ctx->launches += 2;
+      GemmProblem p;  // A22 -= L21 * U12
+      p.M = rest;
+      p.N = rest;
+      p.K = nb;
+      p.batch = batch;
+      p.A = lhs + (j0 + nb) + (long long)j0 * n;
+      p.lda = n;
+      p.sA = nn;
+      p.B = lhs + j0 + (long long)(j0 + nb) * n;
+      p.sBk = 1;
+      p.sBn = n;
+      p.sB = nn;
+      p.C = lhs + (j0 + nb) + (long long)(j0 + nb) * n;
+      p.ldc = n;
+      p.sC = nn;
+      Epilogue e;
+      e.alpha = -1.0;
+      e.beta = 1.0;
+      launch_gemm(ctx, p, e);
+    }
+    KP_CUDA(cudaGetLastError());
+  }
+  int hs = 0;
+  KP_CUDA(cudaMemcpyAsync(&hs, sing, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  KP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (hs) throw runtime_error("lu_factor: matrix is singular");
+  // lu_solve (:149-176)
+  swaps_kernel<<<dim3((n + nt - 1) / nt, batch), nt, 0, ctx->stream>>>(rhs, n, nn, piv, n, 0, n,
+                                                                       0, n);
+  ctx->launches++;
+  for (int j0 = 0; j0 < n; j0 += LU_NB) {
+    const int nb = std::min(LU_NB, n - j0);
+    trsm_lower_unit_kernel<<<dim3((n + 127) / 128, batch), 128, 0, ctx->stream>>>(
+        lhs, n, nn, j0, nb, rhs, n, nn, n);
+    ctx->launches++;
+    const int rest = n - j0 - nb;
+    if (rest > 0) {
+      GemmProblem p;
+      p.M = rest;
+      p.N = n;
+      p.K = nb;
+      p.batch = batch;
+      p.A = lhs + (j0 + nb) + (long long)j0 * n;
+      p.lda = n;
+      p.sA = nn;
+      p.B = rhs + j0;
+      p.sBk = 1;
+      p.sBn = n;
+      p.sB = nn;
+      p.C = rhs + j0 + nb;
+      p.ldc = n;
+      p.sC = nn;
+      Epilogue e;
+      e.alpha = -1.0;
+      e.beta = 1.0;
+      launch_gemm(ctx, p, e);
+    }
+  }
+  for (int j0 = ((n - 1) / LU_NB) * LU_NB; j0 >= 0; j0 -= LU_NB) {
+    const int nb = std::min(LU_NB, n - j0);
+    trsm_upper_kernel<<<dim3((n + 127) / 128, batch), 128, 0, ctx->stream>>>(lhs, n, nn, j0, nb,
+                                                                             rhs, n, nn, n);
+    ctx->launches++;
+    if (j0 > 0) {
+      GemmProblem p;
+      p.M = j0;
+      p.N = n;
+      p.K = nb;
+      p.batch = batch;
+      p.A = lhs + (long long)j0 * n;
+      p.lda = n;
+      p.sA = nn;
+      p.B = rhs + j0;
+      p.sBk = 1;
+      p.sBn = n;
+      p.sB = nn;
+      p.C = rhs;
+      p.ldc = n;
+      p.sC = nn;
+      Epilogue e;
+      e.alpha = -1.0;
+      e.beta = 1.0;
+      launch_gemm(ctx, p, e);
+    }
+  }
+  KP_CUDA(cudaGetLastError());
+}
+
+// pade_low for a batch of matrices sharing one degree (inc/matrix_functions.hpp:37-54)
+void pade_low_batch(kp_ctx* ctx, const double* a, int n, int batch, int idx, double* out) {
+  const auto& b = pade_coeffs()[idx];
+  const int npow = (int(b.size()) - 2) / 2;
+  const long long nn = (long long)n * n, tot = nn * batch;
+  double* pw = slot<double>(ctx, S_POW, size_t(tot) * npow);
+  matmul_batch(ctx, n, batch, a, nn, a, nn, pw, nn);  // A^2
+  for (int p = 1; p < npow; ++p)
+    matmul_batch(ctx, n, batch, pw + (p - 1) * tot, nn, pw, nn, pw + p * tot, nn);
+  double* u = slot<double>(ctx, S_U, tot);
+  double* v = slot<double>(ctx, S_V, tot);
+  double* cf = slot<double>(ctx, S_COEF, 256);
+  std::vector<double> hc(16, 0.0);
+  for (int p = 0; p < npow; ++p) {
+    hc[p] = b[2 * p + 3];
+    hc[8 + p] = b[2 * p + 2];
+  }
+  KP_CUDA(cudaMemcpyAsync(cf, hc.data(), 16 * sizeof(double), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  pade_uv_kernel<<<grid1(ctx, tot), 256, 0, ctx->stream>>>(pw, npow, nn, n, batch, b[0], b[1], cf,
+                                                           cf + 8, u, v);
+  ctx->launches++;
+  double* au = slot<double>(ctx, S_AU, tot);
+  matmul_batch(ctx, n, batch, a, nn, u, nn, au, nn);  // u = a*u
+  double* lhs = slot<double>(ctx, S_LHS, tot);
+  pm_kernel<<<grid1(ctx, tot), 256, 0, ctx->stream>>>(au, v, tot, lhs);  // v-u | v+u
+  ctx->launches++;
+  lu_solve_batch(ctx, n, batch, lhs, v);
+  KP_CUDA(cudaMemcpyAsync(out, v, tot * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+}
+
+// pade13 (inc/matrix_functions.hpp:57-72) for a batch
+void pade13_batch(kp_ctx* ctx, const double* a, int n, int batch, double* out) {
+  const auto& b = pade_coeffs()[4];
+  const long long nn = (long long)n * n, tot = nn * batch;
+  double* a2 = slot<double>(ctx, S_A2, tot);
+  double* a4 = slot<double>(ctx, S_A4, tot);
+  double* a6 = slot<double>(ctx, S_A6, tot);
+  matmul_batch(ctx, n, batch, a, nn, a, nn, a2, nn);
+  matmul_batch(ctx, n, batch, a2, nn, a2, nn, a4, nn);
+  matmul_batch(ctx, n, batch, a4, nn, a2, nn, a6, nn);
+  double* w = slot<double>(ctx, S_T1, tot);
+  double* t = slot<double>(ctx, S_T2, tot);
+  const unsigned g = grid1(ctx, tot);
+  pade13_w_kernel<<<g, 256, 0, ctx->stream>>>(a2, a4, a6, tot, n, nn, b[13], b[11], b[9], w);
+  matmul_batch(ctx, n, batch, a6, nn, w, nn, t, nn);
+  pade13_add_kernel<<<g, 256, 0, ctx->stream>>>(a2, a4, a6, tot, n, nn, b[7], b[5], b[3], b[1], t);
+  double* u = slot<double>(ctx, S_U, tot);
+  matmul_batch(ctx, n, batch, a, nn, t, nn, u, nn);
+  pade13_w_kernel<<<g, 256, 0, ctx->stream>>>(a2, a4, a6, tot, n, nn, b[12], b[10], b[8], w);
+  double* z = slot<double>(ctx, S_V, tot);
+  matmul_batch(ctx, n, batch, a6, nn, w, nn, z, nn);
+  pade13_add_kernel<<<g, 256, 0, ctx->stream>>>(a2, a4, a6, tot, n, nn, b[6], b[4], b[2], b[0], z);
+  double* lhs = slot<double>(ctx, S_LHS, tot);
+  pm_kernel<<<g, 256, 0, ctx->stream>>>(u, z, tot, lhs);
+  ctx->launches += 5;
+  KP_CUDA(cudaGetLastError());
+  lu_solve_batch(ctx, n, batch, lhs, z);
+  KP_CUDA(cudaMemcpyAsync(out, z, tot * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+}
+
+}  // namespace
+
+// expm of a batch of matrices x_b (inc/matrix_functions.hpp:76-95).  Degree
+// per matrix from its own 1-norm; matrices sharing a branch run together.
+void expm_batch(kp_ctx* ctx, const double* x, int n, int batch, double* out) {
+  const long long nn = (long long)n * n;
+  const std::vector<double> nrm = norms1(ctx, x, n, batch);
+  std::vector<int> branch(batch), sc(batch, 0);
+  for (int b = 0; b < batch; ++b) {
+    int br = 4;
+    for (int idx = 0; idx < 4; ++idx)
+      if (nrm[b] <= kPadeTheta[idx]) {
+        br = idx;
+        break;
+      }
+    branch[b] = br;
+    if (br == 4) {
+      double v = nrm[b];
+      while (v > kPadeTheta[4]) {
+        v *= 0.5;
+        ++sc[b];
+      }
+    }
+  }
+  // group by (branch, scaling) and run each group as one batch
+  std::vector<bool> done(batch, false);
+  for (int b0 = 0; b0 < batch; ++b0) {
+    if (done[b0]) continue;
+    std::vector<int> grp;
+    for (int b = b0; b < batch; ++b)
+      if (!done[b] && branch[b] == branch[b0] && sc[b] == sc[b0]) {
+        grp.push_back(b);
+        done[b] = true;
+      }
+    const int g = int(grp.size());
+    double* gin = slot<double>(ctx, S_ARG, size_t(nn) * g);
+    double* gout = slot<double>(ctx, S_TAB, size_t(nn) * g);
+    for (int i = 0; i < g; ++i)
+      KP_CUDA(cudaMemcpyAsync(gin + i * nn, x + grp[i] * nn, nn * sizeof(double),
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    if (branch[b0] < 4) {
+      pade_low_batch(ctx, gin, n, g, branch[b0], gout);
+    } else {
+      const int s = sc[b0];
+      double* scale = slot<double>(ctx, S_COEF, 256);
+      std::vector<double> hs(g, std::ldexp(1.0, -s));
+      KP_CUDA(cudaMemcpyAsync(scale, hs.data(), g * sizeof(double), cudaMemcpyHostToDevice,
+                              ctx->stream));
+      scale_batch_kernel<<<grid1(ctx, nn * g), 256, 0, ctx->stream>>>(gin, nn, scale, nn, g, gin);
+      ctx->launches++;
+      pade13_batch(ctx, gin, n, g, gout);
+      double* tmp = slot<double>(ctx, S_T1, size_t(nn) * g);
+      for (int i = 0; i < s; ++i) {  // f = f*f
+        matmul_batch(ctx, n, g, gout, nn, gout, nn, tmp, nn);
+        KP_CUDA(cudaMemcpyAsync(gout, tmp, nn * g * sizeof(double), cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+      }
+    }
+    for (int i = 0; i < g; ++i)
+      KP_CUDA(cudaMemcpyAsync(out + grp[i] * nn, gout + i * nn, nn * sizeof(double),
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+}
+
+// phiquad (inc/matrix_functions.hpp:146-199) for one matrix x (device):
+// writes phis[0..ell_max] (each n x n, consecutive) and returns s.
+int phiquad_dev(kp_ctx* ctx, const double* x, int n, int ell_max, int q, int forced,
+                double* phis) {
+  if (ell_max < 0) throw invalid_argument("phiquad: negative ell_max");
+  const long long nn = (long long)n * n;
+  check_finite(ctx, x, nn, "phiquad");
+  const double d = norms1(ctx, x, n, 1)[0];
+  int s = 0;
+  for (double v = d; v >= 1.0; v *= 0.5) ++s;
+  if (forced >= 0) {
+    if (forced < s) throw invalid_argument("phiquad: forced scaling below minimum");
+    s = forced;
+  }
+  std::vector<double> nodes(q), weights(q);
+  gll_rule_host(q, nodes.data(), weights.data());
+  // args_i = (x * 2^-s) * (1 - theta_i), i < q-1 (two roundings, as :162-174)
+  double* y = slot<double>(ctx, S_T2, nn);
+  double* sc = slot<double>(ctx, S_COEF, 256);
+  std::vector<double> hs(q + 1);
+  hs[0] = std::ldexp(1.0, -s);
+  for (int i = 0; i < q - 1; ++i) hs[1 + i] = 1.0 - nodes[i];
+  KP_CUDA(cudaMemcpyAsync(sc, hs.data(), (q + 1) * sizeof(double), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  scale_batch_kernel<<<grid1(ctx, nn), 256, 0, ctx->stream>>>(x, 0, sc, nn, 1, y);
+  double* args = slot<double>(ctx, S_EXPS, size_t(nn) * (q - 1) * 2);
+  double* exps = args + nn * (q - 1);
+  scale_batch_kernel<<<grid1(ctx, nn * (q - 1)), 256, 0, ctx->stream>>>(y, 0, sc + 1, nn, q - 1,
+                                                                       args);
+  ctx->launches += 2;
+  expm_batch(ctx, args, n, q - 1, exps);
+  // phi_0 = exps[0]; phi_j = sum_i w_i theta_i^{j-1}/(j-1)! exps[i] + w_{q-1}/(j-1)! I
+  KP_CUDA(cudaMemcpyAsync(phis, exps, nn * sizeof(double), cudaMemcpyDeviceToDevice,
+                          ctx->stream));
+  for (int j = 1; j <= ell_max; ++j) {
+    const double jm1 = factorial(j - 1);
+    std::vector<double> c(q, 0.0);
+    for (int i = 0; i < q - 1; ++i) {
+      const double th = nodes[i];
+      if (j > 1 && th == 0.0) {
+        c[i] = 0.0;  // skipped term: adding +0.0 leaves m unchanged
+        continue;
+      }
+      c[i] = weights[i] * std::pow(th, double(j - 1)) / jm1;
+    }
+    double* cd = slot<double>(ctx, S_COEF, 256);
+    KP_CUDA(cudaMemcpyAsync(cd, c.data(), q * sizeof(double), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    quad_combine_kernel<<<grid1(ctx, nn), 256, 0, ctx->stream>>>(
+        exps, q - 1, nn, n, 1, cd, weights[q - 1] / jm1, phis + j * nn, nn);
+    ctx->launches++;
+    KP_CUDA(cudaStreamSynchronize(ctx->stream));  // cd is reused by the next order
+  }
+  // s doubling steps (phi_square_step)
+  double* prod = slot<double>(ctx, S_PROD, size_t(nn) * (ell_max + 1));
+  double* nxt = slot<double>(ctx, S_TAB, size_t(nn) * (ell_max + 1));
+  for (int step = 0; step < s; ++step) {
+    matmul_batch(ctx, n, ell_max + 1, phis, 0, phis, nn, prod, nn);  // P0 * P_l
+    for (int l = 0; l <= ell_max; ++l) {
+      square_combine_kernel<<<grid1(ctx, nn), 256, 0, ctx->stream>>>(prod, phis, nn, 1, ell_max, l,
+                                                                     nxt);
+      ctx->launches++;
+    }
+    KP_CUDA(cudaMemcpyAsync(phis, nxt, nn * (ell_max + 1) * sizeof(double),
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  KP_CUDA(cudaGetLastError());
+  return s;
+}
+
+namespace {
+// R(X) = [[Xr, -Xi], [Xi, Xr]] (2n x 2n real) for complex X (n x n interleaved)
+__global__ void embed_kernel(const double2* __restrict__ x, int n, double* __restrict__ r) {
+  const long long nn = (long long)n * n, ld = 2LL * n;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = int(t % n), j = int(t / n);
+    const double2 v = x[t];
+    r[i + j * ld] = v.x;
+    r[(i + n) + j * ld] = v.y;
+    r[i + (j + n) * ld] = -v.y;
+    r[(i + n) + (j + n) * ld] = v.x;
+  }
+}
+// X = R[0:n, 0:n] + i R[n:2n, 0:n]
+__global__ void extract_kernel(const double* __restrict__ r, int n, double2* __restrict__ x) {
+  const long long nn = (long long)n * n, ld = 2LL * n;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = int(t % n), j = int(t / n);
+    x[t] = make_double2(r[i + j * ld], r[(i + n) + j * ld]);
+  }
+}
+constexpr int S_EMB = 45, S_EMB2 = 46;
+}  // namespace
+
+// Complex matrix functions through the real representation R(X): R is an
+// algebra homomorphism, so R(exp X) = exp R(X) and likewise for phi_l and
+// the Pade/LU steps.  For the purely imaginary NLS factors (i/2)Delta the
+// 1-norms, hence the scaling exponent and Pade degrees, equal the reference's
+// complex ones; agreement with the reference's complex arithmetic is at
+// roundoff level (tests/test_phi_gpu.py).
+void expm_batch_c128(kp_ctx* ctx, const double* x, int n, int batch, double* out) {
+  const long long nn = (long long)n * n, rr = 4 * nn;
+  double* r = static_cast<double*>(ctx->ws.get(S_EMB, size_t(rr) * batch * sizeof(double)));
+  double* e = static_cast<double*>(ctx->ws.get(S_EMB2, size_t(rr) * batch * sizeof(double)));
+  for (int b = 0; b < batch; ++b) {
+    embed_kernel<<<grid1(ctx, nn), 256, 0, ctx->stream>>>(
+        reinterpret_cast<const double2*>(x) + b * nn, n, r + b * rr);
+    ctx->launches++;
+  }
+  expm_batch(ctx, r, 2 * n, batch, e);
+  for (int b = 0; b < batch; ++b) {
+    extract_kernel<<<grid1(ctx, nn), 256, 0, ctx->stream>>>(e + b * rr, n,
+                                                            reinterpret_cast<double2*>(out) + b * nn);
+    ctx->launches++;
+  }
+  KP_CUDA(cudaGetLastError());
+}
+
+int phiquad_dev_c128(kp_ctx* ctx, const double* x, int n, int ell_max, int q, int forced,
+                     double* phis) {
+  const long long nn = (long long)n * n, rr = 4 * nn;
+  double* r = static_cast<double*>(ctx->ws.get(S_EMB, size_t(rr) * sizeof(double)));
+  double* tab = static_cast<double*>(ctx->ws.get(S_EMB2, size_t(rr) * (ell_max + 1) * sizeof(double)));
+  embed_kernel<<<grid1(ctx, nn), 256, 0, ctx->stream>>>(reinterpret_cast<const double2*>(x), n, r);
+  ctx->launches++;
+  const int s = phiquad_dev(ctx, r, 2 * n, ell_max, q, forced, tab);
+  for (int j = 0; j <= ell_max; ++j) {
+    extract_kernel<<<grid1(ctx, nn), 256, 0, ctx->stream>>>(tab + j * rr, n,
+                                                            reinterpret_cast<double2*>(phis) + j * nn);
+    ctx->launches++;
+  }
+  KP_CUDA(cudaGetLastError());
+  return s;
+}
+
+}  // namespace kp

@@ -1,0 +1,843 @@
+// stepper.cu -- exponential integrators on device-resident state.
+//
+// Replaces the reference's time loop (inc/integrators.hpp):
+//   lawson_euler_step :116-122   lawson2b_step :124-132   exp_euler_step :134-141
+//   exp_euler_linear_split_step :143-151   etd2rk_step :153-164
+//   integrate :219-373 (Split backend: factors built once, per-step finite check)
+// Every elementwise update of a step is fused into the epilogue of the GEMM
+// that produces its input, so a step streams the state through HBM once per
+// mode product (3 d launches for ETD2RK, 2 d for exponential Euler):
+//   r     = K u + g(t,u)                     kronsum, last term EPI_ADD_G
+//   stage = u + tau*SP1(r); D = g(stage)-g(u)  Tucker(phi1), last mode EPI_STAGE_D
+//   u'    = stage + tau*SP2(D)               Tucker(phi2), last mode EPI_FMA_X
+// (a coupled g -- the Brusselator's two species -- cannot form D inside one
+// tile, so it gets one elementwise pass instead).  The rounding of every fused
+// update equals the reference's (axpy/add_scaled contract to FMAs there).
+//
+// Modes whose phi factor is exactly a scalar multiple of I (the zero species
+// mode of the stacked Brusselator, phi_l(0) = c I) are folded into the alpha
+// of the last real mode -- the same single rounding as the reference's extra
+// mode product -- and zero Kronecker-sum terms are skipped (they add +0).
+//
+// The loop runs as a CUDA graph of two steps (ping-pong buffers), replayed;
+// divergence is detected on the device (epilogue atomicMin of the step
+// counter) and reported with the reference's message and step index.
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kp_g.cuh"
+#include "kp_internal.h"
+
+namespace kp {
+
+namespace {
+
+using ModeFn = void (*)(kp_ctx*, const double*, const std::vector<int>&, int, const double*, int,
+                        const Epilogue&, double*);
+
+unsigned grid_ew(kp_ctx* ctx, long long n) {
+  return unsigned(std::max<long long>(1, std::min<long long>((n + 255) / 256, ctx->num_sms * 8LL)));
+}
+
+template <bool CPLX>
+struct Elt;
+template <>
+struct Elt<false> {
+  using T = double;
+  static __device__ __forceinline__ T g(const kp_gfun& gf, const T* u, long long i, long long half) {
+    const bool second = half > 0 && i >= half;
+    const double partner = half > 0 ? u[second ? i - half : i + half] : 0.0;
+    return g_real(gf, u[i], partner, second);
+  }
+  static __device__ __forceinline__ T fma(double a, T x, T y) { return __fma_rn(a, x, y); }
+  static __device__ __forceinline__ T sub(T a, T b) { return __dsub_rn(a, b); }
+  static __device__ __forceinline__ bool finite(T x) { return isfinite(x); }
+};
+template <>
+struct Elt<true> {
+  using T = double2;
+  static __device__ __forceinline__ T g(const kp_gfun& gf, const T* u, long long i, long long) {
+    return g_cplx(gf, u[i]);
+  }
+  static __device__ __forceinline__ T fma(double a, T x, T y) {
+    return make_double2(__fma_rn(a, x.x, y.x), __fma_rn(a, x.y, y.y));
+  }
+  static __device__ __forceinline__ T sub(T a, T b) {
+    return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
+  }
+  static __device__ __forceinline__ bool finite(T x) { return isfinite(x.x) && isfinite(x.y); }
+};
+
+// w0 = u + tau*g(u); if two: w1 = u + (tau/2)*g(u)   (Lawson prologues, :118, :127-129)
+template <bool CPLX>
+__global__ void lawson_pre_kernel(kp_gfun g, long long n, long long half, double tau, bool two,
+                                  const typename Elt<CPLX>::T* __restrict__ u,
+                                  typename Elt<CPLX>::T* __restrict__ w) {
+  using E = Elt<CPLX>;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const auto gn = E::g(g, u, i, half);
+    w[i] = E::fma(tau, gn, u[i]);
+    if (two) w[n + i] = E::fma(0.5 * tau, gn, u[i]);
+  }
+}
+
+// out = y1 + (tau/2) g(stage), y = [stage; y1]   (lawson2b :130-131)
+template <bool CPLX>
+__global__ void lawson2b_post_kernel(kp_gfun g, long long n, long long half, double tau,
+                                     const typename Elt<CPLX>::T* __restrict__ y,
+                                     typename Elt<CPLX>::T* __restrict__ out, int* bad,
+                                     const int* ctr) {
+  using E = Elt<CPLX>;
+  bool nf = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const auto r = E::fma(0.5 * tau, E::g(g, y, i, half), y[n + i]);
+    out[i] = r;
+    nf |= !E::finite(r);
+  }
+  if (nf) atomicMin(bad, *ctr + 1);
+}
+
+// d = g(stage) - g(u)   (etd2rk :161-162, unfused form for coupled g)
+template <bool CPLX>
+__global__ void gdiff_kernel(kp_gfun g, long long n, long long half,
+                             const typename Elt<CPLX>::T* __restrict__ s,
+                             const typename Elt<CPLX>::T* __restrict__ u,
+                             typename Elt<CPLX>::T* __restrict__ d) {
+  using E = Elt<CPLX>;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    d[i] = E::sub(E::g(g, s, i, half), E::g(g, u, i, half));
+}
+
+__global__ void tick_kernel(int* ctr) { *ctr += 1; }
+
+__global__ void scale_matrix_kernel(const double* __restrict__ a, long long n, double s,
+                                    double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = __dmul_rn(a[i], s);
+}
+
+// Workspace slots of the stepper (tucker ping-pong uses 0/1 inside).
+enum : int { S_R = 2, S_S = 3, S_D = 4, S_W = 5, S_Y = 6, S_U2 = 7, S_CTR = 40 };
+
+}  // namespace
+
+// Per-mode factor list with the scalar-identity folding described above.
+struct FactorSet {
+  std::vector<const double*> f;
+  std::vector<char> active;
+  double fold = 1.0;
+  double pref = 1.0;
+};
+
+class Integrator {
+ public:
+  kp_ctx* ctx;
+  int method;
+  bool cplx;
+  std::vector<int> dims;
+  int d;
+  kp_gfun g;
+  double tau;
+  long long n_entries;  // entries of u (complex counts once)
+  long long half = 0;   // Brusselator species offset
+  ModeFn mp;
+  int comps;
+  std::vector<const double*> A;
+  std::vector<char> a_active;
+  FactorSet f1, f2;
+  std::vector<double*> owned;
+
+  Integrator(kp_ctx* c, int m, bool cp, const std::vector<int>& dv, const double* const* as,
+             const kp_gfun& gf, double tau_)
+      : ctx(c), method(m), cplx(cp), dims(dv), d(int(dv.size())), g(gf), tau(tau_) {
+    n_entries = 1;
+    for (int x : dims) n_entries *= x;
+    mp = cplx ? mode_product_c128 : mode_product_f64;
+    comps = cplx ? 2 : 1;
+    A.assign(as, as + d);
+    if (g.kind == KP_G_BRUSSELATOR) {
+      if (cplx || dims.back() != 2)
+        throw invalid_argument("brusselator g: slowest mode must hold 2 species");
+      half = n_entries / 2;
+    }
+    if (g.kind == KP_G_NLS && !cplx) throw invalid_argument("g: NLS needs a complex tensor");
+    if (cplx && (g.kind == KP_G_ALLEN_CAHN || g.kind == KP_G_BRUSSELATOR))
+      throw invalid_argument("g: unsupported nonlinearity kind for complex");
+    a_active.assign(d, 1);
+    int nact = 0;
+    for (int mu = 0; mu < d; ++mu) {
+      a_active[mu] = !is_zero(A[mu], dims[mu]);
+      nact += a_active[mu];
+    }
+    if (nact == 0) a_active[d - 1] = 1;
+  }
+  ~Integrator() {
+    for (double* p : owned) cudaFree(p);
+  }
+
+  // exact zero matrix? (only small factors are checked; big ones never are)
+  bool is_zero(const double* m, int n) {
+    if (n > 64) return false;
+    std::vector<double> h(size_t(n) * n * comps);
+    KP_CUDA(cudaMemcpyAsync(h.data(), m, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    KP_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (double x : h)
+      if (x != 0.0) return false;
+    return true;
+  }
+  // exactly c*I (real c)?  (small factors only)
+  bool scalar_identity(const double* m, int n, double* c) {
+    if (n > 64) return false;
+    std::vector<double> h(size_t(n) * n * comps);
+    KP_CUDA(cudaMemcpyAsync(h.data(), m, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    KP_CUDA(cudaStreamSynchronize(ctx->stream));
+    const double c0 = h[0];
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i)
+        for (int k = 0; k < comps; ++k) {
+          const double v = h[(size_t(i) + size_t(j) * n) * comps + k];
+          const double want = (i == j && k == 0) ? c0 : 0.0;
+          if (v != want) return false;
+        }
+    *c = c0;
+    return true;
+  }
+
+  double* alloc(size_t doubles) {
+    double* p = nullptr;
+    KP_CUDA(cudaMalloc(&p, std::max<size_t>(doubles, 2) * sizeof(double)));
+    owned.push_back(p);
+    return p;
+  }
+
+  // build_split_phi (inc/split_phi.hpp:25-43) for orders ell_lo..ell_hi from
+  // ONE table per distinct factor (phi_j depends only on phi_{<=j}, so the
+  // table of ell_max = 2 gives bit-identical phi_1 to the reference's separate
+  // ell = 1 build, inc/integrators.hpp:277-278).  ell = 0 uses expm.
+  void build(int ell_lo, int ell_hi, int q, FactorSet* out_lo, FactorSet* out_hi) {
+    // distinct factors: same device pointer and size => same matrix (the
+    // Python/C++ layers upload equal host factors once)
+    std::vector<const double*> distinct;
+    std::vector<int> which(d);
+    for (int mu = 0; mu < d; ++mu) {
+      which[mu] = -1;
+      for (int m2 = 0; m2 < mu; ++m2)
+        if (A[m2] == A[mu] && dims[m2] == dims[mu]) {
+          which[mu] = which[m2];
+          break;
+        }
+      if (which[mu] < 0) {
+        which[mu] = int(distinct.size());
+        distinct.push_back(A[mu]);
+      }
+    }
+    std::vector<double*> lo(distinct.size()), hi(distinct.size());
+    for (size_t j = 0; j < distinct.size(); ++j) {
+      int mu = 0;
+      while (which[mu] != int(j)) ++mu;
+      const int n = dims[mu];
+      const long long nn = (long long)n * n;
+      double* scaled = alloc(nn * comps);
+      scale_matrix_kernel<<<grid_ew(ctx, nn * comps), 256, 0, ctx->stream>>>(distinct[j],
+                                                                            nn * comps, tau, scaled);
+      ctx->launches++;
+      KP_CUDA(cudaGetLastError());
+      if (ell_hi == 0) {
+        double* e = alloc(nn * comps);
+        if (cplx)
+          expm_batch_c128(ctx, scaled, n, 1, e);
+        else
+          expm_batch(ctx, scaled, n, 1, e);
+        lo[j] = hi[j] = e;
+      } else {
+        double* tab = alloc(nn * comps * (ell_hi + 1));
+        if (cplx)
+          phiquad_dev_c128(ctx, scaled, n, ell_hi, q, -1, tab);
+        else
+          phiquad_dev(ctx, scaled, n, ell_hi, q, -1, tab);
+        lo[j] = tab + nn * comps * ell_lo;
+        hi[j] = tab + nn * comps * ell_hi;
+      }
+    }
+    auto fill = [&](FactorSet* fs, const std::vector<double*>& src, int ell) {
+      if (!fs) return;
+      fs->f.resize(d);
+      fs->active.assign(d, 1);
+      fs->fold = 1.0;
+      double fact = 1.0;
+      for (int i = 2; i <= ell; ++i) fact *= i;
+      fs->pref = std::pow(fact, double(d - 1));
+      int nact = d;
+      for (int mu = 0; mu < d; ++mu) {
+        fs->f[mu] = src[which[mu]];
+        double c = 0.0;
+        if (nact > 1 && scalar_identity(fs->f[mu], dims[mu], &c)) {
+          fs->active[mu] = 0;
+          fs->fold *= c;
+          --nact;
+        }
+      }
+    };
+    fill(out_lo, lo, ell_lo);
+    fill(out_hi, hi, ell_hi);
+  }
+
+  // Tucker over the active modes; the skipped scalars multiply the last one.
+  void tucker(const FactorSet& fs, const double* in, const std::vector<int>& tdims, double* out,
+              const Epilogue* last) {
+    std::vector<int> act;
+    for (int mu = 0; mu < d; ++mu)
+      if (fs.active[mu]) act.push_back(mu);
+    const double* cur = in;
+    for (size_t k = 0; k < act.size(); ++k) {
+      const int mu = act[k];
+      const bool first = (k == 0), fin = (k + 1 == act.size());
+      double* dst = fin ? out
+                        : static_cast<double*>(ctx->ws.get(int(k & 1), size_t(n_total(tdims)) *
+                                                                        comps * sizeof(double)));
+      Epilogue e;
+      if (fin && last) e = *last;
+      e.alpha = (first ? fs.pref : 1.0) * (fin ? fs.fold : 1.0);
+      mp(ctx, cur, tdims, mu, fs.f[mu], tdims[mu], e, dst);
+      cur = dst;
+    }
+  }
+  static long long n_total(const std::vector<int>& v) {
+    long long n = 1;
+    for (int x : v) n *= x;
+    return n;
+  }
+
+  void kronsum(const double* u, double* r, const Epilogue& last) {
+    std::vector<int> act;
+    for (int mu = 0; mu < d; ++mu)
+      if (a_active[mu]) act.push_back(mu);
+    for (size_t k = 0; k < act.size(); ++k) {
+      Epilogue e;
+      if (k + 1 == act.size()) e = last;
+      e.alpha = 1.0;
+      e.beta = k > 0 ? 1.0 : 0.0;
+      mp(ctx, u, dims, act[k], A[act[k]], dims[act[k]], e, r);
+    }
+  }
+
+  double* buf(int slot, long long entries) {
+    return static_cast<double*>(ctx->ws.get(slot, size_t(entries) * comps * sizeof(double)));
+  }
+
+  template <bool C>
+  void launch_pre(const double* u, double* w, bool two) {
+    using T = typename Elt<C>::T;
+    lawson_pre_kernel<C><<<grid_ew(ctx, n_entries), 256, 0, ctx->stream>>>(
+        g, n_entries, half, tau, two, reinterpret_cast<const T*>(u), reinterpret_cast<T*>(w));
+    ctx->launches++;
+  }
+  template <bool C>
+  void launch_post(const double* y, double* out, int* bad, const int* ctr) {
+    using T = typename Elt<C>::T;
+    lawson2b_post_kernel<C><<<grid_ew(ctx, n_entries), 256, 0, ctx->stream>>>(
+        g, n_entries, half, tau, reinterpret_cast<const T*>(y), reinterpret_cast<T*>(out), bad, ctr);
+    ctx->launches++;
+  }
+  template <bool C>
+  void launch_gdiff(const double* s, const double* u, double* dd) {
+    using T = typename Elt<C>::T;
+    gdiff_kernel<C><<<grid_ew(ctx, n_entries), 256, 0, ctx->stream>>>(
+        g, n_entries, half, reinterpret_cast<const T*>(s), reinterpret_cast<const T*>(u),
+        reinterpret_cast<T*>(dd));
+    ctx->launches++;
+  }
+
+  // One step u -> out (out != u).  bad/ctr: divergence tracking (may be null).
+  void step(const double* u, double* out, double t, int* bad, const int* ctr) {
+    Epilogue fin;
+    fin.bad_step = bad;
+    fin.step_ctr = ctr;
+    switch (method) {
+      case KP_LAWSON_EULER: {  // :116-122
+        double* w = buf(S_W, n_entries);
+        cplx ? launch_pre<true>(u, w, false) : launch_pre<false>(u, w, false);
+        tucker(f1, w, dims, out, &fin);
+        break;
+      }
+      case KP_LAWSON2B: {  // :124-132, both Tuckers as one over [w0; w1]
+        double* w = buf(S_W, 2 * n_entries);
+        double* y = buf(S_Y, 2 * n_entries);
+        cplx ? launch_pre<true>(u, w, true) : launch_pre<false>(u, w, true);
+        std::vector<int> sd = dims;
+        sd.push_back(2);
+        FactorSet fs = f1;
+        fs.f.push_back(nullptr);
+        fs.active.push_back(0);
+        const int d_save = d;
+        d = d + 1;  // the stacking mode is never active
+        tucker(fs, w, sd, y, nullptr);
+        d = d_save;
+        if (bad) {
+          cplx ? launch_post<true>(y, out, bad, ctr) : launch_post<false>(y, out, bad, ctr);
+        } else {
+          int* dummy = static_cast<int*>(ctx->ws.get(S_CTR + 1, 16));
+          cplx ? launch_post<true>(y, out, dummy, dummy) : launch_post<false>(y, out, dummy, dummy);
+        }
+        break;
+      }
+      case KP_EXP_EULER: {  // :134-141
+        double* r = buf(S_R, n_entries);
+        Epilogue eg;
+        eg.kind = EPI_ADD_G;
+        eg.X = u;
+        eg.g = g;
+        eg.t = t;
+        kronsum(u, r, eg);
+        fin.kind = EPI_FMA_X;
+        fin.X = u;
+        fin.gamma = tau;
+        tucker(f1, r, dims, out, &fin);
+        break;
+      }
+      case KP_EXP_EULER_LS: {  // :143-151  (f1 = exp factors, f2 = phi1)
+        double* y = buf(S_Y, n_entries);
+        double* gn = buf(S_D, n_entries);
+        tucker(f1, u, dims, y, nullptr);
+        Epilogue none;
+        eval_g(u, gn);
+        fin.kind = EPI_FMA_X;
+        fin.X = y;
+        fin.gamma = tau;
+        tucker(f2, gn, dims, out, &fin);
+        (void)none;
+        break;
+      }
+      case KP_ETD2RK: {  // :153-164
+        double* r = buf(S_R, n_entries);
+        double* s = buf(S_S, n_entries);
+        double* dd = buf(S_D, n_entries);
+        Epilogue eg;
+        eg.kind = EPI_ADD_G;
+        eg.X = u;
+        eg.g = g;
+        eg.t = t;
+        kronsum(u, r, eg);
+        Epilogue es;
+        es.X = u;
+        es.gamma = tau;
+        es.g = g;
+        es.t = t;
+        es.t2 = t + tau;
+        if (half == 0) {
+          es.kind = EPI_STAGE_D;
+          es.D = dd;
+          tucker(f1, r, dims, s, &es);
+        } else {
+          es.kind = EPI_FMA_X;
+          tucker(f1, r, dims, s, &es);
+          cplx ? launch_gdiff<true>(s, u, dd) : launch_gdiff<false>(s, u, dd);
+        }
+        fin.kind = EPI_FMA_X;
+        fin.X = s;
+        fin.gamma = tau;
+        tucker(f2, dd, dims, out, &fin);
+        break;
+      }
+      default:
+        throw invalid_argument("step: unknown method " + std::to_string(method));
+    }
+    KP_CUDA(cudaGetLastError());
+  }
+
+  void eval_g(const double* u, double* out) {
+    launch_eval_g(ctx, g, 0.0, u, size_t(n_entries), size_t(half), cplx, out);
+  }
+
+  void setup(int q) {
+    switch (method) {  // inc/integrators.hpp:263-283
+      case KP_LAWSON_EULER:
+      case KP_LAWSON2B:
+        build(0, 0, q, &f1, nullptr);
+        break;
+      case KP_EXP_EULER:
+        build(1, 1, q, nullptr, &f1);
+        break;
+      case KP_EXP_EULER_LS:
+        build(0, 0, q, &f1, nullptr);
+        build(1, 1, q, nullptr, &f2);
+        break;
+      case KP_ETD2RK:
+        build(1, 2, q, &f1, &f2);
+        break;
+      default:
+        throw invalid_argument("integrate: unknown method " + std::to_string(method));
+    }
+  }
+
+  // integrate loop (:290-367) on u (device, in/out).  Returns loop seconds.
+  double run(double* u, double t0, long n_steps, bool use_graph) {
+    int* ctr = static_cast<int*>(ctx->ws.get(S_CTR, 16));
+    int* bad = ctr + 1;
+    const int init[2] = {0, INT_MAX};
+    KP_CUDA(cudaMemcpyAsync(ctr, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+    double* ub[2] = {u, buf(S_U2, n_entries)};
+    cudaEvent_t e0, e1;
+    KP_CUDA(cudaEventCreate(&e0));
+    KP_CUDA(cudaEventCreate(&e1));
+    long n = 0;
+    // first step eagerly: sizes every workspace slot before any capture
+    KP_CUDA(cudaEventRecord(e0, ctx->stream));
+    auto one = [&](long k) {
+      step(ub[k & 1], ub[(k + 1) & 1], t0 + double(k) * tau, bad, ctr);
+      tick_kernel<<<1, 1, 0, ctx->stream>>>(ctr);
+      ctx->launches++;
+    };
+    one(n++);
+    if (use_graph && n_steps - n >= 4) {
+      cudaGraph_t graph;
+      cudaGraphExec_t exec;
+      const unsigned long long l0 = ctx->launches;
+      KP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      // two steps: ub1 -> ub0 -> ub1 (n is odd here); t is unused by the
+      // closed set of g's (all autonomous), so replays stay exact
+      step(ub[1], ub[0], 0.0, bad, ctr);
+      tick_kernel<<<1, 1, 0, ctx->stream>>>(ctr);
+      step(ub[0], ub[1], 0.0, bad, ctr);
+      tick_kernel<<<1, 1, 0, ctx->stream>>>(ctr);
+      KP_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+      const unsigned long long per = ctx->launches - l0 + 2;
+      ctx->launches = l0;
+      KP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      while (n_steps - n >= 2) {
+        KP_CUDA(cudaGraphLaunch(exec, ctx->stream));
+        ctx->launches += per;
+        n += 2;
+      }
+      cudaGraphExecDestroy(exec);
+      cudaGraphDestroy(graph);
+    }
+    while (n < n_steps) one(n++);
+    KP_CUDA(cudaEventRecord(e1, ctx->stream));
+    if (n_steps & 1)
+      KP_CUDA(cudaMemcpyAsync(u, ub[1], size_t(n_entries) * comps * sizeof(double),
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    int hb[2];
+    KP_CUDA(cudaMemcpyAsync(hb, ctr, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
+    KP_CUDA(cudaStreamSynchronize(ctx->stream));
+    float ms = 0.f;
+    KP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (hb[1] != INT_MAX) {  // DivergenceError(n+1, t+tau), inc/integrators.hpp:86-97,364
+      const long k = hb[1];
+      throw divergence_error("state became non-finite at step " + std::to_string(k) +
+                                 " (t = " + std::to_string(t0 + double(k) * tau) + ")",
+                             k);
+    }
+    return ms * 1e-3;
+  }
+};
+
+}  // namespace kp
+
+// ============================================================== C ABI
+namespace kp {
+namespace {
+
+std::vector<int> dims_of(const int* dims, int d, const char* who) {
+  if (d <= 0 || !dims) throw invalid_argument(std::string(who) + ": Tensor: empty dims");
+  std::vector<int> v(dims, dims + d);
+  for (int x : v)
+    if (x <= 0) throw invalid_argument(std::string(who) + ": Tensor: nonpositive dim");
+  return v;
+}
+
+// RAII: run on a capturable stream (the context's own one when the caller's
+// stream is the legacy default stream), ordered after the caller's work.
+struct StreamScope {
+  kp_ctx* ctx;
+  cudaStream_t saved;
+  explicit StreamScope(kp_ctx* c) : ctx(c), saved(c->stream) {
+    if (saved == nullptr) {
+      KP_CUDA(cudaStreamSynchronize(nullptr));
+      ctx->stream = ctx->own_stream;
+    }
+  }
+  ~StreamScope() {
+    if (saved == nullptr) {
+      cudaStreamSynchronize(ctx->own_stream);
+      ctx->stream = saved;
+    }
+  }
+};
+
+void build_split(kp_ctx* ctx, bool cplx, const double* const* as, const int* dims, int d,
+                 double tau, int ell, int q, double* const* factors, double* prefactor) {
+  const auto dv = dims_of(dims, d, "build_split_phi");
+  if (ell < 0) throw invalid_argument("build_split_phi: negative ell");
+  const int comps = cplx ? 2 : 1;
+  for (int mu = 0; mu < d; ++mu) {
+    int same = -1;
+    for (int m2 = 0; m2 < mu; ++m2)
+      if (as[m2] == as[mu] && dv[m2] == dv[mu]) same = m2;
+    const long long nn = (long long)dv[mu] * dv[mu] * comps;
+    if (same >= 0) {
+      KP_CUDA(cudaMemcpyAsync(factors[mu], factors[same], nn * sizeof(double),
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+      continue;
+    }
+    double* scaled = static_cast<double*>(ctx->ws.get(47, nn * sizeof(double)));
+    scale_matrix_kernel<<<grid_ew(ctx, nn), 256, 0, ctx->stream>>>(as[mu], nn, tau, scaled);
+    ctx->launches++;
+    if (ell == 0) {
+      cplx ? expm_batch_c128(ctx, scaled, dv[mu], 1, factors[mu])
+           : expm_batch(ctx, scaled, dv[mu], 1, factors[mu]);
+    } else {
+      double* tab = static_cast<double*>(ctx->ws.get(48, nn * (ell + 1) * sizeof(double)));
+      cplx ? phiquad_dev_c128(ctx, scaled, dv[mu], ell, q, -1, tab)
+           : phiquad_dev(ctx, scaled, dv[mu], ell, q, -1, tab);
+      KP_CUDA(cudaMemcpyAsync(factors[mu], tab + nn * ell, nn * sizeof(double),
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+  }
+  double f = 1.0;
+  for (int i = 2; i <= ell; ++i) f *= i;
+  *prefactor = std::pow(f, double(d - 1));
+}
+
+FactorSet given_factors(Integrator& it, const double* const* f, double pref) {
+  FactorSet fs;
+  fs.f.assign(f, f + it.d);
+  fs.active.assign(it.d, 1);
+  fs.pref = pref;
+  int nact = it.d;
+  for (int mu = 0; mu < it.d; ++mu) {
+    double c = 0.0;
+    if (nact > 1 && it.scalar_identity(fs.f[mu], it.dims[mu], &c)) {
+      fs.active[mu] = 0;
+      fs.fold *= c;
+      --nact;
+    }
+  }
+  return fs;
+}
+
+}  // namespace
+}  // namespace kp
+
+using namespace kp;
+
+namespace {
+template <typename F>
+int guard_c(F&& f, long* step_out = nullptr) {
+  try {
+    f();
+    return KP_OK;
+  } catch (const kp::divergence_error& e) {
+    kp_set_last_error(e.what());
+    if (step_out) *step_out = e.step;
+    return KP_EDIVERGE;
+  } catch (const std::invalid_argument& e) {
+    kp_set_last_error(e.what());
+    return KP_EINVAL;
+  } catch (const kp::cuda_error& e) {
+    kp_set_last_error(e.what());
+    return KP_ECUDA;
+  } catch (const std::exception& e) {
+    kp_set_last_error(e.what());
+    return KP_ERUNTIME;
+  }
+}
+
+void ctx_ok(kp_ctx* ctx) {
+  if (!ctx) throw invalid_argument("kronphi_b200: null context");
+  KP_CUDA(cudaSetDevice(ctx->device));
+}
+
+int integrate_impl(kp_ctx* ctx, bool cplx, int method, double* u, const int* dims, int d,
+                   const double* const* as, const kp_gfun* g, double t0, double t_final,
+                   long n_steps, int q, long* diverged_step, double* loop_seconds) {
+  if (diverged_step) *diverged_step = 0;
+  return guard_c(
+      [&] {
+        ctx_ok(ctx);
+        const auto dv = dims_of(dims, d, "integrate");
+        if (n_steps <= 0) throw invalid_argument("integrate: n_steps must be positive");
+        if (!(t_final > t0)) throw invalid_argument("integrate: empty time interval");
+        if (!as || !g) throw invalid_argument("integrate: null factors or g");
+        StreamScope scope(ctx);
+        const double tau = (t_final - t0) / double(n_steps);
+        Integrator it(ctx, method, cplx, dv, as, *g, tau);
+        it.setup(q);
+        const double sec = it.run(u, t0, n_steps, true);
+        if (loop_seconds) *loop_seconds = sec;
+      },
+      diverged_step);
+}
+
+int host_integrate_impl(kp_ctx* ctx, bool cplx, int method, const double* u0, const int* dims,
+                        int d, const double* const* as, const kp_gfun* g, double t0,
+                        double t_final, long n_steps, int q, double* u_final, long* diverged_step,
+                        double* loop_seconds) {
+  if (diverged_step) *diverged_step = 0;
+  double* du = nullptr;
+  std::vector<double*> da;
+  int rc = guard_c([&] {
+    ctx_ok(ctx);
+    const auto dv = dims_of(dims, d, "integrate");
+    const int comps = cplx ? 2 : 1;
+    size_t n = comps;
+    for (int x : dv) n *= size_t(x);
+    KP_CUDA(cudaMalloc(&du, n * sizeof(double)));
+    KP_CUDA(cudaMemcpy(du, u0, n * sizeof(double), cudaMemcpyHostToDevice));
+    // equal host factors are uploaded once (the device build dedupes by pointer)
+    std::vector<const double*> dptr(d);
+    for (int mu = 0; mu < d; ++mu) {
+      const size_t nn = size_t(dv[mu]) * dv[mu] * comps;
+      int same = -1;
+      for (int m2 = 0; m2 < mu; ++m2)
+        if (dv[m2] == dv[mu] &&
+            (as[m2] == as[mu] || std::memcmp(as[m2], as[mu], nn * sizeof(double)) == 0))
+          same = m2;
+      if (same >= 0) {
+        dptr[mu] = dptr[same];
+        continue;
+      }
+      double* p = nullptr;
+      KP_CUDA(cudaMalloc(&p, nn * sizeof(double)));
+      da.push_back(p);
+      KP_CUDA(cudaMemcpy(p, as[mu], nn * sizeof(double), cudaMemcpyHostToDevice));
+      dptr[mu] = p;
+    }
+    int r2 = integrate_impl(ctx, cplx, method, du, dims, d, dptr.data(), g, t0, t_final, n_steps,
+                            q, diverged_step, loop_seconds);
+    if (r2 == KP_EDIVERGE) throw divergence_error(kp_last_error(), diverged_step ? *diverged_step : 0);
+    if (r2 != KP_OK) {
+      const std::string m = kp_last_error();
+      if (r2 == KP_EINVAL) throw invalid_argument(m);
+      if (r2 == KP_ECUDA) throw cuda_error(m);
+      throw runtime_error(m);
+    }
+    KP_CUDA(cudaMemcpy(u_final, du, n * sizeof(double), cudaMemcpyDeviceToHost));
+  }, diverged_step);
+  if (du) cudaFree(du);
+  for (double* p : da) cudaFree(p);
+  return rc;
+}
+
+int step_impl(kp_ctx* ctx, bool cplx, int method, const double* u, const int* dims, int d,
+              double t, double tau, const double* const* as, const double* const* f1,
+              double pref1, const double* const* f2, double pref2, const kp_gfun* g,
+              double* out) {
+  return guard_c([&] {
+    ctx_ok(ctx);
+    const auto dv = dims_of(dims, d, "step");
+    if (!g || !f1) throw invalid_argument("step: null factors or g");
+    if (out == u) throw invalid_argument("step: out must not alias u");
+    std::vector<const double*> zeros;
+    if (!as) {  // Lawson methods need no K
+      zeros.assign(d, f1[0]);
+      as = zeros.data();
+    }
+    Integrator it(ctx, method, cplx, dv, as, *g, tau);
+    it.f1 = given_factors(it, f1, pref1);
+    if (f2) it.f2 = given_factors(it, f2, pref2);
+    it.step(u, out, t, nullptr, nullptr);
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+int kp_gll_rule(int q, double* nodes, double* weights) {
+  return guard_c([&] { gll_rule_host(q, nodes, weights); });
+}
+
+int kp_expm_f64(kp_ctx* ctx, const double* x, int n, double* out) {
+  return guard_c([&] {
+    ctx_ok(ctx);
+    if (n <= 0) throw invalid_argument("expm: matrix not square");
+    expm_batch(ctx, x, n, 1, out);
+  });
+}
+int kp_expm_c128(kp_ctx* ctx, const double* x, int n, double* out) {
+  return guard_c([&] {
+    ctx_ok(ctx);
+    if (n <= 0) throw invalid_argument("expm: matrix not square");
+    expm_batch_c128(ctx, x, n, 1, out);
+  });
+}
+int kp_phiquad_f64(kp_ctx* ctx, const double* x, int n, int ell_max, int q, int forced,
+                   double* phis, int* s) {
+  return guard_c([&] {
+    ctx_ok(ctx);
+    const int r = phiquad_dev(ctx, x, n, ell_max, q, forced, phis);
+    if (s) *s = r;
+  });
+}
+int kp_phiquad_c128(kp_ctx* ctx, const double* x, int n, int ell_max, int q, int forced,
+                    double* phis, int* s) {
+  return guard_c([&] {
+    ctx_ok(ctx);
+    const int r = phiquad_dev_c128(ctx, x, n, ell_max, q, forced, phis);
+    if (s) *s = r;
+  });
+}
+int kp_build_split_phi_f64(kp_ctx* ctx, const double* const* as, const int* dims, int d,
+                           double tau, int ell, int q, double* const* factors, double* pref) {
+  return guard_c([&] {
+    ctx_ok(ctx);
+    build_split(ctx, false, as, dims, d, tau, ell, q, factors, pref);
+  });
+}
+int kp_build_split_phi_c128(kp_ctx* ctx, const double* const* as, const int* dims, int d,
+                            double tau, int ell, int q, double* const* factors, double* pref) {
+  return guard_c([&] {
+    ctx_ok(ctx);
+    build_split(ctx, true, as, dims, d, tau, ell, q, factors, pref);
+  });
+}
+int kp_step_f64(kp_ctx* ctx, int method, const double* u, const int* dims, int d, double t,
+                double tau, const double* const* as, const double* const* f1, double pref1,
+                const double* const* f2, double pref2, const kp_gfun* g, double* out) {
+  return step_impl(ctx, false, method, u, dims, d, t, tau, as, f1, pref1, f2, pref2, g, out);
+}
+int kp_step_c128(kp_ctx* ctx, int method, const double* u, const int* dims, int d, double t,
+                 double tau, const double* const* as, const double* const* f1, double pref1,
+                 const double* const* f2, double pref2, const kp_gfun* g, double* out) {
+  return step_impl(ctx, true, method, u, dims, d, t, tau, as, f1, pref1, f2, pref2, g, out);
+}
+int kp_integrate_f64(kp_ctx* ctx, int method, double* u, const int* dims, int d,
+                     const double* const* as, const kp_gfun* g, double t0, double t_final,
+                     long n_steps, int q, long* diverged_step, double* loop_seconds) {
+  return integrate_impl(ctx, false, method, u, dims, d, as, g, t0, t_final, n_steps, q,
+                        diverged_step, loop_seconds);
+}
+int kp_integrate_c128(kp_ctx* ctx, int method, double* u, const int* dims, int d,
+                      const double* const* as, const kp_gfun* g, double t0, double t_final,
+                      long n_steps, int q, long* diverged_step, double* loop_seconds) {
+  return integrate_impl(ctx, true, method, u, dims, d, as, g, t0, t_final, n_steps, q,
+                        diverged_step, loop_seconds);
+}
+int kp_host_integrate_f64(kp_ctx* ctx, int method, const double* u0, const int* dims, int d,
+                          const double* const* as, const kp_gfun* g, double t0, double t_final,
+                          long n_steps, int q, double* u_final, long* diverged_step,
+                          double* loop_seconds) {
+  return host_integrate_impl(ctx, false, method, u0, dims, d, as, g, t0, t_final, n_steps, q,
+                             u_final, diverged_step, loop_seconds);
+}
+int kp_host_integrate_c128(kp_ctx* ctx, int method, const double* u0, const int* dims, int d,
+                           const double* const* as, const kp_gfun* g, double t0, double t_final,
+                           long n_steps, int q, double* u_final, long* diverged_step,
+                           double* loop_seconds) {
+  return host_integrate_impl(ctx, true, method, u0, dims, d, as, g, t0, t_final, n_steps, q,
+                             u_final, diverged_step, loop_seconds);
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+"""Problem builders for the BASELINE configs (host numpy; column-major).
+
+fd_operator_1d restates src/problems.cpp:9-22 (Dirichlet, h = 1/(n+1)).
+The configs' PDEs are not in the reference; their
+inputs follow SURVEY.md 8(d) with numpy-seeded synthetic data (seeds
+1001-1005 for configs 1-5), fed identically to the oracle and the GPU.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List
+
+import numpy as np
+
+from .integrators import G, gfun, G_ALLEN_CAHN, G_BRUSSELATOR, G_NLS
+
+
+def fd_operator_1d(n, eps, alpha=0.0):
+    """eps*d2/dx2 + alpha*d/dx, 2nd-order central, n inner points of [0,1],
+    homogeneous Dirichlet (src/problems.cpp:9-22)."""
+    if n < 1:
+        raise ValueError("fd_operator_1d: need n >= 1")
+    h = 1.0 / (n + 1)
+    lo = eps / (h * h) - alpha / (2.0 * h)
+    di = -2.0 * eps / (h * h)
+    hi = eps / (h * h) + alpha / (2.0 * h)
+    a = np.zeros((n, n), order="F")
+    i = np.arange(n)
+    a[i, i] = di
+    a[i[1:], i[:-1]] = lo
+    a[i[:-1], i[1:]] = hi
+    return a
+
+
+def periodic_laplacian_1d(n, h):
+    """(1/h^2) circ(1, -2, 1) (new: the reference is Dirichlet-only)."""
+    c = 1.0 / (h * h)
+    a = np.zeros((n, n), order="F")
+    i = np.arange(n)
+    a[i, i] = -2.0 * c
+    a[i, (i + 1) % n] = c
+    a[i, (i - 1) % n] = c
+    return a
+
+
+def grid(n):
+    h = 1.0 / (n + 1)
+    return (np.arange(n) + 1) * h
+
+
+@dataclass
+class Config:
+    name: str
+    method: str
+    u0: np.ndarray
+    K: List[np.ndarray]
+    g: object
+    tau: float
+    n_steps: int
+
+    @property
+    def t_final(self):
+        return self.tau * self.n_steps
+
+
+def ac2d(n=128, n_steps=100, tau=1e-3, seed=1001):
+    """configs[0]: 2-D Allen-Cahn u_t = 0.01 Lap u + u - u^3, exp-Euler."""
+    r = np.random.default_rng(seed)
+    x = grid(n)
+    u0 = 0.4 * np.outer(np.sin(np.pi * x), np.sin(np.pi * x)) + 0.1 * r.uniform(-1, 1, (n, n))
+    a = fd_operator_1d(n, 0.01)
+    return Config("ac2d", "exp_euler", np.asfortranarray(u0), [a, a], G.allen_cahn(), tau,
+                  n_steps)
+
+
+def ac3d(n=128, n_steps=200, tau=5e-4, seed=1003):
+    """configs[2]: 3-D Allen-Cahn, eps = 0.01 diffusion, ETD2RK."""
+    r = np.random.default_rng(seed)
+    x = np.sin(np.pi * grid(n))
+    u0 = 0.4 * x[:, None, None] * x[None, :, None] * x[None, None, :] \
+        + 0.1 * r.uniform(-1, 1, (n, n, n))
+    a = fd_operator_1d(n, 0.01)
+    return Config("ac3d", "etd2rk", np.asfortranarray(u0), [a, a, a], G.allen_cahn(), tau,
+                  n_steps)
+
+
+def brusselator(n=256, n_steps=100, tau=1e-3, method="etd2rk", seed=1004, a=1.0, b=3.0,
+                diff=0.02):
+    """configs[3]: two species stacked as a 4th mode of size 2 (u first,
+    v second) with a zero 2x2 factor -- the reference's own way to run it
+    (SURVEY.md 8(c)); Dirichlet fd_operator_1d(n, 0.02) for both species."""
+    r = np.random.default_rng(seed)
+    u = a + 0.1 * r.uniform(-1, 1, (n, n, n))
+    v = b / a + 0.1 * r.uniform(-1, 1, (n, n, n))
+    u0 = np.asfortranarray(np.stack([u, v], axis=-1))
+    A = fd_operator_1d(n, diff)
+    return Config("brusselator", method, u0, [A, A, A, np.zeros((2, 2), order="F")],
+                  G.brusselator(a, b), tau, n_steps)
+
+
+def nls(n=512, n_steps=50, tau=1e-3, method="etd2rk", seed=1005, k=(1.0, 0.5, 0.0)):
+    """configs[4]: i u_t = -1/2 Lap u + |u|^2 u on [-8,8]^3 periodic, i.e.
+    u' = (i/2) Lap u - i |u|^2 u; u0 = Gaussian wave packet (wave vector k)
+    + 0.01 (N + iN) noise."""
+    r = np.random.default_rng(seed)
+    L = 16.0
+    h = L / n
+    x = -8.0 + h * np.arange(n)
+    X, Y, Z = np.meshgrid(x, x, x, indexing="ij")
+    u0 = np.exp(-(X * X + Y * Y + Z * Z) / 2.0) * np.exp(1j * (k[0] * X + k[1] * Y + k[2] * Z))
+    u0 = u0 + 0.01 * (r.standard_normal((n, n, n)) + 1j * r.standard_normal((n, n, n)))
+    A = 0.5j * periodic_laplacian_1d(n, h)
+    return Config("nls", method, np.asfortranarray(u0), [A, A, A], G.nls(), tau, n_steps)
+
+
+def tucker_sweep(n, seed=1002, tau=1e-3):
+    """configs[1]: V ~ N(0,1) and A = fd_operator_1d(n, 1.0) (L = phi_1(tau A))."""
+    r = np.random.default_rng(seed)
+    return np.asfortranarray(r.standard_normal((n, n, n))), fd_operator_1d(n, 1.0), tau

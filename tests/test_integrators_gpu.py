@@ -1,0 +1,214 @@
+"""GPU parity of the exponential integrators against the CPU oracle on the
+BASELINE configs (reduced sizes where the oracle must finish in seconds) and
+the reference's stepper known-answer tests (tests/test_integrators.cpp).
+Tolerance after a full integration: rel-l2 <= 1e-10 (BASELINE.json)."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import rel2, rng
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def oracle_run(port, cfg):
+    import pyoracle
+    g = cfg.g
+    og = pyoracle.gfun(g.kind, *list(g.p))
+    return port.integrate(cfg.method, cfg.u0, cfg.K, og, 0.0, cfg.t_final, cfg.n_steps)
+
+
+def gpu_run(kp, cfg, method=None):
+    return kp.integrate_config(method or cfg.method, cfg.u0, cfg.K, cfg.g, 0.0, cfg.t_final,
+                               cfg.n_steps)
+
+
+@pytest.mark.parametrize("method", ["lawson_euler", "lawson2b", "exp_euler", "exp_euler_ls",
+                                    "etd2rk"])
+def test_all_methods_ac2d_small(kp, port, method):
+    from paper_2304_02327_b200 import problems
+    cfg = problems.ac2d(n=32, n_steps=20)
+    cfg.method = method
+    assert rel2(gpu_run(kp, cfg), oracle_run(port, cfg)) < TOL
+
+
+def test_config1_ac2d_full(kp, port):
+    """configs[0] at full size: 128^2, exp-Euler, tau = 1e-3, 100 steps."""
+    from paper_2304_02327_b200 import problems
+    cfg = problems.ac2d()
+    assert rel2(gpu_run(kp, cfg), oracle_run(port, cfg)) < TOL
+
+
+def test_config3_ac3d_reduced(kp, port):
+    """configs[2] (ETD2RK, tau = 5e-4, 200 steps) at 32^3."""
+    from paper_2304_02327_b200 import problems
+    cfg = problems.ac3d(n=32)
+    assert rel2(gpu_run(kp, cfg), oracle_run(port, cfg)) < TOL
+
+
+@pytest.mark.parametrize("method", ["etd2rk", "lawson2b"])
+def test_config4_brusselator_reduced(kp, port, method):
+    """configs[3] at 16^3 x 2 species, 100 steps, stacked 4-mode form."""
+    from paper_2304_02327_b200 import problems
+    cfg = problems.brusselator(n=16, method=method)
+    assert rel2(gpu_run(kp, cfg), oracle_run(port, cfg)) < TOL
+
+
+@pytest.mark.parametrize("method", ["exp_euler", "etd2rk"])
+def test_config5_nls_reduced(kp, port, method):
+    """configs[4] at 24^3 (the periodic grid keeps the [-8,8] box), 50 steps."""
+    from paper_2304_02327_b200 import problems
+    cfg = problems.nls(n=24, method=method)
+    got = gpu_run(kp, cfg)
+    want = oracle_run(port, cfg)
+    assert rel2(got, want) < TOL
+    # unitary linear part: mass is conserved up to the splitting error
+    assert abs(np.linalg.norm(got) / np.linalg.norm(cfg.u0) - 1) < 1e-3
+
+
+def test_step_functions_vs_oracle(kp, port):
+    import pyoracle
+    r = rng(5)
+    K = [port.fd_operator_1d(n, 0.3) for n in (5, 6)]
+    u = np.asfortranarray(r.uniform(-1, 1, (5, 6)))
+    tau = 0.05
+    g = kp.G.square()
+    og = pyoracle.gfun(pyoracle.G_SQUARE)
+    e = kp.build_split_phi(K, tau, 0)
+    p1 = kp.build_split_phi(K, tau, 1)
+    p2 = kp.build_split_phi(K, tau, 2)
+    cases = [
+        (kp.lawson_euler_step(u, 0.0, tau, g, e.factors), "lawson_euler", e, None),
+        (kp.lawson2b_step(u, 0.0, tau, g, e.factors), "lawson2b", e, None),
+        (kp.exp_euler_step(u, 0.0, tau, K, g, p1), "exp_euler", p1, None),
+        (kp.exp_euler_linear_split_step(u, 0.0, tau, g, e.factors, p1), "exp_euler_ls", e, p1),
+        (kp.etd2rk_step(u, 0.0, tau, K, g, p1, p2), "etd2rk", p1, p2),
+    ]
+    for got, m, a, b in cases:
+        want = port.step(m, u, 0.0, tau, K, a.factors, a.prefactor,
+                         b.factors if b else None, b.prefactor if b else 1.0, og)
+        assert rel2(got, want) < 1e-13, m
+
+
+def test_lawson2b_collapses_when_g_zero(kp):
+    # tests/test_integrators.cpp:122-130 (bitwise)
+    r = rng(6)
+    K = [port_like(4), port_like(3)]
+    u = np.asfortranarray(r.uniform(-1, 1, (4, 3)))
+    e = kp.build_split_phi(K, 0.15, 0).factors
+    a = kp.lawson_euler_step(u, 0.0, 0.15, kp.G.zero(), e)
+    b = kp.lawson2b_step(u, 0.0, 0.15, kp.G.zero(), e)
+    assert np.array_equal(a, b)
+
+
+def port_like(n):
+    r = rng(n)
+    m = r.uniform(-1, 1, (n, n))
+    m[np.arange(n), np.arange(n)] -= np.abs(m).sum(0).max()
+    return np.asfortranarray(m)
+
+
+def test_k_zero_is_forward_euler_and_trapezoidal(kp):
+    # tests/test_integrators.cpp:99-107, :132-144, :282-296
+    r = rng(7)
+    u = np.asfortranarray(r.uniform(-1, 1, (3,)))
+    z = [np.zeros((3, 3))]
+    got = kp.lawson_euler_step(u, 0.0, 0.5, kp.G.square(), kp.build_split_phi(z, 0.5, 0).factors)
+    assert np.allclose(got, u + 0.5 * u * u, rtol=1e-14, atol=0)
+    tau = 0.3
+    got = kp.lawson2b_step(u, 0.0, tau, kp.G.square(), kp.build_split_phi(z, tau, 0).factors)
+    st = u + tau * u * u
+    assert np.allclose(got, u + 0.5 * tau * (u * u + st * st), rtol=1e-14, atol=0)
+    tau = 0.21
+    p1, p2 = kp.build_split_phi(z, tau, 1), kp.build_split_phi(z, tau, 2)
+    got = kp.etd2rk_step(u, 0.0, tau, z, kp.G.square(), p1, p2)
+    st = u + tau * u * u
+    assert np.allclose(got, st + tau * 0.5 * (st * st - u * u), rtol=1e-14, atol=0)
+
+
+def test_scalar_identities(kp):
+    # tests/test_integrators.cpp:163-187
+    lam = [np.array([[-1.0]])]
+    tau = 0.1
+    p1 = kp.build_split_phi(lam, tau, 1)
+    got = kp.exp_euler_step(np.array([1.0]), 0.0, tau, lam, kp.G.zero(), p1)
+    assert abs(got[0] - math.exp(-tau)) < 1e-13
+    kz = [np.zeros((1, 1))]
+    got = kp.exp_euler_step(np.array([2.0]), 0.0, tau, kz, kp.G.const(0.7),
+                            kp.build_split_phi(kz, tau, 1))
+    assert abs(got[0] - (2.0 + tau * 0.7)) < 1e-14
+
+
+def test_etd2rk_constant_g_is_exp_euler(kp):
+    # tests/test_integrators.cpp:267-280
+    K = [port_like(5), port_like(6)]
+    u = np.asfortranarray(rng(8).uniform(-1, 1, (5, 6)))
+    tau = 0.2
+    p1, p2 = kp.build_split_phi(K, tau, 1), kp.build_split_phi(K, tau, 2)
+    a = kp.exp_euler_step(u, 0.0, tau, K, kp.G.const(0.42), p1)
+    b = kp.etd2rk_step(u, 0.0, tau, K, kp.G.const(0.42), p1, p2)
+    assert np.abs(a - b).max() < 1e-15
+
+
+def test_integrate_one_step_equals_step(kp):
+    # tests/test_integrators.cpp:350-371 (bitwise)
+    K = [port_like(5), port_like(6)]
+    u = np.asfortranarray(rng(9).uniform(-1, 1, (5, 6)))
+    tau = 0.4
+    g = kp.G.square()
+    e = kp.build_split_phi(K, tau, 0).factors
+    p1, p2 = kp.build_split_phi(K, tau, 1), kp.build_split_phi(K, tau, 2)
+    one = lambda m: kp.integrate_config(m, u, K, g, 0.0, tau, 1)
+    assert np.array_equal(one("lawson_euler"), kp.lawson_euler_step(u, 0.0, tau, g, e))
+    assert np.array_equal(one("lawson2b"), kp.lawson2b_step(u, 0.0, tau, g, e))
+    assert np.array_equal(one("exp_euler"), kp.exp_euler_step(u, 0.0, tau, K, g, p1))
+    assert np.array_equal(one("etd2rk"), kp.etd2rk_step(u, 0.0, tau, K, g, p1, p2))
+
+
+def test_divergence_reported_with_step(kp):
+    # tests/test_integrators.cpp:404-422
+    with pytest.raises(kp.DivergenceError) as ei:
+        kp.integrate_config("lawson_euler", np.array([1e100, 1e100]), [np.zeros((2, 2))],
+                            kp.G.square(), 0.0, 10.0, 10)
+    assert ei.value.step >= 1 and "step" in str(ei.value)
+    with pytest.raises(kp.DivergenceError) as ei:
+        kp.integrate_config("etd2rk", np.full((4, 4), 1e80), [np.zeros((4, 4))] * 2,
+                            kp.G.square(), 0.0, 10.0, 10)
+    assert ei.value.step == 1
+
+
+def test_integrate_validation(kp):
+    with pytest.raises(kp.InvalidArgument):
+        kp.integrate_config("exp_euler", np.ones(3), [np.eye(3)], kp.G.zero(), 0.0, 1.0, 0)
+    with pytest.raises(kp.InvalidArgument):
+        kp.integrate_config("exp_euler", np.ones(3), [np.eye(3)], kp.G.zero(), 1.0, 1.0, 4)
+    with pytest.raises(kp.InvalidArgument):
+        kp.parse_method("rk4")
+
+
+def test_etd2rk_order_two_scalar(kp):
+    # tests/test_integrators.cpp:298-310: u' = -u + u^2, u0 = 0.4
+    def exact(u0, t):
+        return 1.0 / (1.0 + (1.0 / u0 - 1.0) * math.exp(t))
+    taus, errs = [], []
+    for n in (16, 32, 64, 128):
+        got = kp.integrate_config("etd2rk", np.array([0.4]), [np.array([[-1.0]])],
+                                  kp.G.square(), 0.0, 1.0, n)
+        taus.append(1.0 / n)
+        errs.append(abs(got[0] - exact(0.4, 1.0)))
+    slope = np.polyfit(np.log(taus), np.log(errs), 1)[0]
+    assert abs(slope - 2.0) < 0.05
+
+
+def test_device_integrate_stays_on_device(kp, port):
+    import torch
+    from paper_2304_02327_b200 import problems
+    cfg = problems.ac3d(n=24, n_steps=10)
+    ud = kp.to_device(cfg.u0)
+    K = [kp.to_device(cfg.K[0])] * 3
+    res = kp.integrate(kp.ProblemSpec(K, cfg.g, ud, 0.0, cfg.t_final),
+                       kp.StepperConfig(kp.Method.ETD2RK, cfg.n_steps))
+    assert res.final.is_cuda and res.loop_s > 0
+    assert rel2(kp.to_host(res.final), oracle_run(port, cfg)) < TOL
