@@ -1,0 +1,723 @@
+// kronphi_b200/kronphi.hpp -- header-only C++ drop-in for the reference's
+// hot-path API (namespace kronphi, /root/reference/proj/include/kronphi/),
+// implemented on the C ABI of libkronphi_b200.so (include/kronphi_b200.h).
+//
+// Same type and function names, argument meaning and exception types as the
+// reference (file:line below are into proj/include/kronphi/):
+//   Matrix<T> (matrix.hpp:33-134), Tensor<T> (tensor.hpp:22-109),
+//   vec/unvec/axpy/scale/add_scaled/diff_norm_* (tensor.hpp:113-177),
+//   KroneckerSum<T>, mode_product_into, mode_product, tucker, kronsum_action
+//   (mode_product.hpp:21-121), expm, GLLRule/gll_rule, PhiTable, phiquad
+//   (matrix_functions.hpp:76-204), SplitPhi, build_split_phi, apply_split_phi
+//   (split_phi.hpp:17-62), Method, ProblemSpec, StepperConfig,
+//   IntegrateResult, DivergenceError, the step functions and integrate
+//   (integrators.hpp:24-373).
+// Containers stay host value types; every O(n^3)/O(N n) operation runs on the
+// GPU (upload, DMMA kernels, download).  Differences, by design:
+//   * g is a device nonlinearity from the closed set (kp_gfun: Allen-Cahn,
+//     Brusselator, NLS, zero, square, const) -- a host std::function has no
+//     device equivalent and is rejected (no CPU fallback on the hot path);
+//   * Backend::DenseOracle and Method::RosenbrockEuler are not provided;
+//   * the small elementwise helpers (axpy, scale, ...) run on the host
+//     containers like the reference's.
+// Link with -lkronphi_b200 (paper_2304_02327_b200/lib).
+#pragma once
+
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstddef>
+#include <cstring>
+#include <algorithm>
+#include <initializer_list>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <utility>
+#include <vector>
+
+#include "kronphi_b200.h"
+
+namespace kronphi {
+
+// ------------------------------------------------------------ errors
+
+class DivergenceError : public std::runtime_error {
+ public:
+  DivergenceError(long step, const std::string& msg) : std::runtime_error(msg), step_(step) {}
+  long step() const { return step_; }
+
+ private:
+  long step_;
+};
+
+namespace detail {
+
+inline void check(int rc, long step = 0) {
+  if (rc == KP_OK) return;
+  const std::string m = kp_last_error();
+  if (rc == KP_EINVAL) throw std::invalid_argument(m);
+  if (rc == KP_EDIVERGE) throw DivergenceError(step, m);
+  throw std::runtime_error(m);
+}
+
+// One context per thread (device 0 unless kronphi::set_device is called first).
+inline int& device_slot() {
+  static thread_local int dev = 0;
+  return dev;
+}
+struct CtxHolder {
+  kp_ctx* ctx = nullptr;
+  ~CtxHolder() {
+    if (ctx) kp_ctx_destroy(ctx);
+  }
+};
+inline kp_ctx* ctx() {
+  static thread_local CtxHolder h;
+  if (!h.ctx) check(kp_ctx_create(device_slot(), &h.ctx));
+  return h.ctx;
+}
+
+// RAII device buffer through the C ABI.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t b) : bytes(b) { check(kp_malloc(ctx(), b, &p)); }
+  DevBuf(const void* host, size_t b) : DevBuf(b) { check(kp_upload(ctx(), p, host, b)); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; }
+  ~DevBuf() {
+    if (p) kp_free(ctx(), p);
+  }
+  double* d() const { return static_cast<double*>(p); }
+  void download(void* host) const { check(kp_download(ctx(), host, p, bytes)); }
+};
+
+template <typename T>
+struct is_complex : std::false_type {};
+template <typename T>
+struct is_complex<std::complex<T>> : std::true_type {};
+
+}  // namespace detail
+
+inline void set_device(int device) { detail::device_slot() = device; }
+
+inline double factorial(int k) {
+  double f = 1.0;
+  for (int i = 2; i <= k; ++i) f *= i;
+  return f;
+}
+
+template <typename T>
+double abs_of(const T& x) {
+  return std::abs(x);
+}
+
+enum class Op { none, transpose };
+
+// ------------------------------------------------------------ Matrix<T>
+
+template <typename T>
+class Matrix {
+  static_assert(std::is_same_v<T, double> || std::is_same_v<T, std::complex<double>>,
+                "kronphi_b200 computes in FP64 / complex128");
+
+ public:
+  Matrix() = default;
+  Matrix(int rows, int cols) : rows_(rows), cols_(cols), data_(size_t(rows) * cols, T{}) {
+    if (rows < 0 || cols < 0) throw std::invalid_argument("Matrix: negative size");
+  }
+  Matrix(int rows, int cols, std::vector<T> data)
+      : rows_(rows), cols_(cols), data_(std::move(data)) {
+    if (data_.size() != size_t(rows) * cols)
+      throw std::invalid_argument("Matrix: data size does not match rows*cols");
+  }
+  static Matrix identity(int n) {
+    Matrix m(n, n);
+    for (int i = 0; i < n; ++i) m(i, i) = T(1);
+    return m;
+  }
+  int rows() const { return rows_; }
+  int cols() const { return cols_; }
+  bool square() const { return rows_ == cols_; }
+  size_t size() const { return data_.size(); }
+  T& operator()(int i, int j) { return data_[i + size_t(j) * rows_]; }
+  const T& operator()(int i, int j) const { return data_[i + size_t(j) * rows_]; }
+  T* data() { return data_.data(); }
+  const T* data() const { return data_.data(); }
+  Matrix transposed() const {
+    Matrix o(cols_, rows_);
+    for (int j = 0; j < cols_; ++j)
+      for (int i = 0; i < rows_; ++i) o(j, i) = (*this)(i, j);
+    return o;
+  }
+  double norm1() const {
+    double best = 0.0;
+    for (int j = 0; j < cols_; ++j) {
+      double s = 0.0;
+      for (int i = 0; i < rows_; ++i) s += abs_of((*this)(i, j));
+      best = std::max(best, s);
+    }
+    return best;
+  }
+  double norm_fro() const {
+    double s = 0.0;
+    for (const T& x : data_) s += abs_of(x) * abs_of(x);
+    return std::sqrt(s);
+  }
+  bool all_finite() const {
+    for (const T& x : data_)
+      if (!std::isfinite(std::real(x)) || !std::isfinite(std::imag(x))) return false;
+    return true;
+  }
+  Matrix& operator+=(const Matrix& o) {
+    same(o, "+=");
+    for (size_t i = 0; i < data_.size(); ++i) data_[i] += o.data_[i];
+    return *this;
+  }
+  Matrix& operator-=(const Matrix& o) {
+    same(o, "-=");
+    for (size_t i = 0; i < data_.size(); ++i) data_[i] -= o.data_[i];
+    return *this;
+  }
+  Matrix& operator*=(T s) {
+    for (T& x : data_) x *= s;
+    return *this;
+  }
+  friend Matrix operator+(Matrix a, const Matrix& b) { return a += b; }
+  friend Matrix operator-(Matrix a, const Matrix& b) { return a -= b; }
+  friend Matrix operator*(T s, Matrix a) { return a *= s; }
+  friend bool operator==(const Matrix& a, const Matrix& b) {
+    return a.rows_ == b.rows_ && a.cols_ == b.cols_ && a.data_ == b.data_;
+  }
+
+ private:
+  void same(const Matrix& o, const char* w) const {
+    if (rows_ != o.rows_ || cols_ != o.cols_)
+      throw std::invalid_argument(std::string("Matrix: shape mismatch in ") + w);
+  }
+  int rows_ = 0, cols_ = 0;
+  std::vector<T> data_;
+};
+
+// ------------------------------------------------------------ Tensor<T>
+
+template <typename T>
+class Tensor {
+ public:
+  Tensor() = default;
+  explicit Tensor(std::vector<int> dims) : dims_(std::move(dims)) {
+    data_.assign(checked_size(dims_), T{});
+  }
+  Tensor(std::vector<int> dims, const std::vector<T>& data)
+      : dims_(std::move(dims)), data_(data) {
+    if (data_.size() != checked_size(dims_))
+      throw std::invalid_argument("Tensor: data length != product of dims");
+  }
+  static Tensor no_init(std::vector<int> dims) {
+    Tensor t;
+    t.dims_ = std::move(dims);
+    t.data_.resize(checked_size(t.dims_));
+    return t;
+  }
+  int order() const { return int(dims_.size()); }
+  const std::vector<int>& dims() const { return dims_; }
+  int dim(int mu) const { return dims_[mu]; }
+  size_t size() const { return data_.size(); }
+  T* data() { return data_.data(); }
+  const T* data() const { return data_.data(); }
+  T& operator[](size_t i) { return data_[i]; }
+  const T& operator[](size_t i) const { return data_[i]; }
+  T& at(std::initializer_list<int> idx) { return data_[offset(idx)]; }
+  const T& at(std::initializer_list<int> idx) const { return data_[offset(idx)]; }
+  double norm_inf() const {
+    double b = 0.0;
+    for (const T& x : data_) b = std::max(b, abs_of(x));
+    return b;
+  }
+  double norm_fro() const {
+    double s = 0.0;
+    for (const T& x : data_) s += abs_of(x) * abs_of(x);
+    return std::sqrt(s);
+  }
+  bool all_finite() const {
+    for (const T& x : data_)
+      if (!std::isfinite(std::real(x)) || !std::isfinite(std::imag(x))) return false;
+    return true;
+  }
+
+ private:
+  static size_t checked_size(const std::vector<int>& d) {
+    if (d.empty()) throw std::invalid_argument("Tensor: empty dims");
+    size_t n = 1;
+    for (int x : d) {
+      if (x <= 0) throw std::invalid_argument("Tensor: nonpositive dim");
+      n *= size_t(x);
+    }
+    return n;
+  }
+  size_t offset(std::initializer_list<int> idx) const {
+    if (int(idx.size()) != order()) throw std::invalid_argument("Tensor::at: wrong index count");
+    size_t off = 0, stride = 1;
+    int mu = 0;
+    for (int i : idx) {
+      off += stride * size_t(i);
+      stride *= size_t(dims_[mu++]);
+    }
+    return off;
+  }
+  std::vector<int> dims_;
+  std::vector<T> data_;
+};
+
+template <typename T>
+std::vector<T> vec(const Tensor<T>& t) {
+  return std::vector<T>(t.data(), t.data() + t.size());
+}
+template <typename T>
+Tensor<T> unvec(const std::vector<T>& v, std::vector<int> dims) {
+  return Tensor<T>(std::move(dims), v);
+}
+template <typename T>
+void axpy(T alpha, const Tensor<T>& x, Tensor<T>& y) {
+  if (x.dims() != y.dims()) throw std::invalid_argument("axpy: shape mismatch");
+  for (size_t i = 0; i < y.size(); ++i) y[i] += alpha * x[i];
+}
+template <typename T>
+void scale(Tensor<T>& x, T alpha) {
+  for (size_t i = 0; i < x.size(); ++i) x[i] *= alpha;
+}
+template <typename T>
+Tensor<T> add_scaled(const Tensor<T>& x, T alpha, const Tensor<T>& y) {
+  if (x.dims() != y.dims()) throw std::invalid_argument("add_scaled: shape mismatch");
+  Tensor<T> z = Tensor<T>::no_init(x.dims());
+  for (size_t i = 0; i < z.size(); ++i) z[i] = x[i] + alpha * y[i];
+  return z;
+}
+template <typename T>
+double diff_norm_inf(const Tensor<T>& a, const Tensor<T>& b) {
+  if (a.dims() != b.dims()) throw std::invalid_argument("diff_norm_inf: shape mismatch");
+  double best = 0.0;
+  for (size_t i = 0; i < a.size(); ++i) best = std::max(best, abs_of(a[i] - b[i]));
+  return best;
+}
+template <typename T>
+double diff_norm_fro(const Tensor<T>& a, const Tensor<T>& b) {
+  if (a.dims() != b.dims()) throw std::invalid_argument("diff_norm_fro: shape mismatch");
+  double s = 0.0;
+  for (size_t i = 0; i < a.size(); ++i) s += abs_of(a[i] - b[i]) * abs_of(a[i] - b[i]);
+  return std::sqrt(s);
+}
+
+// ------------------------------------------------------- mode products
+
+template <typename T>
+struct KroneckerSum {
+  std::vector<Matrix<T>> factors;
+  KroneckerSum() = default;
+  explicit KroneckerSum(std::vector<Matrix<T>> fs) : factors(std::move(fs)) {
+    if (factors.empty()) throw std::invalid_argument("KroneckerSum: needs at least one factor");
+    for (size_t mu = 0; mu < factors.size(); ++mu)
+      if (!factors[mu].square())
+        throw std::invalid_argument("KroneckerSum: factor " + std::to_string(mu) +
+                                    " is not square");
+  }
+  int order() const { return int(factors.size()); }
+  std::vector<int> dims() const {
+    std::vector<int> d;
+    for (const auto& f : factors) d.push_back(f.rows());
+    return d;
+  }
+};
+
+namespace detail {
+
+template <typename T>
+void check_mode_sizes(const Tensor<T>& t, const Matrix<T>& m, int mode) {
+  if (mode < 0 || mode >= t.order())
+    throw std::invalid_argument("mode_product: mode " + std::to_string(mode) +
+                                " out of range for order " + std::to_string(t.order()));
+  if (m.cols() != t.dim(mode))
+    throw std::invalid_argument("mode_product: size mismatch on mode " + std::to_string(mode) +
+                                ": matrix has " + std::to_string(m.cols()) +
+                                " columns, tensor dim is " + std::to_string(t.dim(mode)));
+}
+
+template <typename T>
+constexpr size_t bytes_of(size_t n) {
+  return n * sizeof(T);
+}
+
+template <typename T>
+const double* dp(const T* p) {
+  return reinterpret_cast<const double*>(p);
+}
+template <typename T>
+double* dp(T* p) {
+  return reinterpret_cast<double*>(p);
+}
+
+}  // namespace detail
+
+template <typename T>
+void mode_product_into(const Tensor<T>& t, const Matrix<T>& m, int mode, Tensor<T>& out,
+                       bool accumulate = false) {
+  using namespace detail;
+  check_mode_sizes(t, m, mode);
+  if constexpr (std::is_same_v<T, double>) {
+    check(kp_host_mode_product_f64(ctx(), t.data(), t.dims().data(), t.order(), mode, m.data(),
+                                   m.rows(), m.cols(), 1.0, accumulate ? 1.0 : 0.0, out.data()));
+  } else {
+    DevBuf dt(t.data(), bytes_of<T>(t.size())), dm(m.data(), bytes_of<T>(m.size()));
+    DevBuf dout = accumulate ? DevBuf(out.data(), bytes_of<T>(out.size()))
+                             : DevBuf(bytes_of<T>(out.size()));
+    const double one[2] = {1.0, 0.0}, beta[2] = {accumulate ? 1.0 : 0.0, 0.0};
+    check(kp_mode_product_c128(ctx(), dt.d(), t.dims().data(), t.order(), mode, dm.d(), m.rows(),
+                               m.cols(), one, beta, dout.d()));
+    dout.download(out.data());
+  }
+}
+
+template <typename T>
+Tensor<T> mode_product(const Tensor<T>& t, const Matrix<T>& m, int mode) {
+  detail::check_mode_sizes(t, m, mode);
+  std::vector<int> dims = t.dims();
+  dims[mode] = m.rows();
+  Tensor<T> out = Tensor<T>::no_init(std::move(dims));
+  mode_product_into(t, m, mode, out);
+  return out;
+}
+
+namespace detail {
+template <typename T>
+Tensor<T> tucker_pref(const Tensor<T>& t, const std::vector<Matrix<T>>& ms, double pref) {
+  std::vector<const double*> hp;
+  std::vector<int> rows, od = t.dims();
+  for (size_t mu = 0; mu < ms.size(); ++mu) {
+    check_mode_sizes(t, ms[mu], int(mu));
+    hp.push_back(dp(ms[mu].data()));
+    rows.push_back(ms[mu].rows());
+    od[mu] = ms[mu].rows();
+  }
+  Tensor<T> out = Tensor<T>::no_init(od);
+  auto f = std::is_same_v<T, double> ? kp_host_tucker_f64 : kp_host_tucker_c128;
+  check(f(ctx(), dp(t.data()), t.dims().data(), t.order(), hp.data(), rows.data(), pref,
+          dp(out.data())));
+  return out;
+}
+}  // namespace detail
+
+template <typename T>
+Tensor<T> tucker(const Tensor<T>& t, const std::vector<Matrix<T>>& ms) {
+  if (int(ms.size()) != t.order()) throw std::invalid_argument("tucker: expected one factor per mode");
+  return detail::tucker_pref(t, ms, 1.0);
+}
+
+template <typename T>
+Tensor<T> kronsum_action(const Tensor<T>& t, const KroneckerSum<T>& k) {
+  using namespace detail;
+  if (int(k.factors.size()) != t.order())
+    throw std::invalid_argument("kronsum_action: expected one factor per mode");
+  std::vector<const double*> hp;
+  for (int mu = 0; mu < t.order(); ++mu) {
+    check_mode_sizes(t, k.factors[mu], mu);
+    hp.push_back(dp(k.factors[mu].data()));
+  }
+  Tensor<T> out = Tensor<T>::no_init(t.dims());
+  if constexpr (std::is_same_v<T, double>) {
+    check(kp_host_kronsum_f64(ctx(), t.data(), t.dims().data(), t.order(), hp.data(), out.data()));
+  } else {
+    DevBuf dt(t.data(), bytes_of<T>(t.size())), dout(bytes_of<T>(t.size()));
+    std::vector<DevBuf> fb;
+    std::vector<const double*> dptr;
+    for (const auto& f : k.factors) {
+      fb.emplace_back(f.data(), bytes_of<T>(f.size()));
+      dptr.push_back(fb.back().d());
+    }
+    check(kp_kronsum_c128(ctx(), dt.d(), t.dims().data(), t.order(), dptr.data(), dout.d()));
+    dout.download(out.data());
+  }
+  return out;
+}
+
+template <typename T>
+Matrix<T> multiply(const Matrix<T>& a, const Matrix<T>& b, Op opb = Op::none, bool = true) {
+  // C = A op(B) as the mode products A x_0 B (none) or A x_1 B (transpose)
+  const int k = a.cols();
+  const int bk = (opb == Op::none) ? b.rows() : b.cols();
+  if (bk != k) throw std::invalid_argument("multiply: inner dimensions differ");
+  if (opb == Op::none) {
+    Tensor<T> bt({b.rows(), b.cols()}, std::vector<T>(b.data(), b.data() + b.size()));
+    Tensor<T> c = mode_product(bt, a, 0);
+    return Matrix<T>(a.rows(), b.cols(), vec(c));
+  }
+  Tensor<T> at({a.rows(), a.cols()}, std::vector<T>(a.data(), a.data() + a.size()));
+  Tensor<T> c = mode_product(at, b, 1);
+  return Matrix<T>(a.rows(), b.rows(), vec(c));
+}
+
+// ------------------------------------------------------- matrix functions
+
+inline constexpr int kDefaultQuadNodes = 12;
+
+struct GLLRule {
+  int q = 0;
+  std::vector<double> nodes, weights;
+};
+
+inline GLLRule gll_rule(int q) {
+  GLLRule r;
+  r.q = q;
+  r.nodes.resize(std::max(q, 0));
+  r.weights.resize(std::max(q, 0));
+  detail::check(kp_gll_rule(q, r.nodes.data(), r.weights.data()));
+  return r;
+}
+
+template <typename T>
+Matrix<T> expm(const Matrix<T>& x) {
+  using namespace detail;
+  if (!x.square()) throw std::invalid_argument("expm: matrix not square");
+  if (!x.all_finite()) throw std::invalid_argument("expm: non-finite entries");
+  DevBuf dx(x.data(), bytes_of<T>(x.size())), de(bytes_of<T>(x.size()));
+  auto f = std::is_same_v<T, double> ? kp_expm_f64 : kp_expm_c128;
+  check(f(ctx(), dx.d(), x.rows(), de.d()));
+  Matrix<T> e(x.rows(), x.cols());
+  de.download(e.data());
+  return e;
+}
+
+template <typename T>
+struct PhiTable {
+  Matrix<T> base;
+  int ell_max = 0;
+  std::vector<Matrix<T>> phis;
+  int scaling_exponent = 0;
+};
+
+template <typename T>
+PhiTable<T> phiquad(const Matrix<T>& x, int ell_max, const GLLRule& rule,
+                    int forced_scaling = -1) {
+  using namespace detail;
+  if (!x.square()) throw std::invalid_argument("phiquad: matrix not square");
+  if (ell_max < 0) throw std::invalid_argument("phiquad: negative ell_max");
+  if (!x.all_finite()) throw std::invalid_argument("phiquad: non-finite entries");
+  const int n = x.rows();
+  DevBuf dx(x.data(), bytes_of<T>(x.size()));
+  DevBuf dt(bytes_of<T>(x.size() * (ell_max + 1)));
+  int s = 0;
+  auto f = std::is_same_v<T, double> ? kp_phiquad_f64 : kp_phiquad_c128;
+  check(f(ctx(), dx.d(), n, ell_max, rule.q, forced_scaling, dt.d(), &s));
+  std::vector<T> all(x.size() * (ell_max + 1));
+  dt.download(all.data());
+  PhiTable<T> tab;
+  tab.base = x;
+  tab.base *= T(std::ldexp(1.0, -s));
+  tab.ell_max = ell_max;
+  tab.scaling_exponent = s;
+  for (int j = 0; j <= ell_max; ++j)
+    tab.phis.emplace_back(n, n, std::vector<T>(all.begin() + x.size() * j,
+                                               all.begin() + x.size() * (j + 1)));
+  return tab;
+}
+template <typename T>
+PhiTable<T> phiquad(const Matrix<T>& x, int ell_max) {
+  return phiquad(x, ell_max, gll_rule(kDefaultQuadNodes));
+}
+
+// ------------------------------------------------------- split phi
+
+template <typename T>
+struct SplitPhi {
+  int ell = 0;
+  double tau = 0.0;
+  std::vector<Matrix<T>> factors;
+  double prefactor = 1.0;
+};
+
+template <typename T>
+SplitPhi<T> build_split_phi(const KroneckerSum<T>& k, double tau, int ell, const GLLRule& rule) {
+  using namespace detail;
+  if (ell < 0) throw std::invalid_argument("build_split_phi: negative ell");
+  std::vector<DevBuf> in, out;
+  std::vector<const double*> ip;
+  std::vector<double*> op;
+  std::vector<int> dims = k.dims();
+  for (int mu = 0; mu < k.order(); ++mu) {
+    int same = -1;
+    for (int m2 = 0; m2 < mu; ++m2)
+      if (k.factors[m2] == k.factors[mu]) same = m2;
+    if (same >= 0) {
+      ip.push_back(ip[same]);
+    } else {
+      in.emplace_back(k.factors[mu].data(), bytes_of<T>(k.factors[mu].size()));
+      ip.push_back(in.back().d());
+    }
+    out.emplace_back(bytes_of<T>(k.factors[mu].size()));
+    op.push_back(out.back().d());
+  }
+  double pref = 1.0;
+  auto f = std::is_same_v<T, double> ? kp_build_split_phi_f64 : kp_build_split_phi_c128;
+  check(f(ctx(), ip.data(), dims.data(), k.order(), tau, ell, rule.q, op.data(), &pref));
+  SplitPhi<T> sp;
+  sp.ell = ell;
+  sp.tau = tau;
+  sp.prefactor = pref;
+  for (int mu = 0; mu < k.order(); ++mu) {
+    Matrix<T> m(dims[mu], dims[mu]);
+    out[mu].download(m.data());
+    sp.factors.push_back(std::move(m));
+  }
+  return sp;
+}
+template <typename T>
+SplitPhi<T> build_split_phi(const KroneckerSum<T>& k, double tau, int ell) {
+  return build_split_phi(k, tau, ell, gll_rule(kDefaultQuadNodes));
+}
+
+template <typename T>
+Tensor<T> apply_split_phi(const SplitPhi<T>& sp, const Tensor<T>& v) {
+  if (int(sp.factors.size()) != v.order())
+    throw std::invalid_argument("apply_split_phi: order mismatch");
+  return detail::tucker_pref(v, sp.factors, sp.prefactor);
+}
+
+// ------------------------------------------------------- integrators
+
+enum class Method { LawsonEuler, Lawson2b, ExpEuler, ExpEulerLinearSplit, ETD2RK };
+
+inline const char* method_name(Method m) {
+  switch (m) {
+    case Method::LawsonEuler: return "lawson_euler";
+    case Method::Lawson2b: return "lawson2b";
+    case Method::ExpEuler: return "exp_euler";
+    case Method::ExpEulerLinearSplit: return "exp_euler_ls";
+    case Method::ETD2RK: return "etd2rk";
+  }
+  return "?";
+}
+inline Method parse_method(const std::string& s) {
+  for (Method m : {Method::LawsonEuler, Method::Lawson2b, Method::ExpEuler,
+                   Method::ExpEulerLinearSplit, Method::ETD2RK})
+    if (s == method_name(m)) return m;
+  throw std::invalid_argument("unknown method: " + s);
+}
+
+// Device nonlinearities (the reference's GFun is a host std::function).
+using GFun = kp_gfun;
+inline GFun g_zero() { return GFun{KP_G_ZERO, {0, 0, 0, 0}}; }
+inline GFun g_square() { return GFun{KP_G_SQUARE, {0, 0, 0, 0}}; }
+inline GFun g_const(double c) { return GFun{KP_G_CONST, {c, 0, 0, 0}}; }
+inline GFun g_allen_cahn() { return GFun{KP_G_ALLEN_CAHN, {0, 0, 0, 0}}; }
+inline GFun g_brusselator(double a, double b) { return GFun{KP_G_BRUSSELATOR, {a, b, 0, 0}}; }
+inline GFun g_nls() { return GFun{KP_G_NLS, {0, 0, 0, 0}}; }
+
+template <typename T = double>
+struct ProblemSpecT {
+  KroneckerSum<T> K;
+  GFun g = g_zero();
+  Tensor<T> u0;
+  double t0 = 0.0;
+  double t_final = 1.0;
+};
+using ProblemSpec = ProblemSpecT<double>;
+
+struct StepperConfig {
+  Method method = Method::ExpEuler;
+  long n_steps = 1;
+  int quad_nodes = kDefaultQuadNodes;
+};
+
+template <typename T = double>
+struct IntegrateResultT {
+  Tensor<T> final;
+  double wallclock_s = 0.0;  // includes factor precomputation
+  double loop_s = 0.0;       // device time of the time loop
+};
+using IntegrateResult = IntegrateResultT<double>;
+
+template <typename T>
+IntegrateResultT<T> integrate(const ProblemSpecT<T>& p, const StepperConfig& c) {
+  using namespace detail;
+  if (c.n_steps <= 0) throw std::invalid_argument("integrate: n_steps must be positive");
+  if (!(p.t_final > p.t0)) throw std::invalid_argument("integrate: empty time interval");
+  const auto w0 = std::chrono::steady_clock::now();
+  std::vector<const double*> hp;
+  for (const auto& f : p.K.factors) hp.push_back(dp(f.data()));
+  IntegrateResultT<T> r;
+  r.final = Tensor<T>::no_init(p.u0.dims());
+  long dv = 0;
+  double loop = 0.0;
+  auto f = std::is_same_v<T, double> ? kp_host_integrate_f64 : kp_host_integrate_c128;
+  const int rc = f(ctx(), int(c.method), dp(p.u0.data()), p.u0.dims().data(), p.u0.order(),
+                   hp.data(), &p.g, p.t0, p.t_final, c.n_steps, c.quad_nodes,
+                   dp(r.final.data()), &dv, &loop);
+  check(rc, dv);
+  r.loop_s = loop;
+  r.wallclock_s =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+  return r;
+}
+
+namespace detail {
+template <typename T>
+Tensor<T> step(Method m, const Tensor<T>& u, double t, double tau, const KroneckerSum<T>* k,
+               const GFun& g, const std::vector<Matrix<T>>& f1, double pref1,
+               const std::vector<Matrix<T>>* f2, double pref2) {
+  auto upload_all = [](const std::vector<Matrix<T>>& ms, std::vector<DevBuf>& keep) {
+    std::vector<const double*> p;
+    for (const auto& x : ms) {
+      keep.emplace_back(x.data(), bytes_of<T>(x.size()));
+      p.push_back(keep.back().d());
+    }
+    return p;
+  };
+  std::vector<DevBuf> keep;
+  DevBuf du(u.data(), bytes_of<T>(u.size())), dout(bytes_of<T>(u.size()));
+  auto p1 = upload_all(f1, keep);
+  std::vector<const double*> p2, pk;
+  if (f2) p2 = upload_all(*f2, keep);
+  if (k) pk = upload_all(k->factors, keep);
+  auto f = std::is_same_v<T, double> ? kp_step_f64 : kp_step_c128;
+  check(f(ctx(), int(m), du.d(), u.dims().data(), u.order(), t, tau, k ? pk.data() : nullptr,
+          p1.data(), pref1, f2 ? p2.data() : nullptr, pref2, &g, dout.d()));
+  Tensor<T> out = Tensor<T>::no_init(u.dims());
+  dout.download(out.data());
+  return out;
+}
+}  // namespace detail
+
+template <typename T>
+Tensor<T> lawson_euler_step(const Tensor<T>& u, double t, double tau, const GFun& g,
+                            const std::vector<Matrix<T>>& exp_factors) {
+  return detail::step<T>(Method::LawsonEuler, u, t, tau, nullptr, g, exp_factors, 1.0, nullptr,
+                         1.0);
+}
+template <typename T>
+Tensor<T> lawson2b_step(const Tensor<T>& u, double t, double tau, const GFun& g,
+                        const std::vector<Matrix<T>>& exp_factors) {
+  return detail::step<T>(Method::Lawson2b, u, t, tau, nullptr, g, exp_factors, 1.0, nullptr, 1.0);
+}
+template <typename T>
+Tensor<T> exp_euler_step(const Tensor<T>& u, double t, double tau, const KroneckerSum<T>& k,
+                         const GFun& g, const SplitPhi<T>& phi1) {
+  return detail::step<T>(Method::ExpEuler, u, t, tau, &k, g, phi1.factors, phi1.prefactor,
+                         nullptr, 1.0);
+}
+template <typename T>
+Tensor<T> exp_euler_linear_split_step(const Tensor<T>& u, double t, double tau, const GFun& g,
+                                      const std::vector<Matrix<T>>& exp_factors,
+                                      const SplitPhi<T>& phi1) {
+  return detail::step<T>(Method::ExpEulerLinearSplit, u, t, tau, nullptr, g, exp_factors, 1.0,
+                         &phi1.factors, phi1.prefactor);
+}
+template <typename T>
+Tensor<T> etd2rk_step(const Tensor<T>& u, double t, double tau, const KroneckerSum<T>& k,
+                      const GFun& g, const SplitPhi<T>& phi1, const SplitPhi<T>& phi2) {
+  return detail::step<T>(Method::ETD2RK, u, t, tau, &k, g, phi1.factors, phi1.prefactor,
+                         &phi2.factors, phi2.prefactor);
+}
+
+}  // namespace kronphi

@@ -1,0 +1,164 @@
+// C++ drop-in check: reference-style test cases written against the
+// reference's headers/names ("kronphi/..."), compiled against
+// include/kronphi_b200 and run on the GPU (tests/test_cpp_api.py).
+// Cases restate /root/reference/proj/tests/test_tensor.cpp,
+// test_matrix_functions.cpp, test_split_phi.cpp, test_integrators.cpp.
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <string>
+
+#include "kronphi/integrators.hpp"
+#include "kronphi/matrix_functions.hpp"
+#include "kronphi/mode_product.hpp"
+#include "kronphi/split_phi.hpp"
+#include "kronphi/tensor.hpp"
+
+using namespace kronphi;
+
+static int failures = 0;
+#define CHECK(c)                                                        \
+  do {                                                                  \
+    if (!(c)) {                                                         \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);          \
+      ++failures;                                                       \
+    }                                                                   \
+  } while (0)
+
+static std::mt19937_64 rng(777);
+static double urand() { return std::uniform_real_distribution<double>(-1, 1)(rng); }
+static Tensor<double> random_tensor(std::vector<int> dims) {
+  Tensor<double> t(std::move(dims));
+  for (size_t i = 0; i < t.size(); ++i) t[i] = urand();
+  return t;
+}
+static Matrix<double> random_matrix(int r, int c) {
+  Matrix<double> m(r, c);
+  for (size_t i = 0; i < m.size(); ++i) m.data()[i] = urand();
+  return m;
+}
+static Matrix<double> random_stable(int n) {
+  Matrix<double> m = random_matrix(n, n);
+  const double s = m.norm1();
+  for (int i = 0; i < n; ++i) m(i, i) -= s;
+  return m;
+}
+
+int main() {
+  {  // row permutation KAT (test_tensor.cpp:89-99)
+    const Tensor<double> t({2, 2}, {1, 3, 2, 4});
+    Matrix<double> m(2, 2);
+    m(0, 1) = 1;
+    m(1, 0) = 1;
+    const Tensor<double> got = mode_product(t, m, 0);
+    CHECK(got.at({0, 0}) == 3 && got.at({0, 1}) == 4 && got.at({1, 0}) == 1 && got.at({1, 1}) == 2);
+  }
+  {  // identity bit-exact (test_tensor.cpp:101-108)
+    const Tensor<double> t = random_tensor({3, 4, 5});
+    for (int mode = 0; mode < 3; ++mode)
+      CHECK(diff_norm_inf(mode_product(t, Matrix<double>::identity(t.dim(mode)), mode), t) == 0.0);
+  }
+  {  // sizing error names the mode (test_tensor.cpp:118-124)
+    const Tensor<double> t = random_tensor({3, 4, 5});
+    bool ok = false;
+    try {
+      mode_product(t, random_matrix(6, 9), 1);
+    } catch (const std::invalid_argument& e) {
+      ok = std::string(e.what()).find("mode 1") != std::string::npos;
+    }
+    CHECK(ok);
+  }
+  {  // tucker in 2d is M1 T M2^T (test_tensor.cpp:159-169)
+    const Tensor<double> t = random_tensor({3, 4});
+    const Matrix<double> m1 = random_matrix(5, 3), m2 = random_matrix(6, 4);
+    const Tensor<double> got = tucker(t, {m1, m2});
+    const Matrix<double> tm(3, 4, vec(t));
+    const Matrix<double> want = multiply(multiply(m1, tm), m2, Op::transpose);
+    double worst = 0;
+    for (int j = 0; j < 6; ++j)
+      for (int i = 0; i < 5; ++i) worst = std::max(worst, std::abs(got.at({i, j}) - want(i, j)));
+    CHECK(worst < 1e-13);
+  }
+  {  // kronsum zero factors (test_tensor.cpp:202-215)
+    const Tensor<double> t3 = random_tensor({2, 3, 4});
+    std::vector<Matrix<double>> zeros;
+    for (int d : t3.dims()) zeros.push_back(Matrix<double>(d, d));
+    CHECK(kronsum_action(t3, KroneckerSum<double>(zeros)).norm_inf() == 0.0);
+  }
+  {  // expm / phiquad closed forms (test_matrix_functions.cpp:56-80, :145-174)
+    CHECK((expm(Matrix<double>(3, 3)) - Matrix<double>::identity(3)).norm1() == 0.0);
+    Matrix<double> x(1, 1);
+    x(0, 0) = 1.0;
+    const auto tab = phiquad(x, 2);
+    CHECK(std::abs(tab.phis[1](0, 0) - (std::exp(1.0) - 1.0)) < 1e-13);
+    CHECK(std::abs(tab.phis[2](0, 0) - (std::exp(1.0) - 2.0)) < 1e-13);
+    x(0, 0) = 2.0;
+    CHECK(phiquad(x, 1).scaling_exponent == 2);
+  }
+  {  // prefactors (test_split_phi.cpp:66-75)
+    const KroneckerSum<double> k3({random_stable(2), random_stable(3), random_stable(2)});
+    CHECK(build_split_phi(k3, 0.1, 2).prefactor == 4.0);
+    CHECK(build_split_phi(k3, 0.1, 1).prefactor == 1.0);
+  }
+  {  // etd2rk with K = 0 is the trapezoidal rule (test_integrators.cpp:282-296)
+    const KroneckerSum<double> kz({Matrix<double>(2, 2)});
+    const Tensor<double> u = random_tensor({2});
+    const double tau = 0.21;
+    const Tensor<double> got = etd2rk_step(u, 0.0, tau, kz, g_square(), build_split_phi(kz, tau, 1),
+                                           build_split_phi(kz, tau, 2));
+    for (int i = 0; i < 2; ++i) {
+      const double g0 = u[i] * u[i], st = u[i] + tau * g0;
+      CHECK(std::abs(got[i] - (st + tau * 0.5 * (st * st - g0))) < 1e-14);
+    }
+  }
+  {  // integrate: one step equals the step function bitwise (test_integrators.cpp:350-371)
+    ProblemSpec p;
+    p.K = KroneckerSum<double>({random_stable(5), random_stable(6)});
+    p.g = g_square();
+    p.u0 = random_tensor({5, 6});
+    p.t_final = 0.4;
+    StepperConfig c;
+    c.method = Method::ETD2RK;
+    c.n_steps = 1;
+    const auto r = integrate(p, c);
+    const auto want = etd2rk_step(p.u0, 0.0, 0.4, p.K, p.g, build_split_phi(p.K, 0.4, 1),
+                                  build_split_phi(p.K, 0.4, 2));
+    CHECK(diff_norm_inf(r.final, want) == 0.0);
+    CHECK(r.wallclock_s >= r.loop_s);
+  }
+  {  // divergence (test_integrators.cpp:404-422)
+    ProblemSpec p;
+    p.K = KroneckerSum<double>({Matrix<double>(2, 2)});
+    p.g = g_square();
+    p.u0 = Tensor<double>({2}, {1e100, 1e100});
+    p.t_final = 10.0;
+    StepperConfig c;
+    c.method = Method::LawsonEuler;
+    c.n_steps = 10;
+    bool caught = false;
+    try {
+      integrate(p, c);
+    } catch (const DivergenceError& e) {
+      caught = e.step() >= 1 && std::string(e.what()).find("step") != std::string::npos;
+    }
+    CHECK(caught);
+  }
+  {  // complex tucker vs the nested-loop contraction
+    using C = std::complex<double>;
+    Tensor<C> t({3, 4});
+    for (size_t i = 0; i < t.size(); ++i) t[i] = C(urand(), urand());
+    Matrix<C> m(5, 3);
+    for (size_t i = 0; i < m.size(); ++i) m.data()[i] = C(urand(), urand());
+    const Tensor<C> got = mode_product(t, m, 0);
+    double worst = 0;
+    for (int j = 0; j < 4; ++j)
+      for (int i = 0; i < 5; ++i) {
+        C acc{};
+        for (int p = 0; p < 3; ++p) acc += m(i, p) * t.at({p, j});
+        worst = std::max(worst, std::abs(got.at({i, j}) - acc));
+      }
+    CHECK(worst < 1e-14);
+  }
+  std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+  return failures ? 1 : 0;
+}
