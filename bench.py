@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--n", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-integrators", action="store_true",
+                    help="skip the integrator-config block (steps/s of configs 0,2,3,4)")
     return ap.parse_args()
 
 
@@ -59,6 +61,58 @@ def config(n, world):
             "dims": [n, n, n], "factor": "L = phi_1(1e-3 * fd_operator_1d(n, 1.0, 0))",
             "seed": SEED, "parallelism": "replicas" if world > 1 else "single",
             "l2": "inputs 1 GiB > 126 MB L2 (no flush needed)"}
+
+
+INTEGRATOR_CONFIGS = [  # (tag, builder kwargs) -- BASELINE.json configs 0, 2, 3, 4
+    ("ac2d_expeuler_128sq", "ac2d", {}),
+    ("ac3d_etd2rk_128cube", "ac3d", {}),
+    ("brusselator_etd2rk_256cube_x2", "brusselator", {"method": "etd2rk"}),
+    ("brusselator_lawson2b_256cube_x2", "brusselator", {"method": "lawson2b"}),
+    ("nls_expeuler_512cube_c128", "nls", {"method": "exp_euler"}),
+    ("nls_etd2rk_512cube_c128", "nls", {"method": "etd2rk"}),
+]
+
+
+def tucker_equivalents(method):
+    """Per step, dense Kronecker sum counted as one Tucker."""
+    return {"exp_euler": 2, "etd2rk": 3, "lawson2b": 2, "lawson_euler": 1,
+            "exp_euler_ls": 2}[method]
+
+
+def run_integrators(kp, peak):
+    """Device-resident integrate() of each config: steps/s of the time loop
+    (CUDA events inside the library), factor build excluded (reported)."""
+    from paper_2304_02327_b200 import problems
+    from paper_2304_02327_b200.integrators import _upload_factors
+    out = {}
+    for tag, builder, kw in INTEGRATOR_CONFIGS:
+        c = getattr(problems, builder)(**kw)
+        ud = kp.to_device(c.u0)
+        K = _upload_factors(c.K)
+        spec = kp.ProblemSpec(K, c.g, ud, 0.0, c.t_final)
+        m = kp.parse_method(c.method)
+        note = None
+        t0 = time.perf_counter()
+        try:
+            r = kp.integrate(spec, kp.StepperConfig(m, c.n_steps))
+            loop, wall = r.loop_s, r.wallclock_s
+        except kp.DivergenceError as e:
+            loop, wall = e.loop_s, time.perf_counter() - t0
+            note = (f"diverged at step {e.step} (as the reference does: split exp-Euler/ETD2RK "
+                    "amplify |1+prod phi1(i t_mu) i sum t_mu| > 1 at tau*||A_mu|| ~ 2; DESIGN.md)")
+        cplx = np.iscomplexobj(c.u0)
+        spatial = [d for d, a in zip(c.u0.shape, c.K) if np.any(a)]
+        species = int(np.prod(c.u0.shape)) // int(np.prod(spatial))
+        fl = tucker_equivalents(c.method) * species * (8.0 if cplx else 2.0) * \
+            float(np.prod(spatial)) * sum(spatial)
+        sps = c.n_steps / loop
+        out[tag] = {"method": c.method, "dims": list(c.u0.shape), "dtype": "c128" if cplx else "f64",
+                    "tau": c.tau, "steps": c.n_steps, "steps_per_s": sps,
+                    "loop_ms": loop * 1e3, "setup_plus_loop_ms": wall * 1e3,
+                    "tflops": fl * sps / 1e12, "frac_of_fp64_peak": fl * sps / 1e12 / peak,
+                    "note": note}
+        del ud, K, spec
+    return out
 
 
 def make_inputs(n):
@@ -273,6 +327,12 @@ def main():
         except Exception:
             traffic = None
 
+    integ = None
+    if not args.no_integrators:
+        del v_d, out_d
+        torch.cuda.empty_cache()
+        integ = run_integrators(kp, peak)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -293,7 +353,7 @@ def main():
                              "algorithmic": "2*N*sum(n_mu) = 412.3 GFLOP per Tucker, "
                                             "137.4 GFLOP per mode-product launch"},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clk.summary()}
+                "clocks": clk.summary(), "integrators": integ}
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

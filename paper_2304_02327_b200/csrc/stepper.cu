@@ -24,6 +24,7 @@
 // counter) and reported with the reference's message and step index.
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -153,6 +154,7 @@ class Integrator {
   std::vector<char> a_active;
   FactorSet f1, f2;
   std::vector<double*> owned;
+  long diverged_at = 0;  // first non-finite step of the last run() (0 = none)
 
   Integrator(kp_ctx* c, int m, bool cp, const std::vector<int>& dv, const double* const* as,
              const kp_gfun& gf, double tau_)
@@ -533,12 +535,7 @@ class Integrator {
     KP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    if (hb[1] != INT_MAX) {  // DivergenceError(n+1, t+tau), inc/integrators.hpp:86-97,364
-      const long k = hb[1];
-      throw divergence_error("state became non-finite at step " + std::to_string(k) +
-                                 " (t = " + std::to_string(t0 + double(k) * tau) + ")",
-                             k);
-    }
+    diverged_at = (hb[1] != INT_MAX) ? long(hb[1]) : 0;
     return ms * 1e-3;
   }
 };
@@ -674,8 +671,15 @@ int integrate_impl(kp_ctx* ctx, bool cplx, int method, double* u, const int* dim
         const double tau = (t_final - t0) / double(n_steps);
         Integrator it(ctx, method, cplx, dv, as, *g, tau);
         it.setup(q);
-        const double sec = it.run(u, t0, n_steps, true);
+        static const bool no_graph = getenv("KP_NO_GRAPH") != nullptr;  // debugging aid
+        const double sec = it.run(u, t0, n_steps, !no_graph);
         if (loop_seconds) *loop_seconds = sec;
+        if (it.diverged_at) {  // DivergenceError(n+1, t+tau), inc/integrators.hpp:86-97,364
+          const long k = it.diverged_at;
+          throw divergence_error("state became non-finite at step " + std::to_string(k) +
+                                     " (t = " + std::to_string(t0 + double(k) * tau) + ")",
+                                 k);
+        }
       },
       diverged_step);
 }

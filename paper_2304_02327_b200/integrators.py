@@ -356,7 +356,11 @@ def integrate(p: ProblemSpec, c: StepperConfig) -> IntegrateResult:
         rc = f(ctx.h, int(c.method), out.data_ptr(), ints(dims), len(dims),
                ptr_array([x.data_ptr() for x in fs]), C.byref(p.g), float(p.t0),
                float(p.t_final), int(c.n_steps), int(c.quad_nodes), C.byref(dv), C.byref(loop))
-    check(rc, step=dv.value)
+    try:
+        check(rc, step=dv.value)
+    except DivergenceError as e:
+        e.loop_s = loop.value  # the loop ran to the end; its device time is still valid
+        raise
     return IntegrateResult(out, time.perf_counter() - t_start, loop.value)
 
 

@@ -212,3 +212,27 @@ def test_device_integrate_stays_on_device(kp, port):
                        kp.StepperConfig(kp.Method.ETD2RK, cfg.n_steps))
     assert res.final.is_cuda and res.loop_s > 0
     assert rel2(kp.to_host(res.final), oracle_run(port, cfg)) < TOL
+
+
+def test_divergence_step_matches_oracle(kp, port):
+    """The BASELINE NLS config (512^3, tau = 1e-3) makes tau*||A_mu|| ~ 2 per
+    direction, where the split exponential Euler amplifies high frequencies
+    (|1 + phi1(i t1) phi1(i t2) i(t1 + t2)| up to ~2.3): the run diverges, in
+    the reference as here.  A 2-D 64^2 analogue (same h = 1/32) must report
+    the same first non-finite step on both sides."""
+    import pyoracle
+    n = 64
+    h = 2.0 / n
+    A = np.asfortranarray(0.5j * pyoracle.periodic_laplacian_1d(n, h))
+    r = rng(11)
+    x = -1.0 + h * np.arange(n)
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    u0 = np.asfortranarray(np.exp(-(X * X + Y * Y) * 8.0) + 0.01 * (r.standard_normal((n, n)) +
+                                                                    1j * r.standard_normal((n, n))))
+    with pytest.raises(pyoracle.Divergence) as eo:
+        port.integrate("exp_euler", u0, [A, A], pyoracle.gfun(pyoracle.G_NLS), 0.0, 0.2, 200)
+    with pytest.raises(kp.DivergenceError) as eg:
+        kp.integrate_config("exp_euler", u0, [A, A], kp.G.nls(), 0.0, 0.2, 200)
+    so = int(str(eo.value).split("step ")[1].split(" ")[0])
+    assert eg.value.step == so
+    assert eg.value.loop_s > 0
