@@ -448,20 +448,35 @@ void launch_gemm(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int cplx)
   const long long tiles128 =
       (long long)((p.M + 127) / 128) * ((p.N + 127) / 128) * p.batch;
   const bool few = tiles128 < ctx->num_sms;
-  // 0: 128x128 (8 warps 64x32), 1: 128x64, 2: 64x128, 3: 64x64, 4: 128x128 (16 warps 32x32)
+  // Tile menu: 0: 128x128 (8 warps 64x32), 1: 128x64, 2: 64x128, 3: 64x64,
+  // 4: 128x128 (16 warps 32x32), 5: 32x32, 6: 64x32, 7: 32x64 (4 warps each).
+  // Chosen from the measured sweep (profiles/gemm_tiles_r01.txt): small tiles
+  // (many co-resident CTAs hide latency, fewer idle slots in the last wave)
+  // win until the problem is large; long K (d=2, n >= 1024) favours big tiles.
   (void)few;
-  int tile = 3;
-  if (kcontig && !bm_small && tiles128 * 2 >= ctx->num_sms) tile = 1;
+  (void)bm_small;
+  (void)bn_small;
+  const long long tiles64 = (long long)((p.M + 63) / 64) * ((p.N + 63) / 64) * p.batch;
+  int tile;
+  if (tiles64 * 2 < ctx->num_sms)
+    tile = 5;
+  else if (kcontig)
+    tile = (p.K >= 1024) ? 1 : (p.K <= 128 ? 5 : 7);
+  else
+    tile = (tiles64 >= 48LL * ctx->num_sms || p.K >= 1024) ? 3 : 6;
   static const int forced = [] {  // benchmarking override
     const char* v = getenv("KP_GEMM_TILE");
     return v ? atoi(v) : -1;
   }();
-  if (forced >= 0 && forced <= 4) tile = forced;
+  if (forced >= 0 && forced <= 7) tile = forced;
   switch (tile) {
     case 0: launch_layout<128, 128, 2, 4>(ctx, p, e, kcontig, vec2, cplx, half); break;
     case 1: launch_layout<128, 64, 4, 2>(ctx, p, e, kcontig, vec2, cplx, half); break;
     case 2: launch_layout<64, 128, 2, 4>(ctx, p, e, kcontig, vec2, cplx, half); break;
     case 4: launch_layout<128, 128, 4, 4>(ctx, p, e, kcontig, vec2, cplx, half); break;
+    case 5: launch_layout<32, 32, 2, 2>(ctx, p, e, kcontig, vec2, cplx, half); break;
+    case 6: launch_layout<64, 32, 2, 2>(ctx, p, e, kcontig, vec2, cplx, half); break;
+    case 7: launch_layout<32, 64, 2, 2>(ctx, p, e, kcontig, vec2, cplx, half); break;
     default: launch_layout<64, 64, 2, 2>(ctx, p, e, kcontig, vec2, cplx, half); break;
   }
 }
