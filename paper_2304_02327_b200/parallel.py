@@ -1,0 +1,308 @@
+"""Slab-sharded integrators across the GPUs of one node.
+
+Partition: the last spatial mode n_d is split into P contiguous slabs (in the
+column-major layout a slab is a contiguous run of n_d/P planes per species).
+Modes 1..d-1 and the pointwise g are local.  Mode d needs every slab: the
+state is re-partitioned along mode d-1 by an all-to-all "pencil transpose"
+(torch.distributed over NCCL/NVLink on GPUs, gloo in the CPU tests), mode d
+is applied locally, and the result goes back.  Every output entry is computed
+from the same inputs in the same k order as on one GPU, so the sharded run is
+bit-identical to the single-GPU one (tests/test_parallel.py checks this on
+CPU with world size 2; the GPU backend reuses the single-GPU kernels).
+
+Operations per step (unfused, same rounding as the fused single-GPU path):
+  ExpEuler : kronsum (3 transposes) + Tucker (2)
+  ETD2RK   : kronsum (3) + Tucker (2) + Tucker (2)
+  Lawson2b : 2 Tuckers over the stacked pair (2)
+The transposes move N_local*(P-1)/P entries each; DESIGN.md 7 has the model.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import List, Optional
+
+import numpy as np
+
+try:
+    import torch
+    import torch.distributed as dist
+except Exception:  # pragma: no cover
+    torch = None
+    dist = None
+
+
+# ------------------------------------------------------------------ layout
+
+@dataclass
+class Layout:
+    """Column-major local tensor viewed as (A, B, C, S):
+    A = prod(n_1..n_{d-2}), B = n_{d-1} (or its pencil share), C = n_d share,
+    S = species (1 if none).  `slab` splits C, `pencil` splits B."""
+    A: int
+    B: int
+    C: int
+    S: int
+    P: int
+
+    @staticmethod
+    def of(spatial, species, P):
+        *lead, nb, nc = ([1] + list(spatial)) if len(spatial) == 1 else list(spatial)
+        A = int(np.prod(lead)) if lead else 1
+        if nc % P or nb % P:
+            raise ValueError(f"slab sharding needs n_(d-1) and n_d divisible by P={P}")
+        return Layout(A, nb, nc, species, P)
+
+    def slab_dims(self, spatial, species):
+        d = list(spatial[:-1]) + [spatial[-1] // self.P]
+        return d + ([species] if species > 1 else [])
+
+    def pencil_dims(self, spatial, species):
+        d = list(spatial[:-2]) + [spatial[-2] // self.P, spatial[-1]]
+        return d + ([species] if species > 1 else [])
+
+
+def slab_to_pencil(x, lay: Layout, comm):
+    """x: flat local slab (A, B, C/P... as column-major (A, B, Cl, S)) ->
+    flat local pencil (A, B/P, C, S)."""
+    A, B, C, S, P = lay.A, lay.B, lay.C, lay.S, lay.P
+    Cl, Bp = C // P, B // P
+    send = x.view(S, Cl, P, Bp, A).permute(2, 0, 1, 3, 4).contiguous().view(-1)
+    recv = torch.empty_like(send)
+    comm.all_to_all(recv, send)
+    return recv.view(P, S, Cl, Bp, A).permute(1, 0, 2, 3, 4).contiguous().view(-1)
+
+
+def pencil_to_slab(y, lay: Layout, comm):
+    A, B, C, S, P = lay.A, lay.B, lay.C, lay.S, lay.P
+    Cl, Bp = C // P, B // P
+    send = y.view(S, P, Cl, Bp, A).permute(1, 0, 2, 3, 4).contiguous().view(-1)
+    recv = torch.empty_like(send)
+    comm.all_to_all(recv, send)
+    return recv.view(P, S, Cl, Bp, A).permute(1, 2, 0, 3, 4).contiguous().view(-1)
+
+
+class Comm:
+    """Equal-split all-to-all on a torch.distributed group (NCCL on GPUs)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.P = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def all_to_all(self, recv, send):
+        if self.P == 1:
+            recv.copy_(send)
+            return
+        if torch.is_complex(send):
+            dist.all_to_all_single(torch.view_as_real(recv), torch.view_as_real(send),
+                                   group=self.group)
+        else:
+            dist.all_to_all_single(recv, send, group=self.group)
+
+
+# ----------------------------------------------------------------- backends
+
+class CudaBackend:
+    """Local compute through the C ABI (the single-GPU kernels)."""
+
+    def __init__(self, device=None):
+        from . import _lib
+        from ._lib import check, ints
+        self.check, self.ints = check, ints
+        dev = torch.cuda.current_device() if device is None else device
+        self.ctx = _lib.default_context(dev)
+        self.device = torch.device("cuda", dev)
+
+    def _sync_stream(self):
+        self.ctx.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def mode_product(self, t, dims, mode, m, alpha, beta, out):
+        import ctypes as C
+        self._sync_stream()
+        lib = self.ctx.lib
+        if torch.is_complex(t):
+            a2 = (C.c_double * 2)(alpha, 0.0)
+            b2 = (C.c_double * 2)(beta, 0.0)
+            self.check(lib.kp_mode_product_c128(self.ctx.h, t.data_ptr(), self.ints(dims),
+                                                len(dims), mode, m.data_ptr(), m.shape[0],
+                                                m.shape[1], a2, b2, out.data_ptr()))
+        else:
+            self.check(lib.kp_mode_product_f64(self.ctx.h, t.data_ptr(), self.ints(dims),
+                                               len(dims), mode, m.data_ptr(), m.shape[0],
+                                               m.shape[1], float(alpha), float(beta),
+                                               out.data_ptr()))
+
+    def eval_g(self, g, u, dims, out):
+        import ctypes as C
+        self._sync_stream()
+        f = self.ctx.lib.kp_eval_g_c128 if torch.is_complex(u) else self.ctx.lib.kp_eval_g_f64
+        self.check(f(self.ctx.h, C.byref(g), 0.0, u.data_ptr(), self.ints(dims), len(dims),
+                     out.data_ptr()))
+
+    def fma(self, alpha, x, y, out):
+        """out = fma(alpha, x, y) elementwise (componentwise for complex)."""
+        self._sync_stream()
+        n = x.numel() * (2 if torch.is_complex(x) else 1)
+        self.check(self.ctx.lib.kp_add_scaled_f64(self.ctx.h, n, y.data_ptr(), float(alpha),
+                                                  x.data_ptr(), out.data_ptr()))
+
+
+# --------------------------------------------------------------- integrator
+
+class ShardedIntegrator:
+    """integrate() (inc/integrators.hpp:219-373) with the state slab-sharded
+    along the last spatial mode.  `factors`: dict method-part -> list of
+    (n x n) torch tensors on this rank's device, identical on every rank."""
+
+    def __init__(self, backend, comm, method, spatial, species, K, g, tau, f1, pref1, f2=None,
+                 pref2=1.0, fold1=1.0, fold2=1.0):
+        self.be, self.comm = backend, comm
+        self.method = method
+        self.spatial = list(spatial)
+        self.S = species
+        self.K = K
+        self.g = g
+        self.tau = tau
+        self.f1, self.f2 = f1, f2
+        self.pref1, self.pref2 = pref1, pref2
+        self.fold1, self.fold2 = fold1, fold2
+        self.lay = Layout.of(self.spatial, species, comm.P)
+        self.sd = self.lay.slab_dims(self.spatial, species)
+        self.pd = self.lay.pencil_dims(self.spatial, species)
+        self.d = len(self.spatial)
+
+    # y = ((pref x) x_1 F_1 ... x_d F_d) * fold ; x, y in slab layout
+    def tucker(self, x, fs, pref, fold):
+        d = self.d
+        cur, dims = x, self.sd
+        for mu in range(d - 1):
+            out = torch.empty_like(cur)
+            self.be.mode_product(cur, dims, mu, fs[mu], pref if mu == 0 else 1.0, 0.0, out)
+            cur = out
+        cp = slab_to_pencil(cur, self.lay, self.comm)
+        out = torch.empty_like(cp)
+        alpha = (pref if d == 1 else 1.0) * fold
+        self.be.mode_product(cp, self.pd, d - 1, fs[d - 1], alpha, 0.0, out)
+        return out  # pencil layout
+
+    # r = K u + g(u); u in slab layout (and u_p = its pencil copy); r in pencil layout
+    def kronsum_g(self, u, u_p):
+        d = self.d
+        r = torch.empty_like(u)
+        for mu in range(d - 1):
+            self.be.mode_product(u, self.sd, mu, self.K[mu], 1.0, 0.0 if mu == 0 else 1.0, r)
+        r_p = slab_to_pencil(r, self.lay, self.comm) if d > 1 else r
+        self.be.mode_product(u_p, self.pd, d - 1, self.K[d - 1], 1.0, 1.0 if d > 1 else 0.0, r_p)
+        gu = torch.empty_like(u_p)
+        self.be.eval_g(self.g, u_p, self.pd, gu)
+        return r_p + gu  # exact IEEE add, as the fused EPI_ADD_G
+
+    def step(self, u):
+        """u (slab) -> u' (slab)."""
+        tau = self.tau
+        m = self.method
+        if m in ("exp_euler", "etd2rk"):
+            u_p = slab_to_pencil(u, self.lay, self.comm)
+            r_p = self.kronsum_g(u, u_p)
+            r = pencil_to_slab(r_p, self.lay, self.comm)
+            y1 = self.tucker(r, self.f1, self.pref1, self.fold1)          # pencil
+            stage = torch.empty_like(y1)
+            self.be.fma(tau, y1, u_p, stage)                              # u + tau*SP1(r)
+            if m == "exp_euler":
+                return pencil_to_slab(stage, self.lay, self.comm)
+            gs, gu = torch.empty_like(stage), torch.empty_like(stage)
+            self.be.eval_g(self.g, stage, self.pd, gs)
+            self.be.eval_g(self.g, u_p, self.pd, gu)
+            dd = pencil_to_slab(gs - gu, self.lay, self.comm)
+            y2 = self.tucker(dd, self.f2, self.pref2, self.fold2)
+            out = torch.empty_like(y2)
+            self.be.fma(tau, y2, stage, out)                              # stage + tau*SP2(d)
+            return pencil_to_slab(out, self.lay, self.comm)
+        if m in ("lawson_euler", "lawson2b"):
+            gn = torch.empty_like(u)
+            self.be.eval_g(self.g, u, self.sd, gn)
+            w = torch.empty_like(u)
+            self.be.fma(tau, gn, u, w)
+            stage = self.tucker(w, self.f1, 1.0, self.fold1)
+            if m == "lawson_euler":
+                return pencil_to_slab(stage, self.lay, self.comm)
+            w2 = torch.empty_like(u)
+            self.be.fma(0.5 * tau, gn, u, w2)
+            out = self.tucker(w2, self.f1, 1.0, self.fold1)
+            gs = torch.empty_like(stage)
+            self.be.eval_g(self.g, stage, self.pd, gs)
+            res = torch.empty_like(out)
+            self.be.fma(0.5 * tau, gs, out, res)
+            return pencil_to_slab(res, self.lay, self.comm)
+        raise ValueError(f"sharded integrate: unsupported method {m}")
+
+    def run(self, u, n_steps):
+        for k in range(n_steps):
+            u = self.step(u)
+            bad = torch.tensor([0.0 if bool(torch.isfinite(u).all()) else 1.0], device=u.device)
+            if self.comm.P > 1:
+                dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+            if bad.item() > 0:
+                from ._lib import DivergenceError
+                raise DivergenceError(3, f"state became non-finite at step {k + 1} "
+                                         f"(t = {(k + 1) * self.tau:f})", k + 1)
+        return u
+
+
+# ------------------------------------------------------------ factor set-up
+
+def split_factors(kp, K, tau, ell):
+    """Device build of phi_ell(tau A_mu) (build_split_phi) and the scalar
+    folding of factors that are exactly c*I (the stacked species mode)."""
+    sp = kp.build_split_phi(K, tau, ell)
+    fs, fold, active = [], 1.0, []
+    for f in sp.factors:
+        h = kp.to_host(f) if hasattr(f, "is_cuda") else np.asarray(f)
+        n = h.shape[0]
+        if n <= 64 and np.array_equal(h, h[0, 0] * np.eye(n)):
+            fold *= float(np.real(h[0, 0]))
+            active.append(False)
+        else:
+            active.append(True)
+        fs.append(f)
+    return fs, sp.prefactor, fold, active
+
+
+def local_slab(x_global, P, rank, species):
+    """The rank's slab of a global column-major tensor (torch or numpy)."""
+    if species > 1:
+        n = x_global.shape[-2] // P
+        return x_global[..., rank * n:(rank + 1) * n, :]
+    n = x_global.shape[-1] // P
+    return x_global[..., rank * n:(rank + 1) * n]
+
+
+def sharded_integrate(kp, backend, comm, method, u_local, dims_local, K, g, t0, t_final,
+                      n_steps):
+    """Slab-sharded integrate.  u_local: this rank's slab as a FLAT torch
+    tensor in column-major order with local dims `dims_local` (the last
+    spatial mode holds n_d/P planes; a stacked Brusselator keeps its species
+    mode last).  K = all factors as the reference takes them (including the
+    zero 2x2 species factor).  Factors are built on every rank with the
+    single-GPU device builder.  Returns the final flat slab."""
+    tau = (t_final - t0) / float(n_steps)
+    k_last = kp.to_host(K[-1])
+    species = 2 if (len(K) >= 2 and k_last.shape[0] == 2 and not np.any(k_last)) else 1
+    spatial_K = list(K[:-1]) if species == 2 else list(K)
+    d = len(spatial_K)
+    spatial = list(dims_local[:d])
+    spatial[-1] *= comm.P
+    f2, p2, fold2 = None, 1.0, 1.0
+    if method in ("lawson_euler", "lawson2b"):
+        f1, p1, fold1, _ = split_factors(kp, K, tau, 0)
+    elif method == "exp_euler":
+        f1, p1, fold1, _ = split_factors(kp, K, tau, 1)
+    elif method == "etd2rk":
+        f1, p1, fold1, _ = split_factors(kp, K, tau, 1)
+        f2, p2, fold2, _ = split_factors(kp, K, tau, 2)
+    else:
+        raise ValueError(f"sharded integrate: unsupported method {method}")
+    it = ShardedIntegrator(backend, comm, method, spatial, species, spatial_K, g, tau, f1[:d],
+                           p1, f2[:d] if f2 else None, p2, fold1, fold2)
+    return it.run(u_local, n_steps)

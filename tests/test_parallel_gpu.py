@@ -1,0 +1,46 @@
+"""The sharded integrator's GPU backend at world size 1 (NCCL): the unfused
+sharded step sequence must reproduce the fused single-GPU integrate bit for
+bit (the property that makes P > 1 bit-identical as well, see
+tests/test_parallel.py for the world-size-2 orchestration on CPU)."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nccl1():
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29571")
+        dist.init_process_group("nccl", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    yield
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,method", [("ac3d", "etd2rk"), ("bru", "etd2rk"),
+                                         ("bru", "lawson2b"), ("nls", "exp_euler")])
+def test_sharded_p1_bitwise_equals_fused(kp, nccl1, case, method):
+    import torch
+    from paper_2304_02327_b200 import parallel, problems
+    if case == "ac3d":
+        cfg = problems.ac3d(n=32, n_steps=6)
+    elif case == "bru":
+        cfg = problems.brusselator(n=16, n_steps=4, method=method)
+    else:
+        cfg = problems.nls(n=16, n_steps=4, method=method)
+    cfg.method = method
+    want = kp.integrate_config(method, cfg.u0, cfg.K, cfg.g, 0.0, cfg.t_final, cfg.n_steps)
+    be = parallel.CudaBackend(0)
+    comm = parallel.Comm()
+    K = [kp.to_device(k) for k in cfg.K]
+    flat = kp.to_device(cfg.u0).permute(*reversed(range(cfg.u0.ndim))).reshape(-1)
+    res = parallel.sharded_integrate(kp, be, comm, method, flat, list(cfg.u0.shape), K, cfg.g,
+                                     0.0, cfg.t_final, cfg.n_steps)
+    got = res.cpu().numpy().reshape(cfg.u0.shape, order="F")
+    assert np.array_equal(got, want), np.abs(got - want).max()
