@@ -115,6 +115,61 @@ def run_integrators(kp, peak):
     return out
 
 
+def run_sharded_integrators(kp, peak, world, rank, local):
+    """N > 1: configs 3 and 4 slab-sharded along mode 3 (paper_2304_02327_b200/
+    parallel.py; NCCL all-to-all pencil transposes).  Loop time = max over
+    ranks (CUDA events on each rank's stream)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2304_02327_b200 import parallel, problems
+    from paper_2304_02327_b200.integrators import _upload_factors
+    comm = parallel.Comm()
+    be = parallel.CudaBackend(local)
+    out = {}
+    for tag, builder, kw in INTEGRATOR_CONFIGS:
+        if builder not in ("brusselator", "nls"):
+            continue
+        n_full = 256 if builder == "brusselator" else 512
+        nl = n_full // world
+        c = getattr(problems, builder)(planes=(rank * nl, (rank + 1) * nl), **kw)
+        ud = kp.to_device(c.u0)
+        flat = ud.permute(*reversed(range(ud.ndim))).reshape(-1)
+        K = _upload_factors(c.K)
+        note = None
+        try:
+            it = parallel.make_sharded_integrator(kp, be, comm, c.method, list(c.u0.shape), K,
+                                                  c.g, 0.0, c.t_final, c.n_steps)
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            try:
+                it.run(flat, c.n_steps)
+            except kp.DivergenceError as e:
+                note = f"diverged at step {e.step} (as on one GPU; DESIGN.md 9)"
+            e1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) * 1e-3], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            loop = float(t.item())
+        except Exception as ex:  # reported, never fatal for the headline
+            out[tag + "_sharded"] = {"error": str(ex)[:300]}
+            continue
+        cplx = np.iscomplexobj(c.u0)
+        spatial = [n_full] * 3
+        species = 2 if builder == "brusselator" else 1
+        fl = tucker_equivalents(c.method) * species * (8.0 if cplx else 2.0) * \
+            float(np.prod(spatial)) * sum(spatial)
+        sps = c.n_steps / loop
+        out[tag + "_sharded"] = {"method": c.method, "global_dims": spatial + (
+            [2] if species == 2 else []), "ranks": world, "steps": c.n_steps,
+            "steps_per_s": sps, "loop_ms": loop * 1e3, "tflops_total": fl * sps / 1e12,
+            "frac_of_fp64_peak_per_gpu": fl * sps / 1e12 / (peak * world), "note": note}
+        del ud, flat, K
+        torch.cuda.empty_cache()
+    return out
+
+
 def make_inputs(n):
     r = np.random.default_rng(SEED)
     v = np.asfortranarray(r.standard_normal((n, n, n)))
@@ -331,7 +386,8 @@ def main():
     if not args.no_integrators:
         del v_d, out_d
         torch.cuda.empty_cache()
-        integ = run_integrators(kp, peak)
+        integ = run_integrators(kp, peak) if world == 1 else \
+            run_sharded_integrators(kp, peak, world, rank, local)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

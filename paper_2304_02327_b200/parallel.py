@@ -238,15 +238,24 @@ class ShardedIntegrator:
         raise ValueError(f"sharded integrate: unsupported method {m}")
 
     def run(self, u, n_steps):
+        """n_steps steps; like the single-GPU loop it runs to the end and then
+        reports the first non-finite step (DivergenceError(step))."""
+        first_bad = 0
+        flag = torch.zeros(1, dtype=torch.float64, device=u.device)
         for k in range(n_steps):
             u = self.step(u)
-            bad = torch.tensor([0.0 if bool(torch.isfinite(u).all()) else 1.0], device=u.device)
-            if self.comm.P > 1:
-                dist.all_reduce(bad, op=dist.ReduceOp.MAX)
-            if bad.item() > 0:
-                from ._lib import DivergenceError
-                raise DivergenceError(3, f"state became non-finite at step {k + 1} "
-                                         f"(t = {(k + 1) * self.tau:f})", k + 1)
+            if not first_bad:
+                flag.fill_(0.0 if bool(torch.isfinite(u).all()) else float(k + 1))
+                if self.comm.P > 1:
+                    # first bad step over ranks: any rank's nonzero flag, smallest k
+                    vals = torch.where(flag > 0, flag, torch.full_like(flag, 1e300))
+                    dist.all_reduce(vals, op=dist.ReduceOp.MIN)
+                    flag.copy_(torch.where(vals < 1e299, vals, torch.zeros_like(vals)))
+                first_bad = int(flag.item())
+        if first_bad:
+            from ._lib import DivergenceError
+            raise DivergenceError(3, f"state became non-finite at step {first_bad} "
+                                     f"(t = {first_bad * self.tau:f})", first_bad)
         return u
 
 
@@ -278,14 +287,13 @@ def local_slab(x_global, P, rank, species):
     return x_global[..., rank * n:(rank + 1) * n]
 
 
-def sharded_integrate(kp, backend, comm, method, u_local, dims_local, K, g, t0, t_final,
-                      n_steps):
-    """Slab-sharded integrate.  u_local: this rank's slab as a FLAT torch
-    tensor in column-major order with local dims `dims_local` (the last
-    spatial mode holds n_d/P planes; a stacked Brusselator keeps its species
-    mode last).  K = all factors as the reference takes them (including the
-    zero 2x2 species factor).  Factors are built on every rank with the
-    single-GPU device builder.  Returns the final flat slab."""
+def make_sharded_integrator(kp, backend, comm, method, dims_local, K, g, t0, t_final,
+                            n_steps):
+    """Factor set-up (on every rank, single-GPU device builder) for a slab-
+    sharded integrate.  dims_local: this rank's slab dims (the last spatial
+    mode holds n_d/P planes; a stacked Brusselator keeps its species mode
+    last).  K = all factors as the reference takes them (including the zero
+    2x2 species factor)."""
     tau = (t_final - t0) / float(n_steps)
     k_last = kp.to_host(K[-1])
     species = 2 if (len(K) >= 2 and k_last.shape[0] == 2 and not np.any(k_last)) else 1
@@ -303,6 +311,14 @@ def sharded_integrate(kp, backend, comm, method, u_local, dims_local, K, g, t0, 
         f2, p2, fold2, _ = split_factors(kp, K, tau, 2)
     else:
         raise ValueError(f"sharded integrate: unsupported method {method}")
-    it = ShardedIntegrator(backend, comm, method, spatial, species, spatial_K, g, tau, f1[:d],
-                           p1, f2[:d] if f2 else None, p2, fold1, fold2)
+    return ShardedIntegrator(backend, comm, method, spatial, species, spatial_K, g, tau,
+                             f1[:d], p1, f2[:d] if f2 else None, p2, fold1, fold2)
+
+
+def sharded_integrate(kp, backend, comm, method, u_local, dims_local, K, g, t0, t_final,
+                      n_steps):
+    """Slab-sharded integrate of this rank's slab (a FLAT torch tensor in
+    column-major order with local dims `dims_local`); returns the final slab."""
+    it = make_sharded_integrator(kp, backend, comm, method, dims_local, K, g, t0, t_final,
+                                 n_steps)
     return it.run(u_local, n_steps)

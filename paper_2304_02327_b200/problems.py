@@ -84,31 +84,45 @@ def ac3d(n=128, n_steps=200, tau=5e-4, seed=1003):
                   n_steps)
 
 
+def _planes(n, planes):
+    return range(n) if planes is None else range(planes[0], planes[1])
+
+
 def brusselator(n=256, n_steps=100, tau=1e-3, method="etd2rk", seed=1004, a=1.0, b=3.0,
-                diff=0.02):
+                diff=0.02, planes=None):
     """configs[3]: two species stacked as a 4th mode of size 2 (u first,
     v second) with a zero 2x2 factor -- the reference's own way to run it
-    (SURVEY.md 8(c)); Dirichlet fd_operator_1d(n, 0.02) for both species."""
-    r = np.random.default_rng(seed)
-    u = a + 0.1 * r.uniform(-1, 1, (n, n, n))
-    v = b / a + 0.1 * r.uniform(-1, 1, (n, n, n))
-    u0 = np.asfortranarray(np.stack([u, v], axis=-1))
+    (SURVEY.md 8(c)); Dirichlet fd_operator_1d(n, 0.02) for both species.
+    The noise of plane k (last spatial mode) comes from rng([seed, k]), so a
+    slab `planes=(k0, k1)` is built without the rest (sharded runs)."""
+    ks = _planes(n, planes)
+    u0 = np.empty((n, n, len(ks), 2), order="F")
+    for j, k in enumerate(ks):
+        r = np.random.default_rng([seed, k])
+        u0[:, :, j, 0] = a + 0.1 * r.uniform(-1, 1, (n, n))
+        u0[:, :, j, 1] = b / a + 0.1 * r.uniform(-1, 1, (n, n))
     A = fd_operator_1d(n, diff)
     return Config("brusselator", method, u0, [A, A, A, np.zeros((2, 2), order="F")],
                   G.brusselator(a, b), tau, n_steps)
 
 
-def nls(n=512, n_steps=50, tau=1e-3, method="etd2rk", seed=1005, k=(1.0, 0.5, 0.0)):
+def nls(n=512, n_steps=50, tau=1e-3, method="etd2rk", seed=1005, k=(1.0, 0.5, 0.0),
+        planes=None):
     """configs[4]: i u_t = -1/2 Lap u + |u|^2 u on [-8,8]^3 periodic, i.e.
     u' = (i/2) Lap u - i |u|^2 u; u0 = Gaussian wave packet (wave vector k)
-    + 0.01 (N + iN) noise."""
-    r = np.random.default_rng(seed)
+    + 0.01 (N + iN) noise (plane k of the noise from rng([seed, k]))."""
     L = 16.0
     h = L / n
     x = -8.0 + h * np.arange(n)
-    X, Y, Z = np.meshgrid(x, x, x, indexing="ij")
-    u0 = np.exp(-(X * X + Y * Y + Z * Z) / 2.0) * np.exp(1j * (k[0] * X + k[1] * Y + k[2] * Z))
-    u0 = u0 + 0.01 * (r.standard_normal((n, n, n)) + 1j * r.standard_normal((n, n, n)))
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    ks = _planes(n, planes)
+    u0 = np.empty((n, n, len(ks)), dtype=np.complex128, order="F")
+    for j, kk in enumerate(ks):
+        z = x[kk]
+        r = np.random.default_rng([seed, kk])
+        u0[:, :, j] = np.exp(-(X * X + Y * Y + z * z) / 2.0) * \
+            np.exp(1j * (k[0] * X + k[1] * Y + k[2] * z)) + \
+            0.01 * (r.standard_normal((n, n)) + 1j * r.standard_normal((n, n)))
     A = 0.5j * periodic_laplacian_1d(n, h)
     return Config("nls", method, np.asfortranarray(u0), [A, A, A], G.nls(), tau, n_steps)
 
