@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-integrators", action="store_true",
                     help="skip the integrator-config block (steps/s of configs 0,2,3,4)")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the sharded integrator block even at N=1 (testing)")
     return ap.parse_args()
 
 
@@ -293,7 +295,7 @@ def main():
     import torch
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or args.force_sharded:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2304_02327_b200 as kp
@@ -386,7 +388,7 @@ def main():
     if not args.no_integrators:
         del v_d, out_d
         torch.cuda.empty_cache()
-        integ = run_integrators(kp, peak) if world == 1 else \
+        integ = run_integrators(kp, peak) if (world == 1 and not args.force_sharded) else \
             run_sharded_integrators(kp, peak, world, rank, local)
 
     cpu = None
