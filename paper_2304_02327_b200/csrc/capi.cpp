@@ -355,6 +355,107 @@ void d2h(kp_ctx* ctx, double* dst, const double* src, size_t n) {
 }
 
 constexpr int SLOT_HOST_IN = 8, SLOT_HOST_OUT = 9, SLOT_HOST_MATS = 10;
+constexpr int SLOT_PIPE_A = 13, SLOT_PIPE_SUB = 14;
+
+// Host-buffer Tucker with the PCIe copies overlapped with the device work
+// (the e2e drop-in path).  Mode products on distinct modes act plane by plane
+// along the slowest mode, so:
+//   * the input streams in over a copy stream in chunks of planes (slowest
+//     mode); modes 0..d-2 of chunk k run while chunk k+1 is in flight;
+//   * the last mode (which needs every plane) is computed in blocks of OUTPUT
+//     planes -- row blocks of its factor -- and each block is copied back
+//     over a second copy stream while the next one computes.
+// Results are bit-identical to the unpipelined Tucker (same per-entry sums).
+void host_tucker_pipelined(kp_ctx* ctx, ModeFn mp, int comps, const double* t,
+                           const std::vector<int>& dv, const std::vector<const double*>& dm,
+                           const int* rows, double pref, double* out) {
+  const int d = int(dv.size());
+  size_t plane_in = comps, plane_mid = comps, plane_out = comps;
+  for (int mu = 0; mu < d - 1; ++mu) {
+    plane_in *= size_t(dv[mu]);
+    plane_mid *= size_t(rows[mu]);
+    plane_out *= size_t(rows[mu]);
+  }
+  const int nlast = dv[d - 1], rlast = rows[d - 1];
+  double* din = static_cast<double*>(ctx->ws.get(SLOT_HOST_IN, plane_in * nlast * sizeof(double)));
+  double* dmid = static_cast<double*>(ctx->ws.get(SLOT_HOST_OUT, plane_mid * nlast * sizeof(double)));
+  double* dout = static_cast<double*>(ctx->ws.get(SLOT_PIPE_A, plane_out * rlast * sizeof(double)));
+  cudaStream_t s_in, s_out;
+  KP_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+  KP_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+  // pipeline depth: ~16 MiB per chunk, at most 8 (small tensors: one chunk,
+  // i.e. exactly the unpipelined launch sequence)
+  const size_t in_bytes = plane_in * nlast * sizeof(double);
+  const int depth = int(std::min<size_t>(8, std::max<size_t>(1, in_bytes >> 24)));
+  const int nch = std::min(nlast, depth), nblk = std::min(rlast, depth);
+  std::vector<cudaEvent_t> ev(nch + nblk + 1);
+  for (auto& e : ev) KP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  try {
+    // factors were uploaded on ctx->stream: the copy streams start after them
+    KP_CUDA(cudaEventRecord(ev[nch + nblk], ctx->stream));
+    for (int k = 0; k < nch; ++k) {
+      const int p0 = int((long long)nlast * k / nch), p1 = int((long long)nlast * (k + 1) / nch);
+      KP_CUDA(cudaMemcpyAsync(din + plane_in * p0, t + plane_in * p0,
+                              plane_in * (p1 - p0) * sizeof(double), cudaMemcpyHostToDevice, s_in));
+      KP_CUDA(cudaEventRecord(ev[k], s_in));
+      KP_CUDA(cudaStreamWaitEvent(ctx->stream, ev[k], 0));
+      std::vector<int> cd = dv;
+      cd[d - 1] = p1 - p0;
+      const double* cur = din + plane_in * p0;
+      for (int mu = 0; mu < d - 1; ++mu) {
+        std::vector<int> od = cd;
+        od[mu] = rows[mu];
+        size_t n_od = comps;
+        for (int x : od) n_od *= size_t(x);
+        double* dst = (mu == d - 2) ? dmid + plane_mid * p0
+                                    : static_cast<double*>(ctx->ws.get(mu & 1, n_od * sizeof(double)));
+        Epilogue e;
+        e.alpha = (mu == 0) ? pref : 1.0;
+        mp(ctx, cur, cd, mu, dm[mu], rows[mu], e, dst);
+        cd = od;
+        cur = dst;
+      }
+    }
+    // last mode in blocks of output planes, each copied back as it completes
+    std::vector<int> md = dv;
+    for (int mu = 0; mu < d - 1; ++mu) md[mu] = rows[mu];
+    double* sub = static_cast<double*>(
+        ctx->ws.get(SLOT_PIPE_SUB, size_t(rlast) * nlast * comps * sizeof(double)));
+    for (int b = 0; b < nblk; ++b) {
+      const int i0 = int((long long)rlast * b / nblk), i1 = int((long long)rlast * (b + 1) / nblk);
+      const int rb = i1 - i0;
+      // rows i0..i1 of the last factor as a contiguous rb x nlast matrix
+      KP_CUDA(cudaMemcpy2DAsync(sub + size_t(i0) * nlast * comps, rb * comps * sizeof(double),
+                                dm[d - 1] + size_t(i0) * comps, rlast * comps * sizeof(double),
+                                rb * comps * sizeof(double), nlast, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+      Epilogue e;
+      e.alpha = (d == 1) ? pref : 1.0;
+      mp(ctx, d == 1 ? din : dmid, md, d - 1, sub + size_t(i0) * nlast * comps, rb, e,
+         dout + plane_out * i0);
+      KP_CUDA(cudaEventRecord(ev[nch + b], ctx->stream));
+    }
+    for (int b = 0; b < nblk; ++b) {
+      const int i0 = int((long long)rlast * b / nblk), i1 = int((long long)rlast * (b + 1) / nblk);
+      KP_CUDA(cudaStreamWaitEvent(s_out, ev[nch + b], 0));
+      KP_CUDA(cudaMemcpyAsync(out + plane_out * i0, dout + plane_out * i0,
+                              plane_out * (i1 - i0) * sizeof(double), cudaMemcpyDeviceToHost,
+                              s_out));
+    }
+    KP_CUDA(cudaStreamSynchronize(s_out));
+    KP_CUDA(cudaStreamSynchronize(ctx->stream));
+  } catch (...) {
+    cudaStreamSynchronize(s_in);
+    cudaStreamSynchronize(s_out);
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaStreamDestroy(s_in);
+    cudaStreamDestroy(s_out);
+    throw;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  cudaStreamDestroy(s_in);
+  cudaStreamDestroy(s_out);
+}
 
 }  // namespace
 
@@ -393,13 +494,8 @@ int kp_host_tucker_f64(kp_ctx* ctx, const double* t, const int* dims, int d,
       sizes.push_back(size_t(rows[mu]) * dv[mu]);
       od[mu] = rows[mu];
     }
-    const size_t nin = numel(dv), nout = numel(od);
-    double* din = static_cast<double*>(ctx->ws.get(SLOT_HOST_IN, nin * sizeof(double)));
-    double* dout = static_cast<double*>(ctx->ws.get(SLOT_HOST_OUT, nout * sizeof(double)));
     auto dm = upload_mats(ctx, SLOT_HOST_MATS, ms, sizes);
-    h2d(ctx, din, t, nin);
-    tucker_f64(ctx, din, dv, dm.data(), rows, prefactor, dout);
-    d2h(ctx, out, dout, nout);
+    host_tucker_pipelined(ctx, mode_product_f64, 1, t, dv, dm, rows, prefactor, out);
   });
 }
 
@@ -546,13 +642,8 @@ int kp_host_tucker_c128(kp_ctx* ctx, const double* t, const int* dims, int d,
       sizes.push_back(2 * size_t(rows[mu]) * dv[mu]);
       od[mu] = rows[mu];
     }
-    const size_t nin = 2 * numel(dv), nout = 2 * numel(od);
-    double* din = static_cast<double*>(ctx->ws.get(SLOT_HOST_IN, nin * sizeof(double)));
-    double* dout = static_cast<double*>(ctx->ws.get(SLOT_HOST_OUT, nout * sizeof(double)));
     auto dm = upload_mats(ctx, SLOT_HOST_MATS, ms, sizes);
-    h2d(ctx, din, t, nin);
-    tucker_c128(ctx, din, dv, dm.data(), rows, prefactor, dout);
-    d2h(ctx, out, dout, nout);
+    host_tucker_pipelined(ctx, mode_product_c128, 2, t, dv, dm, rows, prefactor, out);
   });
 }
 
