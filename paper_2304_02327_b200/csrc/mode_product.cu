@@ -372,15 +372,17 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
   if (e.bad_step && nonfinite) atomicMin(e.bad_step, *e.step_ctr + 1);
 }
 
-template <int BM, int BN, int WARPS_M, int WARPS_N, bool B_KCONTIG, int VEC, int CPLX>
+template <int BM, int BN, int WARPS_M, int WARPS_N, bool B_KCONTIG, int VEC, int CPLX, int VAR>
 void launch_cfg(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, long long half) {
   // 128x128 with 8 warps of 64x32: one CTA per SM, BK=32 x 3 stages.
   // Every other tile uses 32x32 warp tiles (<= 128 registers) so that two or
   // more CTAs share an SM and hide each other's barrier/load phases: the
   // measured winner (tools/tucker_sweep.py, profiles/gemm_tiles_r01.txt).
   constexpr bool BIG = (BM == 128 && BN == 128 && WARPS_M * WARPS_N == 8);
-  constexpr int BK = BIG ? 32 : 16, STAGES = BIG ? 3 : 4;
-  constexpr int MINB = BIG ? 1 : (WARPS_M * WARPS_N * 32 >= 512 ? 1 : 2);
+  // VAR 1: 3-stage ring and >= 4 CTAs per SM (<= 128 registers) -- more
+  // independent DMMA streams per SM partition
+  constexpr int BK = BIG ? 32 : 16, STAGES = BIG ? 3 : (VAR == 1 ? 3 : 4);
+  constexpr int MINB = BIG ? 1 : (VAR == 1 ? 4 : (WARPS_M * WARPS_N * 32 >= 512 ? 1 : 2));
   using CF = Cfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, B_KCONTIG, VEC>;
   auto kern = dmma_gemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, B_KCONTIG, VEC, CPLX, MINB>;
   static bool attr_set = false;  // per instantiation
@@ -406,23 +408,23 @@ void launch_cfg(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, long long 
   KP_CUDA(cudaGetLastError());
 }
 
-template <int BM, int BN, int WARPS_M, int WARPS_N>
+template <int BM, int BN, int WARPS_M, int WARPS_N, int VAR = 0>
 void launch_layout(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, bool kcontig, bool vec2,
                    int cplx, long long half) {
   if (cplx == 1) {
-    launch_cfg<BM, BN, WARPS_M, WARPS_N, true, 2, 1>(ctx, p, e, half);
+    launch_cfg<BM, BN, WARPS_M, WARPS_N, true, 2, 1, VAR>(ctx, p, e, half);
   } else if (cplx == 2) {
-    launch_cfg<BM, BN, WARPS_M, WARPS_N, false, 2, 2>(ctx, p, e, half);
+    launch_cfg<BM, BN, WARPS_M, WARPS_N, false, 2, 2, VAR>(ctx, p, e, half);
   } else if (kcontig) {
     if (vec2)
-      launch_cfg<BM, BN, WARPS_M, WARPS_N, true, 2, 0>(ctx, p, e, half);
+      launch_cfg<BM, BN, WARPS_M, WARPS_N, true, 2, 0, VAR>(ctx, p, e, half);
     else
-      launch_cfg<BM, BN, WARPS_M, WARPS_N, true, 1, 0>(ctx, p, e, half);
+      launch_cfg<BM, BN, WARPS_M, WARPS_N, true, 1, 0, VAR>(ctx, p, e, half);
   } else {
     if (vec2)
-      launch_cfg<BM, BN, WARPS_M, WARPS_N, false, 2, 0>(ctx, p, e, half);
+      launch_cfg<BM, BN, WARPS_M, WARPS_N, false, 2, 0, VAR>(ctx, p, e, half);
     else
-      launch_cfg<BM, BN, WARPS_M, WARPS_N, false, 1, 0>(ctx, p, e, half);
+      launch_cfg<BM, BN, WARPS_M, WARPS_N, false, 1, 0, VAR>(ctx, p, e, half);
   }
 }
 
@@ -449,7 +451,8 @@ void launch_gemm(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int cplx)
       (long long)((p.M + 127) / 128) * ((p.N + 127) / 128) * p.batch;
   const bool few = tiles128 < ctx->num_sms;
   // Tile menu: 0: 128x128 (8 warps 64x32), 1: 128x64, 2: 64x128, 3: 64x64,
-  // 4: 128x128 (16 warps 32x32), 5: 32x32, 6: 64x32, 7: 32x64 (4 warps each).
+  // 4: 128x128 (16 warps 32x32), 5: 32x32, 6: 64x32, 7: 32x64 (4 warps each),
+  // 8/9/10: 64x64 / 32x64 / 64x32 with a 3-stage ring and >= 4 CTAs per SM.
   // Chosen from the measured sweep (profiles/gemm_tiles_r01.txt): small tiles
   // (many co-resident CTAs hide latency, fewer idle slots in the last wave)
   // win until the problem is large; long K (d=2, n >= 1024) favours big tiles.
@@ -461,14 +464,14 @@ void launch_gemm(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int cplx)
   if (tiles64 * 2 < ctx->num_sms)
     tile = 5;
   else if (kcontig)
-    tile = (p.K >= 1024) ? 1 : (p.K <= 128 ? 5 : 7);
+    tile = (p.K >= 1024) ? 1 : 9;
   else
-    tile = (tiles64 >= 48LL * ctx->num_sms || p.K >= 1024) ? 3 : 6;
+    tile = (tiles64 >= 16LL * ctx->num_sms || p.K >= 1024) ? 8 : 6;
   static const int forced = [] {  // benchmarking override
     const char* v = getenv("KP_GEMM_TILE");
     return v ? atoi(v) : -1;
   }();
-  if (forced >= 0 && forced <= 7) tile = forced;
+  if (forced >= 0 && forced <= 10) tile = forced;
   switch (tile) {
     case 0: launch_layout<128, 128, 2, 4>(ctx, p, e, kcontig, vec2, cplx, half); break;
     case 1: launch_layout<128, 64, 4, 2>(ctx, p, e, kcontig, vec2, cplx, half); break;
@@ -477,6 +480,9 @@ void launch_gemm(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int cplx)
     case 5: launch_layout<32, 32, 2, 2>(ctx, p, e, kcontig, vec2, cplx, half); break;
     case 6: launch_layout<64, 32, 2, 2>(ctx, p, e, kcontig, vec2, cplx, half); break;
     case 7: launch_layout<32, 64, 2, 2>(ctx, p, e, kcontig, vec2, cplx, half); break;
+    case 8: launch_layout<64, 64, 2, 2, 1>(ctx, p, e, kcontig, vec2, cplx, half); break;
+    case 9: launch_layout<32, 64, 2, 2, 1>(ctx, p, e, kcontig, vec2, cplx, half); break;
+    case 10: launch_layout<64, 32, 2, 2, 1>(ctx, p, e, kcontig, vec2, cplx, half); break;
     default: launch_layout<64, 64, 2, 2>(ctx, p, e, kcontig, vec2, cplx, half); break;
   }
 }
