@@ -1,0 +1,270 @@
+// banded.cu -- the Kronecker-sum action for banded factors as one stencil pass.
+//
+// SURVEY.md 8(f) row 1.  In every BASELINE config the A_mu are tridiagonal
+// (fd_operator_1d, src/problems.cpp:9-22) or periodic tridiagonal (NLS), yet
+// kronsum_action (inc/mode_product.hpp:111-121) multiplies them densely: d
+// GEMMs of 2 N n FLOP.  With at most three nonzeros per row the action is a
+// (2d+1)-point stencil: one HBM-bound pass that reads u and writes r.
+//
+// Rounding follows the reference's dense CPU GEMM exactly: per output entry
+// and mode the k loop is an FMA chain in increasing column order (the zero
+// products of the dense loop add nothing), restarted at every KC = 256 slice
+// boundary and folded into C like compute_tile (inc/kernels.hpp:241-263,
+// :297); mode 0 stores, modes >= 1 accumulate (beta = 1, :65).  So for real
+// data this pass reproduces the reference's kronsum_action bit for bit (the
+// dense DMMA path agrees only to roundoff).  The optional g(t,u) of the
+// ETD2RK / exp-Euler prologue is added last, as the reference's axpy does.
+//
+// Band detection (once per factor): a device scan collects, per row, up to
+// three (column, value) pairs in increasing column order; more nonzeros =>
+// not banded (dense path).
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "kp_g.cuh"
+#include "kp_internal.h"
+
+namespace kp {
+namespace {
+
+constexpr int KC = 256;  // inc/kernels.hpp:104
+
+// rows of A (n x n, column-major; complex when comps == 2) -> 3 slots per row
+__global__ void band_scan_kernel(const double* __restrict__ a, int n, int comps,
+                                 int* __restrict__ cols, double* __restrict__ vals,
+                                 int* __restrict__ too_many) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int cnt = 0;
+  for (int j = 0; j < n; ++j) {
+    const double re = a[(size_t(i) + size_t(j) * n) * comps];
+    const double im = comps == 2 ? a[(size_t(i) + size_t(j) * n) * comps + 1] : 0.0;
+    if (re != 0.0 || im != 0.0) {
+      if (cnt == 3) {
+        *too_many = 1;
+        return;
+      }
+      cols[i * 3 + cnt] = j;
+      vals[(i * 3 + cnt) * 2] = re;
+      vals[(i * 3 + cnt) * 2 + 1] = im;
+      ++cnt;
+    }
+  }
+  for (; cnt < 3; ++cnt) cols[i * 3 + cnt] = -1;
+}
+
+struct BandArgs {
+  int d;
+  int n[4];
+  long long stride[4];
+  const int* cols[4];
+  const double* vals[4];  // (re, im) pairs
+  int active[4];
+};
+
+// Adds one mode's term at entry idx into the running value c: the
+// reference's FMA chain per KC slice, each slice folded as c = c + acc
+// (mode 0's first slice stores: has_c == false).
+__device__ __forceinline__ void term_real(const BandArgs& b, int mu, int imu, long long idx,
+                                          const double* __restrict__ u, double& c, bool& has_c) {
+  const int* cs = b.cols[mu] + imu * 3;
+  const double* v = b.vals[mu] + imu * 6;
+  double acc = 0.0;
+  int slice = -1;
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    const int j = cs[s];
+    if (j < 0) break;
+    const int sl = j / KC;
+    if (sl != slice) {
+      if (slice >= 0) {
+        c = has_c ? __dadd_rn(c, acc) : acc;
+        has_c = true;
+      }
+      slice = sl;
+      acc = 0.0;
+    }
+    acc = __fma_rn(v[2 * s], u[idx + (long long)(j - imu) * b.stride[mu]], acc);
+  }
+  if (slice >= 0) {
+    c = has_c ? __dadd_rn(c, acc) : acc;
+    has_c = true;
+  }
+}
+
+__device__ __forceinline__ double2 cmul_add(double2 a, double2 x, double2 acc) {
+  // acc + a*x with the product formed first (generic complex micro-kernel)
+  const double re = __dsub_rn(__dmul_rn(a.x, x.x), __dmul_rn(a.y, x.y));
+  const double im = __dadd_rn(__dmul_rn(a.x, x.y), __dmul_rn(a.y, x.x));
+  return make_double2(__dadd_rn(acc.x, re), __dadd_rn(acc.y, im));
+}
+
+__device__ __forceinline__ void term_cplx(const BandArgs& b, int mu, int imu, long long idx,
+                                          const double2* __restrict__ u, double2& c,
+                                          bool& has_c) {
+  const int* cs = b.cols[mu] + imu * 3;
+  const double* v = b.vals[mu] + imu * 6;
+  double2 acc = make_double2(0.0, 0.0);
+  int slice = -1;
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    const int j = cs[s];
+    if (j < 0) break;
+    const int sl = j / KC;
+    if (sl != slice) {
+      if (slice >= 0) {
+        c = has_c ? make_double2(__dadd_rn(c.x, acc.x), __dadd_rn(c.y, acc.y)) : acc;
+        has_c = true;
+      }
+      slice = sl;
+      acc = make_double2(0.0, 0.0);
+    }
+    acc = cmul_add(make_double2(v[2 * s], v[2 * s + 1]),
+                   u[idx + (long long)(j - imu) * b.stride[mu]], acc);
+  }
+  if (slice >= 0) {
+    c = has_c ? make_double2(__dadd_rn(c.x, acc.x), __dadd_rn(c.y, acc.y)) : acc;
+    has_c = true;
+  }
+}
+
+// r = sum_mu u x_mu A_mu (+ g(t,u) when with_g), one entry per thread
+template <bool CPLX>
+__global__ void kronsum_band_kernel(BandArgs b, long long total, const double* __restrict__ u,
+                                    double* __restrict__ r, bool with_g, kp_gfun g,
+                                    long long half) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long rem = idx;
+    int ii[4];
+#pragma unroll
+    for (int mu = 0; mu < 4; ++mu) {
+      if (mu < b.d) {
+        ii[mu] = int(rem % b.n[mu]);
+        rem /= b.n[mu];
+      }
+    }
+    if constexpr (!CPLX) {
+      double acc = 0.0;
+      bool has = false;
+#pragma unroll
+      for (int mu = 0; mu < 4; ++mu) {
+        if (mu >= b.d || !b.active[mu]) continue;
+        term_real(b, mu, ii[mu], idx, u, acc, has);
+      }
+      if (with_g) {
+        const bool second = half > 0 && idx >= half;
+        const double partner = half > 0 ? u[second ? idx - half : idx + half] : 0.0;
+        acc = __dadd_rn(acc, g_real(g, u[idx], partner, second));
+      }
+      r[idx] = acc;
+    } else {
+      const double2* uc = reinterpret_cast<const double2*>(u);
+      double2 acc = make_double2(0.0, 0.0);
+      bool has = false;
+#pragma unroll
+      for (int mu = 0; mu < 4; ++mu) {
+        if (mu >= b.d || !b.active[mu]) continue;
+        term_cplx(b, mu, ii[mu], idx, uc, acc, has);
+      }
+      if (with_g) {
+        const double2 gg = g_cplx(g, uc[idx]);
+        acc = make_double2(__dadd_rn(acc.x, gg.x), __dadd_rn(acc.y, gg.y));
+      }
+      reinterpret_cast<double2*>(r)[idx] = acc;
+    }
+  }
+}
+
+}  // namespace
+
+// Scan a factor into caller-provided device arrays (3n ints, 6n doubles);
+// false if some row has more than three nonzeros.
+bool band_scan(kp_ctx* ctx, const double* a, int n, bool cplx, int* dc, double* dv) {
+  int* flag = reinterpret_cast<int*>(ctx->d_flag) + 8;
+  KP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+  band_scan_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(a, n, cplx ? 2 : 1, dc, dv, flag);
+  ctx->launches++;
+  KP_CUDA(cudaGetLastError());
+  KP_CUDA(cudaMemcpyAsync(ctx->h_flag + 8, flag, sizeof(int), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  KP_CUDA(cudaStreamSynchronize(ctx->stream));
+  return ctx->h_flag[8] == 0;
+}
+
+// Scan a factor into fresh allocations (owned by the caller).
+bool band_of(kp_ctx* ctx, const double* a, int n, bool cplx, int** cols, double** vals) {
+  int* dc = nullptr;
+  double* dv = nullptr;
+  KP_CUDA(cudaMalloc(&dc, sizeof(int) * 3 * size_t(n)));
+  KP_CUDA(cudaMalloc(&dv, sizeof(double) * 6 * size_t(n)));
+  if (!band_scan(ctx, a, n, cplx, dc, dv)) {
+    cudaFree(dc);
+    cudaFree(dv);
+    return false;
+  }
+  *cols = dc;
+  *vals = dv;
+  return true;
+}
+
+// kronsum_action through the stencil when every factor is banded (workspace
+// slots 30..37 hold the row structures); false = caller takes the dense path.
+bool kronsum_try_banded(kp_ctx* ctx, bool cplx, const double* t, const std::vector<int>& dims,
+                        const double* const* as, double* out) {
+  const int d = int(dims.size());
+  if (!banded_kronsum_enabled() || d > 4) return false;
+  std::vector<const int*> cols(d);
+  std::vector<const double*> vals(d);
+  std::vector<char> active(d, 1);
+  for (int mu = 0; mu < d; ++mu) {
+    int* c = static_cast<int*>(ctx->ws.get(30 + mu, sizeof(int) * 3 * size_t(dims[mu])));
+    double* v = static_cast<double*>(ctx->ws.get(34 + mu, sizeof(double) * 6 * size_t(dims[mu])));
+    if (!band_scan(ctx, as[mu], dims[mu], cplx, c, v)) return false;
+    cols[mu] = c;
+    vals[mu] = v;
+  }
+  kronsum_banded(ctx, cplx, t, dims, cols, vals, active, out, false, kp_gfun{}, 0);
+  return true;
+}
+
+// KP_KRONSUM=dense selects the reference's dense form (read per call, so a
+// process can compare both)
+bool banded_kronsum_enabled() {
+  const char* v = getenv("KP_KRONSUM");
+  return !(v && std::string(v) == "dense");
+}
+
+// r = sum_mu u x_mu A_mu (+ g) with banded factors.  dims: up to 4 modes;
+// inactive modes (zero factors) are skipped; cols/vals from band_of.
+void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<int>& dims,
+                    const std::vector<const int*>& cols, const std::vector<const double*>& vals,
+                    const std::vector<char>& active, double* r, bool with_g, const kp_gfun& g,
+                    long long half) {
+  const int d = int(dims.size());
+  if (d > 4) throw invalid_argument("kronsum (banded): order > 4 unsupported");
+  BandArgs b{};
+  b.d = d;
+  long long st = 1;
+  for (int mu = 0; mu < d; ++mu) {
+    b.n[mu] = dims[mu];
+    b.stride[mu] = st;
+    st *= dims[mu];
+    b.cols[mu] = cols[mu];
+    b.vals[mu] = vals[mu];
+    b.active[mu] = active[mu];
+  }
+  const long long total = st;
+  const unsigned grid =
+      unsigned(std::max<long long>(1, std::min<long long>((total + 255) / 256, ctx->num_sms * 16LL)));
+  if (cplx)
+    kronsum_band_kernel<true><<<grid, 256, 0, ctx->stream>>>(b, total, u, r, with_g, g, half);
+  else
+    kronsum_band_kernel<false><<<grid, 256, 0, ctx->stream>>>(b, total, u, r, with_g, g, half);
+  ctx->launches++;
+  KP_CUDA(cudaGetLastError());
+}
+
+}  // namespace kp

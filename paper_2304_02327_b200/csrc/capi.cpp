@@ -318,7 +318,8 @@ int kp_kronsum_f64(kp_ctx* ctx, const double* t, const int* dims, int d, const d
     const auto dv = check_dims(dims, d, "kronsum_action");
     if (!as) throw invalid_argument("kronsum_action: expected one factor per mode");
     if (out == t) throw invalid_argument("kronsum_action: out must not alias the input");
-    kronsum_generic(ctx, mode_product_f64, t, dv, as, out);
+    if (!kronsum_try_banded(ctx, false, t, dv, as, out))
+      kronsum_generic(ctx, mode_product_f64, t, dv, as, out);
   });
 }
 
@@ -511,7 +512,8 @@ int kp_host_kronsum_f64(kp_ctx* ctx, const double* t, const int* dims, int d,
     double* dout = static_cast<double*>(ctx->ws.get(SLOT_HOST_OUT, n * sizeof(double)));
     auto dm = upload_mats(ctx, SLOT_HOST_MATS, as, sizes);
     h2d(ctx, din, t, n);
-    kronsum_generic(ctx, mode_product_f64, din, dv, dm.data(), dout);
+    if (!kronsum_try_banded(ctx, false, din, dv, dm.data(), dout))
+      kronsum_generic(ctx, mode_product_f64, din, dv, dm.data(), dout);
     d2h(ctx, out, dout, n);
   });
 }
@@ -626,7 +628,8 @@ int kp_kronsum_c128(kp_ctx* ctx, const double* t, const int* dims, int d,
     const auto dv = check_dims(dims, d, "kronsum_action");
     if (!as) throw invalid_argument("kronsum_action: expected one factor per mode");
     if (out == t) throw invalid_argument("kronsum_action: out must not alias the input");
-    kronsum_generic(ctx, mode_product_c128, t, dv, as, out);
+    if (!kronsum_try_banded(ctx, true, t, dv, as, out))
+      kronsum_generic(ctx, mode_product_c128, t, dv, as, out);
   });
 }
 

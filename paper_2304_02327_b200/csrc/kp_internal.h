@@ -129,6 +129,16 @@ void expm_batch_c128(kp_ctx* ctx, const double* x, int n, int batch, double* out
 int phiquad_dev_c128(kp_ctx* ctx, const double* x, int n, int ell_max, int q, int forced,
                      double* phis);
 
+// ---- banded Kronecker sum (banded.cu) ----
+bool banded_kronsum_enabled();  // KP_KRONSUM=dense disables
+bool band_of(kp_ctx* ctx, const double* a, int n, bool cplx, int** cols, double** vals);
+bool kronsum_try_banded(kp_ctx* ctx, bool cplx, const double* t, const std::vector<int>& dims,
+                        const double* const* as, double* out);
+void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<int>& dims,
+                    const std::vector<const int*>& cols, const std::vector<const double*>& vals,
+                    const std::vector<char>& active, double* r, bool with_g, const kp_gfun& g,
+                    long long half);
+
 // ---- elementwise (elementwise.cu) ----
 // z = fma(b, y, x): axpy is (b=alpha, y=x, x=y, z=y), add_scaled is (b=alpha, y=y, x=x)
 void launch_fma(kp_ctx* ctx, size_t n, double b, const double* y, const double* x, double* z);

@@ -155,6 +155,10 @@ class Integrator {
   FactorSet f1, f2;
   std::vector<double*> owned;
   long diverged_at = 0;  // first non-finite step of the last run() (0 = none)
+  // banded Kronecker sum (banded.cu): per-mode 3-slot row structure
+  bool banded = false;
+  std::vector<const int*> band_cols;
+  std::vector<const double*> band_vals;
 
   Integrator(kp_ctx* c, int m, bool cp, const std::vector<int>& dv, const double* const* as,
              const kp_gfun& gf, double tau_)
@@ -179,9 +183,37 @@ class Integrator {
       nact += a_active[mu];
     }
     if (nact == 0) a_active[d - 1] = 1;
+    if (banded_kronsum_enabled() && d <= 4 && (method == KP_EXP_EULER || method == KP_ETD2RK)) {
+      banded = true;
+      band_cols.assign(d, nullptr);
+      band_vals.assign(d, nullptr);
+      for (int mu = 0; mu < d && banded; ++mu) {
+        if (!a_active[mu]) continue;
+        int same = -1;
+        for (int m2 = 0; m2 < mu; ++m2)
+          if (a_active[m2] && A[m2] == A[mu] && dims[m2] == dims[mu]) same = m2;
+        if (same >= 0) {
+          band_cols[mu] = band_cols[same];
+          band_vals[mu] = band_vals[same];
+          continue;
+        }
+        int* c = nullptr;
+        double* v = nullptr;
+        if (band_of(ctx, A[mu], dims[mu], cplx, &c, &v)) {
+          band_cols[mu] = c;
+          band_vals[mu] = v;
+          owned_i.push_back(c);
+          owned.push_back(v);
+        } else {
+          banded = false;
+        }
+      }
+    }
   }
+  std::vector<int*> owned_i;
   ~Integrator() {
     for (double* p : owned) cudaFree(p);
+    for (int* p : owned_i) cudaFree(p);
   }
 
   // exact zero matrix? (only small factors are checked; big ones never are)
@@ -320,6 +352,11 @@ class Integrator {
   }
 
   void kronsum(const double* u, double* r, const Epilogue& last) {
+    if (banded) {  // one stencil pass, the reference's per-entry rounding (banded.cu)
+      kronsum_banded(ctx, cplx, u, dims, band_cols, band_vals, a_active, r,
+                     last.kind == EPI_ADD_G, last.g, half);
+      return;
+    }
     std::vector<int> act;
     for (int mu = 0; mu < d; ++mu)
       if (a_active[mu]) act.push_back(mu);

@@ -202,3 +202,33 @@ def test_tucker_baseline_size_properties(kp, n):
     fwd = kp.tucker(t1, [kp.to_device(pm.numpy())] * 3)
     back = kp.tucker(fwd, [kp.to_device(pm.numpy().T)] * 3)
     assert torch.equal(back, t1)
+
+
+@pytest.mark.parametrize("dims", [(16, 12, 10), (300, 5, 4), (7, 260, 3), (64, 64, 64),
+                                  (20, 20, 20, 2)])
+def test_banded_kronsum_bitwise_vs_reference(kp, port, dims):
+    """Tridiagonal / periodic factors take the stencil path (banded.cu), which
+    follows the reference's dense FMA-chain rounding (incl. the KC=256 slices
+    at n=260, 300): bit-identical to the reference's kronsum_action."""
+    import pyoracle
+    r = rng(31)
+    t = rand(r, dims)
+    As = []
+    for mu, n in enumerate(dims):
+        if n == 2:
+            As.append(np.zeros((2, 2), order="F"))       # stacked-species factor
+        elif mu % 2:
+            As.append(port.fd_operator_1d(n, 0.3, 0.1))  # Dirichlet tridiagonal
+        else:
+            As.append(pyoracle.periodic_laplacian_1d(n, 0.7))  # periodic
+    got = kp.kronsum_action(t, As)
+    want = port.kronsum(t, As)
+    assert np.array_equal(got, want)
+
+
+def test_banded_kronsum_complex(kp, port):
+    import pyoracle
+    r = rng(32)
+    t = rand(r, (24, 20, 18), True)
+    As = [np.asfortranarray(0.5j * pyoracle.periodic_laplacian_1d(n, 0.5)) for n in t.shape]
+    assert rel2(kp.kronsum_action(t, As), port.kronsum(t, As)) < 1e-15
