@@ -116,6 +116,22 @@ int kp_kronsum_f64(kp_ctx* ctx, const double* t, const int* dims, int d,
 int kp_kronsum_c128(kp_ctx* ctx, const double* t, const int* dims, int d,
                     const double* const* as, double* out);
 
+/* The Kronecker-sum action on one slab of a slab-sharded tensor, for banded
+ * factors (at most three nonzeros per row: the configs' tridiagonal and
+ * periodic operators) -- kronsum_action (inc/mode_product.hpp:111-121) as a
+ * stencil with the reference's rounding.  u_ext holds the rank's slab of
+ * mode `slab_mode` (interior dims `dims`) plus one halo plane on each side
+ * (global planes k0-1 and k0+dims[slab_mode], modulo n_glob); r receives
+ * the interior.  as[mu] are the full n x n factors (n_glob for slab_mode).
+ * g (nullable) is added as in r = K u + g(u); the Brusselator's species mode
+ * must be the last mode. */
+int kp_kronsum_slab_f64(kp_ctx* ctx, const double* u_ext, const int* dims, int d,
+                        const double* const* as, int slab_mode, int k0, int n_glob,
+                        const kp_gfun* g, double* r);
+int kp_kronsum_slab_c128(kp_ctx* ctx, const double* u_ext, const int* dims, int d,
+                         const double* const* as, int slab_mode, int k0, int n_glob,
+                         const kp_gfun* g, double* r);
+
 /* Host-buffer variants (the drop-in path: host in, host out, H2D/D2H inside). */
 int kp_host_mode_product_f64(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
                              const double* m, int rows, int cols, double alpha, double beta,

@@ -71,6 +71,8 @@ _SIGS = {
     "kp_tucker_c128": (_I, [_CTX, _VP, _PI, _I, _PPD, _PI, _D, _VP]),
     "kp_kronsum_f64": (_I, [_CTX, _VP, _PI, _I, _PPD, _VP]),
     "kp_kronsum_c128": (_I, [_CTX, _VP, _PI, _I, _PPD, _VP]),
+    "kp_kronsum_slab_f64": (_I, [_CTX, _VP, _PI, _I, _PPD, _I, _I, _I, C.c_void_p, _VP]),
+    "kp_kronsum_slab_c128": (_I, [_CTX, _VP, _PI, _I, _PPD, _I, _I, _I, C.c_void_p, _VP]),
     "kp_host_mode_product_f64": (_I, [_CTX, _VP, _PI, _I, _I, _VP, _I, _I, _D, _D, _VP]),
     "kp_host_tucker_f64": (_I, [_CTX, _VP, _PI, _I, _PPD, _PI, _D, _VP]),
     "kp_host_tucker_c128": (_I, [_CTX, _VP, _PI, _I, _PPD, _PI, _D, _VP]),

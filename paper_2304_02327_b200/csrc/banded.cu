@@ -57,18 +57,32 @@ __global__ void band_scan_kernel(const double* __restrict__ a, int n, int comps,
 
 struct BandArgs {
   int d;
-  int n[4];
-  long long stride[4];
+  int n[4];               // output (interior) extents
+  long long stride[4];    // input strides (the input may carry halo planes)
   const int* cols[4];
   const double* vals[4];  // (re, im) pairs
   int active[4];
+  // slab sharding: mode `slab` holds global planes k0.. of n_glob with `halo`
+  // extra planes on each side in the input; -1 = unsharded
+  int slab, k0, n_glob, halo;
+  int species;            // index of the 2-species mode for a coupled g, -1 none
 };
+
+// input offset (in elements of `stride[mu]`) of column j relative to row i
+__device__ __forceinline__ long long col_off(const BandArgs& b, int mu, int i, int j) {
+  if (mu != b.slab) return (long long)(j - i);
+  const int lo = b.k0 - b.halo;
+  int loc = (j - lo) % b.n_glob;
+  if (loc < 0) loc += b.n_glob;
+  return (long long)(loc - (i - lo));
+}
 
 // Adds one mode's term at entry idx into the running value c: the
 // reference's FMA chain per KC slice, each slice folded as c = c + acc
 // (mode 0's first slice stores: has_c == false).
 __device__ __forceinline__ void term_real(const BandArgs& b, int mu, int imu, long long idx,
                                           const double* __restrict__ u, double& c, bool& has_c) {
+  // imu: GLOBAL row of mode mu; idx: input index of the entry
   const int* cs = b.cols[mu] + imu * 3;
   const double* v = b.vals[mu] + imu * 6;
   double acc = 0.0;
@@ -86,7 +100,7 @@ __device__ __forceinline__ void term_real(const BandArgs& b, int mu, int imu, lo
       slice = sl;
       acc = 0.0;
     }
-    acc = __fma_rn(v[2 * s], u[idx + (long long)(j - imu) * b.stride[mu]], acc);
+    acc = __fma_rn(v[2 * s], u[idx + col_off(b, mu, imu, j) * b.stride[mu]], acc);
   }
   if (slice >= 0) {
     c = has_c ? __dadd_rn(c, acc) : acc;
@@ -122,7 +136,7 @@ __device__ __forceinline__ void term_cplx(const BandArgs& b, int mu, int imu, lo
       acc = make_double2(0.0, 0.0);
     }
     acc = cmul_add(make_double2(v[2 * s], v[2 * s + 1]),
-                   u[idx + (long long)(j - imu) * b.stride[mu]], acc);
+                   u[idx + col_off(b, mu, imu, j) * b.stride[mu]], acc);
   }
   if (slice >= 0) {
     c = has_c ? make_double2(__dadd_rn(c.x, acc.x), __dadd_rn(c.y, acc.y)) : acc;
@@ -130,20 +144,21 @@ __device__ __forceinline__ void term_cplx(const BandArgs& b, int mu, int imu, lo
   }
 }
 
-// r = sum_mu u x_mu A_mu (+ g(t,u) when with_g), one entry per thread
+// r = sum_mu u x_mu A_mu (+ g(t,u) when with_g), one output entry per thread
 template <bool CPLX>
 __global__ void kronsum_band_kernel(BandArgs b, long long total, const double* __restrict__ u,
-                                    double* __restrict__ r, bool with_g, kp_gfun g,
-                                    long long half) {
+                                    double* __restrict__ r, bool with_g, kp_gfun g) {
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
-    long long rem = idx;
+    long long rem = idx, in = 0;
     int ii[4];
 #pragma unroll
     for (int mu = 0; mu < 4; ++mu) {
       if (mu < b.d) {
         ii[mu] = int(rem % b.n[mu]);
         rem /= b.n[mu];
+        in += (long long)(ii[mu] + (mu == b.slab ? b.halo : 0)) * b.stride[mu];
+        if (mu == b.slab) ii[mu] += b.k0;  // global row for the factor lookup
       }
     }
     if constexpr (!CPLX) {
@@ -152,12 +167,13 @@ __global__ void kronsum_band_kernel(BandArgs b, long long total, const double* _
 #pragma unroll
       for (int mu = 0; mu < 4; ++mu) {
         if (mu >= b.d || !b.active[mu]) continue;
-        term_real(b, mu, ii[mu], idx, u, acc, has);
+        term_real(b, mu, ii[mu], in, u, acc, has);
       }
       if (with_g) {
-        const bool second = half > 0 && idx >= half;
-        const double partner = half > 0 ? u[second ? idx - half : idx + half] : 0.0;
-        acc = __dadd_rn(acc, g_real(g, u[idx], partner, second));
+        const bool second = b.species >= 0 && ii[b.species] == 1;
+        const double partner =
+            b.species >= 0 ? u[second ? in - b.stride[b.species] : in + b.stride[b.species]] : 0.0;
+        acc = __dadd_rn(acc, g_real(g, u[in], partner, second));
       }
       r[idx] = acc;
     } else {
@@ -167,10 +183,10 @@ __global__ void kronsum_band_kernel(BandArgs b, long long total, const double* _
 #pragma unroll
       for (int mu = 0; mu < 4; ++mu) {
         if (mu >= b.d || !b.active[mu]) continue;
-        term_cplx(b, mu, ii[mu], idx, uc, acc, has);
+        term_cplx(b, mu, ii[mu], in, uc, acc, has);
       }
       if (with_g) {
-        const double2 gg = g_cplx(g, uc[idx]);
+        const double2 gg = g_cplx(g, uc[in]);
         acc = make_double2(__dadd_rn(acc.x, gg.x), __dadd_rn(acc.y, gg.y));
       }
       reinterpret_cast<double2*>(r)[idx] = acc;
@@ -179,6 +195,12 @@ __global__ void kronsum_band_kernel(BandArgs b, long long total, const double* _
 }
 
 }  // namespace
+
+// forward (defined below)
+void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<int>& dims,
+                    const std::vector<const int*>& cols, const std::vector<const double*>& vals,
+                    const std::vector<char>& active, double* r, bool with_g, const kp_gfun& g,
+                    long long half, int slab, int k0, int n_glob, int halo);
 
 // Scan a factor into caller-provided device arrays (3n ints, 6n doubles);
 // false if some row has more than three nonzeros.
@@ -226,7 +248,7 @@ bool kronsum_try_banded(kp_ctx* ctx, bool cplx, const double* t, const std::vect
     cols[mu] = c;
     vals[mu] = v;
   }
-  kronsum_banded(ctx, cplx, t, dims, cols, vals, active, out, false, kp_gfun{}, 0);
+  kronsum_banded(ctx, cplx, t, dims, cols, vals, active, out, false, kp_gfun{}, 0, -1, 0, 0, 0);
   return true;
 }
 
@@ -242,29 +264,109 @@ bool banded_kronsum_enabled() {
 void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<int>& dims,
                     const std::vector<const int*>& cols, const std::vector<const double*>& vals,
                     const std::vector<char>& active, double* r, bool with_g, const kp_gfun& g,
-                    long long half) {
+                    long long half, int slab, int k0, int n_glob, int halo) {
   const int d = int(dims.size());
   if (d > 4) throw invalid_argument("kronsum (banded): order > 4 unsupported");
   BandArgs b{};
   b.d = d;
-  long long st = 1;
+  b.slab = slab;
+  b.k0 = k0;
+  b.n_glob = n_glob;
+  b.halo = (slab >= 0) ? halo : 0;
+  b.species = -1;
+  if (half > 0) {
+    if (dims.back() != 2) throw invalid_argument("brusselator g: slowest mode must hold 2 species");
+    b.species = d - 1;
+  }
+  long long st = 1, total = 1;
   for (int mu = 0; mu < d; ++mu) {
     b.n[mu] = dims[mu];
     b.stride[mu] = st;
-    st *= dims[mu];
+    st *= dims[mu] + (mu == slab ? 2 * b.halo : 0);
+    total *= dims[mu];
     b.cols[mu] = cols[mu];
     b.vals[mu] = vals[mu];
     b.active[mu] = active[mu];
   }
-  const long long total = st;
   const unsigned grid =
       unsigned(std::max<long long>(1, std::min<long long>((total + 255) / 256, ctx->num_sms * 16LL)));
   if (cplx)
-    kronsum_band_kernel<true><<<grid, 256, 0, ctx->stream>>>(b, total, u, r, with_g, g, half);
+    kronsum_band_kernel<true><<<grid, 256, 0, ctx->stream>>>(b, total, u, r, with_g, g);
   else
-    kronsum_band_kernel<false><<<grid, 256, 0, ctx->stream>>>(b, total, u, r, with_g, g, half);
+    kronsum_band_kernel<false><<<grid, 256, 0, ctx->stream>>>(b, total, u, r, with_g, g);
   ctx->launches++;
   KP_CUDA(cudaGetLastError());
 }
 
 }  // namespace kp
+
+// ---- C ABI: the banded action on a slab with halo planes (sharded runs) ----
+using namespace kp;
+
+extern "C" int kp_kronsum_slab_f64(kp_ctx* ctx, const double* u_ext, const int* dims, int d,
+                                   const double* const* as, int slab_mode, int k0, int n_glob,
+                                   const kp_gfun* g, double* r);
+extern "C" int kp_kronsum_slab_c128(kp_ctx* ctx, const double* u_ext, const int* dims, int d,
+                                    const double* const* as, int slab_mode, int k0, int n_glob,
+                                    const kp_gfun* g, double* r);
+
+namespace {
+int slab_impl(kp_ctx* ctx, bool cplx, const double* u_ext, const int* dims, int d,
+              const double* const* as, int slab_mode, int k0, int n_glob, const kp_gfun* g,
+              double* r) {
+  try {
+    if (!ctx) throw invalid_argument("kronphi_b200: null context");
+    KP_CUDA(cudaSetDevice(ctx->device));
+    if (d <= 0 || d > 4 || !dims || !as)
+      throw invalid_argument("kronsum_slab: order must be 1..4");
+    std::vector<int> dv(dims, dims + d);
+    if (slab_mode < 0 || slab_mode >= d) throw invalid_argument("kronsum_slab: bad slab mode");
+    std::vector<const int*> cols(d);
+    std::vector<const double*> vals(d);
+    std::vector<char> active(d, 1);
+    for (int mu = 0; mu < d; ++mu) {
+      const int n = (mu == slab_mode) ? n_glob : dv[mu];
+      int* c = static_cast<int*>(ctx->ws.get(30 + mu, sizeof(int) * 3 * size_t(n)));
+      double* v = static_cast<double*>(ctx->ws.get(34 + mu, sizeof(double) * 6 * size_t(n)));
+      if (!band_scan(ctx, as[mu], n, cplx, c, v))
+        throw invalid_argument("kronsum_slab: factor " + std::to_string(mu) +
+                               " has more than three nonzeros in a row");
+      cols[mu] = c;
+      vals[mu] = v;
+      // an all-zero factor (the stacked species mode) contributes nothing
+      if (n <= 2) {
+        std::vector<int> hc(3 * size_t(n));
+        KP_CUDA(cudaMemcpy(hc.data(), c, hc.size() * sizeof(int), cudaMemcpyDeviceToHost));
+        bool any = false;
+        for (int x : hc) any |= (x >= 0);
+        active[mu] = any;
+      }
+    }
+    long long half = 0;
+    if (g && g->kind == KP_G_BRUSSELATOR) half = 1;  // species = last mode
+    kronsum_banded(ctx, cplx, u_ext, dv, cols, vals, active, r, g != nullptr,
+                   g ? *g : kp_gfun{}, half, slab_mode, k0, n_glob, 1);
+    return KP_OK;
+  } catch (const std::invalid_argument& e) {
+    kp_set_last_error(e.what());
+    return KP_EINVAL;
+  } catch (const kp::cuda_error& e) {
+    kp_set_last_error(e.what());
+    return KP_ECUDA;
+  } catch (const std::exception& e) {
+    kp_set_last_error(e.what());
+    return KP_ERUNTIME;
+  }
+}
+}  // namespace
+
+extern "C" int kp_kronsum_slab_f64(kp_ctx* ctx, const double* u_ext, const int* dims, int d,
+                                   const double* const* as, int slab_mode, int k0, int n_glob,
+                                   const kp_gfun* g, double* r) {
+  return slab_impl(ctx, false, u_ext, dims, d, as, slab_mode, k0, n_glob, g, r);
+}
+extern "C" int kp_kronsum_slab_c128(kp_ctx* ctx, const double* u_ext, const int* dims, int d,
+                                    const double* const* as, int slab_mode, int k0, int n_glob,
+                                    const kp_gfun* g, double* r) {
+  return slab_impl(ctx, true, u_ext, dims, d, as, slab_mode, k0, n_glob, g, r);
+}

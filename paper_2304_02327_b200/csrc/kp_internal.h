@@ -134,10 +134,13 @@ bool banded_kronsum_enabled();  // KP_KRONSUM=dense disables
 bool band_of(kp_ctx* ctx, const double* a, int n, bool cplx, int** cols, double** vals);
 bool kronsum_try_banded(kp_ctx* ctx, bool cplx, const double* t, const std::vector<int>& dims,
                         const double* const* as, double* out);
+// half > 0: Brusselator g (species = last mode).  slab >= 0: the input holds
+// `halo` extra planes on each side of mode `slab`, whose interior starts at
+// global plane k0 of n_glob (sharded runs); slab = -1: plain tensor.
 void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<int>& dims,
                     const std::vector<const int*>& cols, const std::vector<const double*>& vals,
                     const std::vector<char>& active, double* r, bool with_g, const kp_gfun& g,
-                    long long half);
+                    long long half, int slab = -1, int k0 = 0, int n_glob = 0, int halo = 0);
 
 // ---- elementwise (elementwise.cu) ----
 // z = fma(b, y, x): axpy is (b=alpha, y=x, x=y, z=y), add_scaled is (b=alpha, y=y, x=x)

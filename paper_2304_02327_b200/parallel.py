@@ -10,11 +10,14 @@ from the same inputs in the same k order as on one GPU, so the sharded run is
 bit-identical to the single-GPU one (tests/test_parallel.py checks this on
 CPU with world size 2; the GPU backend reuses the single-GPU kernels).
 
-Operations per step (unfused, same rounding as the fused single-GPU path):
-  ExpEuler : kronsum (3 transposes) + Tucker (2)
-  ETD2RK   : kronsum (3) + Tucker (2) + Tucker (2)
-  Lawson2b : 2 Tuckers over the stacked pair (2)
-The transposes move N_local*(P-1)/P entries each; DESIGN.md 7 has the model.
+Per step (unfused, same rounding as the fused single-GPU path), with the
+configs' banded factors the Kronecker sum is the stencil pass of banded.cu on
+the slab plus a one-plane halo exchange (batch_isend_irecv):
+  ExpEuler : halo + 3 all-to-alls (Tucker in, u to pencil, result back)
+  ETD2RK   : halo + 5 all-to-alls
+  Lawson2b : 4 all-to-alls (two Tuckers, each in and out)
+(dense factors: the Kronecker sum's last-mode term takes 2 more).  Each
+all-to-all moves N_local (P-1)/P entries per rank; DESIGN.md 7 has the model.
 """
 from __future__ import annotations
 
@@ -82,6 +85,24 @@ def pencil_to_slab(y, lay: Layout, comm):
     return recv.view(P, S, Cl, Bp, A).permute(1, 2, 0, 3, 4).contiguous().view(-1)
 
 
+def halo_extend(x, lay: Layout, comm):
+    """Flat slab (A, B, C/P, S) -> flat (A, B, C/P + 2, S) with one halo plane
+    of the sharded mode on each side: global planes k0-1 and k1 (periodic in
+    the rank index; a Dirichlet factor never reads the wrapped plane)."""
+    A, B, S, P = lay.A, lay.B, lay.S, lay.P
+    Cl = lay.C // P
+    xs = x.view(S, Cl, A * B)
+    first = xs[:, 0, :].contiguous()
+    last = xs[:, Cl - 1, :].contiguous()
+    left, right = torch.empty_like(first), torch.empty_like(last)
+    comm.exchange_halos(first, last, left, right)
+    ext = torch.empty((S, Cl + 2, A * B), dtype=x.dtype, device=x.device)
+    ext[:, 1:Cl + 1, :] = xs
+    ext[:, 0, :] = left
+    ext[:, Cl + 1, :] = right
+    return ext.view(-1)
+
+
 class Comm:
     """Equal-split all-to-all on a torch.distributed group (NCCL on GPUs)."""
 
@@ -99,6 +120,35 @@ class Comm:
                                    group=self.group)
         else:
             dist.all_to_all_single(recv, send, group=self.group)
+
+    def exchange_halos(self, first, last, left, right):
+        """left <- last plane of rank-1, right <- first plane of rank+1 (cyclic)."""
+        if self.P == 1:
+            left.copy_(last)
+            right.copy_(first)
+            return
+        prev, nxt = (self.rank - 1) % self.P, (self.rank + 1) % self.P
+        g = lambda r: dist.get_global_rank(self.group, r) if self.group is not None else r
+        view = torch.view_as_real if torch.is_complex(first) else (lambda t: t)
+        ops = [dist.P2POp(dist.isend, view(last), g(nxt), self.group, 0),
+               dist.P2POp(dist.irecv, view(left), g(prev), self.group, 0),
+               dist.P2POp(dist.isend, view(first), g(prev), self.group, 1),
+               dist.P2POp(dist.irecv, view(right), g(nxt), self.group, 1)]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
+class LocalComm:
+    """World of one rank without torch.distributed (the unsharded reference
+    run of the sharded code path)."""
+    P, rank = 1, 0
+
+    def all_to_all(self, recv, send):
+        recv.copy_(send)
+
+    def exchange_halos(self, first, last, left, right):
+        left.copy_(last)
+        right.copy_(first)
 
 
 # ----------------------------------------------------------------- backends
@@ -140,6 +190,17 @@ class CudaBackend:
         self.check(f(self.ctx.h, C.byref(g), 0.0, u.data_ptr(), self.ints(dims), len(dims),
                      out.data_ptr()))
 
+    def kronsum_slab(self, u_ext, dims, K, slab_mode, k0, n_glob, g, out):
+        """r = K u + g(u) on a slab with halo planes (kp_kronsum_slab_*)."""
+        import ctypes as C
+        from ._lib import ptr_array
+        self._sync_stream()
+        f = self.ctx.lib.kp_kronsum_slab_c128 if torch.is_complex(u_ext) else \
+            self.ctx.lib.kp_kronsum_slab_f64
+        self.check(f(self.ctx.h, u_ext.data_ptr(), self.ints(dims), len(dims),
+                     ptr_array([k.data_ptr() for k in K]), slab_mode, k0, n_glob,
+                     C.cast(C.byref(g), C.c_void_p) if g is not None else None, out.data_ptr()))
+
     def fma(self, alpha, x, y, out):
         """out = fma(alpha, x, y) elementwise (componentwise for complex)."""
         self._sync_stream()
@@ -156,7 +217,9 @@ class ShardedIntegrator:
     (n x n) torch tensors on this rank's device, identical on every rank."""
 
     def __init__(self, backend, comm, method, spatial, species, K, g, tau, f1, pref1, f2=None,
-                 pref2=1.0, fold1=1.0, fold2=1.0):
+                 pref2=1.0, fold1=1.0, fold2=1.0, K_all=None, banded=False):
+        self.K_all = K_all if K_all is not None else K
+        self.banded = banded
         self.be, self.comm = backend, comm
         self.method = method
         self.spatial = list(spatial)
@@ -198,14 +261,28 @@ class ShardedIntegrator:
         self.be.eval_g(self.g, u_p, self.pd, gu)
         return r_p + gu  # exact IEEE add, as the fused EPI_ADD_G
 
+    def kronsum_g_banded(self, u):
+        """r = K u + g(u) in slab layout: banded stencil with a one-plane
+        halo exchange instead of transposes (banded.cu, same rounding as the
+        single-GPU path)."""
+        ext = halo_extend(u, self.lay, self.comm)
+        r = torch.empty_like(u)
+        k0 = self.comm.rank * (self.spatial[-1] // self.comm.P)
+        self.be.kronsum_slab(ext, self.sd, self.K_all, self.d - 1, k0, self.spatial[-1], self.g,
+                             r)
+        return r
+
     def step(self, u):
         """u (slab) -> u' (slab)."""
         tau = self.tau
         m = self.method
         if m in ("exp_euler", "etd2rk"):
             u_p = slab_to_pencil(u, self.lay, self.comm)
-            r_p = self.kronsum_g(u, u_p)
-            r = pencil_to_slab(r_p, self.lay, self.comm)
+            if self.banded:
+                r = self.kronsum_g_banded(u)
+            else:
+                r_p = self.kronsum_g(u, u_p)
+                r = pencil_to_slab(r_p, self.lay, self.comm)
             y1 = self.tucker(r, self.f1, self.pref1, self.fold1)          # pencil
             stage = torch.empty_like(y1)
             self.be.fma(tau, y1, u_p, stage)                              # u + tau*SP1(r)
@@ -311,8 +388,21 @@ def make_sharded_integrator(kp, backend, comm, method, dims_local, K, g, t0, t_f
         f2, p2, fold2, _ = split_factors(kp, K, tau, 2)
     else:
         raise ValueError(f"sharded integrate: unsupported method {method}")
+    banded = hasattr(backend, "kronsum_slab") and banded_kronsum_enabled() and \
+        all(_is_banded(kp.to_host(k)) for k in K)
     return ShardedIntegrator(backend, comm, method, spatial, species, spatial_K, g, tau,
-                             f1[:d], p1, f2[:d] if f2 else None, p2, fold1, fold2)
+                             f1[:d], p1, f2[:d] if f2 else None, p2, fold1, fold2,
+                             K_all=list(K), banded=banded)
+
+
+def banded_kronsum_enabled():
+    import os
+    return os.environ.get("KP_KRONSUM", "") != "dense"
+
+
+def _is_banded(a):
+    """At most three nonzeros per row (the stencil form of banded.cu)."""
+    return bool(np.all(np.count_nonzero(np.asarray(a), axis=1) <= 3))
 
 
 def sharded_integrate(kp, backend, comm, method, u_local, dims_local, K, g, t0, t_final,

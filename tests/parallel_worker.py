@@ -40,6 +40,41 @@ class CpuBackend:
     def fma(self, alpha, x, y, out):
         out.copy_(torch.from_numpy(np.asarray(alpha * x.numpy() + y.numpy())))
 
+    def kronsum_slab(self, u_ext, dims, K, slab_mode, k0, n_glob, g, out):
+        """numpy restatement of kp_kronsum_slab (rows' nonzeros in increasing
+        column order; halo planes at local 0 and Cl+1 of the slab mode)."""
+        d = len(dims)
+        ext = list(dims)
+        ext[slab_mode] += 2
+        U = u_ext.numpy().reshape(ext, order="F")
+        Cl = dims[slab_mode]
+        interior = np.take(U, np.arange(1, Cl + 1), axis=slab_mode)
+        R = None
+        for mu in range(d):
+            A = K[mu].numpy()
+            if not A.any():
+                continue
+            term = np.zeros(dims, dtype=U.dtype)
+            for i in range(dims[mu]):
+                gi = i + k0 if mu == slab_mode else i
+                acc = None
+                for j in np.nonzero(A[gi])[0]:
+                    if mu == slab_mode:
+                        src = np.take(U, [(j - (k0 - 1)) % n_glob], axis=mu)
+                    else:
+                        src = np.take(interior, [j], axis=mu)
+                    p = A[gi, j] * src
+                    acc = p if acc is None else acc + p
+                if acc is not None:
+                    idx = [slice(None)] * d
+                    idx[mu] = slice(i, i + 1)
+                    term[tuple(idx)] = acc
+            R = term if R is None else term + R
+        if g is not None:
+            og = pyoracle.gfun(g.kind, *list(g.p))
+            R = R + port.eval_g(og, 0.0, np.asfortranarray(interior))
+        out.copy_(torch.from_numpy(np.asfortranarray(R).reshape(-1, order="F")))
+
 
 class KP:
     """CPU stand-in for the package's device factor builder (oracle build)."""
@@ -58,13 +93,6 @@ class KP:
     @staticmethod
     def to_host(t):
         return t.numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
-
-
-class OneRank:
-    P, rank = 1, 0
-
-    def all_to_all(self, recv, send):
-        recv.copy_(send)
 
 
 def main():
@@ -94,7 +122,7 @@ def main():
     if rank == 0:
         axis = full.ndim - 2 if species == 2 else full.ndim - 1
         glob = np.concatenate([p.numpy().reshape(loc.shape, order="F") for p in parts], axis=axis)
-        one = parallel.sharded_integrate(KP, be, OneRank(), method,
+        one = parallel.sharded_integrate(KP, be, parallel.LocalComm(), method,
                                          torch.from_numpy(full.reshape(-1, order="F").copy()),
                                          list(full.shape), K, cfg.g, 0.0, cfg.t_final,
                                          cfg.n_steps)

@@ -23,9 +23,10 @@ def nccl1():
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("kronsum", ["banded", "dense"])
 @pytest.mark.parametrize("case,method", [("ac3d", "etd2rk"), ("bru", "etd2rk"),
                                          ("bru", "lawson2b"), ("nls", "exp_euler")])
-def test_sharded_p1_bitwise_equals_fused(kp, nccl1, case, method):
+def test_sharded_p1_bitwise_equals_fused(kp, nccl1, case, method, kronsum):
     import torch
     from paper_2304_02327_b200 import parallel, problems
     if case == "ac3d":
@@ -35,18 +36,19 @@ def test_sharded_p1_bitwise_equals_fused(kp, nccl1, case, method):
     else:
         cfg = problems.nls(n=16, n_steps=4, method=method)
     cfg.method = method
-    # the sharded path applies K densely (its mode d lives in the pencil
-    # layout); compare with the fused single-GPU path in the same form
-    os.environ["KP_KRONSUM"] = "dense"
+    # both Kronecker-sum forms: the banded stencil (halo exchange when
+    # sharded) and the dense one (pencil transposes when sharded)
+    if kronsum == "dense":
+        os.environ["KP_KRONSUM"] = "dense"
     try:
         want = kp.integrate_config(method, cfg.u0, cfg.K, cfg.g, 0.0, cfg.t_final, cfg.n_steps)
+        be = parallel.CudaBackend(0)
+        comm = parallel.Comm()
+        K = [kp.to_device(k) for k in cfg.K]
+        flat = kp.to_device(cfg.u0).permute(*reversed(range(cfg.u0.ndim))).reshape(-1)
+        res = parallel.sharded_integrate(kp, be, comm, method, flat, list(cfg.u0.shape), K,
+                                         cfg.g, 0.0, cfg.t_final, cfg.n_steps)
     finally:
         os.environ.pop("KP_KRONSUM", None)
-    be = parallel.CudaBackend(0)
-    comm = parallel.Comm()
-    K = [kp.to_device(k) for k in cfg.K]
-    flat = kp.to_device(cfg.u0).permute(*reversed(range(cfg.u0.ndim))).reshape(-1)
-    res = parallel.sharded_integrate(kp, be, comm, method, flat, list(cfg.u0.shape), K, cfg.g,
-                                     0.0, cfg.t_final, cfg.n_steps)
     got = res.cpu().numpy().reshape(cfg.u0.shape, order="F")
     assert np.array_equal(got, want), np.abs(got - want).max()
