@@ -101,6 +101,10 @@ def run_integrators(kp, peak):
         spec = kp.ProblemSpec(K, c.g, ud, 0.0, c.t_final)
         m = kp.parse_method(c.method)
         note = None
+        try:  # warm-up (lazy kernel loading, workspace sizing); 2 steps of 50 tau
+            kp.integrate(spec, kp.StepperConfig(m, 2))
+        except kp.DivergenceError:
+            pass
         t0 = time.perf_counter()
         try:
             r = kp.integrate(spec, kp.StepperConfig(m, c.n_steps))
@@ -153,6 +157,10 @@ def run_sharded_integrators(kp, peak, world, rank, local):
         try:
             it = parallel.make_sharded_integrator(kp, be, comm, c.method, list(c.u0.shape), K,
                                                   c.g, 0.0, c.t_final, c.n_steps)
+            try:  # warm-up (untimed)
+                it.run(flat.clone(), 2)
+            except kp.DivergenceError:
+                pass
             dist.barrier()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -525,21 +525,25 @@ class Integrator {
     const int init[2] = {0, INT_MAX};
     KP_CUDA(cudaMemcpyAsync(ctr, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
     double* ub[2] = {u, buf(S_U2, n_entries)};
-    cudaEvent_t e0, e1;
-    KP_CUDA(cudaEventCreate(&e0));
-    KP_CUDA(cudaEventCreate(&e1));
+    // device time of the loop = [e0,e1] (first, eager step) + [e2,e3] (graph
+    // replays + tail); the host-side capture/instantiation between e1 and e2
+    // is set-up, not stepping, and is excluded
+    cudaEvent_t ev[4];
+    for (auto& e : ev) KP_CUDA(cudaEventCreate(&e));
     long n = 0;
-    // first step eagerly: sizes every workspace slot before any capture
-    KP_CUDA(cudaEventRecord(e0, ctx->stream));
     auto one = [&](long k) {
       step(ub[k & 1], ub[(k + 1) & 1], t0 + double(k) * tau, bad, ctr);
       tick_kernel<<<1, 1, 0, ctx->stream>>>(ctr);
       ctx->launches++;
     };
+    // first step eagerly: sizes every workspace slot before any capture
+    KP_CUDA(cudaEventRecord(ev[0], ctx->stream));
     one(n++);
+    KP_CUDA(cudaEventRecord(ev[1], ctx->stream));
+    cudaGraphExec_t exec = nullptr;
+    unsigned long long per = 0;
     if (use_graph && n_steps - n >= 4) {
       cudaGraph_t graph;
-      cudaGraphExec_t exec;
       const unsigned long long l0 = ctx->launches;
       KP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
       // two steps: ub1 -> ub0 -> ub1 (n is odd here); t is unused by the
@@ -549,29 +553,33 @@ class Integrator {
       step(ub[0], ub[1], 0.0, bad, ctr);
       tick_kernel<<<1, 1, 0, ctx->stream>>>(ctr);
       KP_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
-      const unsigned long long per = ctx->launches - l0 + 2;
+      per = ctx->launches - l0 + 2;
       ctx->launches = l0;
       KP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      cudaGraphDestroy(graph);
+    }
+    KP_CUDA(cudaEventRecord(ev[2], ctx->stream));
+    if (exec) {
       while (n_steps - n >= 2) {
         KP_CUDA(cudaGraphLaunch(exec, ctx->stream));
         ctx->launches += per;
         n += 2;
       }
-      cudaGraphExecDestroy(exec);
-      cudaGraphDestroy(graph);
     }
     while (n < n_steps) one(n++);
-    KP_CUDA(cudaEventRecord(e1, ctx->stream));
+    KP_CUDA(cudaEventRecord(ev[3], ctx->stream));
+    if (exec) cudaGraphExecDestroy(exec);
     if (n_steps & 1)
       KP_CUDA(cudaMemcpyAsync(u, ub[1], size_t(n_entries) * comps * sizeof(double),
                               cudaMemcpyDeviceToDevice, ctx->stream));
     int hb[2];
     KP_CUDA(cudaMemcpyAsync(hb, ctr, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
     KP_CUDA(cudaStreamSynchronize(ctx->stream));
-    float ms = 0.f;
-    KP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    float ms1 = 0.f, ms2 = 0.f;
+    KP_CUDA(cudaEventElapsedTime(&ms1, ev[0], ev[1]));
+    KP_CUDA(cudaEventElapsedTime(&ms2, ev[2], ev[3]));
+    for (auto& e : ev) cudaEventDestroy(e);
+    const float ms = ms1 + ms2;
     diverged_at = (hb[1] != INT_MAX) ? long(hb[1]) : 0;
     return ms * 1e-3;
   }
