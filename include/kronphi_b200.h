@@ -60,10 +60,19 @@ typedef struct kp_ctx kp_ctx;
 #define KP_G_ALLEN_CAHN 3  /* u - u^3 */
 #define KP_G_BRUSSELATOR 4 /* species stacked as the slowest mode (size 2); p[0]=a, p[1]=b */
 #define KP_G_NLS 5         /* -i |u|^2 u, complex */
+#define KP_G_ADR 6         /* 1/(1+u^2) + e^t psi_a - 1/(1+e^{2t} u0^2): the reference's
+                              ADR source (src/problems.cpp:101-115); aux[0] = psi_a,
+                              aux[1] = u0^2 (device arrays shaped like u) */
 
+/* step_ctr/t0/tau: when step_ctr is set (the integrators do this), a
+ * time-dependent g reads t = t0 + (*step_ctr) * tau (+ the stage offset) from
+ * the device step counter, so captured CUDA-graph steps see the right t. */
 typedef struct {
   int kind;
   double p[4];
+  const double* aux[2];
+  const int* step_ctr;
+  double t0, tau;
 } kp_gfun;
 
 /* ---------------- context, memory, errors ---------------- */

@@ -52,12 +52,15 @@ enum {
   KPO_G_ALLEN_CAHN = 3,  /* g = u - u^3                    BASELINE configs 1,3 */
   KPO_G_BRUSSELATOR = 4, /* (a-(b+1)u+u^2 v, b u-u^2 v), species stacked as the
                             slowest mode of size 2; p0=a, p1=b   BASELINE config 4 */
-  KPO_G_NLS = 5          /* g = -i |u|^2 u (complex only)   BASELINE config 5 */
+  KPO_G_NLS = 5,         /* g = -i |u|^2 u (complex only)   BASELINE config 5 */
+  KPO_G_ADR = 6          /* 1/(1+u^2) + e^t psi_a - 1/(1+e^{2t} u0^2), aux = {psi_a, u0^2}
+                            src/problems.cpp:101-115 */
 };
 
 typedef struct {
   int kind;
   double p[4];
+  const double* aux[2];
 } kpo_gfun;
 
 const char* kpo_last_error(void);

@@ -46,14 +46,22 @@ class Divergence(OracleError):
 
 
 class GFun(C.Structure):
-    _fields_ = [("kind", C.c_int), ("p", C.c_double * 4)]
+    _fields_ = [("kind", C.c_int), ("p", C.c_double * 4), ("aux", C.c_void_p * 2)]
 
 
-def gfun(kind, *params):
+G_ADR = 6
+
+
+def gfun(kind, *params, aux=None):
+    """aux: host arrays (ADR: psi_a, u0^2), kept alive on the descriptor."""
     g = GFun()
     g.kind = kind
     for i, v in enumerate(params):
         g.p[i] = v
+    if aux is not None:
+        g._keep = [np.asfortranarray(a, dtype=np.float64) for a in aux]
+        for i, a in enumerate(g._keep):
+            g.aux[i] = a.ctypes.data
     return g
 
 
@@ -250,6 +258,20 @@ class Oracle:
         if s < 0:
             raise OracleError(2, self.fn("last_error")().decode())
         return s
+
+    def run_adr(self, n1, n2, n3, method, n_steps):
+        """The reference's own ADR experiment (reference harness only):
+        final state and rel. inf-norm error vs e^t u0 at T = 1."""
+        if self.kind != "reference":
+            raise RuntimeError("run_adr needs the reference harness")
+        out = np.zeros((n1, n2, n3), order="F")
+        err, sec = C.c_double(0), C.c_double(0)
+        f = self.fn("run_adr")
+        f.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_long, C.POINTER(C.c_double),
+                      C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        self._check(f(n1, n2, n3, METHODS.get(method, method), n_steps, _dp(out), C.byref(err),
+                      C.byref(sec)))
+        return out, err.value, sec.value
 
     def num_threads(self):
         return self.fn("num_threads")() if self.kind == "reference" else 1

@@ -393,6 +393,25 @@ int kpr_integrate_c128(int method, const double* u0, const int* dims, int d,
   });
 }
 
+// The reference's own ADR experiment (src/problems.cpp:45-128 build_adr,
+// run_adr's error measure src/bench_runner.cpp:181-203): integrate with the
+// reference's g and report the final state and the relative inf-norm error
+// against e^t u0.
+int kpr_run_adr(int n1, int n2, int n3, int method, long n_steps, double* u_final,
+                double* rel_err, double* seconds) {
+  return guard([&] {
+    const ADRProblem p = build_adr(n1, n2, n3);
+    StepperConfig c;
+    c.method = to_method(method);
+    c.n_steps = n_steps;
+    const IntegrateResult r = integrate(p.to_problem_spec(), c);
+    from(r.final.data(), r.final.size(), u_final);
+    const Tensor<double> ex = p.exact(1.0);
+    *rel_err = diff_norm_inf(r.final, ex) / ex.norm_inf();
+    if (seconds) *seconds = r.wallclock_s;
+  });
+}
+
 // ---- timing helpers for bench.py's reference arm (steady_clock, in-process;
 // inputs are built once outside the timed region) ----
 

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(HERE, "lib", "libkronphi_b200.so")
 
 KP_OK, KP_EINVAL, KP_ERUNTIME, KP_EDIVERGE, KP_ECUDA = range(5)
 LAWSON_EULER, LAWSON2B, EXP_EULER, EXP_EULER_LS, ETD2RK = range(5)
-G_ZERO, G_SQUARE, G_CONST, G_ALLEN_CAHN, G_BRUSSELATOR, G_NLS = range(6)
+G_ZERO, G_SQUARE, G_CONST, G_ALLEN_CAHN, G_BRUSSELATOR, G_NLS, G_ADR = range(7)
 
 
 class KronphiError(RuntimeError):
@@ -43,7 +43,10 @@ class DivergenceError(KronphiError):
 
 
 class GFun(C.Structure):
-    _fields_ = [("kind", C.c_int), ("p", C.c_double * 4)]
+    """kp_gfun (include/kronphi_b200.h): nonlinearity id, parameters, device
+    auxiliary fields (ADR) and the integrators' step-counter time hook."""
+    _fields_ = [("kind", C.c_int), ("p", C.c_double * 4), ("aux", C.c_void_p * 2),
+                ("step_ctr", C.c_void_p), ("t0", C.c_double), ("tau", C.c_double)]
 
 
 _D, _I, _L, _SZ = C.c_double, C.c_int, C.c_long, C.c_size_t

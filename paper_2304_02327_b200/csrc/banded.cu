@@ -147,7 +147,7 @@ __device__ __forceinline__ void term_cplx(const BandArgs& b, int mu, int imu, lo
 // r = sum_mu u x_mu A_mu (+ g(t,u) when with_g), one output entry per thread
 template <bool CPLX>
 __global__ void kronsum_band_kernel(BandArgs b, long long total, const double* __restrict__ u,
-                                    double* __restrict__ r, bool with_g, kp_gfun g) {
+                                    double* __restrict__ r, bool with_g, kp_gfun g, double t) {
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     long long rem = idx, in = 0;
@@ -173,7 +173,7 @@ __global__ void kronsum_band_kernel(BandArgs b, long long total, const double* _
         const bool second = b.species >= 0 && ii[b.species] == 1;
         const double partner =
             b.species >= 0 ? u[second ? in - b.stride[b.species] : in + b.stride[b.species]] : 0.0;
-        acc = __dadd_rn(acc, g_real(g, u[in], partner, second));
+        acc = __dadd_rn(acc, g_real(g, u[in], partner, second, idx, t));
       }
       r[idx] = acc;
     } else {
@@ -200,7 +200,7 @@ __global__ void kronsum_band_kernel(BandArgs b, long long total, const double* _
 void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<int>& dims,
                     const std::vector<const int*>& cols, const std::vector<const double*>& vals,
                     const std::vector<char>& active, double* r, bool with_g, const kp_gfun& g,
-                    long long half, int slab, int k0, int n_glob, int halo);
+                    long long half, int slab, int k0, int n_glob, int halo, double t);
 
 // Scan a factor into caller-provided device arrays (3n ints, 6n doubles);
 // false if some row has more than three nonzeros.
@@ -248,7 +248,8 @@ bool kronsum_try_banded(kp_ctx* ctx, bool cplx, const double* t, const std::vect
     cols[mu] = c;
     vals[mu] = v;
   }
-  kronsum_banded(ctx, cplx, t, dims, cols, vals, active, out, false, kp_gfun{}, 0, -1, 0, 0, 0);
+  kronsum_banded(ctx, cplx, t, dims, cols, vals, active, out, false, kp_gfun{}, 0, -1, 0, 0, 0,
+                 0.0);
   return true;
 }
 
@@ -264,7 +265,7 @@ bool banded_kronsum_enabled() {
 void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<int>& dims,
                     const std::vector<const int*>& cols, const std::vector<const double*>& vals,
                     const std::vector<char>& active, double* r, bool with_g, const kp_gfun& g,
-                    long long half, int slab, int k0, int n_glob, int halo) {
+                    long long half, int slab, int k0, int n_glob, int halo, double t) {
   const int d = int(dims.size());
   if (d > 4) throw invalid_argument("kronsum (banded): order > 4 unsupported");
   BandArgs b{};
@@ -291,9 +292,9 @@ void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<i
   const unsigned grid =
       unsigned(std::max<long long>(1, std::min<long long>((total + 255) / 256, ctx->num_sms * 16LL)));
   if (cplx)
-    kronsum_band_kernel<true><<<grid, 256, 0, ctx->stream>>>(b, total, u, r, with_g, g);
+    kronsum_band_kernel<true><<<grid, 256, 0, ctx->stream>>>(b, total, u, r, with_g, g, t);
   else
-    kronsum_band_kernel<false><<<grid, 256, 0, ctx->stream>>>(b, total, u, r, with_g, g);
+    kronsum_band_kernel<false><<<grid, 256, 0, ctx->stream>>>(b, total, u, r, with_g, g, t);
   ctx->launches++;
   KP_CUDA(cudaGetLastError());
 }
@@ -345,7 +346,7 @@ int slab_impl(kp_ctx* ctx, bool cplx, const double* u_ext, const int* dims, int 
     long long half = 0;
     if (g && g->kind == KP_G_BRUSSELATOR) half = 1;  // species = last mode
     kronsum_banded(ctx, cplx, u_ext, dv, cols, vals, active, r, g != nullptr,
-                   g ? *g : kp_gfun{}, half, slab_mode, k0, n_glob, 1);
+                   g ? *g : kp_gfun{}, half, slab_mode, k0, n_glob, 1, 0.0);
     return KP_OK;
   } catch (const std::invalid_argument& e) {
     kp_set_last_error(e.what());

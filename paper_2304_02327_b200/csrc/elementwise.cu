@@ -35,13 +35,13 @@ __global__ void scale_kernel(size_t n, double a, const double* __restrict__ x,
     y[i] = __dmul_rn(a, x[i]);
 }
 
-__global__ void g_real_kernel(kp_gfun g, size_t n, size_t half, const double* __restrict__ u,
-                              double* __restrict__ out) {
+__global__ void g_real_kernel(kp_gfun g, double t, size_t n, size_t half,
+                              const double* __restrict__ u, double* __restrict__ out) {
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const bool second = half > 0 && i >= half;
     const double partner = half > 0 ? u[second ? i - half : i + half] : 0.0;
-    out[i] = g_real(g, u[i], partner, second);
+    out[i] = g_real(g, u[i], partner, second, (long long)i, t);
   }
 }
 
@@ -94,14 +94,14 @@ void launch_scale(kp_ctx* ctx, size_t n, double a, const double* x, double* y) {
   KP_CUDA(cudaGetLastError());
 }
 
-void launch_eval_g(kp_ctx* ctx, const kp_gfun& g, double /*t*/, const double* u, size_t n,
+void launch_eval_g(kp_ctx* ctx, const kp_gfun& g, double t, const double* u, size_t n,
                    size_t half, bool cplx, double* out) {
   if (n == 0) return;
   if (cplx)
     g_cplx_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(
         g, n, reinterpret_cast<const double2*>(u), reinterpret_cast<double2*>(out));
   else
-    g_real_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(g, n, half, u, out);
+    g_real_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(g, t, n, half, u, out);
   ctx->launches++;
   KP_CUDA(cudaGetLastError());
 }

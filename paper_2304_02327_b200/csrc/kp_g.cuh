@@ -11,12 +11,26 @@
 
 namespace kp {
 
+// Time of a g evaluation: absolute t, or (integrators) the device step
+// counter's t0 + n tau plus the stage offset t.
+__device__ __forceinline__ double g_time(const kp_gfun& g, double t) {
+  return g.step_ctr ? g.t0 + double(*g.step_ctr) * g.tau + t : t;
+}
+
 // Real g at one entry.  x = u at this entry; partner = the other species'
 // value at the same grid point (Brusselator only); second = whether this
-// entry belongs to the second species (v).
-__device__ __forceinline__ double g_real(const kp_gfun& g, double x, double partner,
-                                         bool second) {
+// entry belongs to the second species (v); idx = the entry's linear index
+// (auxiliary fields); t = time argument (see g_time).
+__device__ __forceinline__ double g_real(const kp_gfun& g, double x, double partner, bool second,
+                                         long long idx, double t) {
   switch (g.kind) {
+    case KP_G_ADR: {  // src/problems.cpp:101-115 (FMA where g++ contracts a*b + c)
+      const double et = exp(g_time(g, t));
+      const double e2t = __dmul_rn(et, et);
+      const double a = __ddiv_rn(1.0, __fma_rn(x, x, 1.0));
+      const double b = __ddiv_rn(1.0, __fma_rn(e2t, g.aux[1][idx], 1.0));
+      return __dsub_rn(__fma_rn(et, g.aux[0][idx], a), b);
+    }
     case KP_G_SQUARE:
       return __dmul_rn(x, x);
     case KP_G_CONST:

@@ -140,7 +140,8 @@ bool kronsum_try_banded(kp_ctx* ctx, bool cplx, const double* t, const std::vect
 void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<int>& dims,
                     const std::vector<const int*>& cols, const std::vector<const double*>& vals,
                     const std::vector<char>& active, double* r, bool with_g, const kp_gfun& g,
-                    long long half, int slab = -1, int k0 = 0, int n_glob = 0, int halo = 0);
+                    long long half, int slab = -1, int k0 = 0, int n_glob = 0, int halo = 0,
+                    double t = 0.0);
 
 // ---- elementwise (elementwise.cu) ----
 // z = fma(b, y, x): axpy is (b=alpha, y=x, x=y, z=y), add_scaled is (b=alpha, y=y, x=x)

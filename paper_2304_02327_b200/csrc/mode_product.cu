@@ -69,12 +69,12 @@ __device__ __forceinline__ double epi_one(const Epilogue& e, double v, const dou
       const double base = (e.beta != 0.0) ? __fma_rn(e.beta, C[idx], v) : v;
       const bool second = half > 0 && idx >= half;
       const double partner = half > 0 ? e.X[second ? idx - half : idx + half] : 0.0;
-      return __dadd_rn(base, g_real(e.g, e.X[idx], partner, second));
+      return __dadd_rn(base, g_real(e.g, e.X[idx], partner, second, idx, e.t));
     }
     case EPI_STAGE_D: {
       const double x = e.X[idx];
       const double s = __fma_rn(e.gamma, v, x);
-      *dval = __dsub_rn(g_real(e.g, s, 0.0, false), g_real(e.g, x, 0.0, false));
+      *dval = __dsub_rn(g_real(e.g, s, 0.0, false, idx, e.t2), g_real(e.g, x, 0.0, false, idx, e.t));
       return s;
     }
     default:

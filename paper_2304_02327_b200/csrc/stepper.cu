@@ -48,10 +48,11 @@ struct Elt;
 template <>
 struct Elt<false> {
   using T = double;
-  static __device__ __forceinline__ T g(const kp_gfun& gf, const T* u, long long i, long long half) {
+  static __device__ __forceinline__ T g(const kp_gfun& gf, const T* u, long long i, long long half,
+                                        double t) {
     const bool second = half > 0 && i >= half;
     const double partner = half > 0 ? u[second ? i - half : i + half] : 0.0;
-    return g_real(gf, u[i], partner, second);
+    return g_real(gf, u[i], partner, second, i, t);
   }
   static __device__ __forceinline__ T fma(double a, T x, T y) { return __fma_rn(a, x, y); }
   static __device__ __forceinline__ T sub(T a, T b) { return __dsub_rn(a, b); }
@@ -60,7 +61,8 @@ struct Elt<false> {
 template <>
 struct Elt<true> {
   using T = double2;
-  static __device__ __forceinline__ T g(const kp_gfun& gf, const T* u, long long i, long long) {
+  static __device__ __forceinline__ T g(const kp_gfun& gf, const T* u, long long i, long long,
+                                        double) {
     return g_cplx(gf, u[i]);
   }
   static __device__ __forceinline__ T fma(double a, T x, T y) {
@@ -74,13 +76,14 @@ struct Elt<true> {
 
 // w0 = u + tau*g(u); if two: w1 = u + (tau/2)*g(u)   (Lawson prologues, :118, :127-129)
 template <bool CPLX>
-__global__ void lawson_pre_kernel(kp_gfun g, long long n, long long half, double tau, bool two,
+__global__ void lawson_pre_kernel(kp_gfun g, double t, long long n, long long half, double tau,
+                                  bool two,
                                   const typename Elt<CPLX>::T* __restrict__ u,
                                   typename Elt<CPLX>::T* __restrict__ w) {
   using E = Elt<CPLX>;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    const auto gn = E::g(g, u, i, half);
+    const auto gn = E::g(g, u, i, half, t);
     w[i] = E::fma(tau, gn, u[i]);
     if (two) w[n + i] = E::fma(0.5 * tau, gn, u[i]);
   }
@@ -88,7 +91,7 @@ __global__ void lawson_pre_kernel(kp_gfun g, long long n, long long half, double
 
 // out = y1 + (tau/2) g(stage), y = [stage; y1]   (lawson2b :130-131)
 template <bool CPLX>
-__global__ void lawson2b_post_kernel(kp_gfun g, long long n, long long half, double tau,
+__global__ void lawson2b_post_kernel(kp_gfun g, double t2, long long n, long long half, double tau,
                                      const typename Elt<CPLX>::T* __restrict__ y,
                                      typename Elt<CPLX>::T* __restrict__ out, int* bad,
                                      const int* ctr) {
@@ -96,7 +99,7 @@ __global__ void lawson2b_post_kernel(kp_gfun g, long long n, long long half, dou
   bool nf = false;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    const auto r = E::fma(0.5 * tau, E::g(g, y, i, half), y[n + i]);
+    const auto r = E::fma(0.5 * tau, E::g(g, y, i, half, t2), y[n + i]);
     out[i] = r;
     nf |= !E::finite(r);
   }
@@ -105,14 +108,14 @@ __global__ void lawson2b_post_kernel(kp_gfun g, long long n, long long half, dou
 
 // d = g(stage) - g(u)   (etd2rk :161-162, unfused form for coupled g)
 template <bool CPLX>
-__global__ void gdiff_kernel(kp_gfun g, long long n, long long half,
+__global__ void gdiff_kernel(kp_gfun g, double t, double t2, long long n, long long half,
                              const typename Elt<CPLX>::T* __restrict__ s,
                              const typename Elt<CPLX>::T* __restrict__ u,
                              typename Elt<CPLX>::T* __restrict__ d) {
   using E = Elt<CPLX>;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    d[i] = E::sub(E::g(g, s, i, half), E::g(g, u, i, half));
+    d[i] = E::sub(E::g(g, s, i, half, t2), E::g(g, u, i, half, t));
 }
 
 __global__ void tick_kernel(int* ctr) { *ctr += 1; }
@@ -354,7 +357,7 @@ class Integrator {
   void kronsum(const double* u, double* r, const Epilogue& last) {
     if (banded) {  // one stencil pass, the reference's per-entry rounding (banded.cu)
       kronsum_banded(ctx, cplx, u, dims, band_cols, band_vals, a_active, r,
-                     last.kind == EPI_ADD_G, last.g, half);
+                     last.kind == EPI_ADD_G, last.g, half, -1, 0, 0, 0, last.t);
       return;
     }
     std::vector<int> act;
@@ -374,24 +377,24 @@ class Integrator {
   }
 
   template <bool C>
-  void launch_pre(const double* u, double* w, bool two) {
+  void launch_pre(const double* u, double* w, bool two, double t) {
     using T = typename Elt<C>::T;
     lawson_pre_kernel<C><<<grid_ew(ctx, n_entries), 256, 0, ctx->stream>>>(
-        g, n_entries, half, tau, two, reinterpret_cast<const T*>(u), reinterpret_cast<T*>(w));
+        g, t, n_entries, half, tau, two, reinterpret_cast<const T*>(u), reinterpret_cast<T*>(w));
     ctx->launches++;
   }
   template <bool C>
-  void launch_post(const double* y, double* out, int* bad, const int* ctr) {
+  void launch_post(const double* y, double* out, int* bad, const int* ctr, double t2) {
     using T = typename Elt<C>::T;
     lawson2b_post_kernel<C><<<grid_ew(ctx, n_entries), 256, 0, ctx->stream>>>(
-        g, n_entries, half, tau, reinterpret_cast<const T*>(y), reinterpret_cast<T*>(out), bad, ctr);
+        g, t2, n_entries, half, tau, reinterpret_cast<const T*>(y), reinterpret_cast<T*>(out), bad, ctr);
     ctx->launches++;
   }
   template <bool C>
-  void launch_gdiff(const double* s, const double* u, double* dd) {
+  void launch_gdiff(const double* s, const double* u, double* dd, double t) {
     using T = typename Elt<C>::T;
     gdiff_kernel<C><<<grid_ew(ctx, n_entries), 256, 0, ctx->stream>>>(
-        g, n_entries, half, reinterpret_cast<const T*>(s), reinterpret_cast<const T*>(u),
+        g, t, t + tau, n_entries, half, reinterpret_cast<const T*>(s), reinterpret_cast<const T*>(u),
         reinterpret_cast<T*>(dd));
     ctx->launches++;
   }
@@ -404,14 +407,14 @@ class Integrator {
     switch (method) {
       case KP_LAWSON_EULER: {  // :116-122
         double* w = buf(S_W, n_entries);
-        cplx ? launch_pre<true>(u, w, false) : launch_pre<false>(u, w, false);
+        cplx ? launch_pre<true>(u, w, false, t) : launch_pre<false>(u, w, false, t);
         tucker(f1, w, dims, out, &fin);
         break;
       }
       case KP_LAWSON2B: {  // :124-132, both Tuckers as one over [w0; w1]
         double* w = buf(S_W, 2 * n_entries);
         double* y = buf(S_Y, 2 * n_entries);
-        cplx ? launch_pre<true>(u, w, true) : launch_pre<false>(u, w, true);
+        cplx ? launch_pre<true>(u, w, true, t) : launch_pre<false>(u, w, true, t);
         std::vector<int> sd = dims;
         sd.push_back(2);
         FactorSet fs = f1;
@@ -422,10 +425,12 @@ class Integrator {
         tucker(fs, w, sd, y, nullptr);
         d = d_save;
         if (bad) {
-          cplx ? launch_post<true>(y, out, bad, ctr) : launch_post<false>(y, out, bad, ctr);
+          cplx ? launch_post<true>(y, out, bad, ctr, t + tau)
+               : launch_post<false>(y, out, bad, ctr, t + tau);
         } else {
           int* dummy = static_cast<int*>(ctx->ws.get(S_CTR + 1, 16));
-          cplx ? launch_post<true>(y, out, dummy, dummy) : launch_post<false>(y, out, dummy, dummy);
+          cplx ? launch_post<true>(y, out, dummy, dummy, t + tau)
+               : launch_post<false>(y, out, dummy, dummy, t + tau);
         }
         break;
       }
@@ -448,7 +453,7 @@ class Integrator {
         double* gn = buf(S_D, n_entries);
         tucker(f1, u, dims, y, nullptr);
         Epilogue none;
-        eval_g(u, gn);
+        eval_g(u, gn, t);
         fin.kind = EPI_FMA_X;
         fin.X = y;
         fin.gamma = tau;
@@ -479,7 +484,7 @@ class Integrator {
         } else {
           es.kind = EPI_FMA_X;
           tucker(f1, r, dims, s, &es);
-          cplx ? launch_gdiff<true>(s, u, dd) : launch_gdiff<false>(s, u, dd);
+          cplx ? launch_gdiff<true>(s, u, dd, t) : launch_gdiff<false>(s, u, dd, t);
         }
         fin.kind = EPI_FMA_X;
         fin.X = s;
@@ -493,8 +498,8 @@ class Integrator {
     KP_CUDA(cudaGetLastError());
   }
 
-  void eval_g(const double* u, double* out) {
-    launch_eval_g(ctx, g, 0.0, u, size_t(n_entries), size_t(half), cplx, out);
+  void eval_g(const double* u, double* out, double t) {
+    launch_eval_g(ctx, g, t, u, size_t(n_entries), size_t(half), cplx, out);
   }
 
   void setup(int q) {
@@ -531,8 +536,12 @@ class Integrator {
     cudaEvent_t ev[4];
     for (auto& e : ev) KP_CUDA(cudaEventCreate(&e));
     long n = 0;
+    // time-dependent g's read t = t0 + (*ctr) tau on the device (graph-safe)
+    g.step_ctr = ctr;
+    g.t0 = t0;
+    g.tau = tau;
     auto one = [&](long k) {
-      step(ub[k & 1], ub[(k + 1) & 1], t0 + double(k) * tau, bad, ctr);
+      step(ub[k & 1], ub[(k + 1) & 1], 0.0, bad, ctr);
       tick_kernel<<<1, 1, 0, ctx->stream>>>(ctr);
       ctx->launches++;
     };

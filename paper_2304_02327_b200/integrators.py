@@ -78,7 +78,7 @@ def parse_method(s):
     raise InvalidArgument(1, f"unknown method: {s}")
 
 
-G_ZERO, G_SQUARE, G_CONST, G_ALLEN_CAHN, G_BRUSSELATOR, G_NLS = range(6)
+G_ZERO, G_SQUARE, G_CONST, G_ALLEN_CAHN, G_BRUSSELATOR, G_NLS, G_ADR = range(7)
 
 
 def gfun(kind, *params) -> GFun:
@@ -97,6 +97,27 @@ class G:
     allen_cahn = staticmethod(lambda: gfun(G_ALLEN_CAHN))
     brusselator = staticmethod(lambda a=1.0, b=3.0: gfun(G_BRUSSELATOR, a, b))
     nls = staticmethod(lambda: gfun(G_NLS))
+
+    @staticmethod
+    def adr(psi_a, u0_sq):
+        """The reference's ADR source g (src/problems.cpp:101-115).  The
+        fields (host numpy or device torch, shaped like u) are uploaded at the
+        first device use and kept alive by the descriptor."""
+        g = gfun(G_ADR)
+        g._aux_src = [psi_a, u0_sq]
+        return g
+
+
+def _bind_aux(g):
+    """Device pointers for a g with auxiliary fields (ADR)."""
+    src = getattr(g, "_aux_src", None)
+    if src is None or getattr(g, "_aux_dev", None) is not None:
+        return g
+    dev = [x if _is_torch(x) else to_device(np.asarray(x)) for x in src]
+    for i, t in enumerate(dev):
+        g.aux[i] = t.data_ptr()
+    g._aux_dev = dev
+    return g
 
 
 # ------------------------------------------------------------ matrix functions
@@ -249,6 +270,7 @@ def _step(method, u, t, tau, K, g, f1, pref1, f2, pref2):
     dims = list(ud.shape)
     out = fortran_empty(dims, dt, ud.device)
     ctx = _ctx_for(ud)
+    _bind_aux(g)
     f = ctx.lib.kp_step_c128 if cplx else ctx.lib.kp_step_f64
     check(f(ctx.h, int(method), ud.data_ptr(), ints(dims), len(dims), float(t), float(tau),
             ptr_array([x.data_ptr() for x in Kd]) if Kd else None,
@@ -335,6 +357,7 @@ def integrate(p: ProblemSpec, c: StepperConfig) -> IntegrateResult:
     t_start = time.perf_counter()
     dv = C.c_long(0)
     loop = C.c_double(0)
+    _bind_aux(p.g)
     if host:
         dtype = np.complex128 if cplx else np.float64
         uh = np.asfortranarray(u0, dtype=dtype)

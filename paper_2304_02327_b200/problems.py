@@ -127,6 +127,33 @@ def nls(n=512, n_steps=50, tau=1e-3, method="etd2rk", seed=1005, k=(1.0, 0.5, 0.
     return Config("nls", method, np.asfortranarray(u0), [A, A, A], G.nls(), tau, n_steps)
 
 
+def adr(n1=40, n2=41, n3=42, n_steps=440, method="etd2rk", eps=0.75, alpha=0.1):
+    """The reference's own benchmark problem (src/problems.cpp:45-128): 3-D
+    advection-diffusion-reaction u_t = eps Lap u + alpha sum d_mu u + 1/(1+u^2)
+    + Psi(t,x) on [0,1]^3 with the manufactured exact solution e^t u0,
+    u0 = 64 x(1-x) y(1-y) z(1-z); T = 1 (tau = 1/n_steps).  Returns the
+    Config plus the exact solution at T = 1."""
+    p = lambda x: x * (1.0 - x)
+    dp = lambda x: 1.0 - 2.0 * x
+    gx = [grid(n) for n in (n1, n2, n3)]
+    P = [p(x) for x in gx]
+    D = [dp(x) for x in gx]
+    p1, p2, p3 = P[0][:, None, None], P[1][None, :, None], P[2][None, None, :]
+    d1, d2, d3 = D[0][:, None, None], D[1][None, :, None], D[2][None, None, :]
+    u0 = 64.0 * p1 * p2 * p3
+    lap = 64.0 * (-2.0) * (p2 * p3 + p1 * p3 + p1 * p2)
+    adv = 64.0 * (d1 * p2 * p3 + d2 * p1 * p3 + d3 * p1 * p2)
+    psi_a = np.asfortranarray(u0 - eps * lap - alpha * adv)
+    u0 = np.asfortranarray(u0)
+    K = [fd_operator_1d(n, eps, alpha) for n in (n1, n2, n3)]
+    from .integrators import G
+    g = G.adr(psi_a, np.asfortranarray(u0 * u0))
+    cfg = Config("adr", method, u0, K, g, 1.0 / n_steps, n_steps)
+    cfg.fields = (psi_a, np.asfortranarray(u0 * u0))
+    cfg.exact = np.exp(1.0) * u0
+    return cfg
+
+
 def tucker_sweep(n, seed=1002, tau=1e-3):
     """configs[1]: V ~ N(0,1) and A = fd_operator_1d(n, 1.0) (L = phi_1(tau A))."""
     r = np.random.default_rng(seed)
