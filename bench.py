@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-integrators", action="store_true",
                     help="skip the integrator-config block (steps/s of configs 0,2,3,4)")
+    ap.add_argument("--no-paper", action="store_true",
+                    help="skip the paper's ADR wall-clock runs")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the sharded integrator block even at N=1 (testing)")
     return ap.parse_args()
@@ -130,6 +132,61 @@ def run_integrators(kp, peak):
                     if c.method in ("exp_euler", "etd2rk") else None,
                     "note": note}
         del ud, K, spec
+    return out
+
+
+# The paper's own experiments (PAPER.md tables; published MATLAB wall-clocks
+# on an i7-10750H): ADR 40x41x42 and 80x81x82, T = 1.
+PAPER_RUNS = [  # (tag, dims, method, steps, published seconds, PAPER.md lines)
+    ("adr40_etd2rk_440", (40, 41, 42), "etd2rk", 440, 0.4505, "1360-1367"),
+    ("adr40_expeuler_1650", (40, 41, 42), "exp_euler", 1650, 1.0202, "1304-1311"),
+    ("adr40_lawsoneuler_32800", (40, 41, 42), "lawson_euler", 32800, 10.0065, "1284-1291"),
+    ("adr40_lawson2b_17500", (40, 41, 42), "lawson2b", 17500, 11.6447, "1340-1347"),
+    ("adr80_etd2rk_440", (80, 81, 82), "etd2rk", 440, 7.8158, "1568-1575"),
+    ("adr80_expeuler_1650", (80, 81, 82), "exp_euler", 1650, 17.8601, "1514-1521"),
+    ("adr80_lawson2b_9000", (80, 81, 82), "lawson2b", 9000, 102.317, "1548-1555"),
+    # LQR Riccati (src/problems.cpp:130-284), T = 0.025: dims = (n_hat,)
+    ("riccati30_etd2rk_170", (30,), "etd2rk", 170, 13.052, "952-959"),
+    ("riccati30_rosenbrock_170", (30,), "rosenbrock_euler", 170, 25.640, "941-948"),
+    ("riccati40_etd2rk_170", (40,), "etd2rk", 170, 80.723, "1085-1092"),
+    ("riccati40_rosenbrock_170", (40,), "rosenbrock_euler", 170, 163.33, "1072-1079"),
+]
+
+
+def run_paper_experiments(kp):
+    """Whole-integration wall-clock (factor build + loop, host in/out) of the
+    paper's ADR and Riccati runs, the quantity PAPER.md publishes; plus, for
+    ADR, the error vs the exact solution e^t u0 (the paper's table entry) and,
+    for Riccati, the relative distance between the Rosenbrock and ETD2RK
+    final states (both ~5e-6 from the converged solution at 170 steps)."""
+    from paper_2304_02327_b200 import problems
+    out = {}
+    finals = {}
+    for tag, dims, method, steps, pub, lines in PAPER_RUNS:
+        if len(dims) == 1:
+            c = problems.riccati(dims[0], n_steps=steps, method=method)
+        else:
+            c = problems.adr(*dims, n_steps=steps, method=method)
+        t_end = c.t_final
+        kp.integrate_config(method, c.u0, c.K, c.g, 0.0, t_end, 2)  # warm-up (lazy loading)
+        t0 = time.perf_counter()
+        res = kp.integrate(kp.ProblemSpec(c.K, c.g, c.u0, 0.0, t_end),
+                           kp.StepperConfig(kp.parse_method(method), steps))
+        wall = time.perf_counter() - t0
+        rec = {"dims": list(dims), "method": method, "steps": steps, "t_final": t_end,
+               "wallclock_s": wall, "loop_s": res.loop_s,
+               "published_matlab_s": pub, "speedup_vs_published": pub / wall,
+               "source": f"PAPER.md:{lines}"}
+        if len(dims) == 1:
+            key = dims[0]
+            if key in finals:
+                a, b = res.final, finals[key]
+                rec["rel_fro_vs_other_method"] = float(np.linalg.norm(a - b) / np.linalg.norm(b))
+            finals[key] = res.final
+        else:
+            rec["rel_inf_error"] = float(np.abs(res.final - c.exact).max() /
+                                         np.abs(c.exact).max())
+        out[tag] = rec
     return out
 
 
@@ -411,6 +468,10 @@ def main():
         integ = run_integrators(kp, peak) if (world == 1 and not args.force_sharded) else \
             run_sharded_integrators(kp, peak, world, rank, local)
 
+    paper = None
+    if world == 1 and not args.no_paper:
+        paper = run_paper_experiments(kp)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -431,7 +492,7 @@ def main():
                              "algorithmic": "2*N*sum(n_mu) = 412.3 GFLOP per Tucker, "
                                             "137.4 GFLOP per mode-product launch"},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clk.summary(), "integrators": integ}
+                "clocks": clk.summary(), "integrators": integ, "paper_adr": paper}
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

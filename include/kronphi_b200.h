@@ -51,6 +51,7 @@ typedef struct kp_ctx kp_ctx;
 #define KP_EXP_EULER 2
 #define KP_EXP_EULER_LS 3
 #define KP_ETD2RK 4
+#define KP_ROSENBROCK_EULER 5 /* per-step phi_1 of the Jacobian factors (RICCATI g only) */
 
 /* Closed set of device nonlinearities g(t,u) replacing the reference's host
  * std::function (inc/integrators.hpp:60,112). */
@@ -63,6 +64,12 @@ typedef struct kp_ctx kp_ctx;
 #define KP_G_ADR 6         /* 1/(1+u^2) + e^t psi_a - 1/(1+e^{2t} u0^2): the reference's
                               ADR source (src/problems.cpp:101-115); aux[0] = psi_a,
                               aux[1] = u0^2 (device arrays shaped like u) */
+
+#define KP_G_RICCATI 7     /* C + U B U = C - (U b)(U^T b)^T on an n x n state (d = 2):
+                              the reference's LQR Riccati g (src/problems.cpp:263-276);
+                              aux[0] = b (n), aux[1] = C (n x n); Rosenbrock-Euler's
+                              Jacobian factors J = A^T - w b^T (:212-250) need the K
+                              factors to be {A^T, A^T} */
 
 /* step_ctr/t0/tau: when step_ctr is set (the integrators do this), a
  * time-dependent g reads t = t0 + (*step_ctr) * tau (+ the stage offset) from
@@ -193,9 +200,12 @@ int kp_build_split_phi_c128(kp_ctx* ctx, const double* const* as, const int* dim
 /* ---------------- steppers (inc/integrators.hpp) ---------------- */
 /* One step out = step(u).  f1/f2 as in the reference's step functions:
  * Lawson methods f1 = exp factors; ExpEuler f1 = phi1; ExpEulerLS f1 = exp,
- * f2 = phi1; ETD2RK f1 = phi1, f2 = phi2 (pref1/pref2 = split prefactors).
+ * f2 = phi1; ETD2RK f1 = phi1, f2 = phi2 (pref1/pref2 = split prefactors);
+ * RosenbrockEuler f1 = the Jacobian factors J_mu (phi_1(tau J_mu) built in the
+ * call, equal pointers share one build, :166-194; f2 unused).
  * Replaces lawson_euler_step, lawson2b_step, exp_euler_step,
- * exp_euler_linear_split_step, etd2rk_step (:116-164).  out must not alias u. */
+ * exp_euler_linear_split_step, etd2rk_step, rosenbrock_euler_step (:116-194).
+ * out must not alias u. */
 int kp_step_f64(kp_ctx* ctx, int method, const double* u, const int* dims, int d, double t,
                 double tau, const double* const* as, const double* const* f1, double pref1,
                 const double* const* f2, double pref2, const kp_gfun* g, double* out);
@@ -206,6 +216,8 @@ int kp_step_c128(kp_ctx* ctx, int method, const double* u, const int* dims, int 
  * built once on the device, n_steps steps on device-resident state u (in:
  * u0, out: final state), per-step finite check.  On divergence returns
  * KP_EDIVERGE with *diverged_step = first non-finite step (1-based).
+ * RosenbrockEuler needs g = KP_G_RICCATI (its jacobian_factors are rebuilt on
+ * the device every step), otherwise KP_EINVAL like the reference (:223-225).
  * *loop_seconds (may be NULL) = device time of the time loop. */
 int kp_integrate_f64(kp_ctx* ctx, int method, double* u, const int* dims, int d,
                      const double* const* as, const kp_gfun* g, double t0, double t_final,

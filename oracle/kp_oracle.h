@@ -39,7 +39,8 @@ enum {
   KPO_LAWSON2B = 1,
   KPO_EXP_EULER = 2,
   KPO_EXP_EULER_LS = 3,
-  KPO_ETD2RK = 4
+  KPO_ETD2RK = 4,
+  KPO_ROSENBROCK_EULER = 5 /* :166-194; Jacobian factors of the Riccati g only */
 };
 
 /* Closed set of pointwise nonlinearities g(t,u) (the reference takes a host
@@ -53,8 +54,10 @@ enum {
   KPO_G_BRUSSELATOR = 4, /* (a-(b+1)u+u^2 v, b u-u^2 v), species stacked as the
                             slowest mode of size 2; p0=a, p1=b   BASELINE config 4 */
   KPO_G_NLS = 5,         /* g = -i |u|^2 u (complex only)   BASELINE config 5 */
-  KPO_G_ADR = 6          /* 1/(1+u^2) + e^t psi_a - 1/(1+e^{2t} u0^2), aux = {psi_a, u0^2}
+  KPO_G_ADR = 6,         /* 1/(1+u^2) + e^t psi_a - 1/(1+e^{2t} u0^2), aux = {psi_a, u0^2}
                             src/problems.cpp:101-115 */
+  KPO_G_RICCATI = 7      /* C - (U b)(U^T b)^T on an n x n state, aux = {b, C}
+                            src/problems.cpp:188-200, 263-276 */
 };
 
 typedef struct {

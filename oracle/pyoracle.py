@@ -27,7 +27,8 @@ REF_LIB = os.path.join(HERE, "_ref", "libkronphi_ref.so")
 # kp_oracle.h enums
 LAWSON_EULER, LAWSON2B, EXP_EULER, EXP_EULER_LS, ETD2RK = range(5)
 METHODS = {"lawson_euler": LAWSON_EULER, "lawson2b": LAWSON2B, "exp_euler": EXP_EULER,
-           "exp_euler_ls": EXP_EULER_LS, "etd2rk": ETD2RK}
+           "exp_euler_ls": EXP_EULER_LS, "etd2rk": ETD2RK,
+           "rosenbrock_euler": 5}
 G_ZERO, G_SQUARE, G_CONST, G_ALLEN_CAHN, G_BRUSSELATOR, G_NLS = range(6)
 
 
@@ -50,6 +51,7 @@ class GFun(C.Structure):
 
 
 G_ADR = 6
+G_RICCATI = 7  # aux = (b, C) on an n x n state, src/problems.cpp:188-200, 263-276
 
 
 def gfun(kind, *params, aux=None):
@@ -272,6 +274,21 @@ class Oracle:
         self._check(f(n1, n2, n3, METHODS.get(method, method), n_steps, _dp(out), C.byref(err),
                       C.byref(sec)))
         return out, err.value, sec.value
+
+    def run_riccati(self, n_hat, method, n_steps, t_final):
+        """The reference's LQR Riccati experiment (build_riccati +
+        to_problem_spec + integrate, reference harness only): final state."""
+        if self.kind != "reference":
+            raise RuntimeError("run_riccati needs the reference harness")
+        n = n_hat * n_hat
+        out = np.zeros((n, n), order="F")
+        sec = C.c_double(0)
+        f = self.fn("run_riccati")
+        f.argtypes = [C.c_int, C.c_int, C.c_long, C.c_double, C.POINTER(C.c_double),
+                      C.POINTER(C.c_double)]
+        self._check(f(n_hat, METHODS.get(method, method), n_steps, t_final, _dp(out),
+                      C.byref(sec)))
+        return out, sec.value
 
     def num_threads(self):
         return self.fn("num_threads")() if self.kind == "reference" else 1

@@ -412,6 +412,21 @@ int kpr_run_adr(int n1, int n2, int n3, int method, long n_steps, double* u_fina
   });
 }
 
+// The reference's LQR Riccati problem (src/problems.cpp:130-284) through its
+// own integrate() (Rosenbrock uses its jacobian_factors callback).
+int kpr_run_riccati(int n_hat, int method, long n_steps, double t_final, double* u_final,
+                    double* seconds) {
+  return guard([&] {
+    const RiccatiProblem p = build_riccati(n_hat);
+    StepperConfig c;
+    c.method = method == KPO_ROSENBROCK_EULER ? Method::RosenbrockEuler : to_method(method);
+    c.n_steps = n_steps;
+    const IntegrateResult r = integrate(p.to_problem_spec(t_final), c);
+    from(r.final.data(), r.final.size(), u_final);
+    if (seconds) *seconds = r.wallclock_s;
+  });
+}
+
 // ---- timing helpers for bench.py's reference arm (steady_clock, in-process;
 // inputs are built once outside the timed region) ----
 

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(HERE, "lib", "libkronphi_b200.so")
 
 KP_OK, KP_EINVAL, KP_ERUNTIME, KP_EDIVERGE, KP_ECUDA = range(5)
 LAWSON_EULER, LAWSON2B, EXP_EULER, EXP_EULER_LS, ETD2RK = range(5)
-G_ZERO, G_SQUARE, G_CONST, G_ALLEN_CAHN, G_BRUSSELATOR, G_NLS, G_ADR = range(7)
+G_ZERO, G_SQUARE, G_CONST, G_ALLEN_CAHN, G_BRUSSELATOR, G_NLS, G_ADR, G_RICCATI = range(8)
 
 
 class KronphiError(RuntimeError):

@@ -542,6 +542,12 @@ int kp_eval_g_f64(kp_ctx* ctx, const kp_gfun* g, double t, const double* u, cons
     const auto dv = check_dims(dims, d, "g");
     if (!g) throw invalid_argument("g: null descriptor");
     if (g->kind == KP_G_NLS) throw invalid_argument("g: NLS needs a complex tensor");
+    if (g->kind == KP_G_RICCATI) {  // src/problems.cpp:263-276, nonlocal
+      if (d != 2 || dv[0] != dv[1]) throw invalid_argument("riccati g: needs an n x n state");
+      riccati_g(ctx, *g, u, dv[0],
+                static_cast<double*>(ctx->ws.get(50, 2 * size_t(dv[0]) * sizeof(double))), gout);
+      return;
+    }
     size_t half = 0;
     if (g->kind == KP_G_BRUSSELATOR) {
       if (dv.back() != 2)
@@ -558,7 +564,8 @@ int kp_eval_g_c128(kp_ctx* ctx, const kp_gfun* g, double t, const double* u, con
     need_ctx(ctx);
     const auto dv = check_dims(dims, d, "g");
     if (!g) throw invalid_argument("g: null descriptor");
-    if (g->kind == KP_G_ALLEN_CAHN || g->kind == KP_G_BRUSSELATOR)
+    if (g->kind == KP_G_ALLEN_CAHN || g->kind == KP_G_BRUSSELATOR || g->kind == KP_G_ADR ||
+        g->kind == KP_G_RICCATI)
       throw invalid_argument("g: unsupported nonlinearity kind for complex");
     launch_eval_g(ctx, *g, t, u, numel(dv), 0, true, gout);
   });

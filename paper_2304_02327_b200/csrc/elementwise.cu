@@ -60,6 +60,15 @@ __global__ void finite_kernel(size_t n, const double* __restrict__ x, int* flag)
   if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) *flag = 0;
 }
 
+__global__ void finite_flag_kernel(size_t n, const double* __restrict__ x, int* bad,
+                                   const int* ctr) {
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  bool ok = true;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    ok &= isfinite(x[i]);
+  if (!ok) atomicMin(bad, *ctr + 1);
+}
+
 __global__ void dmma_peak_kernel(double* out, int iters) {
   double c[16][2];
 #pragma unroll
@@ -102,6 +111,13 @@ void launch_eval_g(kp_ctx* ctx, const kp_gfun& g, double t, const double* u, siz
         g, n, reinterpret_cast<const double2*>(u), reinterpret_cast<double2*>(out));
   else
     g_real_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(g, t, n, half, u, out);
+  ctx->launches++;
+  KP_CUDA(cudaGetLastError());
+}
+
+void finite_flag(kp_ctx* ctx, size_t n, const double* x, int* bad, const int* ctr) {
+  if (n == 0) return;
+  finite_flag_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(n, x, bad, ctr);
   ctx->launches++;
   KP_CUDA(cudaGetLastError());
 }

@@ -81,6 +81,7 @@ enum EpiKind : int {
   EPI_FMA_X = 1,    // C = fma(gamma, alpha*acc, X)             (add_scaled)
   EPI_ADD_G = 2,    // C = (alpha*acc + beta*C) + g(t, X)        (kronsum + g)
   EPI_STAGE_D = 3,  // S = fma(gamma, alpha*acc, X); C = S; D = g(t2, S) - g(t, X)
+  EPI_ADD_X = 4,    // C = (alpha*acc + beta*C) + X   (kronsum + a precomputed g)
 };
 
 struct Epilogue {
@@ -129,6 +130,11 @@ void expm_batch_c128(kp_ctx* ctx, const double* x, int n, int batch, double* out
 int phiquad_dev_c128(kp_ctx* ctx, const double* x, int n, int ell_max, int q, int forced,
                      double* phis);
 
+// ---- Riccati problem (riccati.cu) ----
+void riccati_g(kp_ctx* ctx, const kp_gfun& g, const double* u, int n, double* wz, double* out);
+int riccati_jacobians(kp_ctx* ctx, const kp_gfun& g, const double* u, const double* at, int n,
+                      double* wz, double* j1, double* j2);
+
 // ---- banded Kronecker sum (banded.cu) ----
 bool banded_kronsum_enabled();  // KP_KRONSUM=dense disables
 bool band_of(kp_ctx* ctx, const double* a, int n, bool cplx, int** cols, double** vals);
@@ -152,6 +158,8 @@ void launch_eval_g(kp_ctx* ctx, const kp_gfun& g, double t, const double* u, siz
                    size_t half, bool cplx, double* out);
 void launch_scale(kp_ctx* ctx, size_t n, double a, const double* x, double* y);
 int all_finite(kp_ctx* ctx, size_t n, const double* x);
+// device divergence flag: atomicMin(*bad, *ctr + 1) if x has a non-finite entry
+void finite_flag(kp_ctx* ctx, size_t n, const double* x, int* bad, const int* ctr);
 double measure_fp64_peak(kp_ctx* ctx);
 
 }  // namespace kp

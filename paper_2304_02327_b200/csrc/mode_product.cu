@@ -71,6 +71,10 @@ __device__ __forceinline__ double epi_one(const Epilogue& e, double v, const dou
       const double partner = half > 0 ? e.X[second ? idx - half : idx + half] : 0.0;
       return __dadd_rn(base, g_real(e.g, e.X[idx], partner, second, idx, e.t));
     }
+    case EPI_ADD_X: {
+      const double base = (e.beta != 0.0) ? __fma_rn(e.beta, C[idx], v) : v;
+      return __dadd_rn(base, e.X[idx]);
+    }
     case EPI_STAGE_D: {
       const double x = e.X[idx];
       const double s = __fma_rn(e.gamma, v, x);
@@ -93,6 +97,11 @@ __device__ __forceinline__ double2 epi_pair_c(const Epilogue& e, double2 v, cons
       if (e.beta != 0.0) b = make_double2(__fma_rn(e.beta, C[idx], v.x), __fma_rn(e.beta, C[idx + 1], v.y));
       const double2 gx = g_cplx(e.g, make_double2(e.X[idx], e.X[idx + 1]));
       return make_double2(__dadd_rn(b.x, gx.x), __dadd_rn(b.y, gx.y));
+    }
+    case EPI_ADD_X: {
+      double2 b = v;
+      if (e.beta != 0.0) b = make_double2(__fma_rn(e.beta, C[idx], v.x), __fma_rn(e.beta, C[idx + 1], v.y));
+      return make_double2(__dadd_rn(b.x, e.X[idx]), __dadd_rn(b.y, e.X[idx + 1]));
     }
     case EPI_STAGE_D: {
       const double2 x = make_double2(e.X[idx], e.X[idx + 1]);

@@ -128,7 +128,10 @@ __global__ void scale_matrix_kernel(const double* __restrict__ a, long long n, d
 }
 
 // Workspace slots of the stepper (tucker ping-pong uses 0/1 inside).
-enum : int { S_R = 2, S_S = 3, S_D = 4, S_W = 5, S_Y = 6, S_U2 = 7, S_CTR = 40 };
+enum : int {
+  S_R = 2, S_S = 3, S_D = 4, S_W = 5, S_Y = 6, S_U2 = 7, S_CTR = 40,
+  S_G = 49, S_WZ = 50, S_J1 = 51, S_J2 = 52, S_J3 = 53, S_PHI1 = 54, S_PHI2 = 55
+};
 
 }  // namespace
 
@@ -155,9 +158,12 @@ class Integrator {
   int comps;
   std::vector<const double*> A;
   std::vector<char> a_active;
-  FactorSet f1, f2;
+  FactorSet f1, f2, fj;  // fj: Rosenbrock's per-step factors
+  int q_nodes = 12;
+  bool given_jacobians = false;  // kp_step: J factors supplied by the caller
   std::vector<double*> owned;
   long diverged_at = 0;  // first non-finite step of the last run() (0 = none)
+  bool nonlocal = false;  // g needs more than the entry itself (Riccati): own buffers
   // banded Kronecker sum (banded.cu): per-mode 3-slot row structure
   bool banded = false;
   std::vector<const int*> band_cols;
@@ -177,6 +183,10 @@ class Integrator {
       half = n_entries / 2;
     }
     if (g.kind == KP_G_NLS && !cplx) throw invalid_argument("g: NLS needs a complex tensor");
+    nonlocal = (g.kind == KP_G_RICCATI);
+    if (nonlocal && (cplx || d != 2 || dims[0] != dims[1] || !g.aux[0] || !g.aux[1]))
+      throw invalid_argument("riccati g: needs a real n x n state and aux = {b, C}");
+
     if (cplx && (g.kind == KP_G_ALLEN_CAHN || g.kind == KP_G_BRUSSELATOR))
       throw invalid_argument("g: unsupported nonlinearity kind for complex");
     a_active.assign(d, 1);
@@ -186,7 +196,8 @@ class Integrator {
       nact += a_active[mu];
     }
     if (nact == 0) a_active[d - 1] = 1;
-    if (banded_kronsum_enabled() && d <= 4 && (method == KP_EXP_EULER || method == KP_ETD2RK)) {
+    if (banded_kronsum_enabled() && !nonlocal && d <= 4 &&
+        (method == KP_EXP_EULER || method == KP_ETD2RK || method == KP_ROSENBROCK_EULER)) {
       banded = true;
       band_cols.assign(d, nullptr);
       band_vals.assign(d, nullptr);
@@ -404,6 +415,12 @@ class Integrator {
     Epilogue fin;
     fin.bad_step = bad;
     fin.step_ctr = ctr;
+    if (method == KP_ROSENBROCK_EULER && !given_jacobians) rosenbrock_factors(u);
+    if (nonlocal) {
+      step_nonlocal(u, out, t, fin);
+      KP_CUDA(cudaGetLastError());
+      return;
+    }
     switch (method) {
       case KP_LAWSON_EULER: {  // :116-122
         double* w = buf(S_W, n_entries);
@@ -434,7 +451,8 @@ class Integrator {
         }
         break;
       }
-      case KP_EXP_EULER: {  // :134-141
+      case KP_EXP_EULER:          // :134-141
+      case KP_ROSENBROCK_EULER: {  // :166-194 (factors rebuilt above)
         double* r = buf(S_R, n_entries);
         Epilogue eg;
         eg.kind = EPI_ADD_G;
@@ -445,7 +463,7 @@ class Integrator {
         fin.kind = EPI_FMA_X;
         fin.X = u;
         fin.gamma = tau;
-        tucker(f1, r, dims, out, &fin);
+        tucker(method == KP_ROSENBROCK_EULER ? fj : f1, r, dims, out, &fin);
         break;
       }
       case KP_EXP_EULER_LS: {  // :143-151  (f1 = exp factors, f2 = phi1)
@@ -499,7 +517,115 @@ class Integrator {
   }
 
   void eval_g(const double* u, double* out, double t) {
+    if (nonlocal) {
+      riccati_g(ctx, g, u, dims[0], buf(S_WZ, 2LL * dims[0]), out);
+      return;
+    }
     launch_eval_g(ctx, g, t, u, size_t(n_entries), size_t(half), cplx, out);
+  }
+
+  // nonlocal-g step: g values come from eval_g into buffers, the GEMM
+  // epilogues only add them (same operations, unfused)
+  void step_nonlocal(const double* u, double* out, double t, Epilogue fin) {
+    double* gn = buf(S_G, n_entries);
+    eval_g(u, gn, t);
+    switch (method) {
+      case KP_LAWSON_EULER:
+      case KP_LAWSON2B: {
+        double* w = buf(S_W, 2 * n_entries);
+        launch_fma(ctx, size_t(n_entries), tau, gn, u, w);  // u + tau g
+        if (method == KP_LAWSON_EULER) {
+          tucker(f1, w, dims, out, &fin);
+          return;
+        }
+        launch_fma(ctx, size_t(n_entries), 0.5 * tau, gn, u, w + n_entries);
+        double* stage = buf(S_S, n_entries);
+        double* y = buf(S_Y, n_entries);
+        tucker(f1, w, dims, stage, nullptr);
+        tucker(f1, w + n_entries, dims, y, nullptr);
+        double* gs = buf(S_D, n_entries);
+        eval_g(stage, gs, t + tau);
+        Epilogue none;
+        (void)none;
+        launch_fma(ctx, size_t(n_entries), 0.5 * tau, gs, y, out);  // y + tau/2 g(stage)
+        check_finite_into(out, fin);
+        return;
+      }
+      case KP_EXP_EULER:
+      case KP_ROSENBROCK_EULER: {
+        double* r = buf(S_R, n_entries);
+        Epilogue ex;
+        ex.kind = EPI_ADD_X;
+        ex.X = gn;
+        kronsum(u, r, ex);
+        fin.kind = EPI_FMA_X;
+        fin.X = u;
+        fin.gamma = tau;
+        tucker(method == KP_ROSENBROCK_EULER ? fj : f1, r, dims, out, &fin);
+        return;
+      }
+      case KP_EXP_EULER_LS: {
+        double* y = buf(S_Y, n_entries);
+        tucker(f1, u, dims, y, nullptr);
+        fin.kind = EPI_FMA_X;
+        fin.X = y;
+        fin.gamma = tau;
+        tucker(f2, gn, dims, out, &fin);
+        return;
+      }
+      case KP_ETD2RK: {
+        double* r = buf(S_R, n_entries);
+        double* s = buf(S_S, n_entries);
+        double* dd = buf(S_D, n_entries);
+        Epilogue ex;
+        ex.kind = EPI_ADD_X;
+        ex.X = gn;
+        kronsum(u, r, ex);
+        Epilogue es;
+        es.kind = EPI_FMA_X;
+        es.X = u;
+        es.gamma = tau;
+        tucker(f1, r, dims, s, &es);
+        eval_g(s, dd, t + tau);
+        launch_fma(ctx, size_t(n_entries), -1.0, gn, dd, dd);  // g(stage) - g(u)
+        fin.kind = EPI_FMA_X;
+        fin.X = s;
+        fin.gamma = tau;
+        tucker(f2, dd, dims, out, &fin);
+        return;
+      }
+      default:
+        throw invalid_argument("step: unknown method " + std::to_string(method));
+    }
+  }
+
+  // non-finite check of an elementwise result (the GEMM epilogues do it inline)
+  void check_finite_into(const double* x, const Epilogue& fin) {
+    if (fin.bad_step) finite_flag(ctx, size_t(n_entries) * comps, x, fin.bad_step, fin.step_ctr);
+  }
+
+  // Rosenbrock-Euler (inc/integrators.hpp:166-194): phi_1 of the current
+  // Jacobian factors, rebuilt every step (one build when they coincide)
+  void rosenbrock_factors(const double* u) {
+    const int n = dims[0];
+    const long long nn = (long long)n * n;
+    double* j1 = buf(S_J1, nn);
+    double* j2 = buf(S_J2, nn);
+    const int nf = riccati_jacobians(ctx, g, u, A[0], n, buf(S_WZ, 2LL * n), j1, j2);
+    double* scaled = buf(S_J3, nn);
+    fj.f.assign(2, nullptr);
+    fj.active.assign(2, 1);
+    fj.fold = 1.0;
+    fj.pref = 1.0;
+    for (int k = 0; k < nf; ++k) {
+      scale_matrix_kernel<<<grid_ew(ctx, nn), 256, 0, ctx->stream>>>(k == 0 ? j1 : j2, nn, tau,
+                                                                      scaled);
+      ctx->launches++;
+      double* tab = k == 0 ? buf(S_PHI1, 2 * nn) : buf(S_PHI2, 2 * nn);
+      phiquad_dev(ctx, scaled, n, 1, q_nodes, -1, tab);
+      fj.f[k] = tab + nn;
+    }
+    if (nf == 1) fj.f[1] = fj.f[0];
   }
 
   void setup(int q) {
@@ -517,6 +643,11 @@ class Integrator {
         break;
       case KP_ETD2RK:
         build(1, 2, q, &f1, &f2);
+        break;
+      case KP_ROSENBROCK_EULER:  // :224-226
+        if (!nonlocal)
+          throw invalid_argument("integrate: Rosenbrock-Euler requires jacobian_factors");
+        q_nodes = q;  // factors are built per step from the Jacobian
         break;
       default:
         throw invalid_argument("integrate: unknown method " + std::to_string(method));
@@ -551,7 +682,7 @@ class Integrator {
     KP_CUDA(cudaEventRecord(ev[1], ctx->stream));
     cudaGraphExec_t exec = nullptr;
     unsigned long long per = 0;
-    if (use_graph && n_steps - n >= 4) {
+    if (use_graph && method != KP_ROSENBROCK_EULER && n_steps - n >= 4) {
       cudaGraph_t graph;
       const unsigned long long l0 = ctx->launches;
       KP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
@@ -803,8 +934,33 @@ int step_impl(kp_ctx* ctx, bool cplx, int method, const double* u, const int* di
       as = zeros.data();
     }
     Integrator it(ctx, method, cplx, dv, as, *g, tau);
-    it.f1 = given_factors(it, f1, pref1);
-    if (f2) it.f2 = given_factors(it, f2, pref2);
+    if (method == KP_ROSENBROCK_EULER) {
+      // rosenbrock_euler_step(u, t, tau, k, g, jac_factors, rule): f1 = J_mu;
+      // phi_1(tau J_mu) per call, identical factors share one build (:176-186)
+      it.given_jacobians = true;
+      it.fj.f.assign(d, nullptr);
+      it.fj.active.assign(d, 1);
+      for (int mu = 0; mu < d; ++mu) {
+        int same = -1;
+        for (int m2 = 0; m2 < mu; ++m2)
+          if (f1[m2] == f1[mu] && dv[m2] == dv[mu]) same = m2;
+        if (same >= 0) {
+          it.fj.f[mu] = it.fj.f[same];
+          continue;
+        }
+        const long long nn = (long long)dv[mu] * dv[mu] * (cplx ? 2 : 1);
+        double* scaled = it.alloc(nn);
+        scale_matrix_kernel<<<grid_ew(ctx, nn), 256, 0, ctx->stream>>>(f1[mu], nn, tau, scaled);
+        ctx->launches++;
+        double* tab = it.alloc(2 * nn);
+        cplx ? phiquad_dev_c128(ctx, scaled, dv[mu], 1, 12, -1, tab)
+             : phiquad_dev(ctx, scaled, dv[mu], 1, 12, -1, tab);
+        it.fj.f[mu] = tab + nn;
+      }
+    } else {
+      it.f1 = given_factors(it, f1, pref1);
+      if (f2) it.f2 = given_factors(it, f2, pref2);
+    }
     it.step(u, out, t, nullptr, nullptr);
   });
 }

@@ -54,17 +54,18 @@ kDefaultQuadNodes = 12  # inc/matrix_functions.hpp:107
 
 
 class Method(enum.IntEnum):
-    """inc/integrators.hpp:24-31 (RosenbrockEuler is out of scope here)."""
+    """inc/integrators.hpp:24-31."""
     LawsonEuler = 0
     Lawson2b = 1
     ExpEuler = 2
     ExpEulerLinearSplit = 3
     ETD2RK = 4
+    RosenbrockEuler = 5
 
 
 _NAMES = {Method.LawsonEuler: "lawson_euler", Method.Lawson2b: "lawson2b",
           Method.ExpEuler: "exp_euler", Method.ExpEulerLinearSplit: "exp_euler_ls",
-          Method.ETD2RK: "etd2rk"}
+          Method.ETD2RK: "etd2rk", Method.RosenbrockEuler: "rosenbrock_euler"}
 
 
 def method_name(m):
@@ -78,7 +79,7 @@ def parse_method(s):
     raise InvalidArgument(1, f"unknown method: {s}")
 
 
-G_ZERO, G_SQUARE, G_CONST, G_ALLEN_CAHN, G_BRUSSELATOR, G_NLS, G_ADR = range(7)
+G_ZERO, G_SQUARE, G_CONST, G_ALLEN_CAHN, G_BRUSSELATOR, G_NLS, G_ADR, G_RICCATI = range(8)
 
 
 def gfun(kind, *params) -> GFun:
@@ -107,13 +108,24 @@ class G:
         g._aux_src = [psi_a, u0_sq]
         return g
 
+    @staticmethod
+    def riccati(b, c_mat):
+        """The reference's LQR Riccati g(U) = C - (U b)(U^T b)^T
+        (src/problems.cpp:263-276) on an n x n state; b (n) and C (n x n)
+        are uploaded at the first device use.  With K = {A^T, A^T} it also
+        drives Rosenbrock-Euler's Jacobian factors (:212-250)."""
+        g = gfun(G_RICCATI)
+        g._aux_src = [b, c_mat]
+        return g
+
 
 def _bind_aux(g):
-    """Device pointers for a g with auxiliary fields (ADR)."""
+    """Device pointers for a g with auxiliary fields (ADR, Riccati)."""
     src = getattr(g, "_aux_src", None)
     if src is None or getattr(g, "_aux_dev", None) is not None:
         return g
-    dev = [x if _is_torch(x) else to_device(np.asarray(x)) for x in src]
+    dev = [x if _is_torch(x) else to_device(np.asfortranarray(x, dtype=np.float64))
+           for x in src]
     for i, t in enumerate(dev):
         g.aux[i] = t.data_ptr()
     g._aux_dev = dev
@@ -280,6 +292,21 @@ def _step(method, u, t, tau, K, g, f1, pref1, f2, pref2):
     return to_host(out) if host else out
 
 
+def eval_g(g, t, u):
+    """g(t, u) on the device (the closed set of include/kronphi_b200.h
+    KP_G_*; the reference's ProblemSpec::g, inc/integrators.hpp:60)."""
+    host = not _is_torch(u)
+    cplx = _is_cplx(u)
+    ud = to_device(u) if host else u
+    dims = list(ud.shape)
+    out = fortran_empty(dims, ud.dtype, ud.device)
+    ctx = _ctx_for(ud)
+    _bind_aux(g)
+    f = ctx.lib.kp_eval_g_c128 if cplx else ctx.lib.kp_eval_g_f64
+    check(f(ctx.h, C.byref(g), float(t), ud.data_ptr(), ints(dims), len(dims), out.data_ptr()))
+    return to_host(out) if host else out
+
+
 def lawson_euler_step(u, t, tau, g, exp_factors):
     """inc/integrators.hpp:116-122"""
     return _step(Method.LawsonEuler, u, t, tau, None, g, list(exp_factors), 1.0, None, 1.0)
@@ -307,6 +334,16 @@ def etd2rk_step(u, t, tau, k, g, phi1: SplitPhi, phi2: SplitPhi):
     k = _factor_list(k)
     return _step(Method.ETD2RK, u, t, tau, k.factors, g, phi1.factors, phi1.prefactor,
                  phi2.factors, phi2.prefactor)
+
+
+def rosenbrock_euler_step(u, t, tau, k, g, jac_factors, q=kDefaultQuadNodes):
+    """inc/integrators.hpp:166-194: phi_1(tau J_mu) rebuilt from the given
+    Jacobian factors on the device (the same object twice shares one build)."""
+    if q != kDefaultQuadNodes:
+        raise InvalidArgument(1, "rosenbrock_euler_step: the device step uses the default rule")
+    k = _factor_list(k)
+    return _step(Method.RosenbrockEuler, u, t, tau, k.factors, g, list(jac_factors), 1.0,
+                 None, 1.0)
 
 
 # --------------------------------------------------------------- integrate

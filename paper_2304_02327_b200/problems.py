@@ -8,7 +8,7 @@ inputs follow SURVEY.md 8(d) with numpy-seeded synthetic data (seeds
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import List
+from typing import List, Optional
 
 import numpy as np
 
@@ -57,10 +57,11 @@ class Config:
     g: object
     tau: float
     n_steps: int
+    t_end: Optional[float] = None  # exact T when tau = T / n_steps was given
 
     @property
     def t_final(self):
-        return self.tau * self.n_steps
+        return self.t_end if self.t_end is not None else self.tau * self.n_steps
 
 
 def ac2d(n=128, n_steps=100, tau=1e-3, seed=1001):
@@ -151,6 +152,41 @@ def adr(n1=40, n2=41, n3=42, n_steps=440, method="etd2rk", eps=0.75, alpha=0.1):
     cfg = Config("adr", method, u0, K, g, 1.0 / n_steps, n_steps)
     cfg.fields = (psi_a, np.asfortranarray(u0 * u0))
     cfg.exact = np.exp(1.0) * u0
+    return cfg
+
+
+def riccati(n_hat=30, n_steps=170, method="etd2rk", t_final=0.025, alpha=100.0):
+    """The reference's LQR differential Riccati problem (src/problems.cpp:130-186,
+    RiccatiProblem::to_problem_spec :252-283): U' = A^T U + U A + C + U B U on
+    the n x n state, n = n_hat^2, with A = I (x) D1 + D2 (x) I (D1 = dxx - 10x dx,
+    D2 = dyy - 100y dy, h = 1/(n_hat+1)), B = -b b^T, C = alpha c c^T (b, c
+    indicators of x in (0.1,0.3] / (0.7,0.9]), U0 = 0, K = {A^T, A^T}.
+    cfg.a_t = A^T; cfg.b, cfg.c_mat the g data."""
+    if n_hat < 2:
+        raise ValueError("build_riccati: need n_hat >= 2")
+    h = 1.0 / (n_hat + 1)
+    x = (np.arange(n_hat) + 1) * h
+    a1, a2 = -10.0 * x, -100.0 * x
+    d1 = np.zeros((n_hat, n_hat))
+    d2 = np.zeros((n_hat, n_hat))
+    i = np.arange(n_hat)
+    d1[i, i] = -2.0 / (h * h)
+    d2[i, i] = -2.0 / (h * h)
+    d1[i[1:], i[1:] - 1] = 1.0 / (h * h) - a1[1:] / (2.0 * h)
+    d2[i[1:], i[1:] - 1] = 1.0 / (h * h) - a2[1:] / (2.0 * h)
+    d1[i[:-1], i[:-1] + 1] = 1.0 / (h * h) + a1[:-1] / (2.0 * h)
+    d2[i[:-1], i[:-1] + 1] = 1.0 / (h * h) + a2[:-1] / (2.0 * h)
+    eye = np.eye(n_hat)
+    a = np.kron(eye, d1) + np.kron(d2, eye)  # rows i + j n_hat (x fastest)
+    a_t = np.asfortranarray(a.T)
+    b = np.tile(((x > 0.1) & (x <= 0.3)).astype(np.float64), n_hat)
+    c = np.tile(((x > 0.7) & (x <= 0.9)).astype(np.float64), n_hat)
+    c_mat = np.asfortranarray(np.outer(alpha * c, c))
+    n = n_hat * n_hat
+    from .integrators import G
+    cfg = Config(f"riccati{n_hat}", method, np.zeros((n, n), order="F"), [a_t, a_t],
+                 G.riccati(b, c_mat), t_final / n_steps, n_steps, t_final)
+    cfg.a_t, cfg.b, cfg.c_mat = a_t, b, c_mat
     return cfg
 
 

@@ -151,3 +151,30 @@ def test_divergence(port):
     with pytest.raises(pyoracle.Divergence, match="step"):
         port.integrate("lawson_euler", np.array([1e100, 1e100]), [np.zeros((2, 2))],
                        pyoracle.gfun(pyoracle.G_SQUARE), 0.0, 10.0, 10)
+
+
+@pytest.mark.parametrize("method", ["etd2rk", "rosenbrock_euler", "exp_euler"])
+def test_riccati_restatement_vs_live_reference(port, ref, method):
+    """The Riccati problem data (problems.riccati restating build_riccati,
+    src/problems.cpp:130-186), its g (:263-276) and the oracle's
+    Rosenbrock-Euler (inc/integrators.hpp:166-194 with the Jacobian factors
+    of :212-250) against the reference's own build + integrate.  ~1e-16:
+    the residual difference is the reference's vectorised LU rounding inside
+    phiquad (see test_phiquad)."""
+    import pyoracle
+    from paper_2304_02327_b200 import problems
+    c = problems.riccati(6)
+    g = pyoracle.gfun(pyoracle.G_RICCATI, aux=[c.b, c.c_mat])
+    for steps in (1, 7):
+        want, _ = ref.run_riccati(6, method, steps, 0.025)
+        got = port.integrate(method, c.u0, c.K, g, 0.0, 0.025, steps)
+        assert rel2(got, want) < 1e-14
+
+
+def test_riccati_rosenbrock_needs_riccati_g(port):
+    import pyoracle
+    from paper_2304_02327_b200 import problems
+    c = problems.riccati(3)
+    with pytest.raises(pyoracle.InvalidArgument, match="jacobian_factors"):
+        port.integrate("rosenbrock_euler", c.u0, c.K, pyoracle.gfun(pyoracle.G_ZERO), 0.0,
+                       0.025, 2)
