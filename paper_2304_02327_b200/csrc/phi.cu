@@ -18,11 +18,17 @@
 // branches of the reference (scaling exponent, Pade degree, singularity) read
 // small device results back to the host: a handful of 8-byte syncs per build.
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 #include <cmath>
 #include <string>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "kp_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace kp {
 namespace {
@@ -57,26 +63,35 @@ unsigned grid1(kp_ctx* ctx, long long n, int threads = 256) {
 
 // ---------------------------------------------------------------- kernels
 
-// out[b] = max_j sum_i |x_b(i,j)|, sums in increasing i (inc/matrix.hpp norm1)
+// out[b] = max_j sum_i |x_b(i,j)|, sums in increasing i (inc/matrix.hpp norm1).
+// One warp per 32 columns: 32 x 32 tiles staged through shared memory so the
+// loads are coalesced along the column while each lane keeps its column's
+// sequential sum; the per-warp maxima meet in an atomicMax on the bit pattern
+// (non-negative doubles order like their int64 bits).  out must be zeroed.
 __global__ void norm1_kernel(const double* __restrict__ x, int n, long long stride,
                              double* __restrict__ out) {
-  const double* xb = x + blockIdx.x * stride;
-  double best = 0.0;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    double s = 0.0;
-    const double* col = xb + (long long)j * n;
-    for (int i = 0; i < n; ++i) s = __dadd_rn(s, fabs(col[i]));
-    best = fmax(best, s);
+  __shared__ double tile[32][33];
+  const double* xb = x + blockIdx.y * stride;
+  const int lane = threadIdx.x, c0 = blockIdx.x * 32;
+  double s = 0.0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    double v[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c)  // 32 independent loads in flight
+      v[c] = (i < n && c0 + c < n) ? xb[i + (long long)(c0 + c) * n] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) tile[c][lane] = fabs(v[c]);
+    __syncwarp();
+    const int m = min(32, n - i0);
+    for (int r = 0; r < m; ++r) s = __dadd_rn(s, tile[lane][r]);
+    __syncwarp();
   }
-  __shared__ double red[32];
+  double best = (c0 + lane < n) ? s : 0.0;
   for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    best = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
-    if (threadIdx.x == 0) out[blockIdx.x] = best;
-  }
+  if (lane == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(out + blockIdx.y),
+              static_cast<unsigned long long>(__double_as_longlong(best)));
 }
 
 // y_b = x * scale_b  (per-batch scalar; x shared when xstride == 0)
@@ -145,13 +160,13 @@ __global__ void pade13_add_kernel(const double* __restrict__ a2, const double* _
 }
 
 // lhs = v - u, rhs = v + u
-__global__ void pm_kernel(const double* __restrict__ u, double* __restrict__ v, long long total,
-                          double* __restrict__ lhs) {
+__global__ void pm_kernel(const double* __restrict__ u, const double* __restrict__ v,
+                          long long total, double* __restrict__ lhs, double* __restrict__ rhs) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     const double uu = u[t], vv = v[t];
     lhs[t] = __dsub_rn(vv, uu);
-    v[t] = __dadd_rn(vv, uu);
+    rhs[t] = __dadd_rn(vv, uu);
   }
 }
 
@@ -235,6 +250,260 @@ __global__ void lu_panel_kernel(double* __restrict__ a, int n, long long stride,
       for (int i = j + 1 + tid; i < n; i += nt) colc[i] = __fma_rn(-colj[i], ajc, colc[i]);
     }
     __syncthreads();
+  }
+}
+
+// The same panel factorization with the panel spread over a thread-block
+// cluster: one cluster per matrix, the panel rows j0..n-1 split into
+// contiguous chunks of rows_per (<= 256) rows, one chunk per CTA.  Each row
+// lives in registers: warps 0-7 hold its columns 0..31, warps 8-15 its
+// columns 32..63 (so the live column range is warp-uniform).
+// Per column there is no cluster-wide barrier: every CTA PUSHES its local
+// pivot candidate (|a|, row, and the row's 64 values) into a slot of every
+// CTA's shared memory with st.async, which completes bytes on the receiver's
+// mbarrier; the owner of row j pushes row j the same way.  Each CTA then
+// waits on its own mbarrier, reduces the candidates locally (same tie rule as
+// lu_panel_kernel: largest |a|, then smallest row), takes the pivot row from
+// the winner's slot, the owners of rows j and p swap their registers, the
+// multipliers l_i are formed by the half holding column j and passed through
+// shared memory, and every thread rank-1 updates its live columns.  Slots
+// and mbarriers are double-buffered by column parity: a CTA can run at most
+// one column ahead of any other (it needs their next candidates), so a slot
+// is never overwritten while its previous contents are still in use.
+// The arithmetic is exactly lu_panel_kernel's (x * (1/pivot),
+// fma(-l_i, u_c, a_ic), u_c == 0 skipped): the factors are bitwise identical.
+constexpr int LUC_THREADS = 512;
+constexpr int LUC_HALF = LU_NB / 2;
+constexpr int LUC_ROWS = LUC_THREADS / 2;  // rows per CTA (max)
+constexpr int LUC_MAXCL = 16;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t cluster_addr(uint32_t local, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+// 16 bytes into another CTA's shared memory, completing on its mbarrier
+__device__ __forceinline__ void push16(uint32_t raddr, double x, double y, uint32_t rbar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+          raddr),
+      "d"(x), "d"(y), "r"(rbar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nKP_WAIT%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra KP_WAIT%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// Cluster-wide barrier with release/acquire at cluster scope (setup/teardown).
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// Dynamic index into a thread's register row: a switch on a warp-uniform
+// index compiles to one indirect branch instead of a 32-way select chain.
+#define KP_CASE32(M) M(0) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) \
+  M(13) M(14) M(15) M(16) M(17) M(18) M(19) M(20) M(21) M(22) M(23) M(24) M(25) M(26) M(27) \
+  M(28) M(29) M(30) M(31)
+__device__ __forceinline__ double reg_get(const double (&r)[LUC_HALF], int k) {
+  double v = 0.0;
+  switch (k) {
+#define KP_GET(K) \
+  case K:         \
+    v = r[K];     \
+    break;
+    KP_CASE32(KP_GET)
+#undef KP_GET
+  }
+  return v;
+}
+__device__ __forceinline__ void reg_set(double (&r)[LUC_HALF], int k, double v) {
+  switch (k) {
+#define KP_SET(K) \
+  case K:         \
+    r[K] = v;     \
+    break;
+    KP_CASE32(KP_SET)
+#undef KP_SET
+  }
+}
+// r[k] -= l * u[k] for k >= k0 (u[k] == 0 skipped): Duff's device on a
+// warp-uniform start, so only the live columns are visited.
+__device__ __forceinline__ void row_update_from(double (&r)[LUC_HALF], int k0, double l,
+                                                const double* __restrict__ u) {
+  switch (k0) {
+#define KP_UPD(K)                                   \
+  case K: {                                         \
+    const double ajc = u[K];                        \
+    if (ajc != 0.0) r[K] = __fma_rn(-l, ajc, r[K]); \
+  }                                                 \
+    [[fallthrough]];
+    KP_CASE32(KP_UPD)
+#undef KP_UPD
+    default:
+      break;
+  }
+}
+
+__device__ __forceinline__ void argmax_merge(double& best, int& bi, double ov, int oi) {
+  if (ov > best || (ov == best && oi < bi)) {
+    best = ov;
+    bi = oi;
+  }
+}
+
+__device__ __forceinline__ void warp_argmax(double& best, int& bi) {
+  for (int o = 16; o > 0; o >>= 1)
+    argmax_merge(best, bi, __shfl_xor_sync(0xffffffffu, best, o),
+                 __shfl_xor_sync(0xffffffffu, bi, o));
+}
+
+__global__ void __launch_bounds__(LUC_THREADS, 1)
+    lu_panel_cluster_kernel(double* __restrict__ a, int n, long long stride, int j0, int nb,
+                            int rows_per, int* __restrict__ piv, int* __restrict__ singular) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = int(cl.block_rank());
+  const int ncta = int(cl.num_blocks());
+  __shared__ __align__(16) double in_row[2][LUC_MAXCL][LU_NB];  // candidates' rows
+  __shared__ __align__(16) double in_hdr[2][LUC_MAXCL][2];      // (|a|, row) per rank
+  __shared__ __align__(16) double in_jrow[2][LU_NB];            // row j
+  __shared__ __align__(16) double out_row[LU_NB];   // this CTA's candidate row
+  __shared__ __align__(16) double out_jrow[LU_NB];  // row j (its owner only)
+  __shared__ __align__(8) unsigned long long mbar[2];
+  __shared__ double lmul[LUC_ROWS];  // multipliers of the current column
+  __shared__ double wv[8];
+  __shared__ int wi[8];
+  __shared__ int s_piv[LU_NB];  // pivots, flushed at the end
+  __shared__ int s_sing;
+  double* ab = a + blockIdx.y * stride;
+  int* pb = piv + (long long)blockIdx.y * n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int h = warp >> 3;                // column half of this thread
+  const int lr = (warp & 7) * 32 + lane;  // local row
+  const int r0 = j0 + rank * rows_per;
+  const int rows = max(0, min(n, r0 + rows_per) - r0);
+  const bool has_row = lr < rows;
+  const int row = r0 + lr;
+  const uint32_t bytes_per_col = uint32_t(ncta) * (LU_NB + 2) * 8 + LU_NB * 8;
+  if (tid == 0) {
+    s_sing = 0;
+    for (int b = 0; b < 2; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&mbar[b])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  double r[LUC_HALF];
+#pragma unroll
+  for (int k = 0; k < LUC_HALF; ++k) {
+    const int c = h * LUC_HALF + k;
+    r[k] = (has_row && c < nb) ? ab[row + (long long)(j0 + c) * n] : 0.0;
+  }
+  cluster_barrier();  // every CTA's mbarriers are initialised before any push
+  // push lanes: thread t sends 16 bytes (chunk t % 32) to rank t / 32
+  const int dst = tid >> 5, chunk = lane;
+  const bool pusher = dst < ncta;
+#pragma unroll 1
+  for (int jj = 0; jj < nb; ++jj) {
+    const int j = j0 + jj, buf = jj & 1;
+    const int hj = jj / LUC_HALF, kj = jj % LUC_HALF;
+    const int oj = jj / rows_per;
+    // 1. local argmax over the rows >= j (the warps holding column jj)
+    if (h == hj) {
+      double best = -1.0;
+      int bi = n;
+      if (has_row && row >= j) {
+        best = fabs(reg_get(r, kj));
+        bi = row;
+      }
+      warp_argmax(best, bi);
+      if (lane == 0) {
+        wv[warp & 7] = best;
+        wi[warp & 7] = bi;
+      }
+    }
+    __syncthreads();
+    double lbest = lane < 8 ? wv[lane] : -1.0;
+    int lbi = lane < 8 ? wi[lane] : n;
+    warp_argmax(lbest, lbi);
+    if (has_row && row == lbi) {
+#pragma unroll
+      for (int k = 0; k < LUC_HALF; ++k) out_row[h * LUC_HALF + k] = r[k];
+    }
+    if (has_row && row == j) {
+#pragma unroll
+      for (int k = 0; k < LUC_HALF; ++k) out_jrow[h * LUC_HALF + k] = r[k];
+    }
+    __syncthreads();
+    // 2. push the candidate (and row j) to every rank; expect this column's bytes
+    if (tid == 0) mbar_expect(smem_addr(&mbar[buf]), bytes_per_col);
+    if (pusher) {
+      const uint32_t rbar = cluster_addr(smem_addr(&mbar[buf]), dst);
+      const double2 v = reinterpret_cast<const double2*>(out_row)[chunk];
+      push16(cluster_addr(smem_addr(&in_row[buf][rank][2 * chunk]), dst), v.x, v.y, rbar);
+      if (chunk == 0)
+        push16(cluster_addr(smem_addr(&in_hdr[buf][rank][0]), dst), lbest, double(lbi), rbar);
+      if (rank == oj) {
+        const double2 w = reinterpret_cast<const double2*>(out_jrow)[chunk];
+        push16(cluster_addr(smem_addr(&in_jrow[buf][2 * chunk]), dst), w.x, w.y, rbar);
+      }
+    }
+    mbar_wait(smem_addr(&mbar[buf]), uint32_t((jj >> 1) & 1));
+    // 3. global pivot (every warp, from local copies)
+    double best = -1.0;
+    int bi = n;
+    if (lane < ncta) {
+      best = in_hdr[buf][lane][0];
+      bi = int(in_hdr[buf][lane][1]);
+    }
+    warp_argmax(best, bi);
+    const bool sing = !(best > 0.0);
+    const int p = sing ? j : bi;  // singular column: no swap, pivot row = row j
+    if (tid == 0) {
+      if (sing) s_sing = 1;
+      s_piv[jj] = p;
+    }
+    const int op = (p - j0) / rows_per;
+    const double* prow = (p == j) ? in_jrow[buf] : in_row[buf][op];
+    // 4. swap rows j and p, multipliers of column jj
+    if (p != j && has_row) {
+      if (row == j) {
+#pragma unroll
+        for (int k = 0; k < LUC_HALF; ++k) r[k] = prow[h * LUC_HALF + k];
+      } else if (row == p) {
+#pragma unroll
+        for (int k = 0; k < LUC_HALF; ++k) r[k] = in_jrow[buf][h * LUC_HALF + k];
+      }
+    }
+    const bool below = has_row && row > j;
+    if (h == hj && below) {
+      const double l = __dmul_rn(reg_get(r, kj), 1.0 / prow[jj]);
+      reg_set(r, kj, l);
+      lmul[lr] = l;
+    }
+    __syncthreads();
+    // 5. rank-1 update of the columns > jj
+    const int k0 = jj + 1 - h * LUC_HALF;  // first live column of this half
+    if (below && k0 < LUC_HALF) row_update_from(r, max(k0, 0), lmul[lr], prow + h * LUC_HALF);
+  }
+  cluster_barrier();  // all pushes into every CTA have landed and been consumed
+  if (rank == 0) {
+    if (tid < nb) pb[j0 + tid] = s_piv[tid];
+    if (tid == 0 && s_sing) *singular = 1;
+  }
+#pragma unroll
+  for (int k = 0; k < LUC_HALF; ++k) {
+    const int c = h * LUC_HALF + k;
+    if (has_row && c < nb) ab[row + (long long)(j0 + c) * n] = r[k];
   }
 }
 
@@ -411,7 +680,8 @@ enum : int {
 
 std::vector<double> norms1(kp_ctx* ctx, const double* x, int n, int batch) {
   double* d = slot<double>(ctx, S_NORMS, std::max(batch, 1));
-  norm1_kernel<<<batch, 256, 0, ctx->stream>>>(x, n, (long long)n * n, d);
+  KP_CUDA(cudaMemsetAsync(d, 0, batch * sizeof(double), ctx->stream));
+  norm1_kernel<<<dim3((n + 31) / 32, batch), 32, 0, ctx->stream>>>(x, n, (long long)n * n, d);
   ctx->launches++;
   KP_CUDA(cudaGetLastError());
   std::vector<double> h(batch);
@@ -433,6 +703,59 @@ void check_finite(kp_ctx* ctx, const double* x, long long total, const char* who
   if (!h) throw invalid_argument(std::string(who) + ": non-finite entries");
 }
 
+// Launch the cluster panel kernel when the panel rows fit a cluster
+// (<= 16 CTAs of 256 rows); false -> caller uses the one-CTA kernel.  KP_LU_PANEL=simple forces the one-CTA kernel (read per call).
+bool lu_panel_cluster(kp_ctx* ctx, double* a, int n, long long nn, int j0, int nb, int batch,
+                      int* piv, int* sing) {
+  constexpr int kMaxRows = LUC_ROWS;
+  static int max_cluster = 0;  // 0 = not probed yet, -1 = unavailable
+  const char* env = std::getenv("KP_LU_PANEL");
+  if (env && std::string(env) == "simple") return false;
+  if (max_cluster == 0) {  // probe once: 16-CTA clusters are opt-in (non-portable)
+    max_cluster = 8;
+    if (cudaFuncSetAttribute(lu_panel_cluster_kernel,
+                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(16, 1);
+      cfg.blockDim = dim3(LUC_THREADS);
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 16;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, lu_panel_cluster_kernel, &cfg) ==
+              cudaSuccess &&
+          nclusters > 0)
+        max_cluster = 16;
+    }
+    (void)cudaGetLastError();
+  }
+  if (max_cluster < 0) return false;
+  const int rows_total = n - j0;
+  int ncta = std::max(1, (rows_total + kMaxRows - 1) / kMaxRows);
+  if (ncta > max_cluster) return false;
+  const int rows_per = (rows_total + ncta - 1) / ncta;
+  ncta = (rows_total + rows_per - 1) / rows_per;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ncta, batch);
+  cfg.blockDim = dim3(LUC_THREADS);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = ncta;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  KP_CUDA(cudaLaunchKernelEx(&cfg, lu_panel_cluster_kernel, a, n, nn, j0, nb, rows_per, piv,
+                             sing));
+  return true;
+}
+
 // lu_factor + lu_solve(lhs, rhs) for a batch; rhs overwritten with the solution.
 void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs) {
   const long long nn = (long long)n * n;
@@ -442,7 +765,8 @@ void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs) {
   const int nt = 256;
   for (int j0 = 0; j0 < n; j0 += LU_NB) {  // lu_factor (:125-146)
     const int nb = std::min(LU_NB, n - j0);
-    lu_panel_kernel<<<batch, 512, 0, ctx->stream>>>(lhs, n, nn, j0, nb, piv, sing);
+    if (!lu_panel_cluster(ctx, lhs, n, nn, j0, nb, batch, piv, sing))
+      lu_panel_kernel<<<batch, 512, 0, ctx->stream>>>(lhs, n, nn, j0, nb, piv, sing);
     ctx->launches++;
     if (j0 > 0) {
       swaps_kernel<<<dim3((j0 + nt - 1) / nt, batch), nt, 0, ctx->stream>>>(lhs, n, nn, piv, n, j0,
@@ -544,8 +868,11 @@ void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs) {
   KP_CUDA(cudaGetLastError());
 }
 
-// pade_low for a batch of matrices sharing one degree (inc/matrix_functions.hpp:37-54)
-void pade_low_batch(kp_ctx* ctx, const double* a, int n, int batch, int idx, double* out) {
+// pade_low for a batch of matrices sharing one degree (inc/matrix_functions.hpp:37-54):
+// the linear system (v - u) r = v + u, solved by the caller (one LU for all
+// degrees of an expm batch).
+void pade_low_batch(kp_ctx* ctx, const double* a, int n, int batch, int idx, double* lhs_out,
+                    double* rhs_out) {
   const auto& b = pade_coeffs()[idx];
   const int npow = (int(b.size()) - 2) / 2;
   const long long nn = (long long)n * n, tot = nn * batch;
@@ -568,15 +895,13 @@ void pade_low_batch(kp_ctx* ctx, const double* a, int n, int batch, int idx, dou
   ctx->launches++;
   double* au = slot<double>(ctx, S_AU, tot);
   matmul_batch(ctx, n, batch, a, nn, u, nn, au, nn);  // u = a*u
-  double* lhs = slot<double>(ctx, S_LHS, tot);
-  pm_kernel<<<grid1(ctx, tot), 256, 0, ctx->stream>>>(au, v, tot, lhs);  // v-u | v+u
+  pm_kernel<<<grid1(ctx, tot), 256, 0, ctx->stream>>>(au, v, tot, lhs_out, rhs_out);  // v-u | v+u
   ctx->launches++;
-  lu_solve_batch(ctx, n, batch, lhs, v);
-  KP_CUDA(cudaMemcpyAsync(out, v, tot * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
 }
 
-// pade13 (inc/matrix_functions.hpp:57-72) for a batch
-void pade13_batch(kp_ctx* ctx, const double* a, int n, int batch, double* out) {
+// pade13 (inc/matrix_functions.hpp:57-72) for a batch: the system as above
+void pade13_batch(kp_ctx* ctx, const double* a, int n, int batch, double* lhs_out,
+                  double* rhs_out) {
   const auto& b = pade_coeffs()[4];
   const long long nn = (long long)n * n, tot = nn * batch;
   double* a2 = slot<double>(ctx, S_A2, tot);
@@ -597,18 +922,17 @@ void pade13_batch(kp_ctx* ctx, const double* a, int n, int batch, double* out) {
   double* z = slot<double>(ctx, S_V, tot);
   matmul_batch(ctx, n, batch, a6, nn, w, nn, z, nn);
   pade13_add_kernel<<<g, 256, 0, ctx->stream>>>(a2, a4, a6, tot, n, nn, b[6], b[4], b[2], b[0], z);
-  double* lhs = slot<double>(ctx, S_LHS, tot);
-  pm_kernel<<<g, 256, 0, ctx->stream>>>(u, z, tot, lhs);
+  pm_kernel<<<g, 256, 0, ctx->stream>>>(u, z, tot, lhs_out, rhs_out);
   ctx->launches += 5;
   KP_CUDA(cudaGetLastError());
-  lu_solve_batch(ctx, n, batch, lhs, z);
-  KP_CUDA(cudaMemcpyAsync(out, z, tot * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
 }
 
 }  // namespace
 
 // expm of a batch of matrices x_b (inc/matrix_functions.hpp:76-95).  Degree
-// per matrix from its own 1-norm; matrices sharing a branch run together.
+// and scaling per matrix from its own 1-norm; the Pade systems of all
+// matrices are assembled group by group (same degree and scaling) in one
+// group-ordered buffer, solved by ONE batched LU, and each group squared.
 void expm_batch(kp_ctx* ctx, const double* x, int n, int batch, double* out) {
   const long long nn = (long long)n * n;
   const std::vector<double> nrm = norms1(ctx, x, n, batch);
@@ -629,44 +953,56 @@ void expm_batch(kp_ctx* ctx, const double* x, int n, int batch, double* out) {
       }
     }
   }
-  // group by (branch, scaling) and run each group as one batch
+  // group-ordered permutation: groups of equal (branch, scaling)
+  std::vector<int> order;
+  std::vector<std::pair<int, int>> groups;  // (first position, size)
   std::vector<bool> done(batch, false);
   for (int b0 = 0; b0 < batch; ++b0) {
     if (done[b0]) continue;
-    std::vector<int> grp;
+    const int first = int(order.size());
     for (int b = b0; b < batch; ++b)
       if (!done[b] && branch[b] == branch[b0] && sc[b] == sc[b0]) {
-        grp.push_back(b);
+        order.push_back(b);
         done[b] = true;
       }
-    const int g = int(grp.size());
-    double* gin = slot<double>(ctx, S_ARG, size_t(nn) * g);
-    double* gout = slot<double>(ctx, S_TAB, size_t(nn) * g);
-    for (int i = 0; i < g; ++i)
-      KP_CUDA(cudaMemcpyAsync(gin + i * nn, x + grp[i] * nn, nn * sizeof(double),
-                              cudaMemcpyDeviceToDevice, ctx->stream));
+    groups.emplace_back(first, int(order.size()) - first);
+  }
+  double* gin = slot<double>(ctx, S_ARG, size_t(nn) * batch);
+  double* lhs = slot<double>(ctx, S_LHS, size_t(nn) * batch);
+  double* rhs = slot<double>(ctx, S_TAB, size_t(nn) * batch);
+  for (int i = 0; i < batch; ++i)
+    KP_CUDA(cudaMemcpyAsync(gin + i * nn, x + order[i] * nn, nn * sizeof(double),
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+  for (const auto& gr : groups) {
+    const int b0 = order[gr.first], g = gr.second;
+    double* gi = gin + gr.first * nn;
     if (branch[b0] < 4) {
-      pade_low_batch(ctx, gin, n, g, branch[b0], gout);
+      pade_low_batch(ctx, gi, n, g, branch[b0], lhs + gr.first * nn, rhs + gr.first * nn);
     } else {
-      const int s = sc[b0];
       double* scale = slot<double>(ctx, S_COEF, 256);
-      std::vector<double> hs(g, std::ldexp(1.0, -s));
+      std::vector<double> hs(g, std::ldexp(1.0, -sc[b0]));
       KP_CUDA(cudaMemcpyAsync(scale, hs.data(), g * sizeof(double), cudaMemcpyHostToDevice,
                               ctx->stream));
-      scale_batch_kernel<<<grid1(ctx, nn * g), 256, 0, ctx->stream>>>(gin, nn, scale, nn, g, gin);
+      scale_batch_kernel<<<grid1(ctx, nn * g), 256, 0, ctx->stream>>>(gi, nn, scale, nn, g, gi);
       ctx->launches++;
-      pade13_batch(ctx, gin, n, g, gout);
-      double* tmp = slot<double>(ctx, S_T1, size_t(nn) * g);
-      for (int i = 0; i < s; ++i) {  // f = f*f
-        matmul_batch(ctx, n, g, gout, nn, gout, nn, tmp, nn);
-        KP_CUDA(cudaMemcpyAsync(gout, tmp, nn * g * sizeof(double), cudaMemcpyDeviceToDevice,
-                                ctx->stream));
-      }
+      pade13_batch(ctx, gi, n, g, lhs + gr.first * nn, rhs + gr.first * nn);
+      KP_CUDA(cudaStreamSynchronize(ctx->stream));  // S_COEF is reused by the next group
     }
-    for (int i = 0; i < g; ++i)
-      KP_CUDA(cudaMemcpyAsync(out + grp[i] * nn, gout + i * nn, nn * sizeof(double),
-                              cudaMemcpyDeviceToDevice, ctx->stream));
   }
+  lu_solve_batch(ctx, n, batch, lhs, rhs);
+  for (const auto& gr : groups) {
+    const int s = sc[order[gr.first]], g = gr.second;
+    double* f = rhs + gr.first * nn;
+    double* tmp = slot<double>(ctx, S_T1, size_t(nn) * g);
+    for (int i = 0; i < s; ++i) {  // f = f*f
+      matmul_batch(ctx, n, g, f, nn, f, nn, tmp, nn);
+      KP_CUDA(cudaMemcpyAsync(f, tmp, nn * g * sizeof(double), cudaMemcpyDeviceToDevice,
+                              ctx->stream));
+    }
+  }
+  for (int i = 0; i < batch; ++i)
+    KP_CUDA(cudaMemcpyAsync(out + order[i] * nn, rhs + i * nn, nn * sizeof(double),
+                            cudaMemcpyDeviceToDevice, ctx->stream));
 }
 
 // phiquad (inc/matrix_functions.hpp:146-199) for one matrix x (device):

@@ -141,3 +141,19 @@ def test_tau_zero_gives_identity_over_factorial(kp):
         sp = kp.build_split_phi(k, 0.0, ell)
         for f in sp.factors:
             assert np.abs(f - np.eye(f.shape[0]) / math.factorial(ell)).sum(0).max() < 1e-15
+
+
+@pytest.mark.parametrize("n", [70, 300, 900, 1700])
+def test_cluster_lu_panel_bitwise(kp, n, monkeypatch):
+    """The DSMEM cluster panel factorization (phi.cu lu_panel_cluster_kernel)
+    and the one-CTA panel kernel produce bitwise identical expm (same
+    arithmetic, different schedule); n = 1700 needs > 8 CTAs per panel.
+    A matrix with repeated |entries| exercises the pivot tie rule."""
+    r = rng(n)
+    x = r.standard_normal((n, n)) * (3.0 / np.sqrt(n))
+    x[:, 5] = np.round(x[:, 5] * 2) / 2  # ties in one pivot column
+    x = np.asfortranarray(x)
+    got = kp.expm(x)
+    monkeypatch.setenv("KP_LU_PANEL", "simple")
+    want = kp.expm(x)
+    assert np.array_equal(got, want)
