@@ -492,7 +492,7 @@ def main():
                              "algorithmic": "2*N*sum(n_mu) = 412.3 GFLOP per Tucker, "
                                             "137.4 GFLOP per mode-product launch"},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clk.summary(), "integrators": integ, "paper_adr": paper}
+                "clocks": clk.summary(), "integrators": integ, "paper_experiments": paper}
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

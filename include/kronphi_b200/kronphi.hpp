@@ -15,9 +15,17 @@
 // Containers stay host value types; every O(n^3)/O(N n) operation runs on the
 // GPU (upload, DMMA kernels, download).  Differences, by design:
 //   * g is a device nonlinearity from the closed set (kp_gfun: Allen-Cahn,
-//     Brusselator, NLS, zero, square, const) -- a host std::function has no
-//     device equivalent and is rejected (no CPU fallback on the hot path);
-//   * Backend::DenseOracle and Method::RosenbrockEuler are not provided;
+//     Brusselator, NLS, zero, square, const, and the reference's own ADR and
+//     Riccati g's) -- a host std::function has no device equivalent and is
+//     rejected (no CPU fallback on the hot path);
+//   * Method::RosenbrockEuler is provided for the Riccati g, whose Jacobian
+//     factors (the reference's ProblemSpec::jacobian_factors callback,
+//     src/problems.cpp:212-250) are rebuilt on the device every step;
+//     rosenbrock_euler_step takes caller-supplied factors like the reference;
+//   * Backend::DenseOracle is not provided;
+//   * problems: fd_operator_1d, build_adr, build_riccati (problems.hpp) with
+//     to_problem_spec(); their g's auxiliary fields live on the device and are
+//     kept alive by ProblemSpec::device_data;
 //   * the small elementwise helpers (axpy, scale, ...) run on the host
 //     containers like the reference's.
 // Link with -lkronphi_b200 (paper_2304_02327_b200/lib).
@@ -30,6 +38,7 @@
 #include <cstring>
 #include <algorithm>
 #include <initializer_list>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <type_traits>
@@ -586,7 +595,7 @@ Tensor<T> apply_split_phi(const SplitPhi<T>& sp, const Tensor<T>& v) {
 
 // ------------------------------------------------------- integrators
 
-enum class Method { LawsonEuler, Lawson2b, ExpEuler, ExpEulerLinearSplit, ETD2RK };
+enum class Method { LawsonEuler, Lawson2b, ExpEuler, ExpEulerLinearSplit, ETD2RK, RosenbrockEuler };
 
 inline const char* method_name(Method m) {
   switch (m) {
@@ -595,12 +604,13 @@ inline const char* method_name(Method m) {
     case Method::ExpEuler: return "exp_euler";
     case Method::ExpEulerLinearSplit: return "exp_euler_ls";
     case Method::ETD2RK: return "etd2rk";
+    case Method::RosenbrockEuler: return "rosenbrock_euler";
   }
   return "?";
 }
 inline Method parse_method(const std::string& s) {
   for (Method m : {Method::LawsonEuler, Method::Lawson2b, Method::ExpEuler,
-                   Method::ExpEulerLinearSplit, Method::ETD2RK})
+                   Method::ExpEulerLinearSplit, Method::ETD2RK, Method::RosenbrockEuler})
     if (s == method_name(m)) return m;
   throw std::invalid_argument("unknown method: " + s);
 }
@@ -614,6 +624,15 @@ inline GFun g_allen_cahn() { return GFun{KP_G_ALLEN_CAHN, {0, 0, 0, 0}}; }
 inline GFun g_brusselator(double a, double b) { return GFun{KP_G_BRUSSELATOR, {a, b, 0, 0}}; }
 inline GFun g_nls() { return GFun{KP_G_NLS, {0, 0, 0, 0}}; }
 
+// Device copies of a g's auxiliary fields (ADR: psi_a, u0^2; Riccati: b, C).
+struct DeviceFields {
+  std::vector<detail::DevBuf> bufs;
+  const double* add(const double* host, size_t count) {
+    bufs.emplace_back(host, count * sizeof(double));
+    return bufs.back().d();
+  }
+};
+
 template <typename T = double>
 struct ProblemSpecT {
   KroneckerSum<T> K;
@@ -621,6 +640,7 @@ struct ProblemSpecT {
   Tensor<T> u0;
   double t0 = 0.0;
   double t_final = 1.0;
+  std::shared_ptr<DeviceFields> device_data;  // keeps g.aux alive
 };
 using ProblemSpec = ProblemSpecT<double>;
 
@@ -718,6 +738,169 @@ Tensor<T> etd2rk_step(const Tensor<T>& u, double t, double tau, const KroneckerS
                       const GFun& g, const SplitPhi<T>& phi1, const SplitPhi<T>& phi2) {
   return detail::step<T>(Method::ETD2RK, u, t, tau, &k, g, phi1.factors, phi1.prefactor,
                          &phi2.factors, phi2.prefactor);
+}
+// inc/integrators.hpp:166-194: phi_1(tau J_mu) of the given Jacobian factors
+// built on the device in the call (uses the default 12-node rule).
+template <typename T>
+Tensor<T> rosenbrock_euler_step(const Tensor<T>& u, double t, double tau,
+                                const KroneckerSum<T>& k, const GFun& g,
+                                const std::vector<Matrix<T>>& jac_factors) {
+  return detail::step<T>(Method::RosenbrockEuler, u, t, tau, &k, g, jac_factors, 1.0, nullptr,
+                         1.0);
+}
+
+// ------------------------------------------------------- problems (problems.hpp)
+
+// Dirichlet tridiagonal eps*u'' + alpha*u' on n inner points, h = 1/(n+1)
+// (src/problems.cpp:9-22).
+inline Matrix<double> fd_operator_1d(int n, double eps, double alpha) {
+  if (n < 1) throw std::invalid_argument("fd_operator_1d: need n >= 1");
+  const double h = 1.0 / (n + 1);
+  const double sub = eps / (h * h) - alpha / (2.0 * h);
+  const double dia = -2.0 * eps / (h * h);
+  const double sup = eps / (h * h) + alpha / (2.0 * h);
+  Matrix<double> m(n, n);
+  for (int i = 0; i < n; ++i) {
+    m(i, i) = dia;
+    if (i > 0) m(i, i - 1) = sub;
+    if (i + 1 < n) m(i, i + 1) = sup;
+  }
+  return m;
+}
+
+inline Matrix<double> matrix_from_tensor(const Tensor<double>& t) {
+  if (t.order() != 2) throw std::invalid_argument("matrix_from_tensor: tensor order != 2");
+  return Matrix<double>(t.dim(0), t.dim(1), vec(t));
+}
+inline Tensor<double> tensor_from_matrix(const Matrix<double>& m) {
+  return Tensor<double>({m.rows(), m.cols()}, std::vector<double>(m.data(), m.data() + m.size()));
+}
+
+// The 3-D ADR problem with the manufactured solution e^t u0 (src/problems.cpp:45-128):
+// u_t = eps Lap u + alpha sum d_mu u + 1/(1+u^2) + Psi(t,x), T = 1.
+struct ADRProblem {
+  std::vector<int> dims;
+  std::vector<Matrix<double>> factors;
+  double eps = 0.75;
+  double alpha = 0.1;
+  std::vector<std::vector<double>> grids;
+  Tensor<double> u0, u0_sq, psi_a;
+  Tensor<double> exact(double t) const {
+    Tensor<double> e = u0;
+    scale(e, std::exp(t));
+    return e;
+  }
+  ProblemSpec to_problem_spec() const {
+    ProblemSpec spec;
+    spec.K = KroneckerSum<double>(factors);
+    spec.u0 = u0;
+    spec.t0 = 0.0;
+    spec.t_final = 1.0;
+    spec.device_data = std::make_shared<DeviceFields>();
+    spec.g = GFun{KP_G_ADR, {0, 0, 0, 0}};
+    spec.g.aux[0] = spec.device_data->add(psi_a.data(), psi_a.size());
+    spec.g.aux[1] = spec.device_data->add(u0_sq.data(), u0_sq.size());
+    return spec;
+  }
+};
+
+inline ADRProblem build_adr(int n1, int n2, int n3) {
+  ADRProblem pr;
+  pr.dims = {n1, n2, n3};
+  for (int n : pr.dims) {
+    pr.factors.push_back(fd_operator_1d(n, pr.eps, pr.alpha));
+    std::vector<double> x(n);
+    for (int i = 0; i < n; ++i) x[i] = (i + 1) * (1.0 / (n + 1));
+    pr.grids.push_back(std::move(x));
+  }
+  pr.u0 = Tensor<double>(pr.dims);
+  pr.u0_sq = Tensor<double>(pr.dims);
+  pr.psi_a = Tensor<double>(pr.dims);
+  auto q = [](double x) { return x * (1.0 - x); };    // one quadratic factor
+  auto dq = [](double x) { return 1.0 - 2.0 * x; };  // its derivative
+  std::size_t e = 0;
+  for (int k = 0; k < n3; ++k)
+    for (int j = 0; j < n2; ++j)
+      for (int i = 0; i < n1; ++i, ++e) {
+        const double x = pr.grids[0][i], y = pr.grids[1][j], z = pr.grids[2][k];
+        const double qx = q(x), qy = q(y), qz = q(z);
+        const double v = 64.0 * qx * qy * qz;
+        const double lap = 64.0 * (-2.0) * (qy * qz + qx * qz + qx * qy);
+        const double adv = 64.0 * (dq(x) * qy * qz + dq(y) * qx * qz + dq(z) * qx * qy);
+        pr.u0[e] = v;
+        pr.u0_sq[e] = v * v;
+        pr.psi_a[e] = v - pr.eps * lap - pr.alpha * adv;
+      }
+  return pr;
+}
+
+// The 2-D LQR differential Riccati problem (src/problems.cpp:130-284):
+// U' = A^T U + U A + C + U B U, B = -b b^T, C = alpha c c^T, U0 = 0.
+struct RiccatiProblem {
+  int n_hat = 0;
+  Matrix<double> a, a_t;
+  std::vector<double> b, c;
+  double alpha = 100.0;
+  Matrix<double> b_mat, c_mat, u0;
+  // K = {A^T, A^T}, g = C - (U b)(U^T b)^T on the device; Rosenbrock-Euler's
+  // Jacobian factors A^T - (U b) b^T are formed on the device from the same g.
+  ProblemSpec to_problem_spec(double t_final = 0.025) const {
+    ProblemSpec spec;
+    spec.K = KroneckerSum<double>({a_t, a_t});
+    spec.u0 = tensor_from_matrix(u0);
+    spec.t0 = 0.0;
+    spec.t_final = t_final;
+    spec.device_data = std::make_shared<DeviceFields>();
+    spec.g = GFun{KP_G_RICCATI, {0, 0, 0, 0}};
+    spec.g.aux[0] = spec.device_data->add(b.data(), b.size());
+    spec.g.aux[1] = spec.device_data->add(c_mat.data(), c_mat.size());
+    return spec;
+  }
+};
+
+inline RiccatiProblem build_riccati(int n_hat) {
+  if (n_hat < 2) throw std::invalid_argument("build_riccati: need n_hat >= 2");
+  RiccatiProblem pr;
+  pr.n_hat = n_hat;
+  const int n = n_hat * n_hat;
+  const double h = 1.0 / (n_hat + 1);
+  // 1-D operators dxx + a(x) dx with a = -10x (x direction), -100y (y direction)
+  auto op = [&](double coef) {
+    Matrix<double> d(n_hat, n_hat);
+    for (int i = 0; i < n_hat; ++i) {
+      const double adv = coef * ((i + 1) * h);
+      d(i, i) = -2.0 / (h * h);
+      if (i > 0) d(i, i - 1) = 1.0 / (h * h) - adv / (2.0 * h);
+      if (i + 1 < n_hat) d(i, i + 1) = 1.0 / (h * h) + adv / (2.0 * h);
+    }
+    return d;
+  };
+  const Matrix<double> dx = op(-10.0), dy = op(-100.0);
+  pr.a = Matrix<double>(n, n);  // I (x) Dx + Dy (x) I, x fastest
+  for (int j = 0; j < n_hat; ++j)
+    for (int i = 0; i < n_hat; ++i) {
+      const int r = i + j * n_hat;
+      for (int i2 = 0; i2 < n_hat; ++i2) pr.a(r, i2 + j * n_hat) += dx(i, i2);
+      for (int j2 = 0; j2 < n_hat; ++j2) pr.a(r, i + j2 * n_hat) += dy(j, j2);
+    }
+  pr.a_t = pr.a.transposed();
+  pr.b.assign(n, 0.0);
+  pr.c.assign(n, 0.0);
+  for (int j = 0; j < n_hat; ++j)
+    for (int i = 0; i < n_hat; ++i) {
+      const double x = (i + 1) * h;
+      pr.b[i + j * n_hat] = (x > 0.1 && x <= 0.3) ? 1.0 : 0.0;
+      pr.c[i + j * n_hat] = (x > 0.7 && x <= 0.9) ? 1.0 : 0.0;
+    }
+  pr.b_mat = Matrix<double>(n, n);
+  pr.c_mat = Matrix<double>(n, n);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      pr.b_mat(i, j) = -pr.b[i] * pr.b[j];
+      pr.c_mat(i, j) = pr.alpha * pr.c[i] * pr.c[j];
+    }
+  pr.u0 = Matrix<double>(n, n);
+  return pr;
 }
 
 }  // namespace kronphi

@@ -9,6 +9,7 @@
 #include <string>
 
 #include "kronphi/integrators.hpp"
+#include "kronphi/problems.hpp"
 #include "kronphi/matrix_functions.hpp"
 #include "kronphi/mode_product.hpp"
 #include "kronphi/split_phi.hpp"
@@ -158,6 +159,47 @@ int main() {
         worst = std::max(worst, std::abs(got.at({i, j}) - acc));
       }
     CHECK(worst < 1e-14);
+  }
+  {  // Riccati (src/problems.cpp:130-284): Rosenbrock through integrate equals
+     // the step loop with host-formed Jacobian factors A^T - (U b) b^T
+    const RiccatiProblem pr = build_riccati(4);
+    const int n = 16;
+    CHECK(pr.a.rows() == n && pr.a_t(1, 0) == pr.a(0, 1));
+    const ProblemSpec spec = pr.to_problem_spec(0.025);
+    StepperConfig c;
+    c.method = Method::RosenbrockEuler;
+    c.n_steps = 6;
+    const auto r = integrate(spec, c);
+    Tensor<double> u = spec.u0;
+    const double tau = 0.025 / 6;
+    for (int s = 0; s < 6; ++s) {
+      std::vector<double> w(n, 0.0);
+      for (int p = 0; p < n; ++p)
+        for (int i = 0; i < n; ++i) w[i] += u[i + size_t(p) * n] * pr.b[p];
+      Matrix<double> j = pr.a_t;
+      for (int jj = 0; jj < n; ++jj)
+        for (int ii = 0; ii < n; ++ii) j(ii, jj) -= w[ii] * pr.b[jj];
+      u = rosenbrock_euler_step(u, s * tau, tau, spec.K, spec.g, {j, j});
+    }
+    CHECK(diff_norm_inf(r.final, u) <= 1e-12 * u.norm_inf());
+    c.method = Method::ETD2RK;
+    const auto r2 = integrate(spec, c);
+    CHECK(diff_norm_inf(r.final, r2.final) <= 1e-2 * r2.final.norm_inf());
+    CHECK(parse_method("rosenbrock_euler") == Method::RosenbrockEuler);
+  }
+  {  // ADR (src/problems.cpp:45-128): second-order convergence to e^t u0
+    const ADRProblem pr = build_adr(10, 11, 12);
+    const ProblemSpec spec = pr.to_problem_spec();
+    StepperConfig c;
+    c.method = Method::ETD2RK;
+    double err[2];
+    for (int k = 0; k < 2; ++k) {
+      c.n_steps = 20 << k;
+      const auto r = integrate(spec, c);
+      const Tensor<double> ex = pr.exact(1.0);
+      err[k] = diff_norm_inf(r.final, ex) / ex.norm_inf();
+    }
+    CHECK(err[0] < 1e-3 && err[1] < err[0] / 3.0 && err[1] > err[0] / 5.0);
   }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
