@@ -178,6 +178,10 @@ int kp_all_finite_f64(kp_ctx* ctx, size_t n, const double* x, int* all_finite);
 /* ---------------- matrix functions (inc/matrix_functions.hpp) ---------------- */
 /* q-point Gauss-Legendre-Lobatto rule on [0,1] (host; src/gll_rule.cpp:35-72) */
 int kp_gll_rule(int q, double* nodes, double* weights);
+/* x = a^{-1} b by blocked LU with partial pivoting (solve = lu_factor +
+ * lu_solve, inc/linsolve.hpp:95-151); a: n x n, b and x: n x nrhs, device,
+ * column-major (x may alias b).  Singular a -> KP_ERUNTIME. */
+int kp_solve_f64(kp_ctx* ctx, const double* a, int n, const double* b, int nrhs, double* x);
 /* out = e^x, n x n (expm, inc/matrix_functions.hpp:76-95) */
 int kp_expm_f64(kp_ctx* ctx, const double* x, int n, double* out);
 int kp_expm_c128(kp_ctx* ctx, const double* x, int n, double* out);

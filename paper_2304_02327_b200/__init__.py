@@ -11,7 +11,7 @@ from ._lib import (DivergenceError, InvalidArgument, KronphiError, CudaError, Co
 from .api import (KroneckerSum, fortran_empty, fortran_zeros, kronsum_action, mode_product,
                   mode_product_into, to_device, to_host, tucker)
 from .integrators import (G, G_ADR, G_ALLEN_CAHN, G_BRUSSELATOR, G_CONST, G_NLS, G_RICCATI,
-                          G_SQUARE, G_ZERO, eval_g, rosenbrock_euler_step,
+                          G_SQUARE, G_ZERO, eval_g, rosenbrock_euler_step, solve,
                           GLLRule, IntegrateResult, Method, PhiTable, ProblemSpec, SplitPhi,
                           StepperConfig, apply_split_phi, build_split_phi, etd2rk_step,
                           exp_euler_linear_split_step, exp_euler_step, expm, gfun, gll_rule,
@@ -22,7 +22,7 @@ __all__ = [
     "DivergenceError", "InvalidArgument", "KronphiError", "CudaError", "Context",
     "default_context", "LIB_PATH", "KroneckerSum", "fortran_empty", "fortran_zeros",
     "kronsum_action", "mode_product", "mode_product_into", "to_device", "to_host", "tucker",
-    "G", "G_ADR", "G_RICCATI", "eval_g", "rosenbrock_euler_step", "G_ALLEN_CAHN", "G_BRUSSELATOR", "G_CONST", "G_NLS", "G_SQUARE", "G_ZERO", "GLLRule",
+    "G", "G_ADR", "G_RICCATI", "eval_g", "rosenbrock_euler_step", "solve", "G_ALLEN_CAHN", "G_BRUSSELATOR", "G_CONST", "G_NLS", "G_SQUARE", "G_ZERO", "GLLRule",
     "IntegrateResult", "Method", "PhiTable", "ProblemSpec", "SplitPhi", "StepperConfig",
     "apply_split_phi", "build_split_phi", "etd2rk_step", "exp_euler_linear_split_step",
     "exp_euler_step", "expm", "gfun", "gll_rule", "integrate", "integrate_config",

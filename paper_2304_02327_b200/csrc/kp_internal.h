@@ -122,6 +122,8 @@ void mode_product_c128(kp_ctx* ctx, const double* t, const std::vector<int>& dim
 void gll_rule_host(int q, double* nodes, double* weights);
 // expm of `batch` consecutive n x n matrices (inc/matrix_functions.hpp:76-95)
 void expm_batch(kp_ctx* ctx, const double* x, int n, int batch, double* out);
+// x = a^{-1} b (lu_factor + lu_solve, inc/linsolve.hpp:95-151); a n x n, b/x n x nrhs
+void solve_dev(kp_ctx* ctx, const double* a, int n, const double* b, int nrhs, double* x);
 // phiquad (inc/matrix_functions.hpp:146-199): phis = ell_max+1 consecutive
 // n x n matrices; returns the scaling exponent
 int phiquad_dev(kp_ctx* ctx, const double* x, int n, int ell_max, int q, int forced, double* phis);

@@ -757,7 +757,9 @@ bool lu_panel_cluster(kp_ctx* ctx, double* a, int n, long long nn, int j0, int n
 }
 
 // lu_factor + lu_solve(lhs, rhs) for a batch; rhs overwritten with the solution.
-void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs) {
+void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs, int nrhs = -1) {
+  if (nrhs < 0) nrhs = n;  // rhs_b: n x nrhs, column-major, stride rs between matrices
+  const long long rs = (long long)n * nrhs;
   const long long nn = (long long)n * n;
   int* piv = slot<int>(ctx, S_PIV, size_t(n) * batch);
   int* sing = slot<int>(ctx, S_SING, 4);
@@ -807,19 +809,19 @@ void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs) {
   KP_CUDA(cudaStreamSynchronize(ctx->stream));
   if (hs) throw runtime_error("lu_factor: matrix is singular");
   // lu_solve (:149-176)
-  swaps_kernel<<<dim3((n + nt - 1) / nt, batch), nt, 0, ctx->stream>>>(rhs, n, nn, piv, n, 0, n,
-                                                                       0, n);
+  swaps_kernel<<<dim3((nrhs + nt - 1) / nt, batch), nt, 0, ctx->stream>>>(rhs, n, rs, piv, n, 0,
+                                                                          n, 0, nrhs);
   ctx->launches++;
   for (int j0 = 0; j0 < n; j0 += LU_NB) {
     const int nb = std::min(LU_NB, n - j0);
-    trsm_lower_unit_kernel<<<dim3((n + 127) / 128, batch), 128, 0, ctx->stream>>>(
-        lhs, n, nn, j0, nb, rhs, n, nn, n);
+    trsm_lower_unit_kernel<<<dim3((nrhs + 127) / 128, batch), 128, 0, ctx->stream>>>(
+        lhs, n, nn, j0, nb, rhs, n, rs, nrhs);
     ctx->launches++;
     const int rest = n - j0 - nb;
     if (rest > 0) {
       GemmProblem p;
       p.M = rest;
-      p.N = n;
+      p.N = nrhs;
       p.K = nb;
       p.batch = batch;
       p.A = lhs + (j0 + nb) + (long long)j0 * n;
@@ -828,10 +830,10 @@ void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs) {
       p.B = rhs + j0;
       p.sBk = 1;
       p.sBn = n;
-      p.sB = nn;
+      p.sB = rs;
       p.C = rhs + j0 + nb;
       p.ldc = n;
-      p.sC = nn;
+      p.sC = rs;
       Epilogue e;
       e.alpha = -1.0;
       e.beta = 1.0;
@@ -840,13 +842,13 @@ void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs) {
   }
   for (int j0 = ((n - 1) / LU_NB) * LU_NB; j0 >= 0; j0 -= LU_NB) {
     const int nb = std::min(LU_NB, n - j0);
-    trsm_upper_kernel<<<dim3((n + 127) / 128, batch), 128, 0, ctx->stream>>>(lhs, n, nn, j0, nb,
-                                                                             rhs, n, nn, n);
+    trsm_upper_kernel<<<dim3((nrhs + 127) / 128, batch), 128, 0, ctx->stream>>>(lhs, n, nn, j0, nb,
+                                                                                rhs, n, rs, nrhs);
     ctx->launches++;
     if (j0 > 0) {
       GemmProblem p;
       p.M = j0;
-      p.N = n;
+      p.N = nrhs;
       p.K = nb;
       p.batch = batch;
       p.A = lhs + (long long)j0 * n;
@@ -855,10 +857,10 @@ void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs) {
       p.B = rhs + j0;
       p.sBk = 1;
       p.sBn = n;
-      p.sB = nn;
+      p.sB = rs;
       p.C = rhs;
       p.ldc = n;
-      p.sC = nn;
+      p.sC = rs;
       Epilogue e;
       e.alpha = -1.0;
       e.beta = 1.0;
@@ -1003,6 +1005,16 @@ void expm_batch(kp_ctx* ctx, const double* x, int n, int batch, double* out) {
   for (int i = 0; i < batch; ++i)
     KP_CUDA(cudaMemcpyAsync(out + order[i] * nn, rhs + i * nn, nn * sizeof(double),
                             cudaMemcpyDeviceToDevice, ctx->stream));
+}
+
+void solve_dev(kp_ctx* ctx, const double* a, int n, const double* b, int nrhs, double* x) {
+  const long long nn = (long long)n * n;
+  double* lu = slot<double>(ctx, S_LHS, size_t(nn));
+  KP_CUDA(cudaMemcpyAsync(lu, a, nn * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (x != b)
+    KP_CUDA(cudaMemcpyAsync(x, b, (long long)n * nrhs * sizeof(double), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+  lu_solve_batch(ctx, n, 1, lu, x, nrhs);
 }
 
 // phiquad (inc/matrix_functions.hpp:146-199) for one matrix x (device):

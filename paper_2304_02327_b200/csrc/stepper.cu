@@ -973,6 +973,14 @@ int kp_gll_rule(int q, double* nodes, double* weights) {
   return guard_c([&] { gll_rule_host(q, nodes, weights); });
 }
 
+int kp_solve_f64(kp_ctx* ctx, const double* a, int n, const double* b, int nrhs, double* x) {
+  return guard_c([&] {
+    ctx_ok(ctx);
+    if (n <= 0 || nrhs < 0) throw invalid_argument("solve: size mismatch");
+    if (!a || !b || !x) throw invalid_argument("solve: null pointer");
+    if (nrhs > 0) solve_dev(ctx, a, n, b, nrhs, x);
+  });
+}
 int kp_expm_f64(kp_ctx* ctx, const double* x, int n, double* out) {
   return guard_c([&] {
     ctx_ok(ctx);

@@ -34,6 +34,7 @@ _CTX, _PG, _PL = C.c_void_p, C.POINTER(GFun), C.POINTER(C.c_long)
 for _name, _res, _args in [
     ("kp_gll_rule", _I, [_I, _PD, _PD]),
     ("kp_expm_f64", _I, [_CTX, _VP, _I, _VP]),
+    ("kp_solve_f64", _I, [_CTX, _VP, _I, _VP, _I, _VP]),
     ("kp_expm_c128", _I, [_CTX, _VP, _I, _VP]),
     ("kp_phiquad_f64", _I, [_CTX, _VP, _I, _I, _I, _I, _VP, _PI]),
     ("kp_phiquad_c128", _I, [_CTX, _VP, _I, _I, _I, _I, _VP, _PI]),
@@ -170,6 +171,30 @@ def expm(x):
     out = fortran_empty(list(xd.shape), xd.dtype, xd.device)
     f = ctx.lib.kp_expm_c128 if cplx else ctx.lib.kp_expm_f64
     check(f(ctx.h, xd.data_ptr(), xd.shape[0], out.data_ptr()))
+    return to_host(out) if host else out
+
+
+def solve(a, b):
+    """a^{-1} b by the device blocked LU with partial pivoting
+    (inc/linsolve.hpp:148-151: lu_factor + lu_solve); b is n or n x nrhs."""
+    ad, host, cplx = _dev_matrix(a)
+    if cplx:
+        raise InvalidArgument(1, "solve: real matrices only")
+    n = ad.shape[0]
+    if ad.shape[1] != n:
+        raise InvalidArgument(1, "solve: matrix not square")
+    vec = np.ndim(b) == 1 if not _is_torch(b) else b.dim() == 1
+    bd = (to_device(np.asarray(b, dtype=np.float64)) if not _is_torch(b) else b).to(torch.float64)
+    if vec:
+        bd = bd.reshape(n, 1)
+    if bd.shape[0] != n:
+        raise InvalidArgument(1, "solve: size mismatch")
+    nrhs = bd.shape[1]
+    x = fortran_empty([n, nrhs], torch.float64, ad.device)
+    x.copy_(bd)
+    ctx = _ctx_for(ad)
+    check(ctx.lib.kp_solve_f64(ctx.h, ad.data_ptr(), n, x.data_ptr(), nrhs, x.data_ptr()))
+    out = x.reshape(n) if vec else x
     return to_host(out) if host else out
 
 
