@@ -155,6 +155,14 @@ int kp_host_mode_product_f64(kp_ctx* ctx, const double* t, const int* dims, int 
 int kp_host_tucker_f64(kp_ctx* ctx, const double* t, const int* dims, int d,
                        const double* const* ms, const int* rows, double prefactor,
                        double* out);
+/* Streamed host Tucker: count tensors (same dims and factors), ts[i] ->
+ * outs[i] (host, column-major).  Uploads of tensor i+1 overlap the last mode
+ * and the download of tensor i (two device buffer sets), so a sequence of
+ * tucker() calls costs ~max(H2D, D2H, compute) per tensor instead of their
+ * sum.  Results are bitwise those of kp_host_tucker_f64 per tensor. */
+int kp_host_tucker_stream_f64(kp_ctx* ctx, int count, const double* const* ts, const int* dims,
+                              int d, const double* const* ms, const int* rows, double prefactor,
+                              double* const* outs);
 int kp_host_tucker_c128(kp_ctx* ctx, const double* t, const int* dims, int d,
                         const double* const* ms, const int* rows, double prefactor,
                         double* out);

@@ -78,6 +78,7 @@ _SIGS = {
     "kp_kronsum_slab_c128": (_I, [_CTX, _VP, _PI, _I, _PPD, _I, _I, _I, C.c_void_p, _VP]),
     "kp_host_mode_product_f64": (_I, [_CTX, _VP, _PI, _I, _I, _VP, _I, _I, _D, _D, _VP]),
     "kp_host_tucker_f64": (_I, [_CTX, _VP, _PI, _I, _PPD, _PI, _D, _VP]),
+    "kp_host_tucker_stream_f64": (_I, [_CTX, _I, _VP, _PI, _I, _PPD, _PI, _D, _VP]),
     "kp_host_tucker_c128": (_I, [_CTX, _VP, _PI, _I, _PPD, _PI, _D, _VP]),
     "kp_host_kronsum_f64": (_I, [_CTX, _VP, _PI, _I, _PPD, _VP]),
     "kp_axpy_f64": (_I, [_CTX, _SZ, _D, _VP, _VP]),

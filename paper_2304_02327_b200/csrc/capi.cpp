@@ -357,6 +357,7 @@ void d2h(kp_ctx* ctx, double* dst, const double* src, size_t n) {
 
 constexpr int SLOT_HOST_IN = 8, SLOT_HOST_OUT = 9, SLOT_HOST_MATS = 10;
 constexpr int SLOT_PIPE_A = 13, SLOT_PIPE_SUB = 14;
+constexpr int SLOT_HOST_IN2 = 60, SLOT_HOST_OUT2 = 61, SLOT_PIPE_A2 = 62;
 
 // Host-buffer Tucker with the PCIe copies overlapped with the device work
 // (the e2e drop-in path).  Mode products on distinct modes act plane by plane
@@ -367,9 +368,9 @@ constexpr int SLOT_PIPE_A = 13, SLOT_PIPE_SUB = 14;
 //     planes -- row blocks of its factor -- and each block is copied back
 //     over a second copy stream while the next one computes.
 // Results are bit-identical to the unpipelined Tucker (same per-entry sums).
-void host_tucker_pipelined(kp_ctx* ctx, ModeFn mp, int comps, const double* t,
+void host_tucker_pipelined(kp_ctx* ctx, ModeFn mp, int comps, const double* const* ts,
                            const std::vector<int>& dv, const std::vector<const double*>& dm,
-                           const int* rows, double pref, double* out) {
+                           const int* rows, double pref, double* const* outs, int count) {
   const int d = int(dv.size());
   size_t plane_in = comps, plane_mid = comps, plane_out = comps;
   for (int mu = 0; mu < d - 1; ++mu) {
@@ -378,76 +379,121 @@ void host_tucker_pipelined(kp_ctx* ctx, ModeFn mp, int comps, const double* t,
     plane_out *= size_t(rows[mu]);
   }
   const int nlast = dv[d - 1], rlast = rows[d - 1];
-  double* din = static_cast<double*>(ctx->ws.get(SLOT_HOST_IN, plane_in * nlast * sizeof(double)));
-  double* dmid = static_cast<double*>(ctx->ws.get(SLOT_HOST_OUT, plane_mid * nlast * sizeof(double)));
-  double* dout = static_cast<double*>(ctx->ws.get(SLOT_PIPE_A, plane_out * rlast * sizeof(double)));
-  cudaStream_t s_in, s_out;
-  KP_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
-  KP_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+  // one buffer set per tensor in flight (two when streaming several tensors:
+  // tensor i+1 uploads while tensor i finishes and downloads)
+  const int nbuf = count > 1 ? 2 : 1;
+  double *din[2], *dmid[2], *dout[2];
+  for (int b = 0; b < nbuf; ++b) {
+    din[b] = static_cast<double*>(
+        ctx->ws.get(b ? SLOT_HOST_IN2 : SLOT_HOST_IN, plane_in * nlast * sizeof(double)));
+    dmid[b] = static_cast<double*>(
+        ctx->ws.get(b ? SLOT_HOST_OUT2 : SLOT_HOST_OUT, plane_mid * nlast * sizeof(double)));
+    dout[b] = static_cast<double*>(
+        ctx->ws.get(b ? SLOT_PIPE_A2 : SLOT_PIPE_A, plane_out * rlast * sizeof(double)));
+  }
+  double* sub = static_cast<double*>(
+      ctx->ws.get(SLOT_PIPE_SUB, size_t(rlast) * nlast * comps * sizeof(double)));
   // pipeline depth: ~16 MiB per chunk, at most 8 (small tensors: one chunk,
   // i.e. exactly the unpipelined launch sequence)
   const size_t in_bytes = plane_in * nlast * sizeof(double);
   const int depth = int(std::min<size_t>(8, std::max<size_t>(1, in_bytes >> 24)));
   const int nch = std::min(nlast, depth), nblk = std::min(rlast, depth);
-  std::vector<cudaEvent_t> ev(nch + nblk + 1);
+  // chunk scratch (ping-pong slots 0/1) sized once for the largest chunk, so
+  // no slot is reallocated under in-flight work
+  {
+    const int pmax = (nlast + nch - 1) / nch + 1;
+    size_t big = 0;
+    std::vector<int> cd = dv;
+    cd[d - 1] = std::min(nlast, pmax);
+    for (int mu = 0; mu < d - 1; ++mu) {
+      cd[mu] = rows[mu];
+      size_t n_od = comps;
+      for (int x : cd) n_od *= size_t(x);
+      big = std::max(big, n_od);
+    }
+    if (d > 1) {
+      ctx->ws.get(0, big * sizeof(double));
+      ctx->ws.get(1, big * sizeof(double));
+    }
+  }
+  cudaStream_t s_in, s_out;
+  KP_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+  KP_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+  // per tensor: nch chunk-arrival events, nblk block-done events, one
+  // "inputs consumed" and one "outputs downloaded" event per buffer set
+  std::vector<cudaEvent_t> ev(size_t(count) * (nch + nblk) + 1 + 2 * nbuf);
   for (auto& e : ev) KP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t* ev_start = &ev[size_t(count) * (nch + nblk)];
+  cudaEvent_t* ev_in_free = ev_start + 1;     // [nbuf]
+  cudaEvent_t* ev_out_free = ev_in_free + nbuf;  // [nbuf]
   try {
     // factors were uploaded on ctx->stream: the copy streams start after them
-    KP_CUDA(cudaEventRecord(ev[nch + nblk], ctx->stream));
-    for (int k = 0; k < nch; ++k) {
-      const int p0 = int((long long)nlast * k / nch), p1 = int((long long)nlast * (k + 1) / nch);
-      KP_CUDA(cudaMemcpyAsync(din + plane_in * p0, t + plane_in * p0,
-                              plane_in * (p1 - p0) * sizeof(double), cudaMemcpyHostToDevice, s_in));
-      KP_CUDA(cudaEventRecord(ev[k], s_in));
-      KP_CUDA(cudaStreamWaitEvent(ctx->stream, ev[k], 0));
-      std::vector<int> cd = dv;
-      cd[d - 1] = p1 - p0;
-      const double* cur = din + plane_in * p0;
-      for (int mu = 0; mu < d - 1; ++mu) {
-        std::vector<int> od = cd;
-        od[mu] = rows[mu];
-        size_t n_od = comps;
-        for (int x : od) n_od *= size_t(x);
-        double* dst = (mu == d - 2) ? dmid + plane_mid * p0
-                                    : static_cast<double*>(ctx->ws.get(mu & 1, n_od * sizeof(double)));
-        Epilogue e;
-        e.alpha = (mu == 0) ? pref : 1.0;
-        mp(ctx, cur, cd, mu, dm[mu], rows[mu], e, dst);
-        cd = od;
-        cur = dst;
-      }
-    }
-    // last mode in blocks of output planes, each copied back as it completes
+    KP_CUDA(cudaEventRecord(*ev_start, ctx->stream));
+    KP_CUDA(cudaStreamWaitEvent(s_in, *ev_start, 0));
     std::vector<int> md = dv;
     for (int mu = 0; mu < d - 1; ++mu) md[mu] = rows[mu];
-    double* sub = static_cast<double*>(
-        ctx->ws.get(SLOT_PIPE_SUB, size_t(rlast) * nlast * comps * sizeof(double)));
-    for (int b = 0; b < nblk; ++b) {
-      const int i0 = int((long long)rlast * b / nblk), i1 = int((long long)rlast * (b + 1) / nblk);
-      const int rb = i1 - i0;
-      // rows i0..i1 of the last factor as a contiguous rb x nlast matrix
-      KP_CUDA(cudaMemcpy2DAsync(sub + size_t(i0) * nlast * comps, rb * comps * sizeof(double),
-                                dm[d - 1] + size_t(i0) * comps, rlast * comps * sizeof(double),
-                                rb * comps * sizeof(double), nlast, cudaMemcpyDeviceToDevice,
-                                ctx->stream));
-      Epilogue e;
-      e.alpha = (d == 1) ? pref : 1.0;
-      mp(ctx, d == 1 ? din : dmid, md, d - 1, sub + size_t(i0) * nlast * comps, rb, e,
-         dout + plane_out * i0);
-      KP_CUDA(cudaEventRecord(ev[nch + b], ctx->stream));
-    }
-    for (int b = 0; b < nblk; ++b) {
-      const int i0 = int((long long)rlast * b / nblk), i1 = int((long long)rlast * (b + 1) / nblk);
-      KP_CUDA(cudaStreamWaitEvent(s_out, ev[nch + b], 0));
-      KP_CUDA(cudaMemcpyAsync(out + plane_out * i0, dout + plane_out * i0,
-                              plane_out * (i1 - i0) * sizeof(double), cudaMemcpyDeviceToHost,
-                              s_out));
+    for (int i = 0; i < count; ++i) {
+      const int b = i % nbuf;
+      cudaEvent_t* ech = &ev[size_t(i) * (nch + nblk)];
+      cudaEvent_t* eblk = ech + nch;
+      if (i >= nbuf) KP_CUDA(cudaStreamWaitEvent(s_in, ev_in_free[b], 0));
+      for (int k = 0; k < nch; ++k) {
+        const int p0 = int((long long)nlast * k / nch), p1 = int((long long)nlast * (k + 1) / nch);
+        KP_CUDA(cudaMemcpyAsync(din[b] + plane_in * p0, ts[i] + plane_in * p0,
+                                plane_in * (p1 - p0) * sizeof(double), cudaMemcpyHostToDevice,
+                                s_in));
+        KP_CUDA(cudaEventRecord(ech[k], s_in));
+        KP_CUDA(cudaStreamWaitEvent(ctx->stream, ech[k], 0));
+        std::vector<int> cd = dv;
+        cd[d - 1] = p1 - p0;
+        const double* cur = din[b] + plane_in * p0;
+        for (int mu = 0; mu < d - 1; ++mu) {
+          std::vector<int> od = cd;
+          od[mu] = rows[mu];
+          size_t n_od = comps;
+          for (int x : od) n_od *= size_t(x);
+          double* dst = (mu == d - 2) ? dmid[b] + plane_mid * p0
+                                      : static_cast<double*>(ctx->ws.get(mu & 1, n_od * sizeof(double)));
+          Epilogue e;
+          e.alpha = (mu == 0) ? pref : 1.0;
+          mp(ctx, cur, cd, mu, dm[mu], rows[mu], e, dst);
+          cd = od;
+          cur = dst;
+        }
+      }
+      if (d > 1 && nbuf > 1) KP_CUDA(cudaEventRecord(ev_in_free[b], ctx->stream));
+      // last mode in blocks of output planes, each copied back as it completes
+      if (i >= nbuf) KP_CUDA(cudaStreamWaitEvent(ctx->stream, ev_out_free[b], 0));
+      for (int bl = 0; bl < nblk; ++bl) {
+        const int i0 = int((long long)rlast * bl / nblk), i1 = int((long long)rlast * (bl + 1) / nblk);
+        const int rb = i1 - i0;
+        if (i == 0)  // rows i0..i1 of the last factor as a contiguous rb x nlast matrix
+          KP_CUDA(cudaMemcpy2DAsync(sub + size_t(i0) * nlast * comps, rb * comps * sizeof(double),
+                                    dm[d - 1] + size_t(i0) * comps, rlast * comps * sizeof(double),
+                                    rb * comps * sizeof(double), nlast, cudaMemcpyDeviceToDevice,
+                                    ctx->stream));
+        Epilogue e;
+        e.alpha = (d == 1) ? pref : 1.0;
+        mp(ctx, d == 1 ? din[b] : dmid[b], md, d - 1, sub + size_t(i0) * nlast * comps, rb, e,
+           dout[b] + plane_out * i0);
+        KP_CUDA(cudaEventRecord(eblk[bl], ctx->stream));
+      }
+      if (d == 1 && nbuf > 1) KP_CUDA(cudaEventRecord(ev_in_free[b], ctx->stream));
+      for (int bl = 0; bl < nblk; ++bl) {
+        const int i0 = int((long long)rlast * bl / nblk), i1 = int((long long)rlast * (bl + 1) / nblk);
+        KP_CUDA(cudaStreamWaitEvent(s_out, eblk[bl], 0));
+        KP_CUDA(cudaMemcpyAsync(outs[i] + plane_out * i0, dout[b] + plane_out * i0,
+                                plane_out * (i1 - i0) * sizeof(double), cudaMemcpyDeviceToHost,
+                                s_out));
+      }
+      if (nbuf > 1) KP_CUDA(cudaEventRecord(ev_out_free[b], s_out));
     }
     KP_CUDA(cudaStreamSynchronize(s_out));
     KP_CUDA(cudaStreamSynchronize(ctx->stream));
   } catch (...) {
     cudaStreamSynchronize(s_in);
     cudaStreamSynchronize(s_out);
+    cudaStreamSynchronize(ctx->stream);
     for (auto& e : ev) cudaEventDestroy(e);
     cudaStreamDestroy(s_in);
     cudaStreamDestroy(s_out);
@@ -496,7 +542,23 @@ int kp_host_tucker_f64(kp_ctx* ctx, const double* t, const int* dims, int d,
       od[mu] = rows[mu];
     }
     auto dm = upload_mats(ctx, SLOT_HOST_MATS, ms, sizes);
-    host_tucker_pipelined(ctx, mode_product_f64, 1, t, dv, dm, rows, prefactor, out);
+    host_tucker_pipelined(ctx, mode_product_f64, 1, &t, dv, dm, rows, prefactor, &out, 1);
+  });
+}
+
+int kp_host_tucker_stream_f64(kp_ctx* ctx, int count, const double* const* ts, const int* dims,
+                              int d, const double* const* ms, const int* rows, double prefactor,
+                              double* const* outs) {
+  return guard([&] {
+    need_ctx(ctx);
+    if (count < 0 || (count > 0 && (!ts || !outs)))
+      throw invalid_argument("tucker: bad tensor list");
+    const auto dv = check_dims(dims, d, "tucker");
+    if (count == 0) return;
+    std::vector<size_t> sizes;
+    for (int mu = 0; mu < d; ++mu) sizes.push_back(size_t(rows[mu]) * dv[mu]);
+    auto dm = upload_mats(ctx, SLOT_HOST_MATS, ms, sizes);
+    host_tucker_pipelined(ctx, mode_product_f64, 1, ts, dv, dm, rows, prefactor, outs, count);
   });
 }
 
@@ -653,7 +715,7 @@ int kp_host_tucker_c128(kp_ctx* ctx, const double* t, const int* dims, int d,
       od[mu] = rows[mu];
     }
     auto dm = upload_mats(ctx, SLOT_HOST_MATS, ms, sizes);
-    host_tucker_pipelined(ctx, mode_product_c128, 2, t, dv, dm, rows, prefactor, out);
+    host_tucker_pipelined(ctx, mode_product_c128, 2, &t, dv, dm, rows, prefactor, &out, 1);
   });
 }
 

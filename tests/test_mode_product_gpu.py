@@ -232,3 +232,30 @@ def test_banded_kronsum_complex(kp, port):
     t = rand(r, (24, 20, 18), True)
     As = [np.asfortranarray(0.5j * pyoracle.periodic_laplacian_1d(n, 0.5)) for n in t.shape]
     assert rel2(kp.kronsum_action(t, As), port.kronsum(t, As)) < 1e-15
+
+
+@pytest.mark.parametrize("dims", [(40, 33, 70), (128, 128, 520)])
+def test_host_tucker_stream_bitwise(kp, dims):
+    """kp_host_tucker_stream_f64 (double-buffered upload/download overlap
+    across tensors) returns, per tensor, exactly kp_host_tucker_f64's result."""
+    import ctypes as C
+    from paper_2304_02327_b200._lib import check, ints, ptr_array
+    ctx = kp.default_context(0)
+    r = np.random.default_rng(11)
+    vs = [np.asfortranarray(r.standard_normal(dims)) for _ in range(5)]
+    fs = [np.asfortranarray(r.standard_normal((n, n))) for n in dims]
+    hptr = ptr_array([f.ctypes.data for f in fs])
+    want = []
+    for v in vs:
+        o = np.zeros(dims, order="F")
+        check(ctx.lib.kp_host_tucker_f64(ctx.h, v.ctypes.data, ints(list(dims)), 3, hptr,
+                                         ints(list(dims)), 1.0, o.ctypes.data))
+        want.append(o)
+    outs = [np.zeros(dims, order="F") for _ in vs]
+    ins_p = (C.c_void_p * 5)(*[v.ctypes.data for v in vs])
+    outs_p = (C.c_void_p * 5)(*[o.ctypes.data for o in outs])
+    check(ctx.lib.kp_host_tucker_stream_f64(ctx.h, 5, C.cast(ins_p, C.c_void_p),
+                                            ints(list(dims)), 3, hptr, ints(list(dims)), 1.0,
+                                            C.cast(outs_p, C.c_void_p)))
+    for a, b in zip(outs, want):
+        assert np.array_equal(a, b)
