@@ -54,6 +54,8 @@ def parse():
                     help="skip the integrator-config block (steps/s of configs 0,2,3,4)")
     ap.add_argument("--no-paper", action="store_true",
                     help="skip the paper's ADR wall-clock runs")
+    ap.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
+                    help="N>1 sharded integrators: fused peer stores or NCCL all-to-all")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the sharded integrator block even at N=1 (testing)")
     return ap.parse_args()
@@ -193,16 +195,31 @@ def run_paper_experiments(kp):
     return out
 
 
-def run_sharded_integrators(kp, peak, world, rank, local):
+def run_sharded_integrators(kp, peak, world, rank, local, exchange="peer"):
     """N > 1: configs 3 and 4 slab-sharded along mode 3 (paper_2304_02327_b200/
-    parallel.py; NCCL all-to-all pencil transposes).  Loop time = max over
+    parallel.py).  exchange "peer": the re-partitions are peer stores from the
+    GEMM epilogues / scatter kernels into CUDA-IPC-mapped buffers over NVLink
+    (PeerComm); "nccl": all-to-all collectives (Comm).  Loop time = max over
     ranks (CUDA events on each rank's stream)."""
     import torch
     import torch.distributed as dist
     from paper_2304_02327_b200 import parallel, problems
     from paper_2304_02327_b200.integrators import _upload_factors
-    comm = parallel.Comm()
     be = parallel.CudaBackend(local)
+    comm = parallel.Comm()
+    if exchange == "peer":  # probe the IPC mappings on every rank first
+        ok = 1.0
+        try:
+            pc = parallel.PeerComm(be)
+            pc._slot("probe", 4096)
+        except Exception:
+            ok = 0.0
+        t = torch.tensor([ok], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if float(t.item()) == 1.0:
+            comm = pc
+        else:
+            exchange = "nccl (peer mappings unavailable)"
     out = {}
     for tag, builder, kw in INTEGRATOR_CONFIGS:
         if builder not in ("brusselator", "nls"):
@@ -245,10 +262,13 @@ def run_sharded_integrators(kp, peak, world, rank, local):
         sps = c.n_steps / loop
         out[tag + "_sharded"] = {"method": c.method, "global_dims": spatial + (
             [2] if species == 2 else []), "ranks": world, "steps": c.n_steps,
+            "exchange": exchange,
             "steps_per_s": sps, "loop_ms": loop * 1e3, "tflops_total": fl * sps / 1e12,
             "frac_of_fp64_peak_per_gpu": fl * sps / 1e12 / (peak * world), "note": note}
         del ud, flat, K
         torch.cuda.empty_cache()
+    if isinstance(comm, parallel.PeerComm):
+        comm.close()
     return out
 
 
@@ -377,6 +397,11 @@ def main():
     dist = None
     if world > 1 or args.force_sharded:
         import torch.distributed as dist
+        if world == 1:  # --force-sharded without torchrun: a one-rank group
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29561")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2304_02327_b200 as kp
     ctx = kp.default_context(local)
@@ -491,7 +516,7 @@ def main():
         del v_d, out_d
         torch.cuda.empty_cache()
         integ = run_integrators(kp, peak) if (world == 1 and not args.force_sharded) else \
-            run_sharded_integrators(kp, peak, world, rank, local)
+            run_sharded_integrators(kp, peak, world, rank, local, args.exchange)
 
     paper = None
     if world == 1 and not args.no_paper:

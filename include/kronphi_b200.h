@@ -148,6 +148,42 @@ int kp_kronsum_slab_c128(kp_ctx* ctx, const double* u_ext, const int* dims, int 
                          const double* const* as, int slab_mode, int k0, int n_glob,
                          const kp_gfun* g, double* r);
 
+/* ---------------- multi-GPU: fused exchange over peer memory ----------------
+ * The slab-sharded integrators re-partition the state
+ * between the slab layout (last spatial mode split over P ranks) and the
+ * pencil layout (second-to-last mode split) around the last mode product.
+ * Instead of a GEMM followed by an all-to-all, the GEMM epilogue stores every
+ * output entry straight into the destination rank's buffer (NVLink P2P
+ * stores through CUDA IPC mappings); a plain scatter kernel does the same
+ * for the transposes with no producing GEMM.  Local tensors are column-major
+ *   slab   (A, B,   C/P, S)      pencil (A, B/P, C, S)
+ * with A = prod(n_1..n_{d-2}), B = n_{d-1}, C = n_d (global sizes), S the
+ * species count.  peers[s] is rank s's receive buffer mapped in this process
+ * (peers[rank] = own buffer).  Completion: the caller synchronizes its stream
+ * and barriers with the other ranks before the receivers read. */
+typedef struct {
+  int dir; /* 1: slab -> pencil, 2: pencil -> slab */
+  int P, rank;
+  long long A, B, C, S;
+  double* const* peers; /* host array of P device pointers */
+} kp_scatter;
+/* out = fma(gamma, alpha * (t x_mode m), x) (x == NULL: alpha * (t x_mode m)),
+ * each entry stored at its destination rank/index (real / complex128). */
+int kp_mode_product_scatter_f64(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
+                                const double* m, int rows, double alpha, const double* x,
+                                double gamma, const kp_scatter* sc);
+int kp_mode_product_scatter_c128(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
+                                 const double* m, int rows, double alpha, const double* x,
+                                 double gamma, const kp_scatter* sc);
+/* The transpose alone: the local tensor x (n_elems entries of comps doubles,
+ * 1 = real, 2 = complex) scattered to its destinations. */
+int kp_scatter_copy(kp_ctx* ctx, const double* x, long long n_elems, int comps,
+                    const kp_scatter* sc);
+/* CUDA IPC for the receive buffers (64-byte opaque handles). */
+int kp_ipc_get_handle(const void* dptr, void* handle64);
+int kp_ipc_open_handle(const void* handle64, void** dptr);
+int kp_ipc_close_handle(void* dptr);
+
 /* Host-buffer variants (the drop-in path: host in, host out, H2D/D2H inside). */
 int kp_host_mode_product_f64(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
                              const double* m, int rows, int cols, double alpha, double beta,

@@ -49,6 +49,14 @@ class GFun(C.Structure):
                 ("step_ctr", C.c_void_p), ("t0", C.c_double), ("tau", C.c_double)]
 
 
+class Scatter(C.Structure):
+    """kp_scatter (include/kronphi_b200.h): the slab <-> pencil destination
+    map of the fused exchange and the peer receive buffers."""
+    _fields_ = [("dir", C.c_int), ("P", C.c_int), ("rank", C.c_int), ("A", C.c_longlong),
+                ("B", C.c_longlong), ("C", C.c_longlong), ("S", C.c_longlong),
+                ("peers", C.c_void_p)]
+
+
 _D, _I, _L, _SZ = C.c_double, C.c_int, C.c_long, C.c_size_t
 _PD, _PI, _VP = C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_void_p
 _PPD = C.POINTER(C.POINTER(C.c_double))
@@ -64,6 +72,14 @@ _SIGS = {
     "kp_ctx_synchronize": (_I, [_CTX]),
     "kp_ctx_launch_count": (C.c_ulonglong, [_CTX]),
     "kp_malloc": (_I, [_CTX, _SZ, C.POINTER(_VP)]),
+    "kp_mode_product_scatter_f64": (_I, [_CTX, _VP, _PI, _I, _I, _VP, _I, _D, _VP, _D,
+                                         C.POINTER(Scatter)]),
+    "kp_mode_product_scatter_c128": (_I, [_CTX, _VP, _PI, _I, _I, _VP, _I, _D, _VP, _D,
+                                          C.POINTER(Scatter)]),
+    "kp_scatter_copy": (_I, [_CTX, _VP, C.c_longlong, _I, C.POINTER(Scatter)]),
+    "kp_ipc_get_handle": (_I, [_VP, _VP]),
+    "kp_ipc_open_handle": (_I, [_VP, C.POINTER(_VP)]),
+    "kp_ipc_close_handle": (_I, [_VP]),
     "kp_free": (_I, [_CTX, _VP]),
     "kp_upload": (_I, [_CTX, _VP, _VP, _SZ]),
     "kp_download": (_I, [_CTX, _VP, _VP, _SZ]),

@@ -506,6 +506,113 @@ void host_tucker_pipelined(kp_ctx* ctx, ModeFn mp, int comps, const double* cons
 
 }  // namespace
 
+// ---------------- fused exchange over peer memory (kp_scatter) ----------------
+
+namespace {
+
+constexpr int SLOT_PEERS = 63;
+
+// Epilogue fields of a kp_scatter; checks the local tensor against the
+// layout and uploads the peer pointer table (stream-ordered).
+Epilogue scatter_epilogue(kp_ctx* ctx, const kp_scatter* sc, long long local_elems) {
+  if (!sc || !sc->peers) throw invalid_argument("scatter: null descriptor");
+  if (sc->dir != 1 && sc->dir != 2) throw invalid_argument("scatter: dir must be 1 or 2");
+  if (sc->P < 1 || sc->rank < 0 || sc->rank >= sc->P) throw invalid_argument("scatter: bad rank");
+  if (sc->A < 1 || sc->B < 1 || sc->C < 1 || sc->S < 1 || sc->B % sc->P || sc->C % sc->P)
+    throw invalid_argument("scatter: B and C must be divisible by P");
+  const long long total = sc->A * sc->B * sc->C * sc->S;
+  if (total / sc->P != local_elems)
+    throw invalid_argument("scatter: local tensor does not match the layout");
+  if (sc->A * sc->B * sc->C > 0xffffffffLL || local_elems > 0xffffffffLL)
+    throw invalid_argument("scatter: tensor too large");
+  for (int r = 0; r < sc->P; ++r)
+    if (!sc->peers[r] || (reinterpret_cast<uintptr_t>(sc->peers[r]) % 16))
+      throw invalid_argument("scatter: peer buffers must be non-null and 16-byte aligned");
+  double** dev = static_cast<double**>(ctx->ws.get(SLOT_PEERS, sizeof(double*) * 64));
+  if (sc->P > 64) throw invalid_argument("scatter: at most 64 ranks");
+  KP_CUDA(cudaMemcpyAsync(dev, sc->peers, sizeof(double*) * sc->P, cudaMemcpyHostToDevice,
+                          ctx->stream));
+  Epilogue e;
+  e.sc_dir = sc->dir;
+  e.sc_P = sc->P;
+  e.sc_rank = sc->rank;
+  e.sc_A = unsigned(sc->A);
+  e.sc_B = unsigned(sc->B);
+  e.sc_C = unsigned(sc->C);
+  e.sc_peers = dev;
+  return e;
+}
+
+int mode_product_scatter(kp_ctx* ctx, bool cplx, const double* t, const int* dims, int d,
+                         int mode, const double* m, int rows, double alpha, const double* x,
+                         double gamma, const kp_scatter* sc) {
+  return guard([&] {
+    need_ctx(ctx);
+    const auto dv = check_dims(dims, d, "mode_product");
+    check_mode(dv, mode, dv[mode]);
+    auto od = dv;
+    od[mode] = rows;
+    Epilogue e = scatter_epilogue(ctx, sc, (long long)numel(od));
+    e.alpha = alpha;
+    if (x) {
+      e.kind = EPI_FMA_X;
+      e.X = x;
+      e.gamma = gamma;
+    }
+    // C is never written with a scatter; it only anchors the index arithmetic
+    double* anchor = sc->peers[sc->rank];
+    if (cplx)
+      mode_product_c128(ctx, t, dv, mode, m, rows, e, anchor);
+    else
+      mode_product_f64(ctx, t, dv, mode, m, rows, e, anchor);
+  });
+}
+
+}  // namespace
+
+int kp_mode_product_scatter_f64(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
+                                const double* m, int rows, double alpha, const double* x,
+                                double gamma, const kp_scatter* sc) {
+  return mode_product_scatter(ctx, false, t, dims, d, mode, m, rows, alpha, x, gamma, sc);
+}
+int kp_mode_product_scatter_c128(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
+                                 const double* m, int rows, double alpha, const double* x,
+                                 double gamma, const kp_scatter* sc) {
+  return mode_product_scatter(ctx, true, t, dims, d, mode, m, rows, alpha, x, gamma, sc);
+}
+
+int kp_scatter_copy(kp_ctx* ctx, const double* x, long long n_elems, int comps,
+                    const kp_scatter* sc) {
+  return guard([&] {
+    need_ctx(ctx);
+    if (comps != 1 && comps != 2) throw invalid_argument("scatter: comps must be 1 or 2");
+    if (!x && n_elems > 0) throw invalid_argument("scatter: null input");
+    const Epilogue e = scatter_epilogue(ctx, sc, n_elems);
+    scatter_copy(ctx, x, n_elems, comps, e);
+  });
+}
+
+int kp_ipc_get_handle(const void* dptr, void* handle64) {
+  return guard([&] {
+    if (!dptr || !handle64) throw invalid_argument("ipc: null pointer");
+    cudaIpcMemHandle_t h;
+    KP_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle64, &h, sizeof(h));
+  });
+}
+int kp_ipc_open_handle(const void* handle64, void** dptr) {
+  return guard([&] {
+    if (!dptr || !handle64) throw invalid_argument("ipc: null pointer");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    KP_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+int kp_ipc_close_handle(void* dptr) {
+  return guard([&] { KP_CUDA(cudaIpcCloseMemHandle(dptr)); });
+}
+
 int kp_host_mode_product_f64(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
                              const double* m, int rows, int cols, double alpha, double beta,
                              double* out) {

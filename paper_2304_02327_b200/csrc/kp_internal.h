@@ -95,6 +95,11 @@ struct Epilogue {
   // value written by this epilogue records atomicMin(*bad_step, *step_ctr + 1)
   int* bad_step = nullptr;
   const int* step_ctr = nullptr;
+  // fused exchange (kp_scatter): C's entries go to peer buffers instead
+  int sc_dir = 0;  // 0: store into C; 1: slab -> pencil; 2: pencil -> slab
+  int sc_P = 1, sc_rank = 0;
+  unsigned sc_A = 1, sc_B = 1, sc_C = 1;
+  double* const* sc_peers = nullptr;  // device array of P pointers
 };
 
 struct GemmProblem {
@@ -106,6 +111,10 @@ struct GemmProblem {
   double* C = nullptr;
   long long ldc = 0, sC = 0;
 };
+
+// The plain re-partition (exchange.cu): entry i of x (comps doubles) stored at
+// its kp_scatter destination (e.sc_*).
+void scatter_copy(kp_ctx* ctx, const double* x, long long n, int comps, const Epilogue& e);
 
 // cplx: 0 real, 1 complex rows (mode 0), 2 complex combine (mode >= 1); see mode_product.cu
 void launch_gemm(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int cplx = 0);

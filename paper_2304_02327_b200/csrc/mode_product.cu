@@ -58,6 +58,62 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// Fused exchange (kp_scatter): destination of entry `elem` of the local output
+// tensor (comps doubles per entry) in its owner's receive buffer.
+//   dir 1: slab (A, B, C/P, S)  -> pencil of rank b / (B/P)
+//   dir 2: pencil (A, B/P, C, S) -> slab of rank c / (C/P)
+__device__ __forceinline__ double* scatter_ptr(const Epilogue& e, unsigned elem, int comps) {
+  const unsigned A = e.sc_A, B = e.sc_B, C = e.sc_C, P = unsigned(e.sc_P), r = unsigned(e.sc_rank);
+  const unsigned Bp = B / P, Cl = C / P;
+  const unsigned t = elem / A, a = elem - t * A;
+  unsigned s;
+  unsigned long long idx;
+  if (e.sc_dir == 1) {
+    const unsigned t2 = t / B, b = t - t2 * B;
+    const unsigned sp = t2 / Cl, cl = t2 - sp * Cl;
+    s = b / Bp;
+    idx = a + (unsigned long long)A * ((b - s * Bp) + (unsigned long long)Bp * (r * Cl + cl + (unsigned long long)C * sp));
+  } else {
+    const unsigned t2 = t / Bp, bl = t - t2 * Bp;
+    const unsigned sp = t2 / C, c = t2 - sp * C;
+    s = c / Cl;
+    idx = a + (unsigned long long)A * ((r * Bp + bl) + (unsigned long long)B * ((c - s * Cl) + (unsigned long long)Cl * sp));
+  }
+  return e.sc_peers[s] + idx * comps;
+}
+
+// Store a real pair (entries elem, elem+1 of the local output; `two` = the
+// second exists) either into C or, with a scatter, to the owners' buffers.
+__device__ __forceinline__ void store_pair(const Epilogue& e, double* c, unsigned long long elem,
+                                           double r0, double r1, bool two, int c_vec2) {
+  if (e.sc_dir) {
+    double* p0 = scatter_ptr(e, unsigned(elem), 1);
+    if (two) {
+      // same destination run when elem is even and A is even (pairs never
+      // straddle a row of A then); 16-byte aligned then too
+      if ((e.sc_A % 2 == 0) && (elem % 2 == 0)) {
+        *reinterpret_cast<double2*>(p0) = make_double2(r0, r1);
+      } else {
+        *p0 = r0;
+        *scatter_ptr(e, unsigned(elem + 1), 1) = r1;
+      }
+    } else {
+      *p0 = r0;
+    }
+    return;
+  }
+  if (two) {
+    if (c_vec2) {
+      *reinterpret_cast<double2*>(c) = make_double2(r0, r1);
+    } else {
+      c[0] = r0;
+      c[1] = r1;
+    }
+  } else {
+    c[0] = r0;
+  }
+}
+
 // Epilogue on one output entry.  v = alpha*acc; idx = linear index into C
 // (and X/D, which share C's layout).
 __device__ __forceinline__ double epi_one(const Epilogue& e, double v, const double* C,
@@ -319,7 +375,8 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
           const long long off = mrow + (long long)(ncol >> 1) * p.ldc;
           double2 dv = make_double2(0.0, 0.0);
           const double2 rr = epi_pair_c(e, v, p.C, cq + off, &dv);
-          *reinterpret_cast<double2*>(Cb + off) = rr;
+          double* dst = e.sc_dir ? scatter_ptr(e, unsigned((cq + off) >> 1), 2) : Cb + off;
+          *reinterpret_cast<double2*>(dst) = rr;
           nonfinite |= !isfinite(rr.x) || !isfinite(rr.y);
           if (e.kind == EPI_STAGE_D) *reinterpret_cast<double2*>(e.D + cq + off) = dv;
         }
@@ -349,7 +406,8 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
           // rows (mrow, mrow+1) are (re, im) of one complex entry
           double2 dv = make_double2(0.0, 0.0);
           const double2 rr = epi_pair_c(e, make_double2(v0, v1), p.C, cq + off, &dv);
-          *reinterpret_cast<double2*>(Cb + off) = rr;
+          double* dst = e.sc_dir ? scatter_ptr(e, unsigned((cq + off) >> 1), 2) : Cb + off;
+          *reinterpret_cast<double2*>(dst) = rr;
           nonfinite |= !isfinite(rr.x) || !isfinite(rr.y);
           if (e.kind == EPI_STAGE_D) *reinterpret_cast<double2*>(e.D + cq + off) = dv;
           continue;
@@ -357,24 +415,19 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
         double d0 = 0.0, d1 = 0.0;
         const double r0 = epi_one(e, v0, p.C, cq + off, species_half, &d0);
         nonfinite |= !isfinite(r0);
+        double r1 = 0.0;
         if (two) {
-          const double r1 = epi_one(e, v1, p.C, cq + off + 1, species_half, &d1);
+          r1 = epi_one(e, v1, p.C, cq + off + 1, species_half, &d1);
           nonfinite |= !isfinite(r1);
-          if (c_vec2) {
-            *reinterpret_cast<double2*>(Cb + off) = make_double2(r0, r1);
-            if (e.kind == EPI_STAGE_D)
-              *reinterpret_cast<double2*>(e.D + cq + off) = make_double2(d0, d1);
+        }
+        store_pair(e, Cb + off, (unsigned long long)(cq + off), r0, r1, two, c_vec2);
+        if (e.kind == EPI_STAGE_D) {
+          if (two && c_vec2) {
+            *reinterpret_cast<double2*>(e.D + cq + off) = make_double2(d0, d1);
           } else {
-            Cb[off] = r0;
-            Cb[off + 1] = r1;
-            if (e.kind == EPI_STAGE_D) {
-              e.D[cq + off] = d0;
-              e.D[cq + off + 1] = d1;
-            }
+            e.D[cq + off] = d0;
+            if (two) e.D[cq + off + 1] = d1;
           }
-        } else {
-          Cb[off] = r0;
-          if (e.kind == EPI_STAGE_D) e.D[cq + off] = d0;
         }
       }
   }

@@ -151,6 +151,189 @@ class LocalComm:
         right.copy_(first)
 
 
+def scatter_destinations(lay: Layout, direction: int, rank: int):
+    """Host restatement of the kp_scatter index map (exchange.cu /
+    mode_product.cu scatter_ptr): for every entry of the rank's local tensor
+    (slab for direction 1, pencil for 2), its destination rank and index in
+    that rank's receive buffer.  Used by the tests to check the device map
+    against slab_to_pencil / pencil_to_slab."""
+    A, B, C, S, P = lay.A, lay.B, lay.C, lay.S, lay.P
+    Bp, Cl = B // P, C // P
+    if direction == 1:
+        n = A * B * Cl * S
+        e = np.arange(n, dtype=np.int64)
+        a, t = e % A, e // A
+        b, t = t % B, t // B
+        cl, sp = t % Cl, t // Cl
+        s = b // Bp
+        idx = a + A * ((b - s * Bp) + Bp * (rank * Cl + cl + C * sp))
+    else:
+        n = A * Bp * C * S
+        e = np.arange(n, dtype=np.int64)
+        a, t = e % A, e // A
+        bl, t = t % Bp, t // Bp
+        c, sp = t % C, t // C
+        s = c // Cl
+        idx = a + A * ((rank * Bp + bl) + B * ((c - s * Cl) + Cl * sp))
+    return s, idx
+
+
+class _DevArray:
+    """__cuda_array_interface__ view of a raw device pointer (IPC mappings)."""
+
+    def __init__(self, ptr, n, cplx):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<c16" if cplx else "<f8",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+class PeerComm:
+    """The exchange of the sharded integrators as device-initiated stores
+    into peer memory instead of collectives (include/kronphi_b200.h,
+    kp_scatter).  Every exchange site owns a receive buffer per rank,
+    allocated once (cudaMalloc), shared through CUDA IPC (handles exchanged
+    with torch.distributed) and mapped into every other rank; producers store
+    into the owners' buffers -- from a GEMM epilogue (`mode_product_to`) or a
+    scatter kernel (`slab_to_pencil` / `pencil_to_slab`) -- then every rank
+    synchronizes its stream and meets the others at a barrier before reading.
+    No kernel waits on another rank, so ranks may even share one GPU (the
+    tests run P = 2 on one device).  `group` carries only the barrier and the
+    handle exchange (gloo or NCCL)."""
+
+    fused = True
+
+    def __init__(self, backend, group=None):
+        from ._lib import Scatter, check
+        self.be = backend
+        self.group = group
+        self.P = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self._Scatter, self._check = Scatter, check
+        self.slots = {}  # name -> (nbytes, own ptr, [peer ptrs], opened ptrs)
+
+    # -- buffers ------------------------------------------------------------
+    def _slot(self, name, nbytes):
+        import ctypes as C
+        lib, ctx = self.be.ctx.lib, self.be.ctx
+        cur = self.slots.get(name)
+        if cur is not None and cur[0] >= nbytes:
+            return cur
+        if cur is not None:
+            self._release(name)
+        own = C.c_void_p()
+        self._check(lib.kp_malloc(ctx.h, max(int(nbytes), 16), C.byref(own)))
+        h = (C.c_char * 64)()
+        self._check(lib.kp_ipc_get_handle(own, h))
+        handles = [None] * self.P
+        if self.P > 1:
+            dist.all_gather_object(handles, bytes(h), group=self.group)
+        else:
+            handles[0] = bytes(h)
+        peers, opened = [], []
+        for r in range(self.P):
+            if r == self.rank:
+                peers.append(own.value)
+                continue
+            p = C.c_void_p()
+            hb = (C.c_char * 64).from_buffer_copy(handles[r])
+            self._check(lib.kp_ipc_open_handle(hb, C.byref(p)))
+            peers.append(p.value)
+            opened.append(p.value)
+        self.slots[name] = (int(nbytes), own.value, peers, opened)
+        return self.slots[name]
+
+    def _release(self, name):
+        lib, ctx = self.be.ctx.lib, self.be.ctx
+        nbytes, own, peers, opened = self.slots.pop(name)
+        torch.cuda.synchronize(self.be.device)
+        self.barrier()
+        for p in opened:
+            lib.kp_ipc_close_handle(p)
+        self.barrier()
+        lib.kp_free(ctx.h, own)
+
+    def close(self):
+        for name in list(self.slots):
+            self._release(name)
+
+    def barrier(self):
+        """All ranks' stores into the receive buffers are complete."""
+        torch.cuda.current_stream(self.be.device).synchronize()
+        if self.P > 1:
+            dist.barrier(group=self.group)
+
+    def _desc(self, lay, direction, peers):
+        import ctypes as C
+        arr = (C.c_void_p * self.P)(*peers)
+        sc = self._Scatter(direction, self.P, self.rank, lay.A, lay.B, lay.C, lay.S,
+                           C.cast(arr, C.c_void_p))
+        sc._keep = arr
+        return sc
+
+    def _view(self, name, n, like):
+        _, own, _, _ = self.slots[name]
+        return torch.as_tensor(_DevArray(own, n, torch.is_complex(like)), device=like.device)
+
+    # -- exchanges ----------------------------------------------------------
+    def _transpose(self, x, lay, direction, name):
+        import ctypes as C
+        cplx = torch.is_complex(x)
+        n = x.numel()
+        slot = self._slot(name, n * x.element_size())
+        sc = self._desc(lay, direction, slot[2])
+        self.be._sync_stream()
+        self._check(self.be.ctx.lib.kp_scatter_copy(self.be.ctx.h, x.data_ptr(), n,
+                                                    2 if cplx else 1, C.byref(sc)))
+        self.barrier()
+        return self._view(name, n, x)
+
+    def slab_to_pencil(self, x, lay, name):
+        return self._transpose(x, lay, 1, name)
+
+    def pencil_to_slab(self, y, lay, name):
+        return self._transpose(y, lay, 2, name)
+
+    def mode_product_to(self, t, dims, mode, m, alpha, lay, direction, name, x=None, gamma=0.0):
+        """fma(gamma, alpha (t x_mode m), x) with every entry stored at its
+        owner in the other layout (one kernel: GEMM + exchange); returns this
+        rank's received tensor (flat)."""
+        import ctypes as C
+        cplx = torch.is_complex(t)
+        n_out = 1
+        for i, v in enumerate(dims):
+            n_out *= (m.shape[0] if i == mode else v)
+        esz = 16 if cplx else 8
+        slot = self._slot(name, n_out * esz)
+        sc = self._desc(lay, direction, slot[2])
+        self.be._sync_stream()
+        lib = self.be.ctx.lib
+        f = lib.kp_mode_product_scatter_c128 if cplx else lib.kp_mode_product_scatter_f64
+        self._check(f(self.be.ctx.h, t.data_ptr(), self.be.ints(dims), len(dims), mode,
+                      m.data_ptr(), m.shape[0], float(alpha),
+                      x.data_ptr() if x is not None else None, float(gamma), C.byref(sc)))
+        self.barrier()
+        return self._view(name, n_out, t)
+
+    def exchange_halos(self, first, last, left, right):
+        """left <- last plane of rank-1, right <- first plane of rank+1 (cyclic),
+        as peer stores into the neighbours' halo buffers."""
+        n = first.numel()
+        esz = first.element_size()
+        slot = self._slot("halo", 2 * n * esz)
+        prev, nxt = (self.rank - 1) % self.P, (self.rank + 1) % self.P
+        cplx = torch.is_complex(first)
+        # my last plane -> next rank's left halo (offset 0); first -> prev's right (offset n)
+        dst_l = torch.as_tensor(_DevArray(slot[2][nxt], n, cplx), device=first.device)
+        dst_r = torch.as_tensor(_DevArray(slot[2][prev] + n * esz, n, cplx), device=first.device)
+        dst_l.copy_(last.reshape(-1))
+        dst_r.copy_(first.reshape(-1))
+        self.barrier()
+        mine = self._view("halo", 2 * n, first)
+        left.copy_(mine[:n].view(left.shape))
+        right.copy_(mine[n:].view(right.shape))
+        self.barrier()  # the halo buffer is free again
+
+
 # ----------------------------------------------------------------- backends
 
 class CudaBackend:
@@ -235,17 +418,55 @@ class ShardedIntegrator:
         self.pd = self.lay.pencil_dims(self.spatial, species)
         self.d = len(self.spatial)
 
-    # y = ((pref x) x_1 F_1 ... x_d F_d) * fold ; x, y in slab layout
-    def tucker(self, x, fs, pref, fold):
+    @property
+    def fused(self):
+        return getattr(self.comm, "fused", False)
+
+    def to_pencil(self, x, site):
+        if self.fused:
+            return self.comm.slab_to_pencil(x, self.lay, site)
+        return slab_to_pencil(x, self.lay, self.comm)
+
+    def to_slab(self, y, site):
+        if self.fused:
+            return self.comm.pencil_to_slab(y, self.lay, site)
+        return pencil_to_slab(y, self.lay, self.comm)
+
+    # y = ((pref x) x_1 F_1 ... x_d F_d) * fold ; x in slab layout, y in pencil
+    # layout -- or, with `to_slab_x`, fma(gamma, y, x2) returned in slab layout
+    # (the final update of a step, fused into the last GEMM's epilogue)
+    def tucker(self, x, fs, pref, fold, site="t", final=None):
         d = self.d
         cur, dims = x, self.sd
         for mu in range(d - 1):
+            alpha = pref if mu == 0 else 1.0
+            if self.fused and mu == d - 2:
+                # GEMM + slab -> pencil exchange in one kernel
+                cp = self.comm.mode_product_to(cur, dims, mu, fs[mu], alpha, self.lay, 1, site)
+                break
             out = torch.empty_like(cur)
-            self.be.mode_product(cur, dims, mu, fs[mu], pref if mu == 0 else 1.0, 0.0, out)
+            self.be.mode_product(cur, dims, mu, fs[mu], alpha, 0.0, out)
             cur = out
-        cp = slab_to_pencil(cur, self.lay, self.comm)
-        out = torch.empty_like(cp)
+        else:
+            cp = None
+        if cp is None:
+            cp = slab_to_pencil(cur, self.lay, self.comm) if not self.fused else \
+                self.comm.slab_to_pencil(cur, self.lay, site)
         alpha = (pref if d == 1 else 1.0) * fold
+        if final is not None:
+            x2, gamma, fsite = final
+            if self.fused:  # last mode + fma + pencil -> slab exchange in one kernel
+                return self.comm.mode_product_to(cp, self.pd, d - 1, fs[d - 1], alpha, self.lay,
+                                                 2, fsite, x=x2, gamma=gamma)
+            y = torch.empty_like(cp)
+            self.be.mode_product(cp, self.pd, d - 1, fs[d - 1], alpha, 0.0, y)
+            out = torch.empty_like(y)
+            if x2 is None:
+                out = y
+            else:
+                self.be.fma(gamma, y, x2, out)
+            return pencil_to_slab(out, self.lay, self.comm)
+        out = torch.empty_like(cp)
         self.be.mode_product(cp, self.pd, d - 1, fs[d - 1], alpha, 0.0, out)
         return out  # pencil layout
 
@@ -255,7 +476,7 @@ class ShardedIntegrator:
         r = torch.empty_like(u)
         for mu in range(d - 1):
             self.be.mode_product(u, self.sd, mu, self.K[mu], 1.0, 0.0 if mu == 0 else 1.0, r)
-        r_p = slab_to_pencil(r, self.lay, self.comm) if d > 1 else r
+        r_p = self.to_pencil(r, "kr") if d > 1 else r
         self.be.mode_product(u_p, self.pd, d - 1, self.K[d - 1], 1.0, 1.0 if d > 1 else 0.0, r_p)
         gu = torch.empty_like(u_p)
         self.be.eval_g(self.g, u_p, self.pd, gu)
@@ -277,41 +498,40 @@ class ShardedIntegrator:
         tau = self.tau
         m = self.method
         if m in ("exp_euler", "etd2rk"):
-            u_p = slab_to_pencil(u, self.lay, self.comm)
+            u_p = self.to_pencil(u, "u_p")
             if self.banded:
                 r = self.kronsum_g_banded(u)
             else:
                 r_p = self.kronsum_g(u, u_p)
-                r = pencil_to_slab(r_p, self.lay, self.comm)
-            y1 = self.tucker(r, self.f1, self.pref1, self.fold1)          # pencil
+                r = self.to_slab(r_p, "r")
+            if m == "exp_euler":  # u + tau*SP1(r), back in slab layout
+                return self.tucker(r, self.f1, self.pref1, self.fold1, "t1",
+                                   final=(u_p, tau, "u"))
+            y1 = self.tucker(r, self.f1, self.pref1, self.fold1, "t1")   # pencil
             stage = torch.empty_like(y1)
             self.be.fma(tau, y1, u_p, stage)                              # u + tau*SP1(r)
-            if m == "exp_euler":
-                return pencil_to_slab(stage, self.lay, self.comm)
             gs, gu = torch.empty_like(stage), torch.empty_like(stage)
             self.be.eval_g(self.g, stage, self.pd, gs)
             self.be.eval_g(self.g, u_p, self.pd, gu)
-            dd = pencil_to_slab(gs - gu, self.lay, self.comm)
-            y2 = self.tucker(dd, self.f2, self.pref2, self.fold2)
-            out = torch.empty_like(y2)
-            self.be.fma(tau, y2, stage, out)                              # stage + tau*SP2(d)
-            return pencil_to_slab(out, self.lay, self.comm)
+            dd = self.to_slab(gs - gu, "dd")
+            # stage + tau*SP2(d), back in slab layout
+            return self.tucker(dd, self.f2, self.pref2, self.fold2, "t2", final=(stage, tau, "u"))
         if m in ("lawson_euler", "lawson2b"):
             gn = torch.empty_like(u)
             self.be.eval_g(self.g, u, self.sd, gn)
             w = torch.empty_like(u)
             self.be.fma(tau, gn, u, w)
-            stage = self.tucker(w, self.f1, 1.0, self.fold1)
             if m == "lawson_euler":
-                return pencil_to_slab(stage, self.lay, self.comm)
+                return self.tucker(w, self.f1, 1.0, self.fold1, "t1", final=(None, 0.0, "u"))
+            stage = self.tucker(w, self.f1, 1.0, self.fold1, "t1")
             w2 = torch.empty_like(u)
             self.be.fma(0.5 * tau, gn, u, w2)
-            out = self.tucker(w2, self.f1, 1.0, self.fold1)
+            out = self.tucker(w2, self.f1, 1.0, self.fold1, "t2")
             gs = torch.empty_like(stage)
             self.be.eval_g(self.g, stage, self.pd, gs)
             res = torch.empty_like(out)
             self.be.fma(0.5 * tau, gs, out, res)
-            return pencil_to_slab(res, self.lay, self.comm)
+            return self.to_slab(res, "u")
         raise ValueError(f"sharded integrate: unsupported method {m}")
 
     def run(self, u, n_steps):
@@ -329,6 +549,8 @@ class ShardedIntegrator:
                     dist.all_reduce(vals, op=dist.ReduceOp.MIN)
                     flag.copy_(torch.where(vals < 1e299, vals, torch.zeros_like(vals)))
                 first_bad = int(flag.item())
+        if self.fused:
+            u = u.clone()  # the result lives in an exchange buffer
         if first_bad:
             from ._lib import DivergenceError
             raise DivergenceError(3, f"state became non-finite at step {first_bad} "

@@ -52,3 +52,48 @@ def test_sharded_p1_bitwise_equals_fused(kp, nccl1, case, method, kronsum):
         os.environ.pop("KP_KRONSUM", None)
     got = res.cpu().numpy().reshape(cfg.u0.shape, order="F")
     assert np.array_equal(got, want), np.abs(got - want).max()
+
+
+@pytest.mark.parametrize("case,method,kronsum", [("ac3d", "etd2rk", "banded"),
+                                                 ("ac3d", "exp_euler", "dense"),
+                                                 ("ac2d", "exp_euler", "banded"),
+                                                 ("bru", "lawson2b", "banded"),
+                                                 ("bru", "etd2rk", "dense"),
+                                                 ("nls", "etd2rk", "banded"),
+                                                 ("ac3d", "lawson_euler", "banded")])
+def test_peer_exchange_world2_one_gpu(kp, case, method, kronsum):
+    """P = 2 processes on one GPU exchanging only through the fused peer
+    stores (GEMM epilogue / scatter kernel into CUDA IPC buffers): the
+    gathered result equals the single-GPU integrate bit for bit."""
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(root, "tests", "peer_worker.py"), case, method, kronsum]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "PEER-OK" in out, out[-4000:]
+
+
+def test_peer_exchange_p1_bitwise(kp):
+    """PeerComm at P = 1 (no torch.distributed): the fused GEMM + exchange
+    path reproduces the single-GPU integrate bit for bit."""
+    from paper_2304_02327_b200 import parallel, problems
+    cfg = problems.ac3d(n=24, n_steps=4)
+    want = kp.integrate_config("etd2rk", cfg.u0, cfg.K, cfg.g, 0.0, cfg.t_final, cfg.n_steps)
+    be = parallel.CudaBackend(0)
+    comm = parallel.PeerComm(be)
+    K = [kp.to_device(k) for k in cfg.K]
+    flat = kp.to_device(cfg.u0).permute(*reversed(range(cfg.u0.ndim))).reshape(-1)
+    res = parallel.sharded_integrate(kp, be, comm, "etd2rk", flat, list(cfg.u0.shape), K, cfg.g,
+                                     0.0, cfg.t_final, cfg.n_steps)
+    comm.close()
+    got = res.cpu().numpy().reshape(cfg.u0.shape, order="F")
+    assert np.array_equal(got, want)
