@@ -526,7 +526,7 @@ void launch_gemm(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int cplx)
   if (tiles64 * 2 < ctx->num_sms)
     tile = 5;
   else if (kcontig)
-    tile = (p.K >= 1024) ? 1 : 9;
+    tile = (p.K >= 1024 && p.M > 64) ? 1 : 9;
   else
     tile = (tiles64 >= 16LL * ctx->num_sms || p.K >= 1024) ? 8 : 6;
   static const int forced = [] {  // benchmarking override

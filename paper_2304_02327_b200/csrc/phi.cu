@@ -525,68 +525,58 @@ __global__ void swaps_kernel(double* __restrict__ a, int ld, long long stride,
   }
 }
 
-// b(j0..j0+nb) <- L11^{-1} b per column (trsm_lower_unit, :96-107); L11 staged in smem
-__global__ void trsm_lower_unit_kernel(const double* __restrict__ lu, int n, long long lstride,
-                                       int j0, int nb, double* __restrict__ b, int ldb,
-                                       long long bstride, int nrhs) {
-  __shared__ double L[LU_NB * LU_NB];
-  const double* lb = lu + blockIdx.y * lstride;
-  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
-    const int i = t % nb, r = t / nb;
-    L[i + r * LU_NB] = lb[(j0 + i) + (long long)(j0 + r) * n];
-  }
+// Inverses of the diagonal nb x nb blocks of a factored LU (blockIdx.z = 0:
+// unit lower L, 1: upper U) for the blocks blk0 .. blk0 + gridDim.x - 1:
+// inv[(b * nblk + blk) * 2 + z] is LU_NB x LU_NB column-major (rows/cols
+// beyond nb zero).  Thread t solves for column t of the inverse by
+// substitution in shared memory.
+__global__ void __launch_bounds__(LU_NB) tri_inv_kernel(const double* __restrict__ lu, int n,
+                                                         long long stride, int blk0, int nblk,
+                                                         double* __restrict__ inv) {
+  __shared__ double T[LU_NB][LU_NB + 1];
+  const int blk = blk0 + blockIdx.x, b = blockIdx.y, upper = blockIdx.z;
+  const int j0 = blk * LU_NB, nb = min(LU_NB, n - j0);
+  const double* src = lu + b * stride + j0 + (long long)j0 * n;
+  const int t = threadIdx.x;
+  // the block, padded with the identity beyond nb
+  for (int i = 0; i < LU_NB; ++i)
+    T[i][t] = (i < nb && t < nb) ? src[i + (long long)t * n] : (i == t ? 1.0 : 0.0);
   __syncthreads();
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nrhs) return;
-  double* col = b + blockIdx.y * bstride + (long long)c * ldb + j0;
+  // column t of the inverse: x = e_t, column-oriented substitution with the
+  // whole column in registers (all indices static after unrolling)
   double x[LU_NB];
 #pragma unroll
-  for (int i = 0; i < LU_NB; ++i)
-    if (i < nb) x[i] = col[i];
-#pragma unroll
-  for (int i = 1; i < LU_NB; ++i) {
-    if (i >= nb) break;
-    double s = x[i];
+  for (int i = 0; i < LU_NB; ++i) x[i] = (i == t) ? 1.0 : 0.0;
+  if (!upper) {
 #pragma unroll
     for (int r = 0; r < LU_NB; ++r)
-      if (r < i) s = __fma_rn(-L[i + r * LU_NB], x[r], s);
-    x[i] = s;
-  }
 #pragma unroll
-  for (int i = 0; i < LU_NB; ++i)
-    if (i < nb) col[i] = x[i];
+      for (int i = r + 1; i < LU_NB; ++i) x[i] = __fma_rn(-T[i][r], x[r], x[i]);
+  } else {
+#pragma unroll
+    for (int r = LU_NB - 1; r >= 0; --r) {
+      x[r] = x[r] / T[r][r];
+#pragma unroll
+      for (int i = 0; i < r; ++i) x[i] = __fma_rn(-T[i][r], x[r], x[i]);
+    }
+  }
+  double* dst = inv + ((long long)(b * nblk + blk) * 2 + upper) * LU_NB * LU_NB + t * LU_NB;
+#pragma unroll
+  for (int i = 0; i < LU_NB; ++i) dst[i] = (i < nb && t < nb) ? x[i] : 0.0;
 }
 
-// trsm_upper (:109-120): back substitution with U11 and division by the diagonal
-__global__ void trsm_upper_kernel(const double* __restrict__ lu, int n, long long lstride, int j0,
-                                  int nb, double* __restrict__ b, int ldb, long long bstride,
-                                  int nrhs) {
-  __shared__ double U[LU_NB * LU_NB];
-  const double* lb = lu + blockIdx.y * lstride;
-  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
-    const int i = t % nb, r = t / nb;
-    U[i + r * LU_NB] = lb[(j0 + i) + (long long)(j0 + r) * n];
+// dst_b(0:rows, 0:cols) = src_b(0:rows, 0:cols), column-major blocks
+__global__ void copy_block_kernel(const double* __restrict__ src, long long lds, long long ss,
+                                  double* __restrict__ dst, long long ldd, long long ds, int rows,
+                                  int cols) {
+  const long long total = (long long)rows * cols;
+  const double* s = src + blockIdx.y * ss;
+  double* d = dst + blockIdx.y * ds;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long c = e / rows, r = e - c * rows;
+    d[r + c * ldd] = s[r + c * lds];
   }
-  __syncthreads();
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nrhs) return;
-  double* col = b + blockIdx.y * bstride + (long long)c * ldb + j0;
-  double x[LU_NB];
-#pragma unroll
-  for (int i = 0; i < LU_NB; ++i)
-    if (i < nb) x[i] = col[i];
-#pragma unroll
-  for (int i = LU_NB - 1; i >= 0; --i) {
-    if (i >= nb) continue;
-    double s = x[i];
-#pragma unroll
-    for (int r = 0; r < LU_NB; ++r)
-      if (r > i && r < nb) s = __fma_rn(-U[i + r * LU_NB], x[r], s);
-    x[i] = s / U[i + i * LU_NB];
-  }
-#pragma unroll
-  for (int i = 0; i < LU_NB; ++i)
-    if (i < nb) col[i] = x[i];
 }
 
 // phi_j = sum_i coeff[i] exps[i] + endpoint * I (phiquad, :179-194): each
@@ -675,7 +665,8 @@ T* slot(kp_ctx* ctx, int s, size_t count) {
 // 2..7 steppers, 8..12 host staging / complex factor).
 enum : int {
   S_NORMS = 20, S_PIV, S_LHS, S_POW, S_U, S_V, S_AU, S_ARG, S_EXPS, S_TAB, S_PROD, S_COEF,
-  S_T1, S_T2, S_A2, S_A4, S_A6, S_SING
+  S_T1, S_T2, S_A2, S_A4, S_A6, S_SING,
+  S_TINV = 56, S_X2 = 57, S_U12 = 58
 };
 
 std::vector<double> norms1(kp_ctx* ctx, const double* x, int n, int batch) {
@@ -757,15 +748,54 @@ bool lu_panel_cluster(kp_ctx* ctx, double* a, int n, long long nn, int j0, int n
 }
 
 // lu_factor + lu_solve(lhs, rhs) for a batch; rhs overwritten with the solution.
+// One batched GEMM C_b (+)= alpha * A_b * B_b with A M-contiguous and B
+// K-contiguous (all operands column-major sub-blocks with the given lds).
+void gemm_kb(kp_ctx* ctx, int M, int N, int K, int batch, const double* A, long long lda,
+             long long sA, const double* B, long long ldb, long long sB, double* C, long long ldc,
+             long long sC, double alpha, double beta) {
+  if (M <= 0 || N <= 0 || K <= 0) return;
+  GemmProblem p;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.batch = batch;
+  p.A = A;
+  p.lda = lda;
+  p.sA = sA;
+  p.B = B;
+  p.sBk = 1;
+  p.sBn = ldb;
+  p.sB = sB;
+  p.C = C;
+  p.ldc = ldc;
+  p.sC = sC;
+  Epilogue e;
+  e.alpha = alpha;
+  e.beta = beta;
+  launch_gemm(ctx, p, e);
+}
+
+// lu_factor + lu_solve(lhs, rhs) for a batch; rhs overwritten with the solution.
+// Factorization as the reference's (inc/linsolve.hpp:95-117: 64-wide panels
+// with partial pivoting, GEMM trailing updates); the triangular solves --
+// U12 = L11^{-1} A12 of each panel and the forward/backward substitutions of
+// lu_solve (:119-146) -- multiply by the inverted nb x nb diagonal blocks on
+// the DMMA GEMM, and the substitutions are left-looking (one long-K GEMM per
+// block row instead of a K = 64 update of every remaining row).  Same
+// algorithm to rounding (~1e-16 per operation); tolerance-tested.
 void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs, int nrhs = -1) {
   if (nrhs < 0) nrhs = n;  // rhs_b: n x nrhs, column-major, stride rs between matrices
   const long long rs = (long long)n * nrhs;
   const long long nn = (long long)n * n;
+  const int nblk = (n + LU_NB - 1) / LU_NB;
+  const long long bsz = (long long)LU_NB * LU_NB;
   int* piv = slot<int>(ctx, S_PIV, size_t(n) * batch);
   int* sing = slot<int>(ctx, S_SING, 4);
+  double* tinv = slot<double>(ctx, S_TINV, size_t(batch) * nblk * 2 * bsz);
+  const long long tstride = (long long)nblk * 2 * bsz;  // per matrix
   KP_CUDA(cudaMemsetAsync(sing, 0, sizeof(int), ctx->stream));
   const int nt = 256;
-  for (int j0 = 0; j0 < n; j0 += LU_NB) {  // lu_factor (:125-146)
+  for (int j0 = 0; j0 < n; j0 += LU_NB) {  // lu_factor (:95-117)
     const int nb = std::min(LU_NB, n - j0);
     if (!lu_panel_cluster(ctx, lhs, n, nn, j0, nb, batch, piv, sing))
       lu_panel_kernel<<<batch, 512, 0, ctx->stream>>>(lhs, n, nn, j0, nb, piv, sing);
@@ -775,32 +805,29 @@ void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs, int
                                                                           nb, 0, j0);
       ctx->launches++;
     }
+    // L11^{-1} and U11^{-1} of this (final) diagonal block
+    tri_inv_kernel<<<dim3(1, batch, 2), LU_NB, 0, ctx->stream>>>(lhs, n, nn, j0 / LU_NB, nblk,
+                                                                  tinv);
+    ctx->launches++;
     const int rest = n - j0 - nb;
     if (rest > 0) {
       swaps_kernel<<<dim3((rest + nt - 1) / nt, batch), nt, 0, ctx->stream>>>(
           lhs, n, nn, piv, n, j0, nb, j0 + nb, n);
-      trsm_lower_unit_kernel<<<dim3((rest + 127) / 128, batch), 128, 0, ctx->stream>>>(
-          lhs, n, nn, j0, nb, lhs + (long long)(j0 + nb) * n, n, nn, rest);
-      ctx->launches += 2;
-      GemmProblem p;  // A22 -= L21 * U12
-      p.M = rest;
-      p.N = rest;
-      p.K = nb;
-      p.batch = batch;
-      p.A = lhs + (j0 + nb) + (long long)j0 * n;
-      p.lda = n;
-      p.sA = nn;
-      p.B = lhs + j0 + (long long)(j0 + nb) * n;
-      p.sBk = 1;
-      p.sBn = n;
-      p.sB = nn;
-      p.C = lhs + (j0 + nb) + (long long)(j0 + nb) * n;
-      p.ldc = n;
-      p.sC = nn;
-      Epilogue e;
-      e.alpha = -1.0;
-      e.beta = 1.0;
-      launch_gemm(ctx, p, e);
+      ctx->launches++;
+      // U12 = L11^{-1} A12 (GEMM into scratch, copied back)
+      double* u12 = slot<double>(ctx, S_U12, size_t(batch) * LU_NB * rest);
+      const double* linv = tinv + (long long)(j0 / LU_NB) * 2 * bsz;
+      double* a12 = lhs + j0 + (long long)(j0 + nb) * n;
+      gemm_kb(ctx, nb, rest, nb, batch, linv, LU_NB, tstride, a12, n, nn, u12, LU_NB,
+              (long long)LU_NB * rest, 1.0, 0.0);
+      const long long tot = (long long)nb * rest;
+      copy_block_kernel<<<dim3(unsigned(std::min<long long>((tot + 255) / 256, 4096)), batch), 256,
+                          0, ctx->stream>>>(u12, LU_NB, (long long)LU_NB * rest, a12, n, nn, nb,
+                                            rest);
+      ctx->launches++;
+      // A22 -= L21 * U12
+      gemm_kb(ctx, rest, rest, nb, batch, lhs + (j0 + nb) + (long long)j0 * n, n, nn, a12, n, nn,
+              lhs + (j0 + nb) + (long long)(j0 + nb) * n, n, nn, -1.0, 1.0);
     }
     KP_CUDA(cudaGetLastError());
   }
@@ -808,64 +835,27 @@ void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs, int
   KP_CUDA(cudaMemcpyAsync(&hs, sing, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   KP_CUDA(cudaStreamSynchronize(ctx->stream));
   if (hs) throw runtime_error("lu_factor: matrix is singular");
-  // lu_solve (:149-176)
+  // lu_solve (:119-146): P b, then L y = b (rhs -> x2), then U x = y (x2 -> rhs)
   swaps_kernel<<<dim3((nrhs + nt - 1) / nt, batch), nt, 0, ctx->stream>>>(rhs, n, rs, piv, n, 0,
                                                                           n, 0, nrhs);
   ctx->launches++;
-  for (int j0 = 0; j0 < n; j0 += LU_NB) {
-    const int nb = std::min(LU_NB, n - j0);
-    trsm_lower_unit_kernel<<<dim3((nrhs + 127) / 128, batch), 128, 0, ctx->stream>>>(
-        lhs, n, nn, j0, nb, rhs, n, rs, nrhs);
-    ctx->launches++;
-    const int rest = n - j0 - nb;
-    if (rest > 0) {
-      GemmProblem p;
-      p.M = rest;
-      p.N = nrhs;
-      p.K = nb;
-      p.batch = batch;
-      p.A = lhs + (j0 + nb) + (long long)j0 * n;
-      p.lda = n;
-      p.sA = nn;
-      p.B = rhs + j0;
-      p.sBk = 1;
-      p.sBn = n;
-      p.sB = rs;
-      p.C = rhs + j0 + nb;
-      p.ldc = n;
-      p.sC = rs;
-      Epilogue e;
-      e.alpha = -1.0;
-      e.beta = 1.0;
-      launch_gemm(ctx, p, e);
-    }
+  double* x2 = slot<double>(ctx, S_X2, size_t(batch) * rs);
+  for (int i = 0; i < nblk; ++i) {
+    const int j0 = i * LU_NB, nb = std::min(LU_NB, n - j0);
+    // b_i -= L(i, 0:i) y(0:i)
+    gemm_kb(ctx, nb, nrhs, j0, batch, lhs + j0, n, nn, x2, n, rs, rhs + j0, n, rs, -1.0, 1.0);
+    // y_i = L_ii^{-1} b_i
+    gemm_kb(ctx, nb, nrhs, nb, batch, tinv + (long long)i * 2 * bsz, LU_NB, tstride, rhs + j0, n,
+            rs, x2 + j0, n, rs, 1.0, 0.0);
   }
-  for (int j0 = ((n - 1) / LU_NB) * LU_NB; j0 >= 0; j0 -= LU_NB) {
-    const int nb = std::min(LU_NB, n - j0);
-    trsm_upper_kernel<<<dim3((nrhs + 127) / 128, batch), 128, 0, ctx->stream>>>(lhs, n, nn, j0, nb,
-                                                                                rhs, n, rs, nrhs);
-    ctx->launches++;
-    if (j0 > 0) {
-      GemmProblem p;
-      p.M = j0;
-      p.N = nrhs;
-      p.K = nb;
-      p.batch = batch;
-      p.A = lhs + (long long)j0 * n;
-      p.lda = n;
-      p.sA = nn;
-      p.B = rhs + j0;
-      p.sBk = 1;
-      p.sBn = n;
-      p.sB = rs;
-      p.C = rhs;
-      p.ldc = n;
-      p.sC = rs;
-      Epilogue e;
-      e.alpha = -1.0;
-      e.beta = 1.0;
-      launch_gemm(ctx, p, e);
-    }
+  for (int i = nblk - 1; i >= 0; --i) {
+    const int j0 = i * LU_NB, nb = std::min(LU_NB, n - j0), j1 = j0 + nb;
+    // y_i -= U(i, i+1:) x(i+1:)
+    gemm_kb(ctx, nb, nrhs, n - j1, batch, lhs + j0 + (long long)j1 * n, n, nn, rhs + j1, n, rs,
+            x2 + j0, n, rs, -1.0, 1.0);
+    // x_i = U_ii^{-1} y_i
+    gemm_kb(ctx, nb, nrhs, nb, batch, tinv + ((long long)i * 2 + 1) * bsz, LU_NB, tstride,
+            x2 + j0, n, rs, rhs + j0, n, rs, 1.0, 0.0);
   }
   KP_CUDA(cudaGetLastError());
 }
