@@ -84,9 +84,10 @@ __device__ __forceinline__ double* scatter_ptr(const Epilogue& e, unsigned elem,
 
 // Store a real pair (entries elem, elem+1 of the local output; `two` = the
 // second exists) either into C or, with a scatter, to the owners' buffers.
+template <bool SCAT>
 __device__ __forceinline__ void store_pair(const Epilogue& e, double* c, unsigned long long elem,
                                            double r0, double r1, bool two, int c_vec2) {
-  if (e.sc_dir) {
+  if constexpr (SCAT) {
     double* p0 = scatter_ptr(e, unsigned(elem), 1);
     if (two) {
       // same destination run when elem is even and A is even (pairs never
@@ -194,7 +195,7 @@ struct Cfg {
 // C(2p+1,2i)) at complex offset p + i*P (ldc is then the complex row pitch
 // in doubles, 2P).
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool B_KCONTIG, int VEC,
-          int CPLX, int MINB>
+          int CPLX, int MINB, bool SCAT>
 __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
     dmma_gemm_kernel(GemmProblem p, Epilogue e, int tiles_m, int tiles_n, int n_fastest,
                      int c_vec2, long long species_half) {
@@ -375,7 +376,8 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
           const long long off = mrow + (long long)(ncol >> 1) * p.ldc;
           double2 dv = make_double2(0.0, 0.0);
           const double2 rr = epi_pair_c(e, v, p.C, cq + off, &dv);
-          double* dst = e.sc_dir ? scatter_ptr(e, unsigned((cq + off) >> 1), 2) : Cb + off;
+          double* dst = Cb + off;
+          if constexpr (SCAT) dst = scatter_ptr(e, unsigned((cq + off) >> 1), 2);
           *reinterpret_cast<double2*>(dst) = rr;
           nonfinite |= !isfinite(rr.x) || !isfinite(rr.y);
           if (e.kind == EPI_STAGE_D) *reinterpret_cast<double2*>(e.D + cq + off) = dv;
@@ -406,7 +408,8 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
           // rows (mrow, mrow+1) are (re, im) of one complex entry
           double2 dv = make_double2(0.0, 0.0);
           const double2 rr = epi_pair_c(e, make_double2(v0, v1), p.C, cq + off, &dv);
-          double* dst = e.sc_dir ? scatter_ptr(e, unsigned((cq + off) >> 1), 2) : Cb + off;
+          double* dst = Cb + off;
+          if constexpr (SCAT) dst = scatter_ptr(e, unsigned((cq + off) >> 1), 2);
           *reinterpret_cast<double2*>(dst) = rr;
           nonfinite |= !isfinite(rr.x) || !isfinite(rr.y);
           if (e.kind == EPI_STAGE_D) *reinterpret_cast<double2*>(e.D + cq + off) = dv;
@@ -415,26 +418,43 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
         double d0 = 0.0, d1 = 0.0;
         const double r0 = epi_one(e, v0, p.C, cq + off, species_half, &d0);
         nonfinite |= !isfinite(r0);
-        double r1 = 0.0;
-        if (two) {
-          r1 = epi_one(e, v1, p.C, cq + off + 1, species_half, &d1);
-          nonfinite |= !isfinite(r1);
-        }
-        store_pair(e, Cb + off, (unsigned long long)(cq + off), r0, r1, two, c_vec2);
-        if (e.kind == EPI_STAGE_D) {
-          if (two && c_vec2) {
-            *reinterpret_cast<double2*>(e.D + cq + off) = make_double2(d0, d1);
-          } else {
+        if constexpr (SCAT) {
+          double r1 = 0.0;
+          if (two) {
+            r1 = epi_one(e, v1, p.C, cq + off + 1, species_half, &d1);
+            nonfinite |= !isfinite(r1);
+          }
+          store_pair<SCAT>(e, Cb + off, (unsigned long long)(cq + off), r0, r1, two, c_vec2);
+          if (e.kind == EPI_STAGE_D) {
             e.D[cq + off] = d0;
             if (two) e.D[cq + off + 1] = d1;
           }
+        } else if (two) {
+          const double r1 = epi_one(e, v1, p.C, cq + off + 1, species_half, &d1);
+          nonfinite |= !isfinite(r1);
+          if (c_vec2) {
+            *reinterpret_cast<double2*>(Cb + off) = make_double2(r0, r1);
+            if (e.kind == EPI_STAGE_D)
+              *reinterpret_cast<double2*>(e.D + cq + off) = make_double2(d0, d1);
+          } else {
+            Cb[off] = r0;
+            Cb[off + 1] = r1;
+            if (e.kind == EPI_STAGE_D) {
+              e.D[cq + off] = d0;
+              e.D[cq + off + 1] = d1;
+            }
+          }
+        } else {
+          Cb[off] = r0;
+          if (e.kind == EPI_STAGE_D) e.D[cq + off] = d0;
         }
       }
   }
   if (e.bad_step && nonfinite) atomicMin(e.bad_step, *e.step_ctr + 1);
 }
 
-template <int BM, int BN, int WARPS_M, int WARPS_N, bool B_KCONTIG, int VEC, int CPLX, int VAR>
+template <int BM, int BN, int WARPS_M, int WARPS_N, bool B_KCONTIG, int VEC, int CPLX, int VAR,
+          bool SCAT = false>
 void launch_cfg(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, long long half) {
   // 128x128 with 8 warps of 64x32: one CTA per SM, BK=32 x 3 stages.
   // Every other tile uses 32x32 warp tiles (<= 128 registers) so that two or
@@ -446,7 +466,8 @@ void launch_cfg(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, long long 
   constexpr int BK = BIG ? 32 : 16, STAGES = BIG ? 3 : (VAR == 1 ? 3 : 4);
   constexpr int MINB = BIG ? 1 : (VAR == 1 ? 4 : (WARPS_M * WARPS_N * 32 >= 512 ? 1 : 2));
   using CF = Cfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, B_KCONTIG, VEC>;
-  auto kern = dmma_gemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, B_KCONTIG, VEC, CPLX, MINB>;
+  auto kern = dmma_gemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, B_KCONTIG, VEC, CPLX, MINB,
+                               SCAT>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     KP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -470,23 +491,23 @@ void launch_cfg(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, long long 
   KP_CUDA(cudaGetLastError());
 }
 
-template <int BM, int BN, int WARPS_M, int WARPS_N, int VAR = 0>
+template <int BM, int BN, int WARPS_M, int WARPS_N, int VAR = 0, bool SCAT = false>
 void launch_layout(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, bool kcontig, bool vec2,
                    int cplx, long long half) {
   if (cplx == 1) {
-    launch_cfg<BM, BN, WARPS_M, WARPS_N, true, 2, 1, VAR>(ctx, p, e, half);
+    launch_cfg<BM, BN, WARPS_M, WARPS_N, true, 2, 1, VAR, SCAT>(ctx, p, e, half);
   } else if (cplx == 2) {
-    launch_cfg<BM, BN, WARPS_M, WARPS_N, false, 2, 2, VAR>(ctx, p, e, half);
+    launch_cfg<BM, BN, WARPS_M, WARPS_N, false, 2, 2, VAR, SCAT>(ctx, p, e, half);
   } else if (kcontig) {
     if (vec2)
-      launch_cfg<BM, BN, WARPS_M, WARPS_N, true, 2, 0, VAR>(ctx, p, e, half);
+      launch_cfg<BM, BN, WARPS_M, WARPS_N, true, 2, 0, VAR, SCAT>(ctx, p, e, half);
     else
-      launch_cfg<BM, BN, WARPS_M, WARPS_N, true, 1, 0, VAR>(ctx, p, e, half);
+      launch_cfg<BM, BN, WARPS_M, WARPS_N, true, 1, 0, VAR, SCAT>(ctx, p, e, half);
   } else {
     if (vec2)
-      launch_cfg<BM, BN, WARPS_M, WARPS_N, false, 2, 0, VAR>(ctx, p, e, half);
+      launch_cfg<BM, BN, WARPS_M, WARPS_N, false, 2, 0, VAR, SCAT>(ctx, p, e, half);
     else
-      launch_cfg<BM, BN, WARPS_M, WARPS_N, false, 1, 0, VAR>(ctx, p, e, half);
+      launch_cfg<BM, BN, WARPS_M, WARPS_N, false, 1, 0, VAR, SCAT>(ctx, p, e, half);
   }
 }
 
@@ -529,6 +550,15 @@ void launch_gemm(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int cplx)
     tile = (p.K >= 1024 && p.M > 64) ? 1 : 9;
   else
     tile = (tiles64 >= 16LL * ctx->num_sms || p.K >= 1024) ? 8 : 6;
+  if (e.sc_dir) {
+    // fused exchange: a separate instantiation with the scatter stores (the
+    // plain kernels carry no trace of them), two tile shapes
+    if (tile == 5)
+      launch_layout<32, 32, 2, 2, 0, true>(ctx, p, e, kcontig, vec2, cplx, half);
+    else
+      launch_layout<64, 64, 2, 2, 1, true>(ctx, p, e, kcontig, vec2, cplx, half);
+    return;
+  }
   static const int forced = [] {  // benchmarking override
     const char* v = getenv("KP_GEMM_TILE");
     return v ? atoi(v) : -1;
