@@ -148,15 +148,18 @@ __device__ __forceinline__ void term_cplx(const BandArgs& b, int mu, int imu, lo
 template <bool CPLX>
 __global__ void kronsum_band_kernel(BandArgs b, long long total, const double* __restrict__ u,
                                     double* __restrict__ r, bool with_g, kp_gfun g, double t) {
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    long long rem = idx, in = 0;
+  // entries < 2^32 (checked by the launcher): 32-bit index arithmetic
+  for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < (unsigned)total;
+       idx += gridDim.x * blockDim.x) {
+    unsigned rem = idx;
+    long long in = 0;
     int ii[4];
 #pragma unroll
     for (int mu = 0; mu < 4; ++mu) {
       if (mu < b.d) {
-        ii[mu] = int(rem % b.n[mu]);
-        rem /= b.n[mu];
+        const unsigned q = rem / unsigned(b.n[mu]);
+        ii[mu] = int(rem - q * unsigned(b.n[mu]));
+        rem = q;
         in += (long long)(ii[mu] + (mu == b.slab ? b.halo : 0)) * b.stride[mu];
         if (mu == b.slab) ii[mu] += b.k0;  // global row for the factor lookup
       }
@@ -170,7 +173,11 @@ __global__ void kronsum_band_kernel(BandArgs b, long long total, const double* _
         term_real(b, mu, ii[mu], in, u, acc, has);
       }
       if (with_g) {
-        const bool second = b.species >= 0 && ii[b.species] == 1;
+        int isp = 0;
+#pragma unroll
+        for (int mu = 0; mu < 4; ++mu)
+          if (mu == b.species) isp = ii[mu];
+        const bool second = b.species >= 0 && isp == 1;
         const double partner =
             b.species >= 0 ? u[second ? in - b.stride[b.species] : in + b.stride[b.species]] : 0.0;
         acc = __dadd_rn(acc, g_real(g, u[in], partner, second, idx, t));
@@ -289,6 +296,7 @@ void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<i
     b.vals[mu] = vals[mu];
     b.active[mu] = active[mu];
   }
+  if (total > 0xffffffffLL) throw invalid_argument("kronsum: tensor too large for the stencil path");
   const unsigned grid =
       unsigned(std::max<long long>(1, std::min<long long>((total + 255) / 256, ctx->num_sms * 16LL)));
   if (cplx)
