@@ -490,7 +490,7 @@ def main():
 
         host_step()
         host_stream(2)
-        ksteps = max(2, min(args.steps, 8))
+        ksteps = max(4, min(args.steps, 8))
         single = timed(lambda: [host_step() for _ in range(min(ksteps, 4))], min(ksteps, 4))
         sec = timed(lambda: host_stream(ksteps), ksteps)
         fbytes = sum(f.nbytes for f in hfs)
