@@ -33,6 +33,12 @@ struct Big {
   using TB = cutlass::gemm::GemmShape<64, 128, 16>;
   using Warp = cutlass::gemm::GemmShape<32, 64, 16>;
 };
+// short M (M <= 64, e.g. the block rows of the LU solves): 128 x 64 tiles of
+// C' (64 rows of C), 4 warps of 64 x 32
+struct Narrow {
+  using TB = cutlass::gemm::GemmShape<128, 64, 16>;
+  using Warp = cutlass::gemm::GemmShape<64, 32, 16>;
+};
 // small problems (fewer 64 x 128 tiles than SMs): 32 x 32 tiles, 4 warps of 16 x 16
 struct Small {
   using TB = cutlass::gemm::GemmShape<32, 32, 16>;
@@ -227,8 +233,11 @@ void launch_cutlass_any(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, lo
   // small tiles when the big ones leave SMs idle, or give under ~8 waves of
   // short-K work (n = 128 cubes: 20.4 vs 17.1 TFLOP/s; n = 256: 29.3 vs 30.4)
   const bool small = big_tiles < ctx->num_sms || (big_tiles < 8LL * ctx->num_sms && p.K <= 256);
-  if (forced == 1 || (forced != 2 && small))
+  const long long narrow_tiles = (long long)((p.N + 127) / 128) * ((p.M + 63) / 64) * p.batch;
+  if (forced == 1 || (forced != 2 && small && !(p.M <= 64 && narrow_tiles >= ctx->num_sms)))
     launch_cutlass<B_KCONTIG, SCAT, cg_dmma::Small, CPLX>(ctx, p, e, half);
+  else if (p.M <= 64 && forced != 2)
+    launch_cutlass<B_KCONTIG, SCAT, cg_dmma::Narrow, CPLX>(ctx, p, e, half);
   else
     launch_cutlass<B_KCONTIG, SCAT, cg_dmma::Big, CPLX>(ctx, p, e, half);
 }
