@@ -336,10 +336,11 @@ def cpu_baseline(n, v, ms):
     import pyoracle
     if pyoracle.available("reference"):
         o = pyoracle.Oracle("reference")
-        sec = o.time_tucker(v, ms, reps=2)
+        reps = 8  # ~10 s of CPU work at n = 512
+        sec = o.time_tucker(v, ms, reps=reps)
         return {"value": flops_per_tucker(n) / sec / 1e9, "unit": "GFLOP/s",
                 "cores": o.num_threads(), "kind": "reference",
-                "sample": f"2 timed calls (best) of the reference tucker() on the d=3 n={n} "
+                "sample": f"{reps} timed calls (best) of the reference tucker() on the d=3 n={n} "
                           f"cube after 1 warm-up, OpenMP threads={o.num_threads()}"}
     o = pyoracle.Oracle("port")
     m = min(n, 128)
