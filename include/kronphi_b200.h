@@ -101,6 +101,9 @@ int kp_free(kp_ctx* ctx, void* ptr);
 int kp_upload(kp_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes);
 int kp_download(kp_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes);
 int kp_memset(kp_ctx* ctx, void* dst_dev, int value, size_t bytes);
+/* Device-to-device copy on the context's stream; either side may be a peer
+ * mapping (CUDA IPC) of another GPU's memory (NVLink P2P). */
+int kp_copy(kp_ctx* ctx, void* dst_dev, const void* src_dev, size_t bytes);
 
 /* ---------------- mu-mode / Tucker / Kronecker sum ---------------- */
 /* out = alpha * (t x_mode M) + beta * out.

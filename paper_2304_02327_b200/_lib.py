@@ -84,6 +84,7 @@ _SIGS = {
     "kp_upload": (_I, [_CTX, _VP, _VP, _SZ]),
     "kp_download": (_I, [_CTX, _VP, _VP, _SZ]),
     "kp_memset": (_I, [_CTX, _VP, _I, _SZ]),
+    "kp_copy": (_I, [_CTX, _VP, _VP, _SZ]),
     "kp_mode_product_f64": (_I, [_CTX, _VP, _PI, _I, _I, _VP, _I, _I, _D, _D, _VP]),
     "kp_mode_product_c128": (_I, [_CTX, _VP, _PI, _I, _I, _VP, _I, _I, _PD, _PD, _VP]),
     "kp_tucker_f64": (_I, [_CTX, _VP, _PI, _I, _PPD, _PI, _D, _VP]),

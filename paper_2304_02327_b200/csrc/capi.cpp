@@ -274,6 +274,14 @@ int kp_download(kp_ctx* ctx, void* dst, const void* src, size_t bytes) {
     KP_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
+int kp_copy(kp_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  return guard([&] {
+    need_ctx(ctx);
+    if (bytes && (!dst || !src)) throw invalid_argument("copy: null pointer");
+    if (bytes) KP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
+  });
+}
+
 int kp_memset(kp_ctx* ctx, void* dst, int value, size_t bytes) {
   return guard([&] {
     need_ctx(ctx);

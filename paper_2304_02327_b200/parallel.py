@@ -316,17 +316,18 @@ class PeerComm:
 
     def exchange_halos(self, first, last, left, right):
         """left <- last plane of rank-1, right <- first plane of rank+1 (cyclic),
-        as peer stores into the neighbours' halo buffers."""
+        as peer copies into the neighbours' halo buffers (raw device pointers:
+        the peers' buffers may live on other GPUs)."""
         n = first.numel()
         esz = first.element_size()
         slot = self._slot("halo", 2 * n * esz)
         prev, nxt = (self.rank - 1) % self.P, (self.rank + 1) % self.P
-        cplx = torch.is_complex(first)
+        lib, h = self.be.ctx.lib, self.be.ctx.h
+        lastc, firstc = last.contiguous(), first.contiguous()
+        self.be._sync_stream()
         # my last plane -> next rank's left halo (offset 0); first -> prev's right (offset n)
-        dst_l = torch.as_tensor(_DevArray(slot[2][nxt], n, cplx), device=first.device)
-        dst_r = torch.as_tensor(_DevArray(slot[2][prev] + n * esz, n, cplx), device=first.device)
-        dst_l.copy_(last.reshape(-1))
-        dst_r.copy_(first.reshape(-1))
+        self._check(lib.kp_copy(h, slot[2][nxt], lastc.data_ptr(), n * esz))
+        self._check(lib.kp_copy(h, slot[2][prev] + n * esz, firstc.data_ptr(), n * esz))
         self.barrier()
         mine = self._view("halo", 2 * n, first)
         left.copy_(mine[:n].view(left.shape))
