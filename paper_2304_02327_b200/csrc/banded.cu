@@ -21,6 +21,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "kp_g.cuh"
@@ -201,6 +203,231 @@ __global__ void kronsum_band_kernel(BandArgs b, long long total, const double* _
   }
 }
 
+
+// ---- v2: the same arithmetic, laid out for the memory system ----
+// One thread per (i0, i1) line, marching over a chunk of the slower modes
+// (z = i2 + n2 * i3): the mode-0 / mode-1 row structures (offsets already
+// multiplied by the strides, values, KC slice breaks) live in registers for
+// the whole march, the mode-2 / mode-3 rows are block-uniform loads, warps
+// read 32 consecutive entries (coalesced) and the neighbour planes come from
+// L1/L2.  No integer divisions per entry, 32-bit output index arithmetic.
+// With a 2-species g (Brusselator) each thread computes BOTH species of a
+// grid point, so the partner value is the other centre (no extra HBM read).
+template <bool CPLX>
+struct BandRow {
+  int off[3];  // (column - row) * stride, < 2^31 (checked by the launcher)
+  typename std::conditional<CPLX, double2, double>::type v[3];
+  int n;
+  unsigned brk;  // bit s: entry s starts a new KC slice
+};
+
+template <bool CPLX>
+__device__ __forceinline__ void load_row(const BandArgs& b, int mu, int i, BandRow<CPLX>& rw) {
+  const int ig = (mu == b.slab) ? i + b.k0 : i;  // global row
+  const int* cs = b.cols[mu] + ig * 3;
+  const double* v = b.vals[mu] + ig * 6;
+  rw.n = 0;
+  rw.brk = 0;
+  int prev = -1;
+  // entries past n are padded with (offset 0, value 0): see row_combine
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    rw.off[s] = 0;
+    if constexpr (CPLX)
+      rw.v[s] = make_double2(0.0, 0.0);
+    else
+      rw.v[s] = 0.0;
+  }
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    const int j = __ldg(cs + s);
+    if (j < 0) break;
+    const int sl = j / KC;
+    if (s > 0 && sl != prev) rw.brk |= 1u << s;
+    prev = sl;
+    rw.off[s] = int(col_off(b, mu, ig, j) * b.stride[mu]);
+    if constexpr (CPLX)
+      rw.v[s] = make_double2(__ldg(v + 2 * s), __ldg(v + 2 * s + 1));
+    else
+      rw.v[s] = __ldg(v + 2 * s);
+    rw.n = s + 1;
+  }
+}
+
+// Gather the three u values of one row term (padded entries read the
+// centre: offset 0) and fold them into c with the reference's rounding.
+//
+// Fast path (no KC break in the row): c + fma(v2, x2, fma(v1, x1, fma(v0,
+// x0, 0))).  This equals term_real's chain exactly for finite data: the
+// chain's accumulator is never -0 (it starts from +0, and an exact
+// cancellation rounds to +0), so a padded fma(0, x, acc) = acc + (+-0)
+// returns acc, an empty row adds +0 to a c that is never -0, and the first
+// mode's 0 + acc is acc.  (A non-finite centre turns the padded products
+// into NaN: only diverged states, which the step's finite check rejects
+// either way.)  Rows that straddle a KC = 256 slice boundary take the
+// general chain (uniform per warp for modes >= 1).
+template <bool CPLX, typename T>
+__device__ __forceinline__ void row_gather(const BandRow<CPLX>& rw, const T* __restrict__ u,
+                                           unsigned in, T* x) {
+#pragma unroll
+  for (int s = 0; s < 3; ++s) x[s] = u[in + unsigned(rw.off[s])];
+}
+
+__device__ __forceinline__ void row_combine(const BandRow<false>& rw, const double* x, double& c) {
+  if (rw.brk == 0) {
+    const double acc = __fma_rn(rw.v[2], x[2], __fma_rn(rw.v[1], x[1], __fma_rn(rw.v[0], x[0], 0.0)));
+    c = __dadd_rn(c, acc);
+    return;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    if (s >= rw.n) break;
+    if ((rw.brk >> s) & 1u) {
+      c = __dadd_rn(c, acc);
+      acc = 0.0;
+    }
+    acc = __fma_rn(rw.v[s], x[s], acc);
+  }
+  c = __dadd_rn(c, acc);
+}
+
+__device__ __forceinline__ void row_combine(const BandRow<true>& rw, const double2* x, double2& c) {
+  double2 acc = make_double2(0.0, 0.0);
+  if (rw.brk == 0) {
+    acc = cmul_add(rw.v[2], x[2], cmul_add(rw.v[1], x[1], cmul_add(rw.v[0], x[0], acc)));
+    c = make_double2(__dadd_rn(c.x, acc.x), __dadd_rn(c.y, acc.y));
+    return;
+  }
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    if (s >= rw.n) break;
+    if ((rw.brk >> s) & 1u) {
+      c = make_double2(__dadd_rn(c.x, acc.x), __dadd_rn(c.y, acc.y));
+      acc = make_double2(0.0, 0.0);
+    }
+    acc = cmul_add(rw.v[s], x[s], acc);
+  }
+  c = make_double2(__dadd_rn(c.x, acc.x), __dadd_rn(c.y, acc.y));
+}
+
+// b.n / b.stride / b.active are padded to 4 modes (extent 1, inactive).
+// PAIR: the species mode (3, extent 2) is iterated inside the thread (nz =
+// n2 then).  M3: mode 3 has an active factor.  A block's mode-2 rows
+// (z-chunk <= ZMAX) are decoded once into shared memory.
+constexpr int ZMAX = 32;
+
+template <bool CPLX, bool PAIR, bool M3>
+__global__ void __launch_bounds__(256, (CPLX || PAIR) ? 2 : 3)
+    kronsum_band2_kernel(BandArgs b, int nz, int zchunk, const double* __restrict__ u,
+                         double* __restrict__ r, bool with_g, kp_gfun g, double t) {
+  using T = typename std::conditional<CPLX, double2, double>::type;
+  __shared__ BandRow<CPLX> rows2[ZMAX];
+  const T* __restrict__ ut = reinterpret_cast<const T*>(u);
+  T* __restrict__ rt = reinterpret_cast<T*>(r);
+  const int z0 = blockIdx.z * zchunk;
+  const int z1 = min(nz, z0 + zchunk);
+  const int tid = threadIdx.x + 32 * threadIdx.y;
+  if (b.active[2] && tid < z1 - z0) {
+    const int z = z0 + tid;
+    load_row(b, 2, PAIR ? z : z % b.n[2], rows2[tid]);
+  }
+  __syncthreads();
+  const int i0 = blockIdx.x * 32 + threadIdx.x;
+  const int i1 = blockIdx.y * 8 + threadIdx.y;
+  if (i0 >= b.n[0] || i1 >= b.n[1]) return;
+  BandRow<CPLX> r0, r1;
+  if (b.active[0]) load_row(b, 0, i0, r0);
+  if (b.active[1]) load_row(b, 1, i1, r1);
+  const int h2 = b.slab == 2 ? b.halo : 0, h3 = b.slab == 3 ? b.halo : 0;
+  const unsigned in01 = unsigned(i0 + (b.slab == 0 ? b.halo : 0)) * unsigned(b.stride[0]) +
+                        unsigned(i1 + (b.slab == 1 ? b.halo : 0)) * unsigned(b.stride[1]);
+  const unsigned plane = unsigned(b.n[0]) * unsigned(b.n[1]);
+  const unsigned out01 = unsigned(i0) + unsigned(i1) * unsigned(b.n[0]);
+  const unsigned st2 = unsigned(b.stride[2]), st3 = unsigned(b.stride[3]);
+  const unsigned n2 = unsigned(b.n[2]);
+  const bool a0 = b.active[0], a1 = b.active[1], a2 = b.active[2];
+  BandRow<CPLX> r3a, r3b;
+  if (M3) {
+    if (PAIR) {
+      load_row(b, 3, 0, r3a);
+      load_row(b, 3, 1, r3b);
+    }
+  }
+  // one entry: the Kronecker-sum value (without g) at input index `in`
+  auto entry = [&](unsigned in, const BandRow<CPLX>& q2, const BandRow<CPLX>& q3) -> T {
+    T x0[3], x1[3], x2[3], x3[3];
+    if (a0) row_gather(r0, ut, in, x0);
+    if (a1) row_gather(r1, ut, in, x1);
+    if (a2) row_gather(q2, ut, in, x2);
+    if (M3) row_gather(q3, ut, in, x3);
+    T c;
+    if constexpr (CPLX)
+      c = make_double2(0.0, 0.0);
+    else
+      c = 0.0;
+    if (a0) row_combine(r0, x0, c);
+    if (a1) row_combine(r1, x1, c);
+    if (a2) row_combine(q2, x2, c);
+    if (M3) row_combine(q3, x3, c);
+    return c;
+  };
+  // L1 prefetch PD planes ahead: the march is otherwise one dependent HBM
+  // round trip per plane (latency-bound at the occupancy the rows allow)
+  constexpr int PD = 3;
+  const int zlim = min(z1 + 1, PAIR ? nz + h2 : nz);  // last plane the march reads (+1 neighbour)
+  auto prefetch = [&](int z) {
+    if (z >= zlim) return;
+    unsigned in;
+    if constexpr (PAIR) {
+      in = in01 + (unsigned(z) + h2) * st2 + unsigned(h3) * st3;
+    } else {
+      const unsigned i3 = unsigned(z) / n2, i2 = unsigned(z) - i3 * n2;
+      in = in01 + (i2 + h2) * st2 + (i3 + h3) * st3;
+    }
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(ut + in));
+    if constexpr (PAIR) asm volatile("prefetch.global.L1 [%0];" ::"l"(ut + in + st3));
+  };
+#pragma unroll
+  for (int k = 1; k <= PD; ++k) prefetch(z0 + k);
+  for (int z = z0; z < z1; ++z) {
+    prefetch(z + PD + 1);
+    const BandRow<CPLX>& q2 = rows2[z - z0];
+    if constexpr (PAIR) {
+      const unsigned iz = unsigned(z);
+      const unsigned in0 = in01 + (iz + h2) * st2 + unsigned(h3) * st3;
+      const unsigned in1 = in0 + st3;
+      const unsigned idx0 = out01 + iz * plane;
+      const unsigned idx1 = idx0 + n2 * plane;
+      const T c0 = entry(in0, q2, r3a);
+      const T c1 = entry(in1, q2, r3b);
+      if (with_g) {
+        const double u0 = ut[in0], u1 = ut[in1];
+        rt[idx0] = __dadd_rn(c0, g_real(g, u0, u1, false, idx0, t));
+        rt[idx1] = __dadd_rn(c1, g_real(g, u1, u0, true, idx1, t));
+      } else {
+        rt[idx0] = c0;
+        rt[idx1] = c1;
+      }
+    } else {
+      const unsigned i3 = unsigned(z) / n2, i2 = unsigned(z) - i3 * n2;
+      const unsigned in = in01 + (i2 + h2) * st2 + (i3 + h3) * st3;
+      const unsigned idx = out01 + (i2 + i3 * n2) * plane;
+      BandRow<CPLX> q3;
+      if (M3) load_row(b, 3, int(i3), q3);
+      const T c = entry(in, q2, q3);
+      if (!with_g) {
+        rt[idx] = c;
+      } else if constexpr (CPLX) {
+        const double2 gg = g_cplx(g, ut[in]);
+        rt[idx] = make_double2(__dadd_rn(c.x, gg.x), __dadd_rn(c.y, gg.y));
+      } else {
+        rt[idx] = __dadd_rn(c, g_real(g, ut[in], 0.0, false, idx, t));
+      }
+    }
+  }
+}
+
 }  // namespace
 
 // forward (defined below)
@@ -297,12 +524,67 @@ void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<i
     b.active[mu] = active[mu];
   }
   if (total > 0xffffffffLL) throw invalid_argument("kronsum: tensor too large for the stencil path");
-  const unsigned grid =
-      unsigned(std::max<long long>(1, std::min<long long>((total + 255) / 256, ctx->num_sms * 16LL)));
-  if (cplx)
-    kronsum_band_kernel<true><<<grid, 256, 0, ctx->stream>>>(b, total, u, r, with_g, g, t);
-  else
-    kronsum_band_kernel<false><<<grid, 256, 0, ctx->stream>>>(b, total, u, r, with_g, g, t);
+  static const bool v1 = [] {  // KP_BAND=v1: the one-entry-per-thread kernel (A/B)
+    const char* v = getenv("KP_BAND");
+    return v && std::string(v) == "v1";
+  }();
+  if (v1) {
+    const unsigned grid = unsigned(
+        std::max<long long>(1, std::min<long long>((total + 255) / 256, ctx->num_sms * 16LL)));
+    if (cplx)
+      kronsum_band_kernel<true><<<grid, 256, 0, ctx->stream>>>(b, total, u, r, with_g, g, t);
+    else
+      kronsum_band_kernel<false><<<grid, 256, 0, ctx->stream>>>(b, total, u, r, with_g, g, t);
+  } else {
+    // pad to 4 modes; the 2-species mode (always the last, extent 2) is
+    // moved to slot 3 so a thread can own both species of a grid point
+    BandArgs b2 = b;
+    for (int mu = d; mu < 4; ++mu) {
+      b2.n[mu] = 1;
+      b2.stride[mu] = 0;
+      b2.cols[mu] = nullptr;
+      b2.vals[mu] = nullptr;
+      b2.active[mu] = 0;
+    }
+    bool pair = false;
+    if (b.species >= 0 && !cplx) {
+      const int sp = b.species;  // = d - 1
+      if (sp != 3) {
+        std::swap(b2.n[sp], b2.n[3]);
+        std::swap(b2.stride[sp], b2.stride[3]);
+        std::swap(b2.cols[sp], b2.cols[3]);
+        std::swap(b2.vals[sp], b2.vals[3]);
+        std::swap(b2.active[sp], b2.active[3]);
+        if (b2.slab == sp) b2.slab = 3;
+        else if (b2.slab == 3) b2.slab = sp;
+      }
+      b2.species = 3;
+      pair = true;
+    }
+    const int nz = pair ? b2.n[2] : b2.n[2] * b2.n[3];
+    const long long bxy = (long long)((b2.n[0] + 31) / 32) * ((b2.n[1] + 7) / 8);
+    const long long want = ctx->num_sms * 16LL;  // ~2 waves of 8 resident blocks
+    int zchunk = int(std::min<long long>(ZMAX, std::max<long long>(1, (nz * bxy + want - 1) / want)));
+    if ((nz + zchunk - 1) / zchunk > 65535)
+      throw invalid_argument("kronsum: modes 2-3 too large for the stencil path");
+    dim3 grid(unsigned((b2.n[0] + 31) / 32), unsigned((b2.n[1] + 7) / 8),
+              unsigned((nz + zchunk - 1) / zchunk));
+    if (grid.y > 65535) throw invalid_argument("kronsum: mode 1 too large for the stencil path");
+    long long ext = 1;  // input extent incl. halo planes: 32-bit offsets
+    for (int mu = 0; mu < d; ++mu) ext *= dims[mu] + (mu == slab ? 2 * b.halo : 0);
+    if (ext > 0x7fffffffLL) throw invalid_argument("kronsum: tensor too large for the stencil path");
+    const bool m3 = b2.active[3] != 0;
+    auto go = [&](auto kern) {
+      kern<<<grid, dim3(32, 8), 0, ctx->stream>>>(b2, nz, zchunk, u, r, with_g, g, t);
+    };
+    if (cplx) {
+      m3 ? go(kronsum_band2_kernel<true, false, true>) : go(kronsum_band2_kernel<true, false, false>);
+    } else if (pair) {
+      m3 ? go(kronsum_band2_kernel<false, true, true>) : go(kronsum_band2_kernel<false, true, false>);
+    } else {
+      m3 ? go(kronsum_band2_kernel<false, false, true>) : go(kronsum_band2_kernel<false, false, false>);
+    }
+  }
   ctx->launches++;
   KP_CUDA(cudaGetLastError());
 }

@@ -127,7 +127,16 @@ void tucker_generic(kp_ctx* ctx, ModeFn mp, int comps, const double* t, std::vec
                     const Epilogue* last = nullptr, int slot_base = 0) {
   const int d = int(dims.size());
   const double* cur = t;
-  for (int mu = 0; mu < d; ++mu) {
+  int mu0 = 0;
+  if (comps == 1 && d >= 3) {  // modes 0 and 1 in one pass over small slices
+    double* dst = static_cast<double*>(
+        ctx->ws.get(slot_base + 1, numel(dims) * sizeof(double)));
+    if (fused01_f64(ctx, t, dims, ms[0], rows[0], ms[1], rows[1], pref, Epilogue{}, dst)) {
+      cur = dst;
+      mu0 = 2;
+    }
+  }
+  for (int mu = mu0; mu < d; ++mu) {
     std::vector<int> od = dims;
     od[mu] = rows[mu];
     double* dst;

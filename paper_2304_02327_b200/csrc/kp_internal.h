@@ -127,6 +127,12 @@ void launch_gemm(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int cplx 
 void mode_product_f64(kp_ctx* ctx, const double* t, const std::vector<int>& dims, int mode,
                       const double* m, int rows, const Epilogue& e, double* out);
 
+// Modes 0 and 1 of a Tucker operator fused per N x N slice (fused01.cu):
+// out = e1((alpha0 * in x_0 m0) x_1 m1).  false = not applicable.
+bool fused01_f64(kp_ctx* ctx, const double* in, const std::vector<int>& dims, const double* m0,
+                 int rows0, const double* m1, int rows1, double alpha0, const Epilogue& e1,
+                 double* out);
+
 // Complex mode product (interleaved complex128, cplx.cu).  m is rows x dims[mode].
 void mode_product_c128(kp_ctx* ctx, const double* t, const std::vector<int>& dims, int mode,
                        const double* m, int rows, const Epilogue& e, double* out);

@@ -118,6 +118,54 @@ __global__ void gdiff_kernel(kp_gfun g, double t, double t2, long long n, long l
     d[i] = E::sub(E::g(g, s, i, half, t2), E::g(g, u, i, half, t));
 }
 
+// Two-species (Brusselator) forms of the three kernels above: one thread
+// owns both species of a grid point (i, i + half), so each value is read
+// once (the unpaired kernels re-read the partner from HBM).  Same
+// arithmetic per entry.
+__global__ void lawson_pre_pair_kernel(kp_gfun g, double t, long long half, double tau, bool two,
+                                       const double* __restrict__ u, double* __restrict__ w) {
+  const long long n = 2 * half;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < half;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double a = u[i], b = u[i + half];
+    const double ga = g_real(g, a, b, false, i, t), gb = g_real(g, b, a, true, i + half, t);
+    w[i] = __fma_rn(tau, ga, a);
+    w[i + half] = __fma_rn(tau, gb, b);
+    if (two) {
+      w[n + i] = __fma_rn(0.5 * tau, ga, a);
+      w[n + i + half] = __fma_rn(0.5 * tau, gb, b);
+    }
+  }
+}
+
+__global__ void lawson2b_post_pair_kernel(kp_gfun g, double t2, long long half, double tau,
+                                          const double* __restrict__ y, double* __restrict__ out,
+                                          int* bad, const int* ctr) {
+  const long long n = 2 * half;
+  bool nf = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < half;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double a = y[i], b = y[i + half];
+    const double ra = __fma_rn(0.5 * tau, g_real(g, a, b, false, i, t2), y[n + i]);
+    const double rb = __fma_rn(0.5 * tau, g_real(g, b, a, true, i + half, t2), y[n + i + half]);
+    out[i] = ra;
+    out[i + half] = rb;
+    nf |= !isfinite(ra) || !isfinite(rb);
+  }
+  if (nf) atomicMin(bad, *ctr + 1);
+}
+
+__global__ void gdiff_pair_kernel(kp_gfun g, double t, double t2, long long half,
+                                  const double* __restrict__ s, const double* __restrict__ u,
+                                  double* __restrict__ d) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < half;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double sa = s[i], sb = s[i + half], ua = u[i], ub = u[i + half];
+    d[i] = __dsub_rn(g_real(g, sa, sb, false, i, t2), g_real(g, ua, ub, false, i, t));
+    d[i + half] = __dsub_rn(g_real(g, sb, sa, true, i + half, t2), g_real(g, ub, ua, true, i + half, t));
+  }
+}
+
 __global__ void tick_kernel(int* ctr) { *ctr += 1; }
 
 __global__ void scale_matrix_kernel(const double* __restrict__ a, long long n, double s,
@@ -346,7 +394,19 @@ class Integrator {
     for (int mu = 0; mu < d; ++mu)
       if (fs.active[mu]) act.push_back(mu);
     const double* cur = in;
-    for (size_t k = 0; k < act.size(); ++k) {
+    size_t k0 = 0;
+    if (!cplx && act.size() >= 3 && act[0] == 0 && act[1] == 1) {
+      // modes 0 and 1 in one pass over small slices (fused01.cu); slot 1 =
+      // the buffer the unfused loop would leave mode 1's result in
+      double* dst = static_cast<double*>(
+          ctx->ws.get(1, size_t(n_total(tdims)) * comps * sizeof(double)));
+      if (fused01_f64(ctx, in, tdims, fs.f[0], tdims[0], fs.f[1], tdims[1], fs.pref, Epilogue{},
+                      dst)) {
+        cur = dst;
+        k0 = 2;
+      }
+    }
+    for (size_t k = k0; k < act.size(); ++k) {
       const int mu = act[k];
       const bool first = (k == 0), fin = (k + 1 == act.size());
       double* dst = fin ? out
@@ -390,6 +450,11 @@ class Integrator {
   template <bool C>
   void launch_pre(const double* u, double* w, bool two, double t) {
     using T = typename Elt<C>::T;
+    if (!C && half > 0) {
+      lawson_pre_pair_kernel<<<grid_ew(ctx, half), 256, 0, ctx->stream>>>(g, t, half, tau, two, u, w);
+      ctx->launches++;
+      return;
+    }
     lawson_pre_kernel<C><<<grid_ew(ctx, n_entries), 256, 0, ctx->stream>>>(
         g, t, n_entries, half, tau, two, reinterpret_cast<const T*>(u), reinterpret_cast<T*>(w));
     ctx->launches++;
@@ -397,6 +462,12 @@ class Integrator {
   template <bool C>
   void launch_post(const double* y, double* out, int* bad, const int* ctr, double t2) {
     using T = typename Elt<C>::T;
+    if (!C && half > 0) {
+      lawson2b_post_pair_kernel<<<grid_ew(ctx, half), 256, 0, ctx->stream>>>(g, t2, half, tau, y,
+                                                                             out, bad, ctr);
+      ctx->launches++;
+      return;
+    }
     lawson2b_post_kernel<C><<<grid_ew(ctx, n_entries), 256, 0, ctx->stream>>>(
         g, t2, n_entries, half, tau, reinterpret_cast<const T*>(y), reinterpret_cast<T*>(out), bad, ctr);
     ctx->launches++;
@@ -404,6 +475,11 @@ class Integrator {
   template <bool C>
   void launch_gdiff(const double* s, const double* u, double* dd, double t) {
     using T = typename Elt<C>::T;
+    if (!C && half > 0) {
+      gdiff_pair_kernel<<<grid_ew(ctx, half), 256, 0, ctx->stream>>>(g, t, t + tau, half, s, u, dd);
+      ctx->launches++;
+      return;
+    }
     gdiff_kernel<C><<<grid_ew(ctx, n_entries), 256, 0, ctx->stream>>>(
         g, t, t + tau, n_entries, half, reinterpret_cast<const T*>(s), reinterpret_cast<const T*>(u),
         reinterpret_cast<T*>(dd));
