@@ -187,6 +187,36 @@ int kp_ipc_get_handle(const void* dptr, void* handle64);
 int kp_ipc_open_handle(const void* handle64, void** dptr);
 int kp_ipc_close_handle(void* dptr);
 
+/* ---------------- multi-GPU: NCCL communicator (native plumbing) ----------------
+ * "the multi-GPU communicator init from ncclUniqueId".  One
+ * process per GPU; rank 0 calls kp_comm_unique_id and the caller broadcasts
+ * the 128 bytes (any side channel), then every rank calls kp_comm_create
+ * with its context (device).  NCCL is dlopen'ed on first use.  All
+ * operations are stream-ordered on the context's stream.
+ *   kp_comm_repartition: the slab <-> pencil transpose of the sharded
+ *     integrators (layouts as kp_scatter above; dir 1 slab -> pencil, 2 back;
+ *     comps 1 real / 2 complex) = pack -> grouped ncclSend/Recv -> unpack;
+ *     bit-identical to the peer-memory scatter (pure data movement).
+ *   kp_repartition_pack / _unpack: its two local halves (send buffer =
+ *     P blocks of A*B/P*C/P*S entries, block s for rank s) for callers with
+ *     their own transport.
+ *   kp_comm_halo_f64: left <- last plane of rank-1, right <- first plane of
+ *     rank+1 (cyclic): the one-plane halo of kp_kronsum_slab_*. */
+typedef struct kp_comm kp_comm;
+int kp_comm_unique_id(void* id128);
+int kp_comm_create(kp_ctx* ctx, int nranks, int rank, const void* id128, kp_comm** out);
+int kp_comm_destroy(kp_comm* comm);
+int kp_comm_alltoall_f64(kp_ctx* ctx, kp_comm* comm, const double* send, double* recv,
+                         long long count_per_rank);
+int kp_comm_repartition(kp_ctx* ctx, kp_comm* comm, int dir, long long A, long long B,
+                        long long C, long long S, int comps, const double* x, double* y);
+int kp_repartition_pack(kp_ctx* ctx, int dir, int P, int rank, long long A, long long B,
+                        long long C, long long S, int comps, const double* x, double* send);
+int kp_repartition_unpack(kp_ctx* ctx, int dir, int P, int rank, long long A, long long B,
+                          long long C, long long S, int comps, const double* recv, double* y);
+int kp_comm_halo_f64(kp_ctx* ctx, kp_comm* comm, const double* first, const double* last,
+                     long long count, double* left, double* right);
+
 /* Host-buffer variants (the drop-in path: host in, host out, H2D/D2H inside). */
 int kp_host_mode_product_f64(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
                              const double* m, int rows, int cols, double alpha, double beta,

@@ -33,6 +33,7 @@
 
 #include <chrono>
 #include <cmath>
+#include <array>
 #include <complex>
 #include <cstddef>
 #include <cstring>
@@ -902,5 +903,48 @@ inline RiccatiProblem build_riccati(int n_hat) {
   pr.u0 = Matrix<double>(n, n);
   return pr;
 }
+
+// ---- multi-GPU (new; the reference is single-node CPU): one process per GPU.
+// Rank 0 calls Communicator::unique_id() and ships the 128 bytes to the other
+// ranks by any side channel; every rank then constructs a Communicator
+// (NCCL, on this thread's device).  repartition() is the slab <-> pencil
+// transpose of the sharded integrators (kp_comm_repartition), halo() the
+// one-plane exchange of the banded Kronecker sum (kp_comm_halo_f64); both
+// act on device buffers and are ordered on this thread's context stream.
+class Communicator {
+ public:
+  using Id = std::array<unsigned char, 128>;
+  static Id unique_id() {
+    Id id{};
+    detail::check(kp_comm_unique_id(id.data()));
+    return id;
+  }
+  Communicator(int nranks, int rank, const Id& id) : P_(nranks), rank_(rank) {
+    detail::check(kp_comm_create(detail::ctx(), nranks, rank, id.data(), &c_));
+  }
+  Communicator(const Communicator&) = delete;
+  Communicator& operator=(const Communicator&) = delete;
+  ~Communicator() {
+    if (c_) kp_comm_destroy(c_);
+  }
+  int size() const { return P_; }
+  int rank() const { return rank_; }
+  // dir 1: slab (A, B, C/P, S) -> pencil (A, B/P, C, S); dir 2: back.
+  // comps: 1 real, 2 complex (x, y device pointers, N/P entries each)
+  void repartition(int dir, long long A, long long B, long long C, long long S, int comps,
+                   const double* x, double* y) {
+    detail::check(kp_comm_repartition(detail::ctx(), c_, dir, A, B, C, S, comps, x, y));
+  }
+  // left <- last plane of rank-1, right <- first plane of rank+1 (count doubles)
+  void halo(const double* first, const double* last, long long count, double* left,
+            double* right) {
+    detail::check(kp_comm_halo_f64(detail::ctx(), c_, first, last, count, left, right));
+  }
+  kp_comm* handle() const { return c_; }
+
+ private:
+  kp_comm* c_ = nullptr;
+  int P_ = 1, rank_ = 0;
+};
 
 }  // namespace kronphi

@@ -80,6 +80,17 @@ _SIGS = {
     "kp_ipc_get_handle": (_I, [_VP, _VP]),
     "kp_ipc_open_handle": (_I, [_VP, C.POINTER(_VP)]),
     "kp_ipc_close_handle": (_I, [_VP]),
+    "kp_comm_unique_id": (_I, [_VP]),
+    "kp_comm_create": (_I, [_CTX, _I, _I, _VP, C.POINTER(_VP)]),
+    "kp_comm_destroy": (_I, [_VP]),
+    "kp_comm_alltoall_f64": (_I, [_CTX, _VP, _VP, _VP, C.c_longlong]),
+    "kp_comm_repartition": (_I, [_CTX, _VP, _I, C.c_longlong, C.c_longlong, C.c_longlong,
+                                 C.c_longlong, _I, _VP, _VP]),
+    "kp_repartition_pack": (_I, [_CTX, _I, _I, _I, C.c_longlong, C.c_longlong, C.c_longlong,
+                                 C.c_longlong, _I, _VP, _VP]),
+    "kp_repartition_unpack": (_I, [_CTX, _I, _I, _I, C.c_longlong, C.c_longlong, C.c_longlong,
+                                   C.c_longlong, _I, _VP, _VP]),
+    "kp_comm_halo_f64": (_I, [_CTX, _VP, _VP, _VP, C.c_longlong, _VP, _VP]),
     "kp_free": (_I, [_CTX, _VP]),
     "kp_upload": (_I, [_CTX, _VP, _VP, _SZ]),
     "kp_download": (_I, [_CTX, _VP, _VP, _SZ]),

@@ -68,6 +68,8 @@ class Layout:
 def slab_to_pencil(x, lay: Layout, comm):
     """x: flat local slab (A, B, C/P... as column-major (A, B, Cl, S)) ->
     flat local pencil (A, B/P, C, S)."""
+    if hasattr(comm, "repartition"):  # native: pack -> NCCL -> unpack (comm.cu)
+        return comm.repartition(x, lay, 1)
     A, B, C, S, P = lay.A, lay.B, lay.C, lay.S, lay.P
     Cl, Bp = C // P, B // P
     send = x.view(S, Cl, P, Bp, A).permute(2, 0, 1, 3, 4).contiguous().view(-1)
@@ -77,6 +79,8 @@ def slab_to_pencil(x, lay: Layout, comm):
 
 
 def pencil_to_slab(y, lay: Layout, comm):
+    if hasattr(comm, "repartition"):
+        return comm.repartition(y, lay, 2)
     A, B, C, S, P = lay.A, lay.B, lay.C, lay.S, lay.P
     Cl, Bp = C // P, B // P
     send = y.view(S, P, Cl, Bp, A).permute(1, 0, 2, 3, 4).contiguous().view(-1)
@@ -136,6 +140,60 @@ class Comm:
                dist.P2POp(dist.irecv, view(right), g(nxt), self.group, 1)]
         for w in dist.batch_isend_irecv(ops):
             w.wait()
+
+
+class NcclComm:
+    """The C ABI's own NCCL communicator (kp_comm_*, comm.cu): created from an
+    ncclUniqueId that rank 0 generates and torch.distributed broadcasts (any
+    side channel would do -- this is how a C++ host without Python runs the
+    sharded path).  Re-partitions run as pack -> grouped ncclSend/Recv ->
+    unpack on the context's stream, halos as grouped send/recv."""
+
+    def __init__(self, backend, group=None):
+        import ctypes as C
+        self.be = backend
+        self.lib, self.ctx = backend.ctx.lib, backend.ctx
+        self.group = group
+        self.P = dist.get_world_size(group) if dist and dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist and dist.is_initialized() else 0
+        uid = (C.c_char * 128)()
+        if self.rank == 0:
+            backend.check(self.lib.kp_comm_unique_id(uid))
+        if self.P > 1:
+            obj = [bytes(uid)]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(obj, src=src, group=group)
+            C.memmove(uid, obj[0], 128)
+        h = C.c_void_p()
+        backend.check(self.lib.kp_comm_create(self.ctx.h, self.P, self.rank, uid, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.be.check(self.lib.kp_comm_destroy(self.h))
+            self.h = None
+
+    def all_to_all(self, recv, send):
+        self.be._sync_stream()
+        n = send.numel() * (2 if torch.is_complex(send) else 1)
+        self.be.check(self.lib.kp_comm_alltoall_f64(self.ctx.h, self.h, send.data_ptr(),
+                                                    recv.data_ptr(), n // self.P))
+
+    def repartition(self, x, lay: Layout, direction):
+        self.be._sync_stream()
+        comps = 2 if torch.is_complex(x) else 1
+        y = torch.empty_like(x)
+        self.be.check(self.lib.kp_comm_repartition(self.ctx.h, self.h, direction, lay.A, lay.B,
+                                                   lay.C, lay.S, comps, x.data_ptr(),
+                                                   y.data_ptr()))
+        return y
+
+    def exchange_halos(self, first, last, left, right):
+        self.be._sync_stream()
+        n = first.numel() * (2 if torch.is_complex(first) else 1)
+        self.be.check(self.lib.kp_comm_halo_f64(self.ctx.h, self.h, first.data_ptr(),
+                                                last.data_ptr(), n, left.data_ptr(),
+                                                right.data_ptr()))
 
 
 class LocalComm:

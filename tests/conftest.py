@@ -46,3 +46,24 @@ def rel2(a, b):
 
 def rng(seed):
     return np.random.default_rng(seed)
+
+
+def run_torchrun(script, args, nproc=2, env=None, timeout=600):
+    """torch.distributed.run on 127.0.0.1 with a fresh port; retried when the
+    rendezvous port was taken between probing and binding (EADDRINUSE)."""
+    import socket
+    import subprocess
+    for _ in range(4):
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={nproc}", "--master-addr", "127.0.0.1", "--master-port",
+               str(port), script, *args]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env)
+        out = r.stdout + r.stderr
+        if r.returncode != 0 and "EADDRINUSE" in out:
+            continue
+        return r.returncode, out
+    return r.returncode, out

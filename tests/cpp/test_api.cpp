@@ -5,6 +5,7 @@
 // test_matrix_functions.cpp, test_split_phi.cpp, test_integrators.cpp.
 #include <cmath>
 #include <cstdio>
+#include <vector>
 #include <random>
 #include <string>
 
@@ -200,6 +201,24 @@ int main() {
       err[k] = diff_norm_inf(r.final, ex) / ex.norm_inf();
     }
     CHECK(err[0] < 5e-3 && err[1] < err[0] / 3.0 && err[1] > err[0] / 5.0);
+  }
+  {  // the native NCCL communicator at world size 1: the re-partition is the
+     // identity and the halos wrap onto the rank itself
+    Communicator comm(1, 0, Communicator::unique_id());
+    const long long A = 3, B = 4, C = 2, S = 2, n = A * B * C * S;
+    std::vector<double> h(n);
+    for (long long i = 0; i < n; ++i) h[i] = 0.5 * double(i) - 3.0;
+    detail::DevBuf x(h.data(), n * sizeof(double)), y(n * sizeof(double));
+    comm.repartition(1, A, B, C, S, 1, x.d(), y.d());
+    std::vector<double> got(n);
+    y.download(got.data());
+    CHECK(got == h);
+    detail::DevBuf left(4 * sizeof(double)), right(4 * sizeof(double));
+    comm.halo(x.d(), x.d() + 4, 4, left.d(), right.d());
+    std::vector<double> l(4), r(4);
+    left.download(l.data());
+    right.download(r.data());
+    CHECK(l[0] == h[4] && l[3] == h[7] && r[0] == h[0] && r[3] == h[3]);
   }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
