@@ -27,6 +27,7 @@
 
 #include "kp_g.cuh"
 #include "kp_internal.h"
+#include "kp_launch.cuh"
 
 namespace kp {
 namespace {
@@ -321,6 +322,7 @@ template <bool CPLX, bool PAIR, bool M3>
 __global__ void __launch_bounds__(256, (CPLX || PAIR) ? 2 : 3)
     kronsum_band2_kernel(BandArgs b, int nz, int zchunk, const double* __restrict__ u,
                          double* __restrict__ r, bool with_g, kp_gfun g, double t) {
+  pdl_wait();
   using T = typename std::conditional<CPLX, double2, double>::type;
   __shared__ BandRow<CPLX> rows2[ZMAX];
   const T* __restrict__ ut = reinterpret_cast<const T*>(u);
@@ -575,7 +577,8 @@ void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<i
     if (ext > 0x7fffffffLL) throw invalid_argument("kronsum: tensor too large for the stencil path");
     const bool m3 = b2.active[3] != 0;
     auto go = [&](auto kern) {
-      kern<<<grid, dim3(32, 8), 0, ctx->stream>>>(b2, nz, zchunk, u, r, with_g, g, t);
+      launch_pdl(ctx, kern, grid, dim3(32, 8), 0, b2, nz, zchunk, u, r, with_g, g, t);
+      ctx->launches--;  // counted once below
     };
     if (cplx) {
       m3 ? go(kronsum_band2_kernel<true, false, true>) : go(kronsum_band2_kernel<true, false, false>);

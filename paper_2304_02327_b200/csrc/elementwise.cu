@@ -10,6 +10,7 @@
 
 #include "kp_g.cuh"
 #include "kp_internal.h"
+#include "kp_launch.cuh"
 
 namespace kp {
 namespace {
@@ -23,6 +24,7 @@ unsigned grid_for(kp_ctx* ctx, size_t n_vec, int threads) {
 // z = fma(b, y, a_is_one ? x : a*x)  -- covers axpy (z=y) and add_scaled.
 __global__ void fma_kernel(size_t n, double b, const double* __restrict__ y,
                            const double* __restrict__ x, double* __restrict__ z) {
+  pdl_wait();
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
     z[i] = __fma_rn(b, y[i], x[i]);
@@ -37,6 +39,7 @@ __global__ void scale_kernel(size_t n, double a, const double* __restrict__ x,
 
 __global__ void g_real_kernel(kp_gfun g, double t, size_t n, size_t half,
                               const double* __restrict__ u, double* __restrict__ out) {
+  pdl_wait();
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const bool second = half > 0 && i >= half;
@@ -47,6 +50,7 @@ __global__ void g_real_kernel(kp_gfun g, double t, size_t n, size_t half,
 
 __global__ void g_cplx_kernel(kp_gfun g, size_t n, const double2* __restrict__ u,
                               double2* __restrict__ out) {
+  pdl_wait();
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
     out[i] = g_cplx(g, u[i]);
@@ -62,6 +66,7 @@ __global__ void finite_kernel(size_t n, const double* __restrict__ x, int* flag)
 
 __global__ void finite_flag_kernel(size_t n, const double* __restrict__ x, int* bad,
                                    const int* ctr) {
+  pdl_wait();
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   bool ok = true;
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
@@ -91,8 +96,7 @@ __global__ void dmma_peak_kernel(double* out, int iters) {
 
 void launch_fma(kp_ctx* ctx, size_t n, double b, const double* y, const double* x, double* z) {
   if (n == 0) return;
-  fma_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(n, b, y, x, z);
-  ctx->launches++;
+  launch_pdl(ctx, fma_kernel, dim3(grid_for(ctx, n, 256)), dim3(256), 0, n, b, y, x, z);
   KP_CUDA(cudaGetLastError());
 }
 
@@ -107,18 +111,17 @@ void launch_eval_g(kp_ctx* ctx, const kp_gfun& g, double t, const double* u, siz
                    size_t half, bool cplx, double* out) {
   if (n == 0) return;
   if (cplx)
-    g_cplx_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(
-        g, n, reinterpret_cast<const double2*>(u), reinterpret_cast<double2*>(out));
+    launch_pdl(ctx, g_cplx_kernel, dim3(grid_for(ctx, n, 256)), dim3(256), 0, g, n,
+               reinterpret_cast<const double2*>(u), reinterpret_cast<double2*>(out));
   else
-    g_real_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(g, t, n, half, u, out);
-  ctx->launches++;
+    launch_pdl(ctx, g_real_kernel, dim3(grid_for(ctx, n, 256)), dim3(256), 0, g, t, n, half, u,
+               out);
   KP_CUDA(cudaGetLastError());
 }
 
 void finite_flag(kp_ctx* ctx, size_t n, const double* x, int* bad, const int* ctr) {
   if (n == 0) return;
-  finite_flag_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(n, x, bad, ctr);
-  ctx->launches++;
+  launch_pdl(ctx, finite_flag_kernel, dim3(grid_for(ctx, n, 256)), dim3(256), 0, n, x, bad, ctr);
   KP_CUDA(cudaGetLastError());
 }
 

@@ -21,6 +21,7 @@
 #include <string>
 
 #include "kp_epilogue.cuh"
+#include "kp_launch.cuh"
 
 namespace kp {
 namespace {
@@ -59,6 +60,7 @@ __global__ void __launch_bounds__(F01<N>::NT, 1)
     fused01_kernel(const double* __restrict__ V, const double* __restrict__ M1,
                    const double* __restrict__ M2, double alpha0, Epilogue e,
                    double* __restrict__ out) {
+  pdl_wait();
   using C = F01<N>;
   extern __shared__ __align__(16) double smem[];
   double* Ts = smem;
@@ -210,6 +212,7 @@ __global__ void __launch_bounds__(F01R<N, MR>::NT, 2)
     fused01r_kernel(const double* __restrict__ V, const double* __restrict__ M1,
                     const double* __restrict__ M2, double alpha0, Epilogue e,
                     double* __restrict__ out) {
+  pdl_wait();
   using C = F01R<N, MR>;
   extern __shared__ __align__(16) double smem[];
   double* Th = smem;                 // T block: T(i, c) at i + c * LDT, i < MR
@@ -314,6 +317,7 @@ __global__ void __launch_bounds__(F01R<N, MR>::NT, 2)
       }
     }
   }
+  pdl_trigger();  // the next kernel may start its prologue during our epilogue
   cp_wait<0>();
   __syncthreads();  // mode-1 reads of Th done: stage the W block there
 #pragma unroll
@@ -352,8 +356,7 @@ void launch_fused01r(kp_ctx* ctx, const double* in, long long Q, const double* m
   }
   const long long grid = Q * C::R;
   if (grid > 0x7fffffffLL) throw invalid_argument("fused01: too many slices");
-  kern<<<unsigned(grid), C::NT, C::SMEM, ctx->stream>>>(in, m1, m2, alpha0, e, out);
-  ctx->launches++;
+  launch_pdl(ctx, kern, dim3(unsigned(grid)), dim3(C::NT), C::SMEM, in, m1, m2, alpha0, e, out);
   KP_CUDA(cudaGetLastError());
 }
 
@@ -367,8 +370,8 @@ void launch_fused01(kp_ctx* ctx, const double* in, long long Q, const double* m1
                                  int(F01<N>::SMEM)));
     attr = true;
   }
-  kern<<<unsigned(Q), F01<N>::NT, F01<N>::SMEM, ctx->stream>>>(in, m1, m2, alpha0, e, out);
-  ctx->launches++;
+  launch_pdl(ctx, kern, dim3(unsigned(Q)), dim3(F01<N>::NT), F01<N>::SMEM, in, m1, m2, alpha0, e,
+             out);
   KP_CUDA(cudaGetLastError());
 }
 

@@ -12,6 +12,7 @@
 #include "cutlass/gemm/threadblock/default_mma.h"
 
 #include "kp_epilogue.cuh"
+#include "kp_launch.cuh"
 
 namespace kp {
 namespace {
@@ -32,17 +33,27 @@ constexpr int kStages = 3;
 struct Big {
   using TB = cutlass::gemm::GemmShape<64, 128, 16>;
   using Warp = cutlass::gemm::GemmShape<32, 64, 16>;
+  static constexpr int kMinBlocks = 2;
 };
 // short M (M <= 64, e.g. the block rows of the LU solves): 128 x 64 tiles of
 // C' (64 rows of C), 4 warps of 64 x 32
 struct Narrow {
   using TB = cutlass::gemm::GemmShape<128, 64, 16>;
   using Warp = cutlass::gemm::GemmShape<64, 32, 16>;
+  static constexpr int kMinBlocks = 2;
 };
 // small problems (fewer 64 x 128 tiles than SMs): 32 x 32 tiles, 4 warps of 16 x 16
 struct Small {
   using TB = cutlass::gemm::GemmShape<32, 32, 16>;
   using Warp = cutlass::gemm::GemmShape<16, 16, 16>;
+  static constexpr int kMinBlocks = 2;
+};
+// short-K problems (K <= 256): 64 x 64 tiles, 4 warps of 32 x 32, 4 CTAs/SM --
+// one CTA's epilogue overlaps three others' mainloops
+struct Medium {
+  using TB = cutlass::gemm::GemmShape<64, 64, 16>;
+  using Warp = cutlass::gemm::GemmShape<32, 32, 16>;
+  static constexpr int kMinBlocks = 4;
 };
 template <bool B_KCONTIG, typename CFG>
 using MmaOf = typename cutlass::gemm::threadblock::DefaultMma<
@@ -56,11 +67,12 @@ using MmaOf = typename cutlass::gemm::threadblock::DefaultMma<
 }  // namespace cg_dmma
 
 template <bool B_KCONTIG, bool SCAT, typename CFG, int CPLX>
-__global__ void __launch_bounds__(128, 2)
+__global__ void __launch_bounds__(128, CFG::kMinBlocks)
     cutlass_dmma_kernel(GemmProblem p, Epilogue e,
                         typename cg_dmma::MmaOf<B_KCONTIG, CFG>::IteratorA::Params pa,
                         typename cg_dmma::MmaOf<B_KCONTIG, CFG>::IteratorB::Params pb, int tiles_m2,
                         int tiles_n2, int n_fastest, int c_vec2, long long species_half) {
+  pdl_wait();
   using Mma = cg_dmma::MmaOf<B_KCONTIG, CFG>;
   using TBShape = typename CFG::TB;
   using WarpShape = typename CFG::Warp;
@@ -91,6 +103,7 @@ __global__ void __launch_bounds__(128, 2)
   acc.clear();
   const int kiters = (p.K + TBShape::kK - 1) / TBShape::kK;
   mma(kiters, acc, it_a, it_b, acc);
+  pdl_trigger();  // the next kernel may start its prologue during our epilogue
 
   // epilogue, staged through shared memory: the fragment element
   // D[(mi + ni * kRow) * 2 + i] is C'(row' = 8 mi + g, col' = 8 ni + 2 tig + i) of
@@ -214,9 +227,8 @@ void launch_cutlass(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, long l
                       (e.D == nullptr || (reinterpret_cast<uintptr_t>(e.D) % 16) == 0))
                          ? 1
                          : 0;
-  kern<<<unsigned(total), 128, smem, ctx->stream>>>(p, e, pa, pb, tiles_m2, tiles_n2, n_fastest,
-                                                    c_vec2, half);
-  ctx->launches++;
+  launch_pdl(ctx, kern, dim3(unsigned(total)), dim3(128), size_t(smem), p, e, pa, pb, tiles_m2,
+             tiles_n2, n_fastest, c_vec2, half);
   KP_CUDA(cudaGetLastError());
 }
 
@@ -226,7 +238,7 @@ void launch_cutlass(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, long l
 template <bool B_KCONTIG, bool SCAT, int CPLX = 0>
 void launch_cutlass_any(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, long long half) {
   const long long big_tiles = (long long)((p.N + 63) / 64) * ((p.M + 127) / 128) * p.batch;
-  static const int forced = [] {  // benchmarking override: 1 small, 2 big
+  static const int forced = [] {  // benchmarking override: 1 small, 2 big, 3 medium
     const char* v = getenv("KP_CUTLASS_TILE");
     return v ? atoi(v) : 0;
   }();
@@ -234,6 +246,10 @@ void launch_cutlass_any(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, lo
   // short-K work (n = 128 cubes: 20.4 vs 17.1 TFLOP/s; n = 256: 29.3 vs 30.4)
   const bool small = big_tiles < ctx->num_sms || (big_tiles < 8LL * ctx->num_sms && p.K <= 256);
   const long long narrow_tiles = (long long)((p.N + 127) / 128) * ((p.M + 63) / 64) * p.batch;
+  if (forced == 3) {  // benchmarking override: 64 x 64 tiles, 4 CTAs/SM
+    launch_cutlass<B_KCONTIG, SCAT, cg_dmma::Medium, CPLX>(ctx, p, e, half);
+    return;
+  }
   if (forced == 1 || (forced != 2 && small && !(p.M <= 64 && narrow_tiles >= ctx->num_sms)))
     launch_cutlass<B_KCONTIG, SCAT, cg_dmma::Small, CPLX>(ctx, p, e, half);
   else if (p.M <= 64 && forced != 2)

@@ -31,6 +31,7 @@
 
 #include "kp_g.cuh"
 #include "kp_internal.h"
+#include "kp_launch.cuh"
 
 namespace kp {
 
@@ -80,6 +81,7 @@ __global__ void lawson_pre_kernel(kp_gfun g, double t, long long n, long long ha
                                   bool two,
                                   const typename Elt<CPLX>::T* __restrict__ u,
                                   typename Elt<CPLX>::T* __restrict__ w) {
+  pdl_wait();
   using E = Elt<CPLX>;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -95,6 +97,7 @@ __global__ void lawson2b_post_kernel(kp_gfun g, double t2, long long n, long lon
                                      const typename Elt<CPLX>::T* __restrict__ y,
                                      typename Elt<CPLX>::T* __restrict__ out, int* bad,
                                      const int* ctr) {
+  pdl_wait();
   using E = Elt<CPLX>;
   bool nf = false;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -112,6 +115,7 @@ __global__ void gdiff_kernel(kp_gfun g, double t, double t2, long long n, long l
                              const typename Elt<CPLX>::T* __restrict__ s,
                              const typename Elt<CPLX>::T* __restrict__ u,
                              typename Elt<CPLX>::T* __restrict__ d) {
+  pdl_wait();
   using E = Elt<CPLX>;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
@@ -124,6 +128,7 @@ __global__ void gdiff_kernel(kp_gfun g, double t, double t2, long long n, long l
 // arithmetic per entry.
 __global__ void lawson_pre_pair_kernel(kp_gfun g, double t, long long half, double tau, bool two,
                                        const double* __restrict__ u, double* __restrict__ w) {
+  pdl_wait();
   const long long n = 2 * half;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < half;
        i += (long long)gridDim.x * blockDim.x) {
@@ -141,6 +146,7 @@ __global__ void lawson_pre_pair_kernel(kp_gfun g, double t, long long half, doub
 __global__ void lawson2b_post_pair_kernel(kp_gfun g, double t2, long long half, double tau,
                                           const double* __restrict__ y, double* __restrict__ out,
                                           int* bad, const int* ctr) {
+  pdl_wait();
   const long long n = 2 * half;
   bool nf = false;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < half;
@@ -158,6 +164,7 @@ __global__ void lawson2b_post_pair_kernel(kp_gfun g, double t2, long long half, 
 __global__ void gdiff_pair_kernel(kp_gfun g, double t, double t2, long long half,
                                   const double* __restrict__ s, const double* __restrict__ u,
                                   double* __restrict__ d) {
+  pdl_wait();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < half;
        i += (long long)gridDim.x * blockDim.x) {
     const double sa = s[i], sb = s[i + half], ua = u[i], ub = u[i + half];
@@ -166,7 +173,10 @@ __global__ void gdiff_pair_kernel(kp_gfun g, double t, double t2, long long half
   }
 }
 
-__global__ void tick_kernel(int* ctr) { *ctr += 1; }
+__global__ void tick_kernel(int* ctr) {
+  pdl_wait();
+  *ctr += 1;
+}
 
 __global__ void scale_matrix_kernel(const double* __restrict__ a, long long n, double s,
                                     double* __restrict__ out) {
@@ -451,39 +461,36 @@ class Integrator {
   void launch_pre(const double* u, double* w, bool two, double t) {
     using T = typename Elt<C>::T;
     if (!C && half > 0) {
-      lawson_pre_pair_kernel<<<grid_ew(ctx, half), 256, 0, ctx->stream>>>(g, t, half, tau, two, u, w);
-      ctx->launches++;
+      launch_pdl(ctx, lawson_pre_pair_kernel, dim3(grid_ew(ctx, half)), dim3(256), 0, g, t, half,
+                 tau, two, u, w);
       return;
     }
-    lawson_pre_kernel<C><<<grid_ew(ctx, n_entries), 256, 0, ctx->stream>>>(
-        g, t, n_entries, half, tau, two, reinterpret_cast<const T*>(u), reinterpret_cast<T*>(w));
-    ctx->launches++;
+    launch_pdl(ctx, lawson_pre_kernel<C>, dim3(grid_ew(ctx, n_entries)), dim3(256), 0, g, t,
+               n_entries, half, tau, two, reinterpret_cast<const T*>(u), reinterpret_cast<T*>(w));
   }
   template <bool C>
   void launch_post(const double* y, double* out, int* bad, const int* ctr, double t2) {
     using T = typename Elt<C>::T;
     if (!C && half > 0) {
-      lawson2b_post_pair_kernel<<<grid_ew(ctx, half), 256, 0, ctx->stream>>>(g, t2, half, tau, y,
-                                                                             out, bad, ctr);
-      ctx->launches++;
+      launch_pdl(ctx, lawson2b_post_pair_kernel, dim3(grid_ew(ctx, half)), dim3(256), 0, g, t2,
+                 half, tau, y, out, bad, ctr);
       return;
     }
-    lawson2b_post_kernel<C><<<grid_ew(ctx, n_entries), 256, 0, ctx->stream>>>(
-        g, t2, n_entries, half, tau, reinterpret_cast<const T*>(y), reinterpret_cast<T*>(out), bad, ctr);
-    ctx->launches++;
+    launch_pdl(ctx, lawson2b_post_kernel<C>, dim3(grid_ew(ctx, n_entries)), dim3(256), 0, g, t2,
+               n_entries, half, tau, reinterpret_cast<const T*>(y), reinterpret_cast<T*>(out), bad,
+               ctr);
   }
   template <bool C>
   void launch_gdiff(const double* s, const double* u, double* dd, double t) {
     using T = typename Elt<C>::T;
     if (!C && half > 0) {
-      gdiff_pair_kernel<<<grid_ew(ctx, half), 256, 0, ctx->stream>>>(g, t, t + tau, half, s, u, dd);
-      ctx->launches++;
+      launch_pdl(ctx, gdiff_pair_kernel, dim3(grid_ew(ctx, half)), dim3(256), 0, g, t, t + tau,
+                 half, s, u, dd);
       return;
     }
-    gdiff_kernel<C><<<grid_ew(ctx, n_entries), 256, 0, ctx->stream>>>(
-        g, t, t + tau, n_entries, half, reinterpret_cast<const T*>(s), reinterpret_cast<const T*>(u),
-        reinterpret_cast<T*>(dd));
-    ctx->launches++;
+    launch_pdl(ctx, gdiff_kernel<C>, dim3(grid_ew(ctx, n_entries)), dim3(256), 0, g, t, t + tau,
+               n_entries, half, reinterpret_cast<const T*>(s), reinterpret_cast<const T*>(u),
+               reinterpret_cast<T*>(dd));
   }
 
   // One step u -> out (out != u).  bad/ctr: divergence tracking (may be null).
@@ -749,8 +756,7 @@ class Integrator {
     g.tau = tau;
     auto one = [&](long k) {
       step(ub[k & 1], ub[(k + 1) & 1], 0.0, bad, ctr);
-      tick_kernel<<<1, 1, 0, ctx->stream>>>(ctr);
-      ctx->launches++;
+      launch_pdl(ctx, tick_kernel, dim3(1), dim3(1), 0, ctr);
     };
     // first step eagerly: sizes every workspace slot before any capture
     KP_CUDA(cudaEventRecord(ev[0], ctx->stream));
@@ -765,11 +771,11 @@ class Integrator {
       // two steps: ub1 -> ub0 -> ub1 (n is odd here); t is unused by the
       // closed set of g's (all autonomous), so replays stay exact
       step(ub[1], ub[0], 0.0, bad, ctr);
-      tick_kernel<<<1, 1, 0, ctx->stream>>>(ctr);
+      launch_pdl(ctx, tick_kernel, dim3(1), dim3(1), 0, ctr);
       step(ub[0], ub[1], 0.0, bad, ctr);
-      tick_kernel<<<1, 1, 0, ctx->stream>>>(ctr);
+      launch_pdl(ctx, tick_kernel, dim3(1), dim3(1), 0, ctr);
       KP_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
-      per = ctx->launches - l0 + 2;
+      per = ctx->launches - l0;
       ctx->launches = l0;
       KP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
       cudaGraphDestroy(graph);
