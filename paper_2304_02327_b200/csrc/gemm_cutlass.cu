@@ -21,11 +21,13 @@ namespace {
 // Real GEMMs on CUTLASS's sm80 multistage DMMA mainloop (the header-only
 // threadblock templates, instantiated inside our own kernel) with our
 // epilogues.  The column-major C = A B is computed as the row-major
-// C' = C^T = B^T A^T: A' = B^T (N x K), B' = A^T (K x M).  Tile 64 x 128 of
-// C' (= 128 rows x 64 columns of C), 4 warps of 32 x 64, BK = 16, 3 stages
-// -- the configuration cuBLAS selects for DGEMM on this part.  Every real
-// mode product and every GEMM of the phi builder use this one configuration,
-// so results are reproducible across code paths.
+// C' = C^T = B^T A^T: A' = B^T (N x K), B' = A^T (K x M).  Tile menu (all
+// BK = 16, 3 stages, 4 warps): 64 x 64 at 4 CTAs/SM for K <= 1024 (the
+// cubes), 64 x 128 of C' with 32 x 64 warp tiles at 2 CTAs/SM for longer K
+// (the configuration cuBLAS selects for DGEMM on this part), 128 x 64 for
+// short M and 32 x 32 when the grid would not fill the SMs.  Every
+// accumulator sums k in the same order in all of them (BK slices in order,
+// DMMA k-groups of four in order), so the tile choice never changes a bit.
 namespace cg_dmma {
 using InstShape = cutlass::gemm::GemmShape<8, 8, 4>;
 constexpr int kStages = 3;
@@ -254,6 +256,12 @@ void launch_cutlass_any(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, lo
     launch_cutlass<B_KCONTIG, SCAT, cg_dmma::Small, CPLX>(ctx, p, e, half);
   else if (p.M <= 64 && forced != 2)
     launch_cutlass<B_KCONTIG, SCAT, cg_dmma::Narrow, CPLX>(ctx, p, e, half);
+  else if (forced != 2 && p.K <= 1024)
+    // K <= 1024 (every cube of the sweep and the integrators): 64 x 64 tiles
+    // at 4 CTAs/SM hide each CTA's prologue / epilogue behind three
+    // mainloops: n=256 Tucker 30.6 -> 31.9 TFLOP/s, Brusselator ETD2RK
+    // 247 -> 272 steps/s, n=512 34.4 -> 34.6 (tools/tucker_sweep.py A/B)
+    launch_cutlass<B_KCONTIG, SCAT, cg_dmma::Medium, CPLX>(ctx, p, e, half);
   else
     launch_cutlass<B_KCONTIG, SCAT, cg_dmma::Big, CPLX>(ctx, p, e, half);
 }
