@@ -388,10 +388,31 @@ def run_reference(args, rank, world):
                              "sample": f"{args.steps} full tucker() calls on the n={n} cube"},
             "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+# stdout carries exactly one JSON line: everything else a library prints to
+# fd 1 (NCCL's version banner when NCCL_DEBUG is set, CUDA/torch warnings) is
+# sent to stderr, and the result line goes to the saved original stdout
+_JSON_FD = None
+
+
+def _claim_stdout():
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line):
+    sys.stdout.flush()
+    fd = _JSON_FD if _JSON_FD is not None else 1
+    os.write(fd, (json.dumps(line) + "\n").encode())
 
 
 def main():
+    _claim_stdout()
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -552,7 +573,7 @@ def main():
                                             "137.4 GFLOP per mode-product launch"},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "integrators": integ, "paper_experiments": paper}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist:
         dist.destroy_process_group()
 

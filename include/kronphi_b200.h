@@ -118,6 +118,21 @@ int kp_mode_product_c128(kp_ctx* ctx, const double* t, const int* dims, int d, i
                          const double* m, int rows, int cols, const double* alpha2,
                          const double* beta2, double* out);
 
+/* ETD2RK's stage in the epilogue of the last mode product
+ * (inc/integrators.hpp:157-162): out = fma(gamma, alpha * (t x_mode M), x)
+ * and, when g and d_out are given, d_out = g(t2, out) - g(t1, x) in the same
+ * pass (the coupled Brusselator g as one extra paired pass).  M square
+ * (rows = dims[mode]).  Used by the slab-sharded integrators, whose last mode
+ * runs in the pencil layout; the single-GPU integrate fuses it internally. */
+int kp_mode_product_stage_f64(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
+                              const double* m, int rows, double alpha, const double* x,
+                              double gamma, const kp_gfun* g, double t1, double t2, double* out,
+                              double* d_out);
+int kp_mode_product_stage_c128(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
+                               const double* m, int rows, double alpha, const double* x,
+                               double gamma, const kp_gfun* g, double t1, double t2,
+                               double* out, double* d_out);
+
 /* out = ((prefactor * t) x_1 M_1 x_2 ... x_d M_d).
  * Replaces tucker (inc/mode_product.hpp:101-108) with prefactor = 1 and
  * apply_split_phi (inc/split_phi.hpp:53-62) with prefactor = (l!)^(d-1).
@@ -251,6 +266,10 @@ int kp_eval_g_c128(kp_ctx* ctx, const kp_gfun* g, double t, const double* u, con
                    int d, double* gout);
 /* *all_finite = 1 if every entry is finite (inc/integrators.hpp:101-108) */
 int kp_all_finite_f64(kp_ctx* ctx, size_t n, const double* x, int* all_finite);
+/* Stream-ordered, no host sync: atomicMin(*bad_dev, step) when x (n doubles)
+ * holds a non-finite value -- the per-step finite check of host-driven loops
+ * (inc/integrators.hpp:364), read once after the loop. */
+int kp_mark_nonfinite_f64(kp_ctx* ctx, size_t n, const double* x, int* bad_dev, int step);
 
 /* ---------------- matrix functions (inc/matrix_functions.hpp) ---------------- */
 /* q-point Gauss-Legendre-Lobatto rule on [0,1] (host; src/gll_rule.cpp:35-72) */

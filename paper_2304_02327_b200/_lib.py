@@ -80,6 +80,10 @@ _SIGS = {
     "kp_ipc_get_handle": (_I, [_VP, _VP]),
     "kp_ipc_open_handle": (_I, [_VP, C.POINTER(_VP)]),
     "kp_ipc_close_handle": (_I, [_VP]),
+    "kp_mode_product_stage_f64": (_I, [_CTX, _VP, _PI, _I, _I, _VP, _I, _D, _VP, _D, _VP, _D,
+                                       _D, _VP, _VP]),
+    "kp_mode_product_stage_c128": (_I, [_CTX, _VP, _PI, _I, _I, _VP, _I, _D, _VP, _D, _VP, _D,
+                                        _D, _VP, _VP]),
     "kp_comm_unique_id": (_I, [_VP]),
     "kp_comm_create": (_I, [_CTX, _I, _I, _VP, C.POINTER(_VP)]),
     "kp_comm_destroy": (_I, [_VP]),
@@ -114,6 +118,7 @@ _SIGS = {
     "kp_eval_g_f64": (_I, [_CTX, C.POINTER(GFun), _D, _VP, _PI, _I, _VP]),
     "kp_eval_g_c128": (_I, [_CTX, C.POINTER(GFun), _D, _VP, _PI, _I, _VP]),
     "kp_all_finite_f64": (_I, [_CTX, _SZ, _VP, _PI]),
+    "kp_mark_nonfinite_f64": (_I, [_CTX, _SZ, _VP, _VP, _I]),
     "kp_measure_fp64_peak": (_I, [_CTX, _PD]),
 }
 

@@ -35,27 +35,44 @@ namespace {
 constexpr int KC = 256;  // inc/kernels.hpp:104
 
 // rows of A (n x n, column-major; complex when comps == 2) -> 3 slots per row
+// in increasing column order.  One warp per row: lanes test 32 columns at a
+// time and the ballot hands the nonzeros out in order.  flags[0] |= 1 if a
+// row has more than three nonzeros, flags[1] |= 1 if the factor has any.
 __global__ void band_scan_kernel(const double* __restrict__ a, int n, int comps,
                                  int* __restrict__ cols, double* __restrict__ vals,
-                                 int* __restrict__ too_many) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+                                 int* __restrict__ flags) {
+  const int i = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (i >= n) return;
   int cnt = 0;
-  for (int j = 0; j < n; ++j) {
-    const double re = a[(size_t(i) + size_t(j) * n) * comps];
-    const double im = comps == 2 ? a[(size_t(i) + size_t(j) * n) * comps + 1] : 0.0;
-    if (re != 0.0 || im != 0.0) {
+  bool many = false;
+  for (int j0 = 0; j0 < n && !many; j0 += 32) {
+    const int j = j0 + lane;
+    double re = 0.0, im = 0.0;
+    if (j < n) {
+      re = a[(size_t(i) + size_t(j) * n) * comps];
+      if (comps == 2) im = a[(size_t(i) + size_t(j) * n) * comps + 1];
+    }
+    unsigned m = __ballot_sync(0xffffffffu, re != 0.0 || im != 0.0);
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
       if (cnt == 3) {
-        *too_many = 1;
-        return;
+        many = true;
+        break;
       }
-      cols[i * 3 + cnt] = j;
-      vals[(i * 3 + cnt) * 2] = re;
-      vals[(i * 3 + cnt) * 2 + 1] = im;
+      if (lane == bit) {
+        cols[i * 3 + cnt] = j;
+        vals[(i * 3 + cnt) * 2] = re;
+        vals[(i * 3 + cnt) * 2 + 1] = im;
+      }
       ++cnt;
     }
   }
-  for (; cnt < 3; ++cnt) cols[i * 3 + cnt] = -1;
+  if (lane == 0) {
+    if (many) atomicOr(flags, 1);
+    if (cnt > 0) atomicOr(flags + 1, 1);
+    for (int c = cnt; c < 3 && !many; ++c) cols[i * 3 + c] = -1;
+  }
 }
 
 struct BandArgs {
@@ -438,18 +455,29 @@ void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<i
                     const std::vector<char>& active, double* r, bool with_g, const kp_gfun& g,
                     long long half, int slab, int k0, int n_glob, int halo, double t);
 
-// Scan a factor into caller-provided device arrays (3n ints, 6n doubles);
-// false if some row has more than three nonzeros.
-bool band_scan(kp_ctx* ctx, const double* a, int n, bool cplx, int* dc, double* dv) {
-  int* flag = reinterpret_cast<int*>(ctx->d_flag) + 8;
-  KP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
-  band_scan_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(a, n, cplx ? 2 : 1, dc, dv, flag);
+// Scan a factor into caller-provided device arrays (3n ints, 6n doubles),
+// flags into slot `slot` (< 8) of the context's scratch, no sync;
+// band_flags() then reads every slot back with ONE sync.
+void band_scan_async(kp_ctx* ctx, const double* a, int n, bool cplx, int* dc, double* dv,
+                     int slot) {
+  int* flags = reinterpret_cast<int*>(ctx->d_flag) + 16 + 2 * slot;
+  KP_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), ctx->stream));
+  band_scan_kernel<<<(n + 7) / 8, 256, 0, ctx->stream>>>(a, n, cplx ? 2 : 1, dc, dv, flags);
   ctx->launches++;
   KP_CUDA(cudaGetLastError());
-  KP_CUDA(cudaMemcpyAsync(ctx->h_flag + 8, flag, sizeof(int), cudaMemcpyDeviceToHost,
-                          ctx->stream));
+}
+// (too_many, any_nonzero) of slots 0..nslots-1
+std::vector<std::pair<bool, bool>> band_flags(kp_ctx* ctx, int nslots) {
+  KP_CUDA(cudaMemcpyAsync(ctx->h_flag + 16, reinterpret_cast<int*>(ctx->d_flag) + 16,
+                          2 * nslots * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   KP_CUDA(cudaStreamSynchronize(ctx->stream));
-  return ctx->h_flag[8] == 0;
+  std::vector<std::pair<bool, bool>> f(nslots);
+  for (int k = 0; k < nslots; ++k) f[k] = {ctx->h_flag[16 + 2 * k] != 0, ctx->h_flag[17 + 2 * k] != 0};
+  return f;
+}
+bool band_scan(kp_ctx* ctx, const double* a, int n, bool cplx, int* dc, double* dv) {
+  band_scan_async(ctx, a, n, cplx, dc, dv, 0);
+  return !band_flags(ctx, 1)[0].first;
 }
 
 // Scan a factor into fresh allocations (owned by the caller).
@@ -480,10 +508,12 @@ bool kronsum_try_banded(kp_ctx* ctx, bool cplx, const double* t, const std::vect
   for (int mu = 0; mu < d; ++mu) {
     int* c = static_cast<int*>(ctx->ws.get(30 + mu, sizeof(int) * 3 * size_t(dims[mu])));
     double* v = static_cast<double*>(ctx->ws.get(34 + mu, sizeof(double) * 6 * size_t(dims[mu])));
-    if (!band_scan(ctx, as[mu], dims[mu], cplx, c, v)) return false;
+    band_scan_async(ctx, as[mu], dims[mu], cplx, c, v, mu);
     cols[mu] = c;
     vals[mu] = v;
   }
+  for (const auto& f : band_flags(ctx, d))
+    if (f.first) return false;
   kronsum_banded(ctx, cplx, t, dims, cols, vals, active, out, false, kp_gfun{}, 0, -1, 0, 0, 0,
                  0.0);
   return true;
@@ -622,19 +652,18 @@ int slab_impl(kp_ctx* ctx, bool cplx, const double* u_ext, const int* dims, int 
       const int n = (mu == slab_mode) ? n_glob : dv[mu];
       int* c = static_cast<int*>(ctx->ws.get(30 + mu, sizeof(int) * 3 * size_t(n)));
       double* v = static_cast<double*>(ctx->ws.get(34 + mu, sizeof(double) * 6 * size_t(n)));
-      if (!band_scan(ctx, as[mu], n, cplx, c, v))
-        throw invalid_argument("kronsum_slab: factor " + std::to_string(mu) +
-                               " has more than three nonzeros in a row");
+      band_scan_async(ctx, as[mu], n, cplx, c, v, mu);
       cols[mu] = c;
       vals[mu] = v;
+    }
+    const auto flags = band_flags(ctx, d);  // one sync for every factor
+    for (int mu = 0; mu < d; ++mu) {
+      if (flags[mu].first)
+        throw invalid_argument("kronsum_slab: factor " + std::to_string(mu) +
+                               " has more than three nonzeros in a row");
       // an all-zero factor (the stacked species mode) contributes nothing
-      if (n <= 2) {
-        std::vector<int> hc(3 * size_t(n));
-        KP_CUDA(cudaMemcpy(hc.data(), c, hc.size() * sizeof(int), cudaMemcpyDeviceToHost));
-        bool any = false;
-        for (int x : hc) any |= (x >= 0);
-        active[mu] = any;
-      }
+      const int n = (mu == slab_mode) ? n_glob : dv[mu];
+      if (n <= 2) active[mu] = flags[mu].second;
     }
     long long half = 0;
     if (g && g->kind == KP_G_BRUSSELATOR) half = 1;  // species = last mode

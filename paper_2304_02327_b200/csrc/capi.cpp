@@ -316,6 +316,59 @@ int kp_mode_product_f64(kp_ctx* ctx, const double* t, const int* dims, int d, in
   });
 }
 
+namespace {
+// ETD2RK's stage update in the epilogue of a mode product (see header)
+int mode_product_stage(kp_ctx* ctx, bool cplx, const double* t, const int* dims, int d, int mode,
+                       const double* m, int rows, double alpha, const double* x, double gamma,
+                       const kp_gfun* g, double t1, double t2, double* out, double* d_out) {
+  return guard([&] {
+    need_ctx(ctx);
+    const auto dv = check_dims(dims, d, "mode_product");
+    check_mode(dv, mode, dv[mode]);
+    if (rows != dv[mode]) throw invalid_argument("mode_product_stage: square factor expected");
+    if (!x || out == t || out == x) throw invalid_argument("mode_product_stage: bad buffers");
+    Epilogue e;
+    e.alpha = alpha;
+    e.gamma = gamma;
+    e.X = x;
+    e.kind = EPI_FMA_X;
+    const bool coupled = g && d_out && g->kind == KP_G_BRUSSELATOR;
+    if (coupled && (cplx || dv.back() != 2))
+      throw invalid_argument("brusselator g: slowest mode must hold 2 species");
+    if (g && d_out && !coupled) {
+      e.kind = EPI_STAGE_D;
+      e.D = d_out;
+      e.g = *g;
+      e.t = t1;
+      e.t2 = t2;
+    }
+    if (cplx)
+      mode_product_c128(ctx, t, dv, mode, m, rows, e, out);
+    else
+      mode_product_f64(ctx, t, dv, mode, m, rows, e, out);
+    if (coupled) {
+      const long long n = (long long)numel(dv);
+      gdiff_dev(ctx, *g, t1, t2 - t1, out, x, n, n / 2, false, d_out);
+    }
+  });
+}
+}  // namespace
+
+int kp_mode_product_stage_f64(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
+                              const double* m, int rows, double alpha, const double* x,
+                              double gamma, const kp_gfun* g, double t1, double t2, double* out,
+                              double* d_out) {
+  return mode_product_stage(ctx, false, t, dims, d, mode, m, rows, alpha, x, gamma, g, t1, t2,
+                            out, d_out);
+}
+int kp_mode_product_stage_c128(kp_ctx* ctx, const double* t, const int* dims, int d, int mode,
+                               const double* m, int rows, double alpha, const double* x,
+                               double gamma, const kp_gfun* g, double t1, double t2, double* out,
+                               double* d_out) {
+  return mode_product_stage(ctx, true, t, dims, d, mode, m, rows, alpha, x, gamma, g, t1, t2,
+                            out, d_out);
+}
+
 int kp_tucker_f64(kp_ctx* ctx, const double* t, const int* dims, int d, const double* const* ms,
                   const int* rows, double prefactor, double* out) {
   return guard([&] {
@@ -761,6 +814,14 @@ int kp_all_finite_f64(kp_ctx* ctx, size_t n, const double* x, int* ok) {
   return guard([&] {
     need_ctx(ctx);
     *ok = all_finite(ctx, n, x);
+  });
+}
+
+int kp_mark_nonfinite_f64(kp_ctx* ctx, size_t n, const double* x, int* bad_dev, int step) {
+  return guard([&] {
+    need_ctx(ctx);
+    if (!bad_dev) throw invalid_argument("mark_nonfinite: null flag");
+    finite_mark(ctx, n, x, bad_dev, step);
   });
 }
 

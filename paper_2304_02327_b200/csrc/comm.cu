@@ -292,6 +292,10 @@ int kp_comm_repartition(kp_ctx* ctx, kp_comm* c, int dir, long long A, long long
     long long n = 0;
     const Part p = make_part(dir, c->P, c->rank, A, B, C, S, comps, &n);
     const size_t bytes = size_t(n) * comps * sizeof(double);
+    if (c->P == 1) {  // slab == pencil: the map is the identity
+      if (x != y) KP_CUDA(cudaMemcpyAsync(y, x, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+      return;
+    }
     double* send = static_cast<double*>(ctx->ws.get(SLOT_SEND, bytes));
     double* recv = static_cast<double*>(ctx->ws.get(SLOT_RECV, bytes));
     launch_repartition(ctx, p, dir, true, comps, n, x, send);

@@ -64,6 +64,15 @@ __global__ void finite_kernel(size_t n, const double* __restrict__ x, int* flag)
   if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) *flag = 0;
 }
 
+// atomicMin(bad, step) if x has a non-finite entry (host-driven loops)
+__global__ void finite_mark_kernel(size_t n, const double* __restrict__ x, int* bad, int step) {
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  bool ok = true;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    ok &= isfinite(x[i]);
+  if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicMin(bad, step);
+}
+
 __global__ void finite_flag_kernel(size_t n, const double* __restrict__ x, int* bad,
                                    const int* ctr) {
   pdl_wait();
@@ -122,6 +131,13 @@ void launch_eval_g(kp_ctx* ctx, const kp_gfun& g, double t, const double* u, siz
 void finite_flag(kp_ctx* ctx, size_t n, const double* x, int* bad, const int* ctr) {
   if (n == 0) return;
   launch_pdl(ctx, finite_flag_kernel, dim3(grid_for(ctx, n, 256)), dim3(256), 0, n, x, bad, ctr);
+  KP_CUDA(cudaGetLastError());
+}
+
+void finite_mark(kp_ctx* ctx, size_t n, const double* x, int* bad, int step) {
+  if (n == 0) return;
+  finite_mark_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(n, x, bad, step);
+  ctx->launches++;
   KP_CUDA(cudaGetLastError());
 }
 

@@ -170,6 +170,11 @@ void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<i
                     long long half, int slab = -1, int k0 = 0, int n_glob = 0, int halo = 0,
                     double t = 0.0);
 
+// ---- steppers (stepper.cu) ----
+// d = g(t + tau, s) - g(t, u); half > 0: Brusselator species offset
+void gdiff_dev(kp_ctx* ctx, const kp_gfun& g, double t, double tau, const double* s,
+               const double* u, long long n, long long half, bool cplx, double* dd);
+
 // ---- elementwise (elementwise.cu) ----
 // z = fma(b, y, x): axpy is (b=alpha, y=x, x=y, z=y), add_scaled is (b=alpha, y=y, x=x)
 void launch_fma(kp_ctx* ctx, size_t n, double b, const double* y, const double* x, double* z);
@@ -179,6 +184,8 @@ void launch_eval_g(kp_ctx* ctx, const kp_gfun& g, double t, const double* u, siz
                    size_t half, bool cplx, double* out);
 void launch_scale(kp_ctx* ctx, size_t n, double a, const double* x, double* y);
 int all_finite(kp_ctx* ctx, size_t n, const double* x);
+// atomicMin(*bad, step) if x has a non-finite entry (no host sync)
+void finite_mark(kp_ctx* ctx, size_t n, const double* x, int* bad, int step);
 // device divergence flag: atomicMin(*bad, *ctr + 1) if x has a non-finite entry
 void finite_flag(kp_ctx* ctx, size_t n, const double* x, int* bad, const int* ctr);
 double measure_fp64_peak(kp_ctx* ctx);

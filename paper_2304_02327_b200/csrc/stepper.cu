@@ -193,6 +193,25 @@ enum : int {
 
 }  // namespace
 
+// d = g(t + tau, s) - g(t, u) over n entries (the ETD2RK difference as its own
+// pass, for g's the GEMM epilogue cannot evaluate: the coupled Brusselator).
+void gdiff_dev(kp_ctx* ctx, const kp_gfun& g, double t, double tau, const double* s,
+               const double* u, long long n, long long half, bool cplx, double* dd) {
+  if (n <= 0) return;
+  if (!cplx && half > 0) {
+    launch_pdl(ctx, gdiff_pair_kernel, dim3(grid_ew(ctx, half)), dim3(256), 0, g, t, t + tau,
+               half, s, u, dd);
+  } else if (cplx) {
+    launch_pdl(ctx, gdiff_kernel<true>, dim3(grid_ew(ctx, n)), dim3(256), 0, g, t, t + tau, n,
+               half, reinterpret_cast<const double2*>(s), reinterpret_cast<const double2*>(u),
+               reinterpret_cast<double2*>(dd));
+  } else {
+    launch_pdl(ctx, gdiff_kernel<false>, dim3(grid_ew(ctx, n)), dim3(256), 0, g, t, t + tau, n,
+               half, s, u, dd);
+  }
+  KP_CUDA(cudaGetLastError());
+}
+
 // Per-mode factor list with the scalar-identity folding described above.
 struct FactorSet {
   std::vector<const double*> f;

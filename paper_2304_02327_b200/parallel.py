@@ -425,6 +425,24 @@ class CudaBackend:
                                                m.shape[1], float(alpha), float(beta),
                                                out.data_ptr()))
 
+    def mark_nonfinite(self, x, bad, step):
+        """atomicMin(bad, step) on the device if x has a non-finite entry."""
+        self._sync_stream()
+        n = x.numel() * (2 if torch.is_complex(x) else 1)
+        self.check(self.ctx.lib.kp_mark_nonfinite_f64(self.ctx.h, n, x.data_ptr(),
+                                                      bad.data_ptr(), int(step)))
+
+    def mode_product_stage(self, t, dims, mode, m, alpha, x, gamma, g, out, d_out):
+        """out = fma(gamma, alpha * (t x_mode m), x); d_out = g(out) - g(x) in the
+        same epilogue (kp_mode_product_stage_*)."""
+        import ctypes as C
+        self._sync_stream()
+        f = self.ctx.lib.kp_mode_product_stage_c128 if torch.is_complex(t) else \
+            self.ctx.lib.kp_mode_product_stage_f64
+        self.check(f(self.ctx.h, t.data_ptr(), self.ints(dims), len(dims), mode, m.data_ptr(),
+                     m.shape[0], float(alpha), x.data_ptr(), float(gamma), C.byref(g), 0.0, 0.0,
+                     out.data_ptr(), d_out.data_ptr()))
+
     def eval_g(self, g, u, dims, out):
         import ctypes as C
         self._sync_stream()
@@ -494,7 +512,7 @@ class ShardedIntegrator:
     # y = ((pref x) x_1 F_1 ... x_d F_d) * fold ; x in slab layout, y in pencil
     # layout -- or, with `to_slab_x`, fma(gamma, y, x2) returned in slab layout
     # (the final update of a step, fused into the last GEMM's epilogue)
-    def tucker(self, x, fs, pref, fold, site="t", final=None):
+    def tucker(self, x, fs, pref, fold, site="t", final=None, stage=None):
         d = self.d
         cur, dims = x, self.sd
         for mu in range(d - 1):
@@ -526,6 +544,12 @@ class ShardedIntegrator:
                 self.be.fma(gamma, y, x2, out)
             return pencil_to_slab(out, self.lay, self.comm)
         out = torch.empty_like(cp)
+        if stage is not None:  # (stage, g(stage) - g(x2)), both pencil layout
+            x2, gamma = stage
+            dp = torch.empty_like(cp)
+            self.be.mode_product_stage(cp, self.pd, d - 1, fs[d - 1], alpha, x2, gamma, self.g,
+                                       out, dp)
+            return out, dp
         self.be.mode_product(cp, self.pd, d - 1, fs[d - 1], alpha, 0.0, out)
         return out  # pencil layout
 
@@ -566,13 +590,19 @@ class ShardedIntegrator:
             if m == "exp_euler":  # u + tau*SP1(r), back in slab layout
                 return self.tucker(r, self.f1, self.pref1, self.fold1, "t1",
                                    final=(u_p, tau, "u"))
-            y1 = self.tucker(r, self.f1, self.pref1, self.fold1, "t1")   # pencil
-            stage = torch.empty_like(y1)
-            self.be.fma(tau, y1, u_p, stage)                              # u + tau*SP1(r)
-            gs, gu = torch.empty_like(stage), torch.empty_like(stage)
-            self.be.eval_g(self.g, stage, self.pd, gs)
-            self.be.eval_g(self.g, u_p, self.pd, gu)
-            dd = self.to_slab(gs - gu, "dd")
+            if hasattr(self.be, "mode_product_stage"):
+                # stage = u + tau*SP1(r) and g(stage) - g(u) in the last GEMM's epilogue
+                stage, dp = self.tucker(r, self.f1, self.pref1, self.fold1, "t1",
+                                        stage=(u_p, tau))
+                dd = self.to_slab(dp, "dd")
+            else:
+                y1 = self.tucker(r, self.f1, self.pref1, self.fold1, "t1")   # pencil
+                stage = torch.empty_like(y1)
+                self.be.fma(tau, y1, u_p, stage)                              # u + tau*SP1(r)
+                gs, gu = torch.empty_like(stage), torch.empty_like(stage)
+                self.be.eval_g(self.g, stage, self.pd, gs)
+                self.be.eval_g(self.g, u_p, self.pd, gu)
+                dd = self.to_slab(gs - gu, "dd")
             # stage + tau*SP2(d), back in slab layout
             return self.tucker(dd, self.f2, self.pref2, self.fold2, "t2", final=(stage, tau, "u"))
         if m in ("lawson_euler", "lawson2b"):
@@ -597,17 +627,31 @@ class ShardedIntegrator:
         """n_steps steps; like the single-GPU loop it runs to the end and then
         reports the first non-finite step (DivergenceError(step))."""
         first_bad = 0
-        flag = torch.zeros(1, dtype=torch.float64, device=u.device)
-        for k in range(n_steps):
-            u = self.step(u)
-            if not first_bad:
-                flag.fill_(0.0 if bool(torch.isfinite(u).all()) else float(k + 1))
-                if self.comm.P > 1:
-                    # first bad step over ranks: any rank's nonzero flag, smallest k
-                    vals = torch.where(flag > 0, flag, torch.full_like(flag, 1e300))
-                    dist.all_reduce(vals, op=dist.ReduceOp.MIN)
-                    flag.copy_(torch.where(vals < 1e299, vals, torch.zeros_like(vals)))
-                first_bad = int(flag.item())
+        mark = getattr(self.be, "mark_nonfinite", None)
+        if mark is not None:  # device flag, no host sync per step
+            big = 2 ** 31 - 1
+            bad = torch.full((1,), big, dtype=torch.int32, device=u.device)
+            for k in range(n_steps):
+                u = self.step(u)
+                mark(u, bad, k + 1)
+            if self.comm.P > 1:  # first bad step over ranks
+                vals = bad.to(torch.float64)
+                dist.all_reduce(vals, op=dist.ReduceOp.MIN)
+                bad.copy_(vals.to(torch.int32))
+            b = int(bad.item())
+            first_bad = 0 if b == big else b
+        else:
+            flag = torch.zeros(1, dtype=torch.float64, device=u.device)
+            for k in range(n_steps):
+                u = self.step(u)
+                if not first_bad:
+                    flag.fill_(0.0 if bool(torch.isfinite(u).all()) else float(k + 1))
+                    if self.comm.P > 1:
+                        # first bad step over ranks: any rank's nonzero flag, smallest k
+                        vals = torch.where(flag > 0, flag, torch.full_like(flag, 1e300))
+                        dist.all_reduce(vals, op=dist.ReduceOp.MIN)
+                        flag.copy_(torch.where(vals < 1e299, vals, torch.zeros_like(vals)))
+                    first_bad = int(flag.item())
         if self.fused:
             u = u.clone()  # the result lives in an exchange buffer
         if first_bad:
