@@ -133,6 +133,32 @@ int kp_mode_product_stage_c128(kp_ctx* ctx, const double* t, const int* dims, in
                                double gamma, const kp_gfun* g, double t1, double t2,
                                double* out, double* d_out);
 
+/* C = alpha * A * op(B) + beta * C on device pointers, column-major.
+ * Replaces gemm (inc/kernels.hpp:279-327): A m x k (lda), op(B) k x n with
+ * opb 0 = Op::none (B k x n, ldb) or 1 = Op::transpose (B n x k, ldb), C m x n
+ * (ldc).  _c128: interleaved complex128, alpha2/beta2 = (re, im). */
+int kp_gemm_f64(kp_ctx* ctx, int m, int n, int k, double alpha, const double* a, int lda,
+                const double* b, int ldb, int opb, double beta, double* c, int ldc);
+int kp_gemm_c128(kp_ctx* ctx, int m, int n, int k, const double* alpha2, const double* a,
+                 int lda, const double* b, int ldb, int opb, const double* beta2, double* c,
+                 int ldc);
+/* C_q = alpha * A_q * op(B) + beta * C_q for q < batch, A_q = a + q*a_stride,
+ * C_q = c + q*c_stride (strides in elements).  Replaces gemm_batch_shared_b
+ * (inc/kernels.hpp:332-392). */
+int kp_gemm_batch_shared_b_f64(kp_ctx* ctx, int m, int n, int k, double alpha, const double* a,
+                               int lda, long long a_stride, const double* b, int ldb, int opb,
+                               double beta, double* c, int ldc, long long c_stride, int batch);
+int kp_gemm_batch_shared_b_c128(kp_ctx* ctx, int m, int n, int k, const double* alpha2,
+                                const double* a, int lda, long long a_stride, const double* b,
+                                int ldb, int opb, const double* beta2, double* c, int ldc,
+                                long long c_stride, int batch);
+/* lu_factor (inc/linsolve.hpp:95-117): a (n x n) factored in place (unit
+ * lower L below the diagonal, U on and above), piv = n device ints; a
+ * singular matrix -> KP_ERUNTIME "lu_factor: matrix is singular".
+ * lu_solve (:119-146): b (n x nrhs) overwritten with the solution. */
+int kp_lu_factor_f64(kp_ctx* ctx, double* a, int n, int* piv);
+int kp_lu_solve_f64(kp_ctx* ctx, const double* lu, const int* piv, int n, double* b, int nrhs);
+
 /* out = ((prefactor * t) x_1 M_1 x_2 ... x_d M_d).
  * Replaces tucker (inc/mode_product.hpp:101-108) with prefactor = 1 and
  * apply_split_phi (inc/split_phi.hpp:53-62) with prefactor = (l!)^(d-1).

@@ -468,6 +468,95 @@ Matrix<T> multiply(const Matrix<T>& a, const Matrix<T>& b, Op opb = Op::none, bo
   return Matrix<T>(a.rows(), b.rows(), vec(c));
 }
 
+// ------------------------------------------------------------- GEMM cores
+// gemm / gemm_batch_shared_b (inc/kernels.hpp:279-392) with the reference's
+// host-pointer signatures: operands staged to the device, the DMMA GEMM
+// (kp_gemm_* / kp_gemm_batch_shared_b_*), C downloaded.  double and
+// std::complex<double>; `parallel` is accepted and ignored.
+namespace detail {
+inline size_t span_of(int rows, int cols, int ld) {
+  return (rows <= 0 || cols <= 0) ? 0 : size_t(ld) * size_t(cols - 1) + size_t(rows);
+}
+}  // namespace detail
+
+template <typename T>
+void gemm_batch_shared_b(int m, int n, int k, T alpha, const T* a, int lda, size_t a_stride,
+                         const T* b, int ldb, Op opb, T beta, T* c, int ldc, size_t c_stride,
+                         int batch, bool = true) {
+  using namespace detail;
+  static_assert(std::is_same_v<T, double> || std::is_same_v<T, std::complex<double>>,
+                "gemm: double or std::complex<double>");
+  if (m <= 0 || n <= 0 || batch <= 0) return;
+  const int br = opb == Op::none ? k : n, bc = opb == Op::none ? n : k;
+  const size_t ea = k > 0 ? a_stride * size_t(batch - 1) + span_of(m, k, lda) : 0;
+  const size_t eb = span_of(br, bc, ldb);
+  const size_t ec = c_stride * size_t(batch - 1) + span_of(m, n, ldc);
+  // k == 0: A and B are never read (C = beta C)
+  DevBuf da = ea ? DevBuf(a, bytes_of<T>(ea)) : DevBuf(bytes_of<T>(1));
+  DevBuf db = eb ? DevBuf(b, bytes_of<T>(eb)) : DevBuf(bytes_of<T>(1));
+  DevBuf dc(c, bytes_of<T>(ec));
+  const int op = opb == Op::none ? 0 : 1;
+  if constexpr (std::is_same_v<T, double>) {
+    check(kp_gemm_batch_shared_b_f64(ctx(), m, n, k, alpha, da.d(), lda, (long long)a_stride,
+                                     db.d(), ldb, op, beta, dc.d(), ldc, (long long)c_stride,
+                                     batch));
+  } else {
+    const double al[2] = {alpha.real(), alpha.imag()}, be[2] = {beta.real(), beta.imag()};
+    check(kp_gemm_batch_shared_b_c128(ctx(), m, n, k, al, da.d(), lda, (long long)a_stride,
+                                      db.d(), ldb, op, be, dc.d(), ldc, (long long)c_stride,
+                                      batch));
+  }
+  dc.download(c);
+}
+
+template <typename T>
+void gemm(int m, int n, int k, T alpha, const T* a, int lda, const T* b, int ldb, Op opb, T beta,
+          T* c, int ldc, bool parallel = true) {
+  gemm_batch_shared_b(m, n, k, alpha, a, lda, 0, b, ldb, opb, beta, c, ldc, 0, 1, parallel);
+}
+
+// ------------------------------------------------------ LU (linsolve.hpp)
+// lu_factor / lu_solve / solve (inc/linsolve.hpp:95-151) on the device blocked
+// LU (64-wide panels, partial pivoting, GEMM trailing updates); double.
+template <typename T>
+struct LUFactors {
+  Matrix<T> lu;          // unit-lower L below the diagonal, U on and above
+  std::vector<int> piv;  // step j exchanged rows j and piv[j]
+};
+
+template <typename T>
+LUFactors<T> lu_factor(Matrix<T> a) {
+  using namespace detail;
+  static_assert(std::is_same_v<T, double>, "lu_factor: the B200 path factors double matrices");
+  if (!a.square()) throw std::invalid_argument("lu_factor: matrix not square");
+  const int n = a.rows();
+  LUFactors<T> f{Matrix<T>(n, n), std::vector<int>(size_t(n))};
+  if (n == 0) return f;
+  DevBuf da(a.data(), bytes_of<T>(a.size())), dp(sizeof(int) * size_t(n));
+  check(kp_lu_factor_f64(ctx(), da.d(), n, static_cast<int*>(dp.p)));
+  da.download(f.lu.data());
+  dp.download(f.piv.data());
+  return f;
+}
+
+template <typename T>
+Matrix<T> lu_solve(const LUFactors<T>& f, Matrix<T> b) {
+  using namespace detail;
+  const int n = f.lu.rows();
+  if (b.rows() != n) throw std::invalid_argument("lu_solve: RHS row mismatch");
+  if (n == 0 || b.cols() == 0) return b;
+  DevBuf dl(f.lu.data(), bytes_of<T>(f.lu.size())), dp(f.piv.data(), sizeof(int) * size_t(n));
+  DevBuf db(b.data(), bytes_of<T>(b.size()));
+  check(kp_lu_solve_f64(ctx(), dl.d(), static_cast<const int*>(dp.p), n, db.d(), b.cols()));
+  db.download(b.data());
+  return b;
+}
+
+template <typename T>
+Matrix<T> solve(const Matrix<T>& a, Matrix<T> b) {
+  return lu_solve(lu_factor(a), std::move(b));
+}
+
 // ------------------------------------------------------- matrix functions
 
 inline constexpr int kDefaultQuadNodes = 12;

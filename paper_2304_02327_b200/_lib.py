@@ -84,6 +84,14 @@ _SIGS = {
                                        _D, _VP, _VP]),
     "kp_mode_product_stage_c128": (_I, [_CTX, _VP, _PI, _I, _I, _VP, _I, _D, _VP, _D, _VP, _D,
                                         _D, _VP, _VP]),
+    "kp_gemm_f64": (_I, [_CTX, _I, _I, _I, _D, _VP, _I, _VP, _I, _I, _D, _VP, _I]),
+    "kp_gemm_c128": (_I, [_CTX, _I, _I, _I, _VP, _VP, _I, _VP, _I, _I, _VP, _VP, _I]),
+    "kp_gemm_batch_shared_b_f64": (_I, [_CTX, _I, _I, _I, _D, _VP, _I, C.c_longlong, _VP, _I, _I,
+                                        _D, _VP, _I, C.c_longlong, _I]),
+    "kp_gemm_batch_shared_b_c128": (_I, [_CTX, _I, _I, _I, _VP, _VP, _I, C.c_longlong, _VP, _I,
+                                         _I, _VP, _VP, _I, C.c_longlong, _I]),
+    "kp_lu_factor_f64": (_I, [_CTX, _VP, _I, _VP]),
+    "kp_lu_solve_f64": (_I, [_CTX, _VP, _VP, _I, _VP, _I]),
     "kp_comm_unique_id": (_I, [_VP]),
     "kp_comm_create": (_I, [_CTX, _I, _I, _VP, C.POINTER(_VP)]),
     "kp_comm_destroy": (_I, [_VP]),

@@ -143,6 +143,10 @@ void gll_rule_host(int q, double* nodes, double* weights);
 void expm_batch(kp_ctx* ctx, const double* x, int n, int batch, double* out);
 // x = a^{-1} b (lu_factor + lu_solve, inc/linsolve.hpp:95-151); a n x n, b/x n x nrhs
 void solve_dev(kp_ctx* ctx, const double* a, int n, const double* b, int nrhs, double* x);
+// lu_factor / lu_solve (inc/linsolve.hpp:95-146) split: a factored in place,
+// piv = n device ints; b (n x nrhs) overwritten with the solution
+void lu_factor_dev(kp_ctx* ctx, double* a, int n, int* piv);
+void lu_solve_dev(kp_ctx* ctx, const double* lu, const int* piv, int n, double* b, int nrhs);
 // phiquad (inc/matrix_functions.hpp:146-199): phis = ell_max+1 consecutive
 // n x n matrices; returns the scaling exponent
 int phiquad_dev(kp_ctx* ctx, const double* x, int n, int ell_max, int q, int forced, double* phis);

@@ -783,13 +783,12 @@ void gemm_kb(kp_ctx* ctx, int M, int N, int K, int batch, const double* A, long 
 // the DMMA GEMM, and the substitutions are left-looking (one long-K GEMM per
 // block row instead of a K = 64 update of every remaining row).  Same
 // algorithm to rounding (~1e-16 per operation); tolerance-tested.
-void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs, int nrhs = -1) {
-  if (nrhs < 0) nrhs = n;  // rhs_b: n x nrhs, column-major, stride rs between matrices
-  const long long rs = (long long)n * nrhs;
+// lu_factor phase: lhs factored in place, pivots in piv (n per matrix), the
+// inverted diagonal blocks in the S_TINV slot for the solve phase.
+void lu_factor_phase(kp_ctx* ctx, int n, int batch, double* lhs, int* piv) {
   const long long nn = (long long)n * n;
   const int nblk = (n + LU_NB - 1) / LU_NB;
   const long long bsz = (long long)LU_NB * LU_NB;
-  int* piv = slot<int>(ctx, S_PIV, size_t(n) * batch);
   int* sing = slot<int>(ctx, S_SING, 4);
   double* tinv = slot<double>(ctx, S_TINV, size_t(batch) * nblk * 2 * bsz);
   const long long tstride = (long long)nblk * 2 * bsz;  // per matrix
@@ -835,6 +834,18 @@ void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs, int
   KP_CUDA(cudaMemcpyAsync(&hs, sing, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   KP_CUDA(cudaStreamSynchronize(ctx->stream));
   if (hs) throw runtime_error("lu_factor: matrix is singular");
+}
+
+// lu_solve phase on factors from lu_factor_phase (tinv: the S_TINV slot it
+// left, or recomputed by the caller); rhs_b: n x nrhs, column-major.
+void lu_solve_phase(kp_ctx* ctx, int n, int batch, const double* lhs, const int* piv,
+                    const double* tinv, double* rhs, int nrhs) {
+  const long long rs = (long long)n * nrhs;
+  const long long nn = (long long)n * n;
+  const int nblk = (n + LU_NB - 1) / LU_NB;
+  const long long bsz = (long long)LU_NB * LU_NB;
+  const long long tstride = (long long)nblk * 2 * bsz;
+  const int nt = 256;
   // lu_solve (:119-146): P b, then L y = b (rhs -> x2), then U x = y (x2 -> rhs)
   swaps_kernel<<<dim3((nrhs + nt - 1) / nt, batch), nt, 0, ctx->stream>>>(rhs, n, rs, piv, n, 0,
                                                                           n, 0, nrhs);
@@ -858,6 +869,16 @@ void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs, int
             x2 + j0, n, rs, rhs + j0, n, rs, 1.0, 0.0);
   }
   KP_CUDA(cudaGetLastError());
+}
+
+
+void lu_solve_batch(kp_ctx* ctx, int n, int batch, double* lhs, double* rhs, int nrhs = -1) {
+  if (nrhs < 0) nrhs = n;
+  int* piv = slot<int>(ctx, S_PIV, size_t(n) * batch);
+  lu_factor_phase(ctx, n, batch, lhs, piv);
+  const int nblk = (n + LU_NB - 1) / LU_NB;
+  const double* tinv = slot<double>(ctx, S_TINV, size_t(batch) * nblk * 2 * LU_NB * LU_NB);
+  lu_solve_phase(ctx, n, batch, lhs, piv, tinv, rhs, nrhs);
 }
 
 // pade_low for a batch of matrices sharing one degree (inc/matrix_functions.hpp:37-54):
@@ -995,6 +1016,23 @@ void expm_batch(kp_ctx* ctx, const double* x, int n, int batch, double* out) {
   for (int i = 0; i < batch; ++i)
     KP_CUDA(cudaMemcpyAsync(out + order[i] * nn, rhs + i * nn, nn * sizeof(double),
                             cudaMemcpyDeviceToDevice, ctx->stream));
+}
+
+// lu_factor (inc/linsolve.hpp:95-117) of one n x n matrix in place; piv: n
+// device ints (the row swapped into position j at step j).
+void lu_factor_dev(kp_ctx* ctx, double* a, int n, int* piv) { lu_factor_phase(ctx, n, 1, a, piv); }
+
+// lu_solve (inc/linsolve.hpp:119-146) with factors from lu_factor_dev: b
+// (n x nrhs) overwritten with the solution.
+void lu_solve_dev(kp_ctx* ctx, const double* lu, const int* piv, int n, double* b, int nrhs) {
+  const int nblk = (n + LU_NB - 1) / LU_NB;
+  const long long bsz = (long long)LU_NB * LU_NB;
+  double* tinv = slot<double>(ctx, S_TINV, size_t(nblk) * 2 * bsz);
+  tri_inv_kernel<<<dim3(nblk, 1, 2), LU_NB, 0, ctx->stream>>>(lu, n, (long long)n * n, 0, nblk,
+                                                              tinv);
+  ctx->launches++;
+  KP_CUDA(cudaGetLastError());
+  lu_solve_phase(ctx, n, 1, lu, piv, tinv, b, nrhs);
 }
 
 void solve_dev(kp_ctx* ctx, const double* a, int n, const double* b, int nrhs, double* x) {

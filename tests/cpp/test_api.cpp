@@ -3,13 +3,17 @@
 // include/kronphi_b200 and run on the GPU (tests/test_cpp_api.py).
 // Cases restate /root/reference/proj/tests/test_tensor.cpp,
 // test_matrix_functions.cpp, test_split_phi.cpp, test_integrators.cpp.
+#include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <vector>
 #include <random>
 #include <string>
 
 #include "kronphi/integrators.hpp"
+#include "kronphi/kernels.hpp"
+#include "kronphi/linsolve.hpp"
 #include "kronphi/problems.hpp"
 #include "kronphi/matrix_functions.hpp"
 #include "kronphi/mode_product.hpp"
@@ -201,6 +205,76 @@ int main() {
       err[k] = diff_norm_inf(r.final, ex) / ex.norm_inf();
     }
     CHECK(err[0] < 5e-3 && err[1] < err[0] / 3.0 && err[1] > err[0] / 5.0);
+  }
+  {  // gemm / gemm_batch_shared_b against the naive loops (kernels.hpp)
+    std::mt19937_64 rg(7);
+    std::uniform_real_distribution<double> ud(-1.0, 1.0);
+    for (Op op : {Op::none, Op::transpose}) {
+      const int m = 37, n = 29, k = 300;  // k spans two KC slices
+      const int ldb = op == Op::none ? k : n, bcols = op == Op::none ? n : k;
+      std::vector<double> a(size_t(m) * k), b(size_t(ldb) * bcols), c0(size_t(m) * n),
+          c1;
+      for (auto& x : a) x = ud(rg);
+      for (auto& x : b) x = ud(rg);
+      for (auto& x : c0) x = ud(rg);
+      c1 = c0;
+      gemm_naive(m, n, k, -1.5, a.data(), m, b.data(), ldb, op, 0.5, c0.data(), m);
+      gemm(m, n, k, -1.5, a.data(), m, b.data(), ldb, op, 0.5, c1.data(), m);
+      double err = 0.0;
+      for (size_t i = 0; i < c0.size(); ++i) err = std::max(err, std::abs(c0[i] - c1[i]));
+      CHECK(err < 1e-12);
+    }
+    using Cx = std::complex<double>;
+    const int n = 40;
+    std::vector<Cx> a(size_t(n) * n), b(size_t(n) * n), c0(size_t(n) * n), c1(size_t(n) * n);
+    for (auto& x : a) x = Cx(ud(rg), ud(rg));
+    for (auto& x : b) x = Cx(ud(rg), ud(rg));
+    gemm_naive(n, n, n, Cx(1), a.data(), n, b.data(), n, Op::none, Cx(0), c0.data(), n);
+    gemm(n, n, n, Cx(1), a.data(), n, b.data(), n, Op::none, Cx(0), c1.data(), n);
+    double err = 0.0;
+    for (size_t i = 0; i < c0.size(); ++i) err = std::max(err, std::abs(c0[i] - c1[i]));
+    CHECK(err < 1e-12);
+    // batched, shared B: 3 blocks of a 4-mode-like layout
+    const int P = 6, nm = 5, q = 3;
+    std::vector<double> t(size_t(P) * nm * q), mm(size_t(nm) * nm), o0(size_t(P) * nm * q),
+        o1(size_t(P) * nm * q, 0.0);
+    for (auto& x : t) x = ud(rg);
+    for (auto& x : mm) x = ud(rg);
+    for (int i = 0; i < q; ++i)
+      gemm_naive(P, nm, nm, 1.0, t.data() + size_t(i) * P * nm, P, mm.data(), nm, Op::transpose,
+                 0.0, o0.data() + size_t(i) * P * nm, P);
+    gemm_batch_shared_b(P, nm, nm, 1.0, t.data(), P, size_t(P) * nm, mm.data(), nm,
+                        Op::transpose, 0.0, o1.data(), P, size_t(P) * nm, q);
+    err = 0.0;
+    for (size_t i = 0; i < o0.size(); ++i) err = std::max(err, std::abs(o0[i] - o1[i]));
+    CHECK(err < 1e-13);
+  }
+  {  // solve / lu_factor (linsolve.hpp): residual and the singular case
+    std::mt19937_64 rg(9);
+    std::uniform_real_distribution<double> ud(-1.0, 1.0);
+    const int n = 150, nr = 3;
+    Matrix<double> a(n, n), b(n, nr);
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) a(i, j) = ud(rg) + (i == j ? 4.0 : 0.0);
+    for (int j = 0; j < nr; ++j)
+      for (int i = 0; i < n; ++i) b(i, j) = ud(rg);
+    Matrix<double> x = solve(a, b);
+    double res = 0.0;
+    for (int j = 0; j < nr; ++j)
+      for (int i = 0; i < n; ++i) {
+        double s = -b(i, j);
+        for (int p = 0; p < n; ++p) s += a(i, p) * x(p, j);
+        res = std::max(res, std::abs(s));
+      }
+    CHECK(res < 1e-12);
+    Matrix<double> sing(3, 3);
+    bool threw = false;
+    try {
+      lu_factor(sing);
+    } catch (const std::runtime_error&) {
+      threw = true;
+    }
+    CHECK(threw);
   }
   {  // the native NCCL communicator at world size 1: the re-partition is the
      // identity and the halos wrap onto the rank itself
