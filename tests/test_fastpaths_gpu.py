@@ -45,7 +45,8 @@ def run_general(tmp_path, env, **arrays):
     return np.load(outp)
 
 
-@pytest.mark.parametrize("dims", [(128, 128, 9), (64, 64, 5, 2), (128, 128, 128), (64, 64, 64)])
+@pytest.mark.parametrize("dims", [(128, 128, 9), (64, 64, 5, 2), (128, 128, 128), (64, 64, 64),
+                                  (128, 64, 256), (50, 30, 128), (64, 128, 130)])
 def test_fused01_bitwise(kp, port, tmp_path, dims):
     r = rng(77)
     v = np.asfortranarray(r.standard_normal(dims))
@@ -54,7 +55,7 @@ def test_fused01_bitwise(kp, port, tmp_path, dims):
     want = run_general(tmp_path, {"KP_FUSE01": "0"}, what="tucker", v=v,
                        ms=np.array(ms, dtype=object))
     assert np.array_equal(got, want)
-    if np.prod(dims) <= 64 ** 3:
+    if np.prod(dims) <= 64 ** 3 * 2:
         assert rel2(got, port.tucker(v, ms)) < 1e-12
 
 
@@ -101,7 +102,8 @@ def test_integrate_fastpaths_bitwise(kp, port, tmp_path, case):
         u0 = np.asfortranarray(0.4 + 0.1 * r.uniform(-1, 1, shape))
     gk = getattr(kp, gname)
     got = kp.integrate_config(method, u0, K, kp.gfun(gk, *gp), 0.0, T, steps)
-    want = run_general(tmp_path, {"KP_FUSE01": "0", "KP_BAND": "v1"}, what=method, u0=u0,
+    want = run_general(tmp_path, {"KP_FUSE01": "0", "KP_BAND": "v1"},
+                       what=method, u0=u0,
                        K=np.array(K, dtype=object), gk=gk, gp=np.array(gp, dtype=float),
                        T=T, steps=steps)
     assert np.array_equal(got, want)
