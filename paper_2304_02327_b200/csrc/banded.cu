@@ -336,7 +336,7 @@ __device__ __forceinline__ void row_combine(const BandRow<true>& rw, const doubl
 constexpr int ZMAX = 32;
 
 template <bool CPLX, bool PAIR, bool M3>
-__global__ void __launch_bounds__(256, (CPLX || PAIR) ? 2 : 3)
+__global__ void __launch_bounds__(256, (CPLX || PAIR) ? 3 : 4)
     kronsum_band2_kernel(BandArgs b, int nz, int zchunk, const double* __restrict__ u,
                          double* __restrict__ r, bool with_g, kp_gfun g, double t) {
   pdl_wait();
