@@ -8,6 +8,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -58,6 +60,15 @@ thread_local std::string g_err;
 }  // namespace
 
 void kp_set_last_error(const std::string& m) { g_err = m; }
+
+void ensure_smem_attr(kp_ctx* ctx, const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({kernel, ctx->device})) return;
+  KP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert({kernel, ctx->device});
+}
 
 namespace {
 

@@ -348,12 +348,7 @@ void launch_fused01r(kp_ctx* ctx, const double* in, long long Q, const double* m
                      const double* m2, double alpha0, const Epilogue& e, double* out) {
   using C = F01R<N, MR>;
   auto kern = fused01r_kernel<N, MR>;
-  static bool attr = false;
-  if (!attr) {
-    KP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(C::SMEM)));
-    attr = true;
-  }
+  ensure_smem_attr(ctx, reinterpret_cast<const void*>(kern), int(C::SMEM));
   const long long grid = Q * C::R;
   if (grid > 0x7fffffffLL) throw invalid_argument("fused01: too many slices");
   launch_pdl(ctx, kern, dim3(unsigned(grid)), dim3(C::NT), C::SMEM, in, m1, m2, alpha0, e, out);
@@ -364,12 +359,7 @@ template <int N>
 void launch_fused01(kp_ctx* ctx, const double* in, long long Q, const double* m1,
                     const double* m2, double alpha0, const Epilogue& e, double* out) {
   auto kern = fused01_kernel<N>;
-  static bool attr = false;
-  if (!attr) {
-    KP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(F01<N>::SMEM)));
-    attr = true;
-  }
+  ensure_smem_attr(ctx, reinterpret_cast<const void*>(kern), int(F01<N>::SMEM));
   launch_pdl(ctx, kern, dim3(unsigned(Q)), dim3(F01<N>::NT), F01<N>::SMEM, in, m1, m2, alpha0, e,
              out);
   KP_CUDA(cudaGetLastError());

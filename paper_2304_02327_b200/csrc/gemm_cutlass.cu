@@ -210,11 +210,7 @@ void launch_cutlass(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, long l
                                        cutlass::layout::ColumnMajor>::type;
   auto kern = cutlass_dmma_kernel<B_KCONTIG, SCAT, CFG, CPLX>;
   constexpr int smem = int(sizeof(typename Mma::SharedStorage));
-  static bool attr_set = false;
-  if (!attr_set) {
-    KP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_set = true;
-  }
+  ensure_smem_attr(ctx, reinterpret_cast<const void*>(kern), smem);
   // A' = B^T: element (n, k) at B[k*sBk + n*sBn]
   typename Mma::IteratorA::Params pa(LA(B_KCONTIG ? p.sBn : p.sBk));
   // B' = A^T: element (k, m) at A[m + k*lda] -> row-major K x M, ld = lda

@@ -38,6 +38,11 @@ void kp_set_last_error(const std::string& m);
       throw ::kp::cuda_error(std::string(#call) + ": " + cudaGetErrorString(e_));        \
   } while (0)
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute is per device, so a process driving several GPUs needs it
+// on each (capi.cpp).
+void ensure_smem_attr(kp_ctx* ctx, const void* kernel, int bytes);
+
 // Grow-only device scratch with a few named slots (ping-pong buffers of the
 // Tucker operator, stepper temporaries).  No cudaMalloc on the hot path after
 // the first call at a given size.

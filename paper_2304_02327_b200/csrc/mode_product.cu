@@ -353,12 +353,7 @@ void launch_cfg(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, long long 
   using CF = Cfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, B_KCONTIG, VEC>;
   auto kern = dmma_gemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, B_KCONTIG, VEC, CPLX, MINB,
                                SCAT>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    KP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(CF::SMEM)));
-    attr_set = true;
-  }
+  ensure_smem_attr(ctx, reinterpret_cast<const void*>(kern), int(CF::SMEM));
   const int tiles_m = (p.M + BM - 1) / BM;
   const int tiles_n = (p.N + BN - 1) / BN;
   const long long total = (long long)tiles_m * tiles_n * p.batch;
