@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(128, CFG::kMinBlocks)
       if (e.kind == EPI_STAGE_D) *reinterpret_cast<double2*>(e.D + cq + off) = dv;
     }
     if (e.bad_step && nonfinite) atomicMin(e.bad_step, *e.step_ctr + 1);
+  if (e.step_next && blockIdx.x == 0 && threadIdx.x == 0) *e.step_next = *e.step_ctr + 1;
     return;
   }
 #pragma unroll 1
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(128, CFG::kMinBlocks)
     }
   }
   if (e.bad_step && nonfinite) atomicMin(e.bad_step, *e.step_ctr + 1);
+  if (e.step_next && blockIdx.x == 0 && threadIdx.x == 0) *e.step_next = *e.step_ctr + 1;
 }
 
 template <bool B_KCONTIG, bool SCAT, typename CFG, int CPLX>

@@ -100,6 +100,10 @@ struct Epilogue {
   // value written by this epilogue records atomicMin(*bad_step, *step_ctr + 1)
   int* bad_step = nullptr;
   const int* step_ctr = nullptr;
+  // step counter of the NEXT step (integrate's two alternating slots): the
+  // last kernel of a step writes *step_next = *step_ctr + 1 (one thread), so
+  // no separate counter kernel is launched per step
+  int* step_next = nullptr;
   // fused exchange (kp_scatter): C's entries go to peer buffers instead
   int sc_dir = 0;  // 0: store into C; 1: slab -> pencil; 2: pencil -> slab
   int sc_P = 1, sc_rank = 0;

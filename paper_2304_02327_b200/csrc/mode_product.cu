@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
         }
     }
     if (e.bad_step && nonfinite) atomicMin(e.bad_step, *e.step_ctr + 1);
+  if (e.step_next && blockIdx.x == 0 && threadIdx.x == 0) *e.step_next = *e.step_ctr + 1;
     return;
   }
 #pragma unroll
@@ -336,6 +337,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
       }
   }
   if (e.bad_step && nonfinite) atomicMin(e.bad_step, *e.step_ctr + 1);
+  if (e.step_next && blockIdx.x == 0 && threadIdx.x == 0) *e.step_next = *e.step_ctr + 1;
 }
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, bool B_KCONTIG, int VEC, int CPLX, int VAR,

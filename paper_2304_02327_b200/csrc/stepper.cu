@@ -96,7 +96,7 @@ template <bool CPLX>
 __global__ void lawson2b_post_kernel(kp_gfun g, double t2, long long n, long long half, double tau,
                                      const typename Elt<CPLX>::T* __restrict__ y,
                                      typename Elt<CPLX>::T* __restrict__ out, int* bad,
-                                     const int* ctr) {
+                                     const int* ctr, int* next) {
   pdl_wait();
   using E = Elt<CPLX>;
   bool nf = false;
@@ -107,6 +107,7 @@ __global__ void lawson2b_post_kernel(kp_gfun g, double t2, long long n, long lon
     nf |= !E::finite(r);
   }
   if (nf) atomicMin(bad, *ctr + 1);
+  if (next && blockIdx.x == 0 && threadIdx.x == 0) *next = *ctr + 1;
 }
 
 // d = g(stage) - g(u)   (etd2rk :161-162, unfused form for coupled g)
@@ -145,7 +146,7 @@ __global__ void lawson_pre_pair_kernel(kp_gfun g, double t, long long half, doub
 
 __global__ void lawson2b_post_pair_kernel(kp_gfun g, double t2, long long half, double tau,
                                           const double* __restrict__ y, double* __restrict__ out,
-                                          int* bad, const int* ctr) {
+                                          int* bad, const int* ctr, int* next) {
   pdl_wait();
   const long long n = 2 * half;
   bool nf = false;
@@ -159,6 +160,7 @@ __global__ void lawson2b_post_pair_kernel(kp_gfun g, double t2, long long half, 
     nf |= !isfinite(ra) || !isfinite(rb);
   }
   if (nf) atomicMin(bad, *ctr + 1);
+  if (next && blockIdx.x == 0 && threadIdx.x == 0) *next = *ctr + 1;
 }
 
 __global__ void gdiff_pair_kernel(kp_gfun g, double t, double t2, long long half,
@@ -173,9 +175,9 @@ __global__ void gdiff_pair_kernel(kp_gfun g, double t, double t2, long long half
   }
 }
 
-__global__ void tick_kernel(int* ctr) {
+__global__ void tick_kernel(const int* ctr, int* next) {
   pdl_wait();
-  *ctr += 1;
+  *next = *ctr + 1;
 }
 
 __global__ void scale_matrix_kernel(const double* __restrict__ a, long long n, double s,
@@ -488,16 +490,17 @@ class Integrator {
                n_entries, half, tau, two, reinterpret_cast<const T*>(u), reinterpret_cast<T*>(w));
   }
   template <bool C>
-  void launch_post(const double* y, double* out, int* bad, const int* ctr, double t2) {
+  void launch_post(const double* y, double* out, int* bad, const int* ctr, double t2,
+                   int* next) {
     using T = typename Elt<C>::T;
     if (!C && half > 0) {
       launch_pdl(ctx, lawson2b_post_pair_kernel, dim3(grid_ew(ctx, half)), dim3(256), 0, g, t2,
-                 half, tau, y, out, bad, ctr);
+                 half, tau, y, out, bad, ctr, next);
       return;
     }
     launch_pdl(ctx, lawson2b_post_kernel<C>, dim3(grid_ew(ctx, n_entries)), dim3(256), 0, g, t2,
                n_entries, half, tau, reinterpret_cast<const T*>(y), reinterpret_cast<T*>(out), bad,
-               ctr);
+               ctr, next);
   }
   template <bool C>
   void launch_gdiff(const double* s, const double* u, double* dd, double t) {
@@ -513,7 +516,11 @@ class Integrator {
   }
 
   // One step u -> out (out != u).  bad/ctr: divergence tracking (may be null).
-  void step(const double* u, double* out, double t, int* bad, const int* ctr) {
+  // One step; returns whether its last kernel already wrote *next =
+  // *ctr + 1 (else the caller advances the counter).
+  bool step(const double* u, double* out, double t, int* bad, const int* ctr,
+            int* next = nullptr) {
+    if (g.step_ctr) g.step_ctr = ctr;  // time-dependent g: this step's counter
     Epilogue fin;
     fin.bad_step = bad;
     fin.step_ctr = ctr;
@@ -521,8 +528,9 @@ class Integrator {
     if (nonlocal) {
       step_nonlocal(u, out, t, fin);
       KP_CUDA(cudaGetLastError());
-      return;
+      return false;
     }
+    fin.step_next = ctr ? next : nullptr;
     switch (method) {
       case KP_LAWSON_EULER: {  // :116-122
         double* w = buf(S_W, n_entries);
@@ -544,12 +552,12 @@ class Integrator {
         tucker(fs, w, sd, y, nullptr);
         d = d_save;
         if (bad) {
-          cplx ? launch_post<true>(y, out, bad, ctr, t + tau)
-               : launch_post<false>(y, out, bad, ctr, t + tau);
+          cplx ? launch_post<true>(y, out, bad, ctr, t + tau, fin.step_next)
+               : launch_post<false>(y, out, bad, ctr, t + tau, fin.step_next);
         } else {
           int* dummy = static_cast<int*>(ctx->ws.get(S_CTR + 1, 16));
-          cplx ? launch_post<true>(y, out, dummy, dummy, t + tau)
-               : launch_post<false>(y, out, dummy, dummy, t + tau);
+          cplx ? launch_post<true>(y, out, dummy, dummy, t + tau, nullptr)
+               : launch_post<false>(y, out, dummy, dummy, t + tau, nullptr);
         }
         break;
       }
@@ -616,6 +624,7 @@ class Integrator {
         throw invalid_argument("step: unknown method " + std::to_string(method));
     }
     KP_CUDA(cudaGetLastError());
+    return fin.step_next != nullptr;
   }
 
   void eval_g(const double* u, double* out, double t) {
@@ -758,10 +767,14 @@ class Integrator {
 
   // integrate loop (:290-367) on u (device, in/out).  Returns loop seconds.
   double run(double* u, double t0, long n_steps, bool use_graph) {
-    int* ctr = static_cast<int*>(ctx->ws.get(S_CTR, 16));
-    int* bad = ctr + 1;
-    const int init[2] = {0, INT_MAX};
-    KP_CUDA(cudaMemcpyAsync(ctr, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+    // step counter in two alternating slots (step k reads slot k&1 and its
+    // last kernel writes slot (k+1)&1), divergence flag in between
+    int* cbuf = static_cast<int*>(ctx->ws.get(S_CTR, 16));
+    int* slot[2] = {cbuf, cbuf + 2};
+    int* bad = cbuf + 1;
+    const int init[4] = {0, INT_MAX, 0, 0};
+    KP_CUDA(cudaMemcpyAsync(cbuf, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+    int* ctr = slot[0];
     double* ub[2] = {u, buf(S_U2, n_entries)};
     // device time of the loop = [e0,e1] (first, eager step) + [e2,e3] (graph
     // replays + tail); the host-side capture/instantiation between e1 and e2
@@ -774,8 +787,9 @@ class Integrator {
     g.t0 = t0;
     g.tau = tau;
     auto one = [&](long k) {
-      step(ub[k & 1], ub[(k + 1) & 1], 0.0, bad, ctr);
-      launch_pdl(ctx, tick_kernel, dim3(1), dim3(1), 0, ctr);
+      int *c = slot[k & 1], *c2 = slot[(k + 1) & 1];
+      if (!step(ub[k & 1], ub[(k + 1) & 1], 0.0, bad, c, c2))
+        launch_pdl(ctx, tick_kernel, dim3(1), dim3(1), 0, (const int*)c, c2);
     };
     // first step eagerly: sizes every workspace slot before any capture
     KP_CUDA(cudaEventRecord(ev[0], ctx->stream));
@@ -789,10 +803,8 @@ class Integrator {
       KP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
       // two steps: ub1 -> ub0 -> ub1 (n is odd here); t is unused by the
       // closed set of g's (all autonomous), so replays stay exact
-      step(ub[1], ub[0], 0.0, bad, ctr);
-      launch_pdl(ctx, tick_kernel, dim3(1), dim3(1), 0, ctr);
-      step(ub[0], ub[1], 0.0, bad, ctr);
-      launch_pdl(ctx, tick_kernel, dim3(1), dim3(1), 0, ctr);
+      one(1);  // an odd step (slot 1 -> slot 0), then an even one
+      one(2);
       KP_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
       per = ctx->launches - l0;
       ctx->launches = l0;
@@ -814,7 +826,7 @@ class Integrator {
       KP_CUDA(cudaMemcpyAsync(u, ub[1], size_t(n_entries) * comps * sizeof(double),
                               cudaMemcpyDeviceToDevice, ctx->stream));
     int hb[2];
-    KP_CUDA(cudaMemcpyAsync(hb, ctr, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
+    KP_CUDA(cudaMemcpyAsync(hb, cbuf, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
     KP_CUDA(cudaStreamSynchronize(ctx->stream));
     float ms1 = 0.f, ms2 = 0.f;
     KP_CUDA(cudaEventElapsedTime(&ms1, ev[0], ev[1]));
