@@ -206,7 +206,7 @@ void need(kp_ctx* ctx, kp_comm* c) {
   KP_CUDA(cudaSetDevice(ctx->device));
 }
 
-constexpr int SLOT_SEND = 56, SLOT_RECV = 57;
+constexpr int SLOT_SEND = 64, SLOT_RECV = 65;  // distinct from every other slot (phi.cu uses 20..58)
 
 }  // namespace
 }  // namespace kp

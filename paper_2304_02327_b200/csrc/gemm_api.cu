@@ -94,7 +94,7 @@ void gemm_cplx(kp_ctx* ctx, int m, int n, int k, double2 alpha, const double* a,
   const long long na = (long long)m * k * batch, nb = (long long)br * bc,
                   nc = (long long)m * n * batch;
   double* ws = static_cast<double*>(
-      ctx->ws.get(58, sizeof(double) * size_t(2 * na + 2 * nb + 4 * nc + 4)));
+      ctx->ws.get(66, sizeof(double) * size_t(2 * na + 2 * nb + 4 * nc + 4)));
   double *ar = ws, *ai = ar + na, *bre = ai + na, *bim = bre + nb;
   double *rr = bim + nb, *ii = rr + nc, *ri = ii + nc, *ir = ri + nc;
   auto grid = [&](long long t) {

@@ -966,19 +966,23 @@ void expm_batch(kp_ctx* ctx, const double* x, int n, int batch, double* out) {
       }
     }
   }
-  // group-ordered permutation: groups of equal (branch, scaling)
+  // Order: every degree-13 matrix first, by decreasing scaling exponent,
+  // then one group per low degree.  The degree-13 block then runs as ONE
+  // batch (each matrix scaled by its own 2^-s, one pade13 pass, and the
+  // squarings over the prefix still needing one), so a few large matrices of
+  // different scalings share every GEMM launch instead of each filling a
+  // fraction of a wave on its own.  Per-matrix arithmetic is unchanged.
   std::vector<int> order;
-  std::vector<std::pair<int, int>> groups;  // (first position, size)
-  std::vector<bool> done(batch, false);
-  for (int b0 = 0; b0 < batch; ++b0) {
-    if (done[b0]) continue;
+  for (int b = 0; b < batch; ++b)
+    if (branch[b] == 4) order.push_back(b);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sc[a] > sc[b]; });
+  const int n13 = int(order.size());
+  std::vector<std::pair<int, int>> low;  // (first position, size) per low degree
+  for (int br = 0; br < 4; ++br) {
     const int first = int(order.size());
-    for (int b = b0; b < batch; ++b)
-      if (!done[b] && branch[b] == branch[b0] && sc[b] == sc[b0]) {
-        order.push_back(b);
-        done[b] = true;
-      }
-    groups.emplace_back(first, int(order.size()) - first);
+    for (int b = 0; b < batch; ++b)
+      if (branch[b] == br) order.push_back(b);
+    if (int(order.size()) > first) low.emplace_back(first, int(order.size()) - first);
   }
   double* gin = slot<double>(ctx, S_ARG, size_t(nn) * batch);
   double* lhs = slot<double>(ctx, S_LHS, size_t(nn) * batch);
@@ -986,32 +990,33 @@ void expm_batch(kp_ctx* ctx, const double* x, int n, int batch, double* out) {
   for (int i = 0; i < batch; ++i)
     KP_CUDA(cudaMemcpyAsync(gin + i * nn, x + order[i] * nn, nn * sizeof(double),
                             cudaMemcpyDeviceToDevice, ctx->stream));
-  for (const auto& gr : groups) {
-    const int b0 = order[gr.first], g = gr.second;
-    double* gi = gin + gr.first * nn;
-    if (branch[b0] < 4) {
-      pade_low_batch(ctx, gi, n, g, branch[b0], lhs + gr.first * nn, rhs + gr.first * nn);
-    } else {
-      double* scale = slot<double>(ctx, S_COEF, 256);
-      std::vector<double> hs(g, std::ldexp(1.0, -sc[b0]));
-      KP_CUDA(cudaMemcpyAsync(scale, hs.data(), g * sizeof(double), cudaMemcpyHostToDevice,
-                              ctx->stream));
-      scale_batch_kernel<<<grid1(ctx, nn * g), 256, 0, ctx->stream>>>(gi, nn, scale, nn, g, gi);
-      ctx->launches++;
-      pade13_batch(ctx, gi, n, g, lhs + gr.first * nn, rhs + gr.first * nn);
-      KP_CUDA(cudaStreamSynchronize(ctx->stream));  // S_COEF is reused by the next group
-    }
+  if (n13 > 0) {
+    if (n13 > 256) throw invalid_argument("expm: at most 256 matrices per batch");
+    double* scale = slot<double>(ctx, S_COEF, 256);
+    std::vector<double> hs(n13);
+    for (int i = 0; i < n13; ++i) hs[i] = std::ldexp(1.0, -sc[order[i]]);
+    KP_CUDA(cudaMemcpyAsync(scale, hs.data(), n13 * sizeof(double), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    scale_batch_kernel<<<grid1(ctx, nn * n13), 256, 0, ctx->stream>>>(gin, nn, scale, nn, n13,
+                                                                       gin);
+    ctx->launches++;
+    pade13_batch(ctx, gin, n, n13, lhs, rhs);
+    KP_CUDA(cudaStreamSynchronize(ctx->stream));  // S_COEF is reused by pade_low_batch
   }
+  for (const auto& gr : low)
+    pade_low_batch(ctx, gin + gr.first * nn, n, gr.second, branch[order[gr.first]],
+                   lhs + gr.first * nn, rhs + gr.first * nn);
   lu_solve_batch(ctx, n, batch, lhs, rhs);
-  for (const auto& gr : groups) {
-    const int s = sc[order[gr.first]], g = gr.second;
-    double* f = rhs + gr.first * nn;
+  // squarings: matrix i of the degree-13 block needs sc[order[i]] of them;
+  // sorted by decreasing s, the ones still needing a squaring are a prefix
+  const int smax = n13 > 0 ? sc[order[0]] : 0;
+  for (int it = 0; it < smax; ++it) {
+    int g = 0;
+    while (g < n13 && sc[order[g]] > it) ++g;
     double* tmp = slot<double>(ctx, S_T1, size_t(nn) * g);
-    for (int i = 0; i < s; ++i) {  // f = f*f
-      matmul_batch(ctx, n, g, f, nn, f, nn, tmp, nn);
-      KP_CUDA(cudaMemcpyAsync(f, tmp, nn * g * sizeof(double), cudaMemcpyDeviceToDevice,
-                              ctx->stream));
-    }
+    matmul_batch(ctx, n, g, rhs, nn, rhs, nn, tmp, nn);  // f = f*f
+    KP_CUDA(cudaMemcpyAsync(rhs, tmp, nn * g * sizeof(double), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
   }
   for (int i = 0; i < batch; ++i)
     KP_CUDA(cudaMemcpyAsync(out + order[i] * nn, rhs + i * nn, nn * sizeof(double),
