@@ -46,7 +46,8 @@ def run_general(tmp_path, env, **arrays):
 
 
 @pytest.mark.parametrize("dims", [(128, 128, 9), (64, 64, 5, 2), (128, 128, 128), (64, 64, 64),
-                                  (128, 64, 256), (50, 30, 128), (64, 128, 130)])
+                                  (128, 64, 256), (50, 30, 128), (64, 128, 130), (128, 128),
+                                  (64, 64)])
 def test_fused01_bitwise(kp, port, tmp_path, dims):
     r = rng(77)
     v = np.asfortranarray(r.standard_normal(dims))
@@ -73,6 +74,9 @@ def test_fused01_prefactor_and_phi(kp, port):
 CASES = {
     # (method, u0 shape, K builder, g kind, g params, T, steps)
     "ac3d": ("etd2rk", (64, 64, 64), "ac", "G_ALLEN_CAHN", (), 5e-4 * 6, 6),
+    "ac2d": ("exp_euler", (128, 128), "ac", "G_ALLEN_CAHN", (), 1e-3 * 8, 8),
+    "ac2d_etd": ("etd2rk", (128, 128), "ac", "G_ALLEN_CAHN", (), 1e-3 * 8, 8),
+    "ac2d_l2b": ("lawson2b", (64, 64), "ac", "G_ALLEN_CAHN", (), 1e-3 * 8, 8),
     "bru_etd": ("etd2rk", (32, 32, 32, 2), "bru", "G_BRUSSELATOR", (1.0, 3.0), 1e-3 * 5, 5),
     "bru_l2b": ("lawson2b", (32, 32, 32, 2), "bru", "G_BRUSSELATOR", (1.0, 3.0), 1e-3 * 5, 5),
     "nls": ("etd2rk", (24, 24, 24), "nls", "G_NLS", (), 1e-3 * 4, 4),
@@ -98,7 +102,7 @@ def test_integrate_fastpaths_bitwise(kp, port, tmp_path, case):
              3 + 0.1 * r.uniform(-1, 1, shape[:3] + (1,))], axis=3))
     else:
         A = port.fd_operator_1d(shape[0], 0.01)
-        K = [A] * 3
+        K = [A] * len(shape)
         u0 = np.asfortranarray(0.4 + 0.1 * r.uniform(-1, 1, shape))
     gk = getattr(kp, gname)
     got = kp.integrate_config(method, u0, K, kp.gfun(gk, *gp), 0.0, T, steps)
