@@ -996,7 +996,12 @@ int host_integrate_impl(kp_ctx* ctx, bool cplx, int method, const double* u0, co
     size_t n = comps;
     for (int x : dv) n *= size_t(x);
     KP_CUDA(cudaMalloc(&du, n * sizeof(double)));
-    KP_CUDA(cudaMemcpy(du, u0, n * sizeof(double), cudaMemcpyHostToDevice));
+    // uploads on the context's stream + a sync: a plain cudaMemcpy from
+    // pageable memory may return before its DMA lands, and the integration
+    // runs on the context's NON-blocking stream (it then read stale memory
+    // now and then -- a second integrate() in one process saw the previous
+    // run's state)
+    KP_CUDA(cudaMemcpyAsync(du, u0, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     // equal host factors are uploaded once (the device build dedupes by pointer)
     std::vector<const double*> dptr(d);
     for (int mu = 0; mu < d; ++mu) {
@@ -1013,9 +1018,11 @@ int host_integrate_impl(kp_ctx* ctx, bool cplx, int method, const double* u0, co
       double* p = nullptr;
       KP_CUDA(cudaMalloc(&p, nn * sizeof(double)));
       da.push_back(p);
-      KP_CUDA(cudaMemcpy(p, as[mu], nn * sizeof(double), cudaMemcpyHostToDevice));
+      KP_CUDA(cudaMemcpyAsync(p, as[mu], nn * sizeof(double), cudaMemcpyHostToDevice,
+                              ctx->stream));
       dptr[mu] = p;
     }
+    KP_CUDA(cudaStreamSynchronize(ctx->stream));
     int r2 = integrate_impl(ctx, cplx, method, du, dims, d, dptr.data(), g, t0, t_final, n_steps,
                             q, diverged_step, loop_seconds);
     if (r2 == KP_EDIVERGE) throw divergence_error(kp_last_error(), diverged_step ? *diverged_step : 0);
@@ -1025,7 +1032,9 @@ int host_integrate_impl(kp_ctx* ctx, bool cplx, int method, const double* u0, co
       if (r2 == KP_ECUDA) throw cuda_error(m);
       throw runtime_error(m);
     }
-    KP_CUDA(cudaMemcpy(u_final, du, n * sizeof(double), cudaMemcpyDeviceToHost));
+    KP_CUDA(cudaMemcpyAsync(u_final, du, n * sizeof(double), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    KP_CUDA(cudaStreamSynchronize(ctx->stream));
   }, diverged_step);
   if (du) cudaFree(du);
   for (double* p : da) cudaFree(p);

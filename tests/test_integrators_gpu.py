@@ -236,3 +236,36 @@ def test_divergence_step_matches_oracle(kp, port):
     so = int(str(eo.value).split("step ")[1].split(" ")[0])
     assert eg.value.step == so
     assert eg.value.loop_s > 0
+
+
+def test_config3_ac3d_full_vs_reference(kp, ref):
+    """configs[2] at FULL size (128^3, ETD2RK, tau = 5e-4, 200 steps) against
+    the real reference (oracle/_ref, its own OpenMP CPU build): <= 1e-10."""
+    from paper_2304_02327_b200 import problems
+    cfg = problems.ac3d()
+    got = gpu_run(kp, cfg)
+    want = oracle_run(ref, cfg)
+    assert rel2(got, want) < TOL
+
+
+@pytest.mark.parametrize("method", ["etd2rk", "lawson2b"])
+def test_config4_brusselator_full_size_steps(kp, ref, method):
+    """configs[3] at FULL size (2 x 256^3, tau = 1e-3) for the first 3 steps
+    against the real reference (100 steps would take the CPU minutes)."""
+    from paper_2304_02327_b200 import problems
+    cfg = problems.brusselator(method=method, n_steps=3)  # tau = 1e-3: the first 3 steps
+    got = gpu_run(kp, cfg)
+    want = oracle_run(ref, cfg)
+    assert rel2(got, want) < TOL
+
+
+@pytest.mark.parametrize("method", ["exp_euler", "etd2rk"])
+def test_config5_nls_64_vs_reference(kp, ref, method):
+    """configs[4] at 64^3 (the full-algorithm parity size for
+    the complex path), 50 steps, against the real reference's complex
+    kronsum / split-phi restatement (oracle/ref_harness.cpp)."""
+    from paper_2304_02327_b200 import problems
+    cfg = problems.nls(n=64, method=method)
+    got = gpu_run(kp, cfg)
+    want = oracle_run(ref, cfg)
+    assert rel2(got, want) < TOL
