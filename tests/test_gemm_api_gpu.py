@@ -90,3 +90,27 @@ def test_lu_singular_raises(kp):
     piv = torch.zeros(4, dtype=torch.int32, device="cuda")
     with pytest.raises(KronphiError, match="singular"):
         check(ctx.lib.kp_lu_factor_f64(ctx.h, da.data_ptr(), 4, piv.data_ptr()))
+
+
+def test_invalid_arguments_raise(kp):
+    """Validation errors of the late ABI entry points map to KP_EINVAL
+    (std::invalid_argument in the C++ drop-in) with a message naming the
+    problem -- the reference's error contract."""
+    import torch
+    from paper_2304_02327_b200._lib import check, InvalidArgument
+    ctx = kp.default_context(0)
+    a = torch.zeros(16, dtype=torch.float64, device="cuda")
+    with pytest.raises(InvalidArgument, match="leading dimension"):
+        check(ctx.lib.kp_gemm_f64(ctx.h, 4, 4, 4, 1.0, a.data_ptr(), 2, a.data_ptr(), 4, 0, 0.0,
+                                  a.data_ptr(), 4))
+    with pytest.raises(InvalidArgument, match="opb"):
+        check(ctx.lib.kp_gemm_f64(ctx.h, 2, 2, 2, 1.0, a.data_ptr(), 2, a.data_ptr(), 2, 7, 0.0,
+                                  a.data_ptr(), 2))
+    with pytest.raises(InvalidArgument, match="divisible"):
+        check(ctx.lib.kp_repartition_pack(ctx.h, 1, 3, 0, 2, 4, 4, 1, 1, a.data_ptr(),
+                                          a.data_ptr()))
+    with pytest.raises(InvalidArgument, match="dir"):
+        check(ctx.lib.kp_repartition_pack(ctx.h, 3, 1, 0, 2, 2, 2, 1, 1, a.data_ptr(),
+                                          a.data_ptr()))
+    with pytest.raises(InvalidArgument, match="lu_solve"):
+        check(ctx.lib.kp_lu_solve_f64(ctx.h, a.data_ptr(), None, 4, a.data_ptr(), 1))
