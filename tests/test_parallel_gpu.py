@@ -161,3 +161,41 @@ def test_native_nccl_comm_p1_bitwise(kp, nccl1, case, method, kronsum):
         os.environ.pop("KP_KRONSUM", None)
     got = res.cpu().numpy().reshape(cfg.u0.shape, order="F")
     assert np.array_equal(got, want), np.abs(got - want).max()
+
+
+@pytest.mark.parametrize("case", ["ac", "bru", "nls"])
+def test_mode_product_stage_matches_unfused(kp, case):
+    """kp_mode_product_stage_* (ETD2RK's stage update in the last GEMM's
+    epilogue, used by the sharded step) equals mode product -> fma -> two g
+    evaluations -> subtraction, bit for bit."""
+    import torch
+    from paper_2304_02327_b200 import parallel, problems
+    be = parallel.CudaBackend(0)
+    r = np.random.default_rng(3)
+    if case == "nls":
+        dims, g = [12, 10, 8], problems.G.nls()
+        mk = lambda s: torch.tensor(r.standard_normal(s) + 1j * r.standard_normal(s),
+                                    device="cuda")
+    elif case == "bru":
+        dims, g = [10, 9, 8, 2], problems.G.brusselator(1.0, 3.0)
+        mk = lambda s: torch.tensor(1 + 0.1 * r.standard_normal(s), device="cuda")
+    else:
+        dims, g = [10, 9, 8], problems.G.allen_cahn()
+        mk = lambda s: torch.tensor(r.standard_normal(s), device="cuda")
+    n = int(np.prod(dims))
+    t, x = mk(n), mk(n)
+    mode = 2
+    m = mk(dims[mode] * dims[mode])
+    tau = 1e-3
+    out, dd = torch.empty_like(t), torch.empty_like(t)
+    be.mode_product_stage(t, dims, mode, m.view(dims[mode], dims[mode]), 0.5, x, tau, g, out, dd)
+    y = torch.empty_like(t)
+    be.mode_product(t, dims, mode, m.view(dims[mode], dims[mode]), 0.5, 0.0, y)
+    st = torch.empty_like(t)
+    be.fma(tau, y, x, st)
+    gs, gx = torch.empty_like(t), torch.empty_like(t)
+    be.eval_g(g, st, dims, gs)
+    be.eval_g(g, x, dims, gx)
+    torch.cuda.synchronize()
+    assert torch.equal(out, st)
+    assert torch.equal(dd, gs - gx)
