@@ -192,6 +192,22 @@ int kp_kronsum_slab_c128(kp_ctx* ctx, const double* u_ext, const int* dims, int 
                          const double* const* as, int slab_mode, int k0, int n_glob,
                          const kp_gfun* g, double* r);
 
+/* The same slab action with the band structures scanned once up front
+ * (kp_kronsum_slab_* rescans every call, one host sync each): a loop that
+ * applies the same factors every step creates one kp_band per factor and
+ * calls the _banded form, which never synchronizes.  bands[mu] must hold the
+ * n x n factor of mode mu (n_glob for slab_mode); more than three nonzeros
+ * in a row -> KP_EINVAL. */
+typedef struct kp_band kp_band;
+int kp_band_create(kp_ctx* ctx, const double* a, int n, int cplx, kp_band** out);
+int kp_band_destroy(kp_band* band);
+int kp_kronsum_slab_banded_f64(kp_ctx* ctx, const double* u_ext, const int* dims, int d,
+                               const kp_band* const* bands, int slab_mode, int k0, int n_glob,
+                               const kp_gfun* g, double* r);
+int kp_kronsum_slab_banded_c128(kp_ctx* ctx, const double* u_ext, const int* dims, int d,
+                                const kp_band* const* bands, int slab_mode, int k0, int n_glob,
+                                const kp_gfun* g, double* r);
+
 /* ---------------- multi-GPU: fused exchange over peer memory ----------------
  * The slab-sharded integrators re-partition the state
  * between the slab layout (last spatial mode split over P ranks) and the

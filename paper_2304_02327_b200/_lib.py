@@ -92,6 +92,10 @@ _SIGS = {
                                          _I, _VP, _VP, _I, C.c_longlong, _I]),
     "kp_lu_factor_f64": (_I, [_CTX, _VP, _I, _VP]),
     "kp_lu_solve_f64": (_I, [_CTX, _VP, _VP, _I, _VP, _I]),
+    "kp_band_create": (_I, [_CTX, _VP, _I, _I, C.POINTER(_VP)]),
+    "kp_band_destroy": (_I, [_VP]),
+    "kp_kronsum_slab_banded_f64": (_I, [_CTX, _VP, _PI, _I, _VP, _I, _I, _I, C.c_void_p, _VP]),
+    "kp_kronsum_slab_banded_c128": (_I, [_CTX, _VP, _PI, _I, _VP, _I, _I, _I, C.c_void_p, _VP]),
     "kp_comm_unique_id": (_I, [_VP]),
     "kp_comm_create": (_I, [_CTX, _I, _I, _VP, C.POINTER(_VP)]),
     "kp_comm_destroy": (_I, [_VP]),

@@ -693,3 +693,110 @@ extern "C" int kp_kronsum_slab_c128(kp_ctx* ctx, const double* u_ext, const int*
                                     const kp_gfun* g, double* r) {
   return slab_impl(ctx, true, u_ext, dims, d, as, slab_mode, k0, n_glob, g, r);
 }
+
+// ---- pre-scanned band structures: the slab action without a per-call scan ----
+// kp_kronsum_slab_* scans its factors on every call (one host sync); a
+// host loop that applies the same factors every step (the sharded
+// integrators) scans once with kp_band_create and calls the _banded form,
+// which never synchronizes -- the CPU keeps running ahead of the GPU.
+struct kp_band {
+  int n = 0;
+  bool cplx = false, any = false;
+  int* cols = nullptr;
+  double* vals = nullptr;
+};
+
+extern "C" int kp_band_create(kp_ctx* ctx, const double* a, int n, int cplx, kp_band** out) {
+  try {
+    if (!ctx || !a || !out || n <= 0) throw invalid_argument("band_create: bad arguments");
+    KP_CUDA(cudaSetDevice(ctx->device));
+    auto* b = new kp_band;
+    b->n = n;
+    b->cplx = cplx != 0;
+    try {
+      KP_CUDA(cudaMalloc(&b->cols, sizeof(int) * 3 * size_t(n)));
+      KP_CUDA(cudaMalloc(&b->vals, sizeof(double) * 6 * size_t(n)));
+      band_scan_async(ctx, a, n, b->cplx, b->cols, b->vals, 0);
+      const auto f = band_flags(ctx, 1)[0];
+      if (f.first) throw invalid_argument("band_create: more than three nonzeros in a row");
+      b->any = f.second;
+    } catch (...) {
+      cudaFree(b->cols);
+      cudaFree(b->vals);
+      delete b;
+      throw;
+    }
+    *out = b;
+    return KP_OK;
+  } catch (const std::invalid_argument& e) {
+    kp_set_last_error(e.what());
+    return KP_EINVAL;
+  } catch (const kp::cuda_error& e) {
+    kp_set_last_error(e.what());
+    return KP_ECUDA;
+  } catch (const std::exception& e) {
+    kp_set_last_error(e.what());
+    return KP_ERUNTIME;
+  }
+}
+
+extern "C" int kp_band_destroy(kp_band* b) {
+  if (!b) return KP_OK;
+  cudaFree(b->cols);
+  cudaFree(b->vals);
+  delete b;
+  return KP_OK;
+}
+
+namespace {
+int slab_banded_impl(kp_ctx* ctx, bool cplx, const double* u_ext, const int* dims, int d,
+                     const kp_band* const* bands, int slab_mode, int k0, int n_glob,
+                     const kp_gfun* g, double* r) {
+  try {
+    if (!ctx) throw invalid_argument("kronphi_b200: null context");
+    KP_CUDA(cudaSetDevice(ctx->device));
+    if (d <= 0 || d > 4 || !dims || !bands)
+      throw invalid_argument("kronsum_slab: order must be 1..4");
+    std::vector<int> dv(dims, dims + d);
+    if (slab_mode < 0 || slab_mode >= d) throw invalid_argument("kronsum_slab: bad slab mode");
+    std::vector<const int*> cols(d);
+    std::vector<const double*> vals(d);
+    std::vector<char> active(d, 1);
+    for (int mu = 0; mu < d; ++mu) {
+      const kp_band* b = bands[mu];
+      const int n = (mu == slab_mode) ? n_glob : dv[mu];
+      if (!b || b->n != n || b->cplx != cplx)
+        throw invalid_argument("kronsum_slab: band " + std::to_string(mu) +
+                               " does not match the mode size / type");
+      cols[mu] = b->cols;
+      vals[mu] = b->vals;
+      if (n <= 2) active[mu] = b->any;  // the stacked species mode contributes nothing
+    }
+    long long half = 0;
+    if (g && g->kind == KP_G_BRUSSELATOR) half = 1;
+    kronsum_banded(ctx, cplx, u_ext, dv, cols, vals, active, r, g != nullptr,
+                   g ? *g : kp_gfun{}, half, slab_mode, k0, n_glob, 1, 0.0);
+    return KP_OK;
+  } catch (const std::invalid_argument& e) {
+    kp_set_last_error(e.what());
+    return KP_EINVAL;
+  } catch (const kp::cuda_error& e) {
+    kp_set_last_error(e.what());
+    return KP_ECUDA;
+  } catch (const std::exception& e) {
+    kp_set_last_error(e.what());
+    return KP_ERUNTIME;
+  }
+}
+}  // namespace
+
+extern "C" int kp_kronsum_slab_banded_f64(kp_ctx* ctx, const double* u_ext, const int* dims,
+                                          int d, const kp_band* const* bands, int slab_mode,
+                                          int k0, int n_glob, const kp_gfun* g, double* r) {
+  return slab_banded_impl(ctx, false, u_ext, dims, d, bands, slab_mode, k0, n_glob, g, r);
+}
+extern "C" int kp_kronsum_slab_banded_c128(kp_ctx* ctx, const double* u_ext, const int* dims,
+                                           int d, const kp_band* const* bands, int slab_mode,
+                                           int k0, int n_glob, const kp_gfun* g, double* r) {
+  return slab_banded_impl(ctx, true, u_ext, dims, d, bands, slab_mode, k0, n_glob, g, r);
+}

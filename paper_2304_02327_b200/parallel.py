@@ -451,15 +451,34 @@ class CudaBackend:
                      out.data_ptr()))
 
     def kronsum_slab(self, u_ext, dims, K, slab_mode, k0, n_glob, g, out):
-        """r = K u + g(u) on a slab with halo planes (kp_kronsum_slab_*)."""
+        """r = K u + g(u) on a slab with halo planes.  The factors' band
+        structures are scanned once per factor set (kp_band_create, cached
+        with a reference to the factor tensors) and every step calls
+        kp_kronsum_slab_banded_*, which never syncs the host."""
         import ctypes as C
-        from ._lib import ptr_array
         self._sync_stream()
-        f = self.ctx.lib.kp_kronsum_slab_c128 if torch.is_complex(u_ext) else \
-            self.ctx.lib.kp_kronsum_slab_f64
+        cplx = torch.is_complex(u_ext)
+        key = (cplx,) + tuple((k.data_ptr(), k.numel()) for k in K)
+        cache = self.__dict__.setdefault("_bands", {})
+        if key not in cache:
+            hs = []
+            for k in K:
+                h = C.c_void_p()
+                self.check(self.ctx.lib.kp_band_create(self.ctx.h, k.data_ptr(), k.shape[0],
+                                                       int(cplx), C.byref(h)))
+                hs.append(h)
+            cache[key] = (list(K), hs, (C.c_void_p * len(hs))(*[h.value for h in hs]))
+        _, _, arr = cache[key]
+        f = self.ctx.lib.kp_kronsum_slab_banded_c128 if cplx else \
+            self.ctx.lib.kp_kronsum_slab_banded_f64
         self.check(f(self.ctx.h, u_ext.data_ptr(), self.ints(dims), len(dims),
-                     ptr_array([k.data_ptr() for k in K]), slab_mode, k0, n_glob,
+                     C.cast(arr, C.c_void_p), slab_mode, k0, n_glob,
                      C.cast(C.byref(g), C.c_void_p) if g is not None else None, out.data_ptr()))
+
+    def release_bands(self):
+        for _, hs, _ in self.__dict__.pop("_bands", {}).values():
+            for h in hs:
+                self.ctx.lib.kp_band_destroy(h)
 
     def fma(self, alpha, x, y, out):
         """out = fma(alpha, x, y) elementwise (componentwise for complex)."""
