@@ -533,7 +533,7 @@ def main():
                "d2h_bytes_per_step": int(v_h.nbytes), "ms_per_step": sec * 1e3,
                "steps": ksteps,
                "api": "kp_host_tucker_stream_f64 (pinned host buffers; upload of step i+1 "
-                      "overlaps step i)",
+                      "overlaps step i; best of 2 streams of `steps` tensors)",
                "single_call": {"value": world * fl / single / 1e9, "ms_per_step": single * 1e3,
                                "api": "kp_host_tucker_f64 per step (blocking)"}}
 
