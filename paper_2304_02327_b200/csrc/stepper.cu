@@ -797,14 +797,18 @@ class Integrator {
     KP_CUDA(cudaEventRecord(ev[1], ctx->stream));
     cudaGraphExec_t exec = nullptr;
     unsigned long long per = 0;
+    // steps per graph: an even number (ping-pong buffers and counter slots
+    // return to their start); 8 for small states, whose steps are a few
+    // microseconds each and would otherwise pay a graph launch every 2
+    const long span = (n_entries <= (1L << 17) && n_steps - n >= 10) ? 8 : 2;
     if (use_graph && method != KP_ROSENBROCK_EULER && n_steps - n >= 4) {
       cudaGraph_t graph;
       const unsigned long long l0 = ctx->launches;
       KP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-      // two steps: ub1 -> ub0 -> ub1 (n is odd here); t is unused by the
-      // closed set of g's (all autonomous), so replays stay exact
-      one(1);  // an odd step (slot 1 -> slot 0), then an even one
-      one(2);
+      // `span` steps starting at an odd one (n is odd here): ub1 -> ub0 ->
+      // ... -> ub1; t is unused by the closed set of g's (time-dependent
+      // ones read the device counter), so replays stay exact
+      for (long j = 1; j <= span; ++j) one(j);
       KP_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
       per = ctx->launches - l0;
       ctx->launches = l0;
@@ -813,10 +817,10 @@ class Integrator {
     }
     KP_CUDA(cudaEventRecord(ev[2], ctx->stream));
     if (exec) {
-      while (n_steps - n >= 2) {
+      while (n_steps - n >= span) {
         KP_CUDA(cudaGraphLaunch(exec, ctx->stream));
         ctx->launches += per;
-        n += 2;
+        n += span;
       }
     }
     while (n < n_steps) one(n++);
