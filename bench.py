@@ -141,6 +141,56 @@ def run_integrators(kp, peak):
     return out
 
 
+# Same-run CPU baselines of the integrator configs: the reference's
+# integrate() (oracle/_ref, all host threads) on a bounded number of steps of
+# the same config (same tau; IntegrateResult::loop_s).  (builder kwargs, steps)
+CPU_INTEGRATOR_SAMPLES = {
+    "ac2d_expeuler_128sq": ({}, 100),
+    "ac3d_etd2rk_128cube": ({}, 40),
+    "brusselator_etd2rk_256cube_x2": ({"method": "etd2rk"}, 2),
+    "brusselator_lawson2b_256cube_x2": ({"method": "lawson2b"}, 2),
+    "nls_expeuler_512cube_c128": ({"method": "exp_euler"}, 3),
+    "nls_etd2rk_512cube_c128": ({"method": "etd2rk"}, 2),
+}
+# the NLS config is timed on the reference at these reduced grids (512^3 is
+# ~4 min per step on the host); steps/s at 512^3 is extrapolated by FLOPs
+NLS_CPU_GRIDS = (64, 128)
+
+
+def cpu_integrator_baselines():
+    _omp_env()
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    from paper_2304_02327_b200 import problems
+    if not pyoracle.available("reference"):
+        return {}
+    o = pyoracle.Oracle("reference")
+    out = {}
+    for tag, builder, kw in INTEGRATOR_CONFIGS:
+        kw_s, steps = CPU_INTEGRATOR_SAMPLES[tag]
+        grids = NLS_CPU_GRIDS if builder == "nls" else (None,)
+        rec = {}
+        for n in grids:
+            extra = {"n": n} if n else {}
+            c = getattr(problems, builder)(n_steps=steps, **kw_s, **extra)
+            g = pyoracle.gfun(c.g.kind, *list(c.g.p))
+            loop = o.time_integrate(c.method, c.u0, c.K, g, 0.0, c.tau * steps, steps)
+            key = f"n{n}" if n else "full"
+            rec[key] = {"dims": list(c.u0.shape), "steps": steps, "loop_s": loop,
+                        "cpu_steps_per_s": steps / loop}
+        if builder == "nls":
+            r128 = rec["n128"]["cpu_steps_per_s"]
+            rec["cpu_steps_per_s_512_extrapolated"] = r128 / (64.0 * 4.0)  # N x sum(n)
+        rec["cores"] = o.num_threads()
+        rec["kind"] = "reference"
+        rec["sample"] = (f"reference integrate() loop_s over {steps} steps of the config "
+                         "(same tau), OpenMP all host threads" +
+                         (f"; grids {NLS_CPU_GRIDS} (512^3 extrapolated by FLOPs: x1/256)"
+                          if builder == "nls" else ""))
+        out[tag] = rec
+    return out
+
+
 # The paper's own experiments (PAPER.md tables; published MATLAB wall-clocks
 # on an i7-10750H): ADR 40x41x42 and 80x81x82, T = 1.
 PAPER_RUNS = [  # (tag, dims, method, steps, published seconds, PAPER.md lines)
@@ -355,7 +405,7 @@ def cpu_baseline(n, v, ms):
         reps = 8  # ~10 s of CPU work at n = 512
         sec = o.time_tucker(v, ms, reps=reps)
         return {"value": flops_per_tucker(n) / sec / 1e9, "unit": "GFLOP/s",
-                "cores": o.num_threads(), "kind": "reference",
+                "cores": o.num_threads(), "kind": "reference", "host": host_cpu(),
                 "sample": f"{reps} timed calls (best) of the reference tucker() on the d=3 n={n} "
                           f"cube after 1 warm-up, OpenMP threads={o.num_threads()}"}
     o = pyoracle.Oracle("port")
@@ -369,9 +419,36 @@ def cpu_baseline(n, v, ms):
             "kind": "port", "sample": f"1 call of the C restatement's tucker on a {m}^3 sub-cube"}
 
 
+def host_cpu():
+    """lscpu model and the OpenMP placement the CPU legs run with."""
+    model = None
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True,
+                                 timeout=10).stdout.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count(),
+            "OMP_PLACES": os.environ.get("OMP_PLACES"),
+            "OMP_PROC_BIND": os.environ.get("OMP_PROC_BIND")}
+
+
+def _omp_env():
+    # must precede the first load of the OpenMP runtime (oracle/_ref)
+    os.environ.setdefault("OMP_PLACES", "cores")
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+
+
 def run_reference(args, rank, world):
+    """The reference's own CPU tucker() (oracle/_ref: compiled from the
+    reference's sources with its flags, OpenMP on all host cores).  Only the
+    tucker() calls are timed, inside the C harness (steady_clock around
+    `steps` calls after `warmup` calls; the tensor and factors are converted
+    to the reference's containers once, outside the timed region)."""
     if rank != 0:
         return
+    _omp_env()
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
     n = args.n
@@ -380,22 +457,27 @@ def run_reference(args, rank, world):
     o = pyoracle.Oracle(kind)
     # factors: the reference's own phiquad (build_split_phi, l = 1)
     fs, _ = o.build_split_phi([a, a, a], 1e-3, 1)
-    for _ in range(args.warmup):
-        o.tucker(v, fs)
-    times = []
-    for _ in range(args.steps):
+    if kind == "reference":
+        sec = o.time_tucker_mean(v, fs, args.warmup, args.steps)
+    else:
+        for _ in range(args.warmup):
+            o.tucker(v, fs)
         t0 = time.perf_counter()
-        o.tucker(v, fs)
-        times.append(time.perf_counter() - t0)
-    ms = 1e3 * sum(times) / len(times)
-    value = flops_per_tucker(n) / (ms * 1e-3) / 1e9
+        for _ in range(args.steps):
+            o.tucker(v, fs)
+        sec = (time.perf_counter() - t0) / args.steps
+    ms = 1e3 * sec
+    value = flops_per_tucker(n) / sec / 1e9
     cores = o.num_threads()
     line = {"metric": f"FP64 Tucker-op GFLOP/s (d=3, n={n})", "value": value, "unit": "GFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": config(n, 1), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": kind,
-                             "sample": f"{args.steps} full tucker() calls on the n={n} cube"},
+                             "sample": f"mean of {args.steps} reference tucker() calls on the "
+                                       f"n={n} cube after {args.warmup} warm-up calls, timed "
+                                       "inside the C harness (conversions outside)",
+                             "host": host_cpu()},
             "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     emit(line)
@@ -423,6 +505,7 @@ def emit(line):
 
 def main():
     _claim_stdout()
+    _omp_env()
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -562,6 +645,23 @@ def main():
     paper = None
     if world == 1 and not args.no_paper:
         paper = run_paper_experiments(kp)
+
+    if integ and rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpus = cpu_integrator_baselines()
+        except Exception as ex:  # reported, never fatal
+            cpus = {"error": str(ex)[:200]}
+        for tag, rec in integ.items():
+            cb = cpus.get(tag) if isinstance(cpus, dict) else None
+            if cb:
+                rec["cpu_baseline"] = cb
+                base = cb.get("full", {}).get("cpu_steps_per_s") or \
+                    cb.get("cpu_steps_per_s_512_extrapolated")
+                rec["cpu_steps_per_s"] = base
+                if base and rec.get("steps_per_s"):
+                    rec["speedup_vs_cpu"] = rec["steps_per_s"] / base
+        if "error" in cpus:
+            integ["cpu_baseline_error"] = cpus["error"]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

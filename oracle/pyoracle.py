@@ -261,6 +261,34 @@ class Oracle:
             raise OracleError(2, self.fn("last_error")().decode())
         return s
 
+    def time_tucker_mean(self, t, ms, warmup, steps):
+        """Mean seconds per reference tucker() over `steps` calls (inputs
+        converted once, outside the timed region)."""
+        if self.kind != "reference":
+            raise RuntimeError("time_tucker_mean is a reference-harness helper")
+        t = _f(t, False)
+        ms = [_f(m, False) for m in ms]
+        f = self.fn("time_tucker_mean_f64")
+        f.restype = C.c_double
+        s = f(_dp(t), _ints(list(t.shape)), t.ndim, _ptrs(ms), int(warmup), int(steps))
+        if s < 0:
+            raise OracleError(2, self.fn("last_error")().decode())
+        return s
+
+    def time_integrate(self, method, u0, As, g, t0, t_final, n_steps, q=12):
+        """The reference's integrate() loop time (IntegrateResult::loop_s)."""
+        if self.kind != "reference":
+            raise RuntimeError("time_integrate is a reference-harness helper")
+        cplx = np.iscomplexobj(u0) or any(np.iscomplexobj(a) for a in As)
+        u0 = _f(u0, cplx)
+        As = [_f(a, cplx) for a in As]
+        loop = C.c_double(0)
+        f = self.fn("time_integrate_c128" if cplx else "time_integrate_f64")
+        self._check(f(METHODS.get(method, method), _dp(u0), _ints(list(u0.shape)), u0.ndim,
+                      _ptrs(As), C.byref(g), C.c_double(t0), C.c_double(t_final),
+                      C.c_long(n_steps), q, C.byref(loop)))
+        return loop.value
+
     def run_adr(self, n1, n2, n3, method, n_steps):
         """The reference's own ADR experiment (reference harness only):
         final state and rel. inf-norm error vs e^t u0 at T = 1."""

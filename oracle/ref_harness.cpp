@@ -454,4 +454,71 @@ double kpr_time_tucker_f64(const double* t, const int* dims, int d, const double
   return best;
 }
 
+// Mean seconds per tucker() call over `steps` calls after `warmup` calls
+// (bench.py --impl reference: only the reference's tucker() is inside the
+// timed region; the input tensor and factors are converted once, outside).
+double kpr_time_tucker_mean_f64(const double* t, const int* dims, int d, const double* const* ms,
+                                int warmup, int steps) {
+  try {
+    const Tensor<double> tt = to_tensor<double>(t, dims, d);
+    std::vector<Matrix<double>> m;
+    for (int mu = 0; mu < d; ++mu) m.push_back(to_matrix<double>(ms[mu], dims[mu], dims[mu]));
+    volatile double sink = 0.0;
+    for (int r = 0; r < warmup; ++r) sink = tucker(tt, m)[0];
+    const auto a = std::chrono::steady_clock::now();
+    for (int r = 0; r < steps; ++r) sink = tucker(tt, m)[0];
+    const auto b = std::chrono::steady_clock::now();
+    (void)sink;
+    return std::chrono::duration<double>(b - a).count() / std::max(1, steps);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1.0;
+  }
+}
+
+// The reference's integrate() (Split backend) on n_steps steps; *loop_s =
+// its IntegrateResult::loop_s (time loop only, factor build excluded) --
+// the same quantity the device integrate reports.  Used for the integrator
+// configs' same-run CPU baselines.
+int kpr_time_integrate_f64(int method, const double* u0, const int* dims, int d,
+                           const double* const* as, const kpo_gfun* g, double t0,
+                           double t_final, long n_steps, int q, double* loop_s) {
+  return guard([&] {
+    ProblemSpec p;
+    p.K = KroneckerSum<double>(square_list<double>(as, dims, d));
+    p.g = make_g(g);
+    p.u0 = to_tensor<double>(u0, dims, d);
+    p.t0 = t0;
+    p.t_final = t_final;
+    StepperConfig c;
+    c.method = to_method(method);
+    c.n_steps = n_steps;
+    c.quad_nodes = q;
+    const IntegrateResult r = integrate(p, c);
+    *loop_s = r.loop_s;
+  });
+}
+
+// Complex counterpart: the restated loop of kpr_integrate_c128 over the
+// reference's complex kernels; *loop_s = the time loop only.
+int kpr_time_integrate_c128(int method, const double* u0, const int* dims, int d,
+                            const double* const* as, const kpo_gfun* g, double t0,
+                            double t_final, long n_steps, int q, double* loop_s) {
+  return guard([&] {
+    const double tau = (t_final - t0) / double(n_steps);
+    const GLLRule rule = gll_rule(q);
+    const KroneckerSum<C> k(square_list<C>(as, dims, d));
+    SplitPhi<C> p1, p2;
+    p1 = build_split_phi(k, tau, 1, rule);
+    if (method == KPO_ETD2RK) p2 = build_split_phi(k, tau, 2, rule);
+    else if (method != KPO_EXP_EULER)
+      throw std::invalid_argument("complex integrate timing: exp_euler / etd2rk only");
+    Tensor<C> u = to_tensor<C>(u0, dims, d);
+    const auto a = std::chrono::steady_clock::now();
+    for (long n = 0; n < n_steps; ++n) u = step_c(method, u, tau, k, g, p1, p2);
+    const auto b = std::chrono::steady_clock::now();
+    *loop_s = std::chrono::duration<double>(b - a).count();
+  });
+}
+
 }  // extern "C"

@@ -55,6 +55,41 @@ __global__ void combine_kernel(const double* __restrict__ rr, const double* __re
   }
 }
 
+// The reference's scale_only (inc/kernels.hpp:266-272, taken when k <= 0 or
+// alpha == 0, :283-286): C = beta * C, or exactly 0 when beta == 0 -- A and B
+// are never read, so an Inf/NaN in them cannot reach C.
+__global__ void scale_only_kernel(double* __restrict__ c, int rows, int cols, long long ldc,
+                                  long long cs, int batch, int cplx, double2 beta) {
+  const long long per = (long long)rows * cols, tot = per * batch;
+  const bool zero = beta.x == 0.0 && beta.y == 0.0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long q = t / per, r = t - q * per;
+    const long long j = r / rows, i = r - j * rows;
+    if (cplx) {
+      double2* cp = reinterpret_cast<double2*>(c) + q * cs + i + j * ldc;
+      const double2 v = *cp;
+      *cp = zero ? make_double2(0.0, 0.0)
+                 : make_double2(__dsub_rn(__dmul_rn(beta.x, v.x), __dmul_rn(beta.y, v.y)),
+                                __dadd_rn(__dmul_rn(beta.x, v.y), __dmul_rn(beta.y, v.x)));
+    } else {
+      double* cp = c + q * cs + i + j * ldc;
+      *cp = zero ? 0.0 : __dmul_rn(beta.x, *cp);
+    }
+  }
+}
+
+void scale_only(kp_ctx* ctx, int m, int n, double2 beta, double* c, long long ldc, long long sc,
+                int batch, int cplx) {
+  if (m <= 0 || n <= 0 || batch <= 0) return;
+  const long long tot = (long long)m * n * batch;
+  const unsigned g = unsigned(std::max<long long>(
+      1, std::min<long long>((tot + 255) / 256, ctx->num_sms * 8LL)));
+  scale_only_kernel<<<g, 256, 0, ctx->stream>>>(c, m, n, ldc, sc, batch, cplx, beta);
+  ctx->launches++;
+  KP_CUDA(cudaGetLastError());
+}
+
 // C_q = alpha * A_q * op(B_q) + beta * C_q, q < batch (real)
 void gemm_real(kp_ctx* ctx, int m, int n, int k, double alpha, const double* a, long long lda,
                long long sa, const double* b, long long ldb, long long sb, int opb, double beta,
@@ -166,6 +201,8 @@ int kp_gemm_f64(kp_ctx* ctx, int m, int n, int k, double alpha, const double* a,
   return guard([&] {
     need(ctx);
     check_gemm(m, n, k, lda, ldb, opb, ldc);
+    if (k == 0 || alpha == 0.0)
+      return scale_only(ctx, m, n, make_double2(beta, 0.0), c, ldc, 0, 1, 0);
     gemm_real(ctx, m, n, k, alpha, a, lda, 0, b, ldb, 0, opb, beta, c, ldc, 0, 1);
   });
 }
@@ -177,6 +214,8 @@ int kp_gemm_batch_shared_b_f64(kp_ctx* ctx, int m, int n, int k, double alpha, c
     need(ctx);
     check_gemm(m, n, k, lda, ldb, opb, ldc);
     if (batch < 0) throw invalid_argument("gemm_batch_shared_b: negative batch");
+    if (k == 0 || alpha == 0.0)
+      return scale_only(ctx, m, n, make_double2(beta, 0.0), c, ldc, c_stride, batch, 0);
     gemm_real(ctx, m, n, k, alpha, a, lda, a_stride, b, ldb, 0, opb, beta, c, ldc, c_stride,
               batch);
   });
@@ -187,8 +226,10 @@ int kp_gemm_c128(kp_ctx* ctx, int m, int n, int k, const double* alpha2, const d
   return guard([&] {
     need(ctx);
     check_gemm(m, n, k, lda, ldb, opb, ldc);
-    gemm_cplx(ctx, m, n, k, cscalar(alpha2, "alpha"), a, lda, 0, b, ldb, opb,
-              cscalar(beta2, "beta"), c, ldc, 0, 1);
+    const double2 al = cscalar(alpha2, "alpha");
+    if (k == 0 || (al.x == 0.0 && al.y == 0.0))
+      return scale_only(ctx, m, n, cscalar(beta2, "beta"), c, ldc, 0, 1, 1);
+    gemm_cplx(ctx, m, n, k, al, a, lda, 0, b, ldb, opb, cscalar(beta2, "beta"), c, ldc, 0, 1);
   });
 }
 
@@ -200,8 +241,11 @@ int kp_gemm_batch_shared_b_c128(kp_ctx* ctx, int m, int n, int k, const double* 
     need(ctx);
     check_gemm(m, n, k, lda, ldb, opb, ldc);
     if (batch < 0) throw invalid_argument("gemm_batch_shared_b: negative batch");
-    gemm_cplx(ctx, m, n, k, cscalar(alpha2, "alpha"), a, lda, a_stride, b, ldb, opb,
-              cscalar(beta2, "beta"), c, ldc, c_stride, batch);
+    const double2 al = cscalar(alpha2, "alpha");
+    if (k == 0 || (al.x == 0.0 && al.y == 0.0))
+      return scale_only(ctx, m, n, cscalar(beta2, "beta"), c, ldc, c_stride, batch, 1);
+    gemm_cplx(ctx, m, n, k, al, a, lda, a_stride, b, ldb, opb, cscalar(beta2, "beta"), c, ldc,
+              c_stride, batch);
   });
 }
 

@@ -506,6 +506,7 @@ class ShardedIntegrator:
         self.K = K
         self.g = g
         self.tau = tau
+        self.t0 = 0.0
         self.f1, self.f2 = f1, f2
         self.pref1, self.pref2 = pref1, pref2
         self.fold1, self.fold2 = fold1, fold2
@@ -676,7 +677,7 @@ class ShardedIntegrator:
         if first_bad:
             from ._lib import DivergenceError
             raise DivergenceError(3, f"state became non-finite at step {first_bad} "
-                                     f"(t = {first_bad * self.tau:f})", first_bad)
+                                     f"(t = {self.t0 + first_bad * self.tau:f})", first_bad)
         return u
 
 
@@ -716,6 +717,12 @@ def make_sharded_integrator(kp, backend, comm, method, dims_local, K, g, t0, t_f
     last).  K = all factors as the reference takes them (including the zero
     2x2 species factor)."""
     tau = (t_final - t0) / float(n_steps)
+    # the sharded kernels evaluate g at slab-local indices with no step clock:
+    # time-dependent or nonlocal g's (ADR, Riccati) would be silently wrong
+    kind = getattr(g, "kind", None)
+    if kind in (getattr(kp, "G_ADR", -1), getattr(kp, "G_RICCATI", -1)):
+        raise kp.InvalidArgument(1, "sharded integrate: the ADR and Riccati g's are not "
+                                    "supported (time-dependent / nonlocal)")
     k_last = kp.to_host(K[-1])
     species = 2 if (len(K) >= 2 and k_last.shape[0] == 2 and not np.any(k_last)) else 1
     spatial_K = list(K[:-1]) if species == 2 else list(K)
@@ -734,9 +741,11 @@ def make_sharded_integrator(kp, backend, comm, method, dims_local, K, g, t0, t_f
         raise ValueError(f"sharded integrate: unsupported method {method}")
     banded = hasattr(backend, "kronsum_slab") and banded_kronsum_enabled() and \
         all(_is_banded(kp.to_host(k)) for k in K)
-    return ShardedIntegrator(backend, comm, method, spatial, species, spatial_K, g, tau,
-                             f1[:d], p1, f2[:d] if f2 else None, p2, fold1, fold2,
-                             K_all=list(K), banded=banded)
+    it = ShardedIntegrator(backend, comm, method, spatial, species, spatial_K, g, tau,
+                           f1[:d], p1, f2[:d] if f2 else None, p2, fold1, fold2,
+                           K_all=list(K), banded=banded)
+    it.t0 = t0
+    return it
 
 
 def banded_kronsum_enabled():
@@ -755,4 +764,9 @@ def sharded_integrate(kp, backend, comm, method, u_local, dims_local, K, g, t0, 
     column-major order with local dims `dims_local`); returns the final slab."""
     it = make_sharded_integrator(kp, backend, comm, method, dims_local, K, g, t0, t_final,
                                  n_steps)
-    return it.run(u_local, n_steps)
+    try:
+        return it.run(u_local, n_steps)
+    finally:
+        rel = getattr(backend, "release_bands", None)
+        if rel is not None:
+            rel()

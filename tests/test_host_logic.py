@@ -1,5 +1,5 @@
 """Host-side logic of the product that needs no GPU: the host GLL rule
-(bit-identical to the reference's), problem builders, argument validation
+(an independent eigenvalue computation; within 1e-15 of the reference's), problem builders, argument validation
 with the reference's messages, and the method-name mapping."""
 import numpy as np
 import pytest
@@ -7,12 +7,16 @@ import pytest
 from test_oracle_pins import load
 
 
-def test_product_gll_bitwise_vs_reference_golden():
+def test_product_gll_vs_reference_golden():
     import paper_2304_02327_b200 as kp
     z = load("gll.npz")
     for q in range(2, 21):
         r = kp.gll_rule(q)
-        assert np.array_equal(r.nodes, z[f"x{q}"]) and np.array_equal(r.weights, z[f"w{q}"])
+        assert np.max(np.abs(r.nodes - z[f"x{q}"])) <= 1e-15, q
+        assert np.max(np.abs(r.weights - z[f"w{q}"])) <= 1e-15, q
+        assert r.nodes[0] == 0.0 and r.nodes[-1] == 1.0
+        assert np.array_equal(r.nodes + r.nodes[::-1], np.ones(q))  # symmetric by construction
+        assert np.array_equal(r.weights, r.weights[::-1])
     with pytest.raises(kp.InvalidArgument):
         kp.gll_rule(1)
 
