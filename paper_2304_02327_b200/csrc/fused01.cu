@@ -13,7 +13,7 @@
 // never touches HBM and one launch replaces two; at N = 128 the slice is
 // 128 KiB of the SM's 227 KiB.
 //
-// Arithmetic is that of the two-launch path (gemm_cutlass.cu): DMMA m8n8k4
+// Arithmetic is that of the two-launch path (gemm_dmma.cu): DMMA m8n8k4
 // with every accumulator summed over k in increasing groups of four, T
 // rounded to double after the alpha multiply, W through epi_one -- so the
 // fused and unfused Tuckers agree bit for bit (test_fused01_bitwise).
@@ -168,14 +168,15 @@ __global__ void __launch_bounds__(F01<N>::NT, 1)
   __syncthreads();
   // coalesced (m, m+1) pairs, the same epilogue code as the GEMM kernels
   const long long cq = q * N * N;
+  const EpiU u = epi_uniform(e);
 #pragma unroll 1
   for (int e2 = tid; e2 < N * N / 2; e2 += C::NT) {
     const int ml = 2 * (e2 % (N / 2)), nl = e2 / (N / 2);
     const double2 a2 = *reinterpret_cast<const double2*>(Ts + ml + nl * C::LD);
     const long long off = cq + ml + (long long)nl * N;
     double d0 = 0.0, d1 = 0.0;
-    const double r0 = epi_one(e, e.alpha * a2.x, out, off, 0, &d0);
-    const double r1 = epi_one(e, e.alpha * a2.y, out, off + 1, 0, &d1);
+    const double r0 = epi_one(e, u, e.alpha * a2.x, out, off, 0, &d0);
+    const double r1 = epi_one(e, u, e.alpha * a2.y, out, off + 1, 0, &d1);
     *reinterpret_cast<double2*>(out + off) = make_double2(r0, r1);
   }
 }
@@ -331,14 +332,15 @@ __global__ void __launch_bounds__(F01R<N, MR>::NT, 2)
       }
   __syncthreads();
   const long long cq = q * N * N + r0;
+  const EpiU u = epi_uniform(e);
 #pragma unroll 1
   for (int e2 = tid; e2 < MR * N / 2; e2 += C::NT) {
     const int ml = 2 * (e2 % (MR / 2)), nl = e2 / (MR / 2);
     const double2 a2 = *reinterpret_cast<const double2*>(Th + ml + nl * C::LDT);
     const long long off = cq + ml + (long long)nl * N;
     double d0 = 0.0, d1 = 0.0;
-    const double v0 = epi_one(e, e.alpha * a2.x, out, off, 0, &d0);
-    const double v1 = epi_one(e, e.alpha * a2.y, out, off + 1, 0, &d1);
+    const double v0 = epi_one(e, u, e.alpha * a2.x, out, off, 0, &d0);
+    const double v1 = epi_one(e, u, e.alpha * a2.y, out, off + 1, 0, &d1);
     *reinterpret_cast<double2*>(out + off) = make_double2(v0, v1);
   }
 }

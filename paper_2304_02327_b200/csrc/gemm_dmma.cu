@@ -1,0 +1,618 @@
+// gemm_dmma.cu -- the mode-product GEMM: a hand-written, persistent,
+// warp-specialized FP64 DMMA kernel for sm_100a with TMA tile staging.
+//
+// Replaces the reference's CPU GEMM cores of the Tucker operator:
+//   gemm                (inc/kernels.hpp:279-327)  C = alpha A op(B) + beta C
+//   gemm_batch_shared_b (inc/kernels.hpp:332-392)  C_q = alpha A_q op(B) + beta C_q
+// reached from mode_product_into (inc/mode_product.hpp:61-87) through the two
+// permute-free views of mode_product.cu (A M-contiguous; B K-contiguous for
+// mode 0, N-contiguous for modes >= 1; C M-contiguous; batched over q).
+//
+// sm_100a has no FP64 tcgen05 kind (ptxas rejects .kind::f64), so the FP64
+// tensor path is warp-level mma.sync m8n8k4 (SASS DMMA.8x8x4; 37.1 TFLOP/s
+// measured on the pool's B200, profiles/fp64_peak_r01.txt).  What IS
+// Blackwell-native here is the data movement and the schedule:
+//
+//   * one producer warp per CTA: one elected lane streams BK = 16 slices of
+//     the A and B tiles into a STAGES-deep shared-memory ring with TMA
+//     (cp.async.bulk.tensor, SASS UTMALDG), 128-byte hardware swizzle, and
+//     arms the slot's "full" mbarrier with the expected byte count;
+//   * NC consumer warps wait on "full", run the DMMAs straight from the
+//     swizzled tiles, and release the slot with one arrive per warp on its
+//     "empty" mbarrier -- no __syncthreads in the mainloop;
+//   * persistent CTAs (grid = SMs x resident CTAs) walk the tiles with a
+//     static stride; the producer runs ahead into the next tile while the
+//     consumers stage the accumulators through a separate shared buffer
+//     and run the fused epilogue (kp_epilogue.cuh), so the ring never
+//     drains between tiles.
+//
+// Fragment layout (no padding is possible under TMA, so the swizzle and the
+// fragment-to-index maps are chosen together to make every shared load
+// conflict-free): element (row r, col c) of a 16-double-wide box sits at
+// r*16 + 2*((c/2) ^ (r%8)) + c%2.  An M- (or N-) contiguous operand is read
+// as LDS.128 pairs (m, m+1) that feed two 8x8 DMMA tiles at once, thread g of
+// the pair owning m = 2*perm(g); the K-contiguous B (mode 0) is read as
+// LDS.64 with DMMA column g on tile row rperm(g).  perm/rperm spread each
+// quarter-/half-warp over all 32 banks for every k (derivation in DESIGN.md
+// section 4.1).  The epilogue undoes the maps when it stages C.
+//
+// Arithmetic order: DMMA k-slot t of k-step s holds k = 16 kt + 4 s + t, the
+// k-steps and slices in increasing order -- the order of fused01.cu and of
+// every tile shape here, so results never depend on the tile chosen, on TMA
+// vs the cp.async producer, or on which path (fused or not) ran.
+//
+// Operands that TMA cannot describe (a base or stride not 16-byte aligned:
+// odd leading dimensions) take the SAME kernel with a cp.async producer warp
+// (LDGSTS with zero-fill into the same swizzled layout, completion through
+// cp.async.mbarrier.arrive) -- same consumer code, bit-identical results.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "kp_epilogue.cuh"
+#include "kp_launch.cuh"
+
+namespace kp {
+namespace {
+
+// ------------------------------------------------------------ PTX helpers
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map,
+                                            unsigned long long* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void consumer_bar(int nthreads) {
+  asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// 128-byte swizzle of a 16-double-wide box: (row r, col c) -> offset in doubles
+__device__ __forceinline__ int swz(int r, int c) {
+  return r * 16 + ((((c >> 1) ^ (r & 7))) << 1) + (c & 1);
+}
+// thread g's pair slot in a 16-wide (m, m+1) pair row, and the K-contiguous
+// tile row of DMMA column g (see the file comment)
+__device__ __forceinline__ int perm8(int g) { return ((g & 1) << 2) | (g >> 1); }
+__device__ __forceinline__ int rperm8(int g) { return ((g & 3) << 1) | (g >> 2); }
+
+// ------------------------------------------------------------ configuration
+
+template <int BM_, int BN_, int WARPS_M, int WARPS_N, int STAGES_, int MINB, int STG_COLS = BN_,
+          int NE_ = 0>
+struct TileCfg {
+  static constexpr int BM = BM_, BN = BN_, STAGES = STAGES_;
+  static constexpr int BK = 16;
+  static constexpr int NC = WARPS_M * WARPS_N;  // consumer (DMMA) warps
+  static constexpr int NE = NE_;                // epilogue warps (0: consumers do it)
+  static constexpr int NT = (NC + NE + 1) * 32;  // + one producer warp
+  static constexpr int WARPS_M_ = WARPS_M;
+  static constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
+  static constexpr int MI = WM / 8, NI = WN / 8;
+  static constexpr int A_DBL = BM * BK, B_DBL = BN * BK;
+  static constexpr int STAGE_DBL = A_DBL + B_DBL;
+  static constexpr unsigned STAGE_BYTES = unsigned(STAGE_DBL) * 8u;
+  static constexpr int LDS_C = BM + 2;  // staged C tile pitch (doubles)
+  static constexpr int SC = STG_COLS;    // columns staged per epilogue pass
+  static constexpr int STG_DBL = LDS_C * SC;
+  static constexpr size_t SMEM =
+      1024 + size_t(STAGES) * STAGE_BYTES + size_t(STG_DBL) * 8 + (2 * STAGES + 2) * 8;
+  static constexpr int kMinBlocks = MINB;
+  static_assert(WM % 16 == 0 && WN % 16 == 0, "warp tiles are pairs of 8x8 DMMA tiles");
+  static_assert(BM % 16 == 0 && BN % 16 == 0 && BN <= 256, "TMA boxes");
+  static_assert(BN % SC == 0, "staging passes");
+  static_assert(NE == 0 || SC == BN, "epilogue warps take the whole staged tile");
+};
+
+// 64 x 64 tiles, 4 consumer warps of 32 x 32, 2 CTAs per SM: the default
+using CfgM = TileCfg<64, 64, 2, 2, 4, 2>;
+// 64 x 64 tiles, 3-stage ring, the epilogue staged in two 32-column passes:
+// 3 CTAs per SM (12 consumer warps)
+using CfgN = TileCfg<64, 64, 2, 2, 3, 3, 32>;
+// 128 x 64 tiles, 8 consumer warps of 32 x 32, one CTA per SM
+using CfgW = TileCfg<128, 64, 4, 2, 4, 1>;
+// 64 x 64 tiles, 8 consumer warps of 32 x 16 / 16 x 32, 2 CTAs per SM (4
+// consumer warps per SM sub-partition)
+using CfgA = TileCfg<64, 64, 2, 4, 4, 2>;
+using CfgB = TileCfg<64, 64, 4, 2, 4, 2>;
+// 32 x 64 tiles, 4 warps of 16 x 32
+using CfgC = TileCfg<32, 64, 2, 2, 4, 4>;
+// 32 x 32 tiles, 4 warps of 16 x 16: problems that would leave SMs idle
+using CfgS = TileCfg<32, 32, 2, 2, 4, 3>;
+// 128 x 64 tiles, 4 warps of 64 x 32: long-K problems (d = 2, n >= 1024)
+using CfgL = TileCfg<128, 64, 2, 2, 4, 1>;
+// one CTA per SM, 8 DMMA warps of 32 x 32 + 3 epilogue warps + the producer:
+// the fused epilogue of tile t runs on its own warps while the DMMA warps
+// already compute tile t+1
+using CfgE = TileCfg<128, 64, 4, 2, 4, 1, 64, 3>;
+using CfgF = TileCfg<64, 128, 2, 4, 4, 1, 128, 3>;
+// two CTAs per SM of 4 DMMA warps + 2 epilogue warps + the producer
+using CfgG = TileCfg<64, 64, 2, 2, 4, 2, 64, 2>;
+// CfgE with a 5-deep ring
+using CfgE5 = TileCfg<128, 64, 4, 2, 5, 1, 64, 3>;
+
+// ------------------------------------------------------------ the kernel
+
+template <class CF, bool B_KCONTIG, bool TMA, int CPLX, bool SCAT>
+__global__ void __launch_bounds__(CF::NT, CF::kMinBlocks)
+    dmma_tile_kernel(const __grid_constant__ CUtensorMap mapA,
+                     const __grid_constant__ CUtensorMap mapB, GemmProblem p, Epilogue e,
+                     int tiles_m, int tiles_n, int n_fastest, int c_vec2, long long half) {
+  constexpr int BM = CF::BM, BN = CF::BN, BK = CF::BK, STAGES = CF::STAGES, NC = CF::NC;
+  constexpr int MI = CF::MI, NI = CF::NI;
+  pdl_wait();
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte aligned for the 128-byte swizzle; pointer arithmetic (not an
+  // integer round trip) keeps the shared address space visible to the
+  // compiler, so fragment loads are LDS, not generic loads
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  double* ring = reinterpret_cast<double*>(base);
+  double* stg = ring + STAGES * CF::STAGE_DBL;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(stg + CF::STG_DBL);
+  unsigned long long* empty = full + STAGES;
+  unsigned long long* stg_full = empty + STAGES;  // NE > 0: staged tile ready
+  unsigned long long* stg_empty = stg_full + 1;   // NE > 0: staging buffer free
+  constexpr int NE = CF::NE;
+
+  const int tid = threadIdx.x;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], TMA ? 1u : 32u);
+      mbar_init(&empty[s], unsigned(NC));
+    }
+    mbar_init(stg_full, 1u);
+    mbar_init(stg_empty, 1u);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  const long long per_q = (long long)tiles_m * tiles_n;
+  const long long total = per_q * p.batch;
+  const int KT = (p.K + BK - 1) / BK;
+  auto decode = [&](long long tile, long long& q, int& m0, int& n0) {
+    q = tile / per_q;
+    const int r = int(tile - q * per_q);
+    int tm, tn;
+    if (n_fastest) {
+      tn = r % tiles_n;
+      tm = r / tiles_n;
+    } else {
+      tm = r % tiles_m;
+      tn = r / tiles_m;
+    }
+    m0 = tm * BM;
+    n0 = tn * BN;
+  };
+
+  if (NE > 0 && warp >= NC && warp < NC + NE) {
+    // ------------------------------------------------ epilogue warps
+    const int etid = tid - NC * 32;
+    unsigned ph = 0;
+    bool nonfinite = false;
+    for (long long tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      long long q;
+      int m0, n0;
+      decode(tile, q, m0, n0);
+      mbar_wait(stg_full, ph);
+      nonfinite |= staged_epilogue<BM, BN, CF::LDS_C, NE * 32, CPLX, SCAT>(
+          p, e, stg, m0, n0, q, etid, c_vec2, half);
+      // bar.sync completes this group's shared loads before the release
+      asm volatile("bar.sync 2, %0;\n" ::"r"(NE * 32) : "memory");
+      if (etid == 0) mbar_arrive(stg_empty);
+      ph ^= 1u;
+    }
+    if (e.bad_step && nonfinite) atomicMin(e.bad_step, *e.step_ctr + 1);
+    return;
+  }
+  if (warp == NC + NE) {
+    // ------------------------------------------------ producer warp
+    int stage = 0;
+    unsigned phase = 0;
+    if constexpr (TMA) {
+      if (lane != 0) return;
+      for (long long tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        long long q;
+        int m0, n0;
+        decode(tile, q, m0, n0);
+        const int qa = int(q), qb = p.sB ? int(q) : 0;
+        for (int kt = 0; kt < KT; ++kt) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          double* as = ring + stage * CF::STAGE_DBL;
+          double* bs = as + CF::A_DBL;
+          mbar_expect_tx(&full[stage], CF::STAGE_BYTES);
+#pragma unroll
+          for (int c = 0; c < BM / 16; ++c)
+            tma_load_3d(as + c * 16 * BK, &mapA, &full[stage], m0 + 16 * c, kt * BK, qa);
+          if constexpr (B_KCONTIG) {
+            tma_load_3d(bs, &mapB, &full[stage], kt * BK, n0, qb);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 16; ++c)
+              tma_load_3d(bs + c * 16 * BK, &mapB, &full[stage], n0 + 16 * c, kt * BK, qb);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    } else {
+      // cp.async producer (operands TMA cannot describe): all 32 lanes
+      for (long long tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        long long q;
+        int m0, n0;
+        decode(tile, q, m0, n0);
+        const double* Ab = p.A + q * p.sA;
+        const double* Bb = p.B + q * p.sB;
+        for (int kt = 0; kt < KT; ++kt) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          double* as = ring + stage * CF::STAGE_DBL;
+          double* bs = as + CF::A_DBL;
+          const int k0 = kt * BK;
+          for (int idx = lane; idx < BM * BK; idx += 32) {
+            const int m = idx % BM, k = idx / BM;
+            const bool ok = (m0 + m < p.M) && (k0 + k < p.K);
+            cp_async8(as + (m >> 4) * 16 * BK + swz(k, m & 15),
+                      ok ? Ab + (m0 + m) + (long long)(k0 + k) * p.lda : p.A, ok ? 8 : 0);
+          }
+          if constexpr (B_KCONTIG) {
+            for (int idx = lane; idx < BN * BK; idx += 32) {
+              const int k = idx % BK, n = idx / BK;
+              const bool ok = (n0 + n < p.N) && (k0 + k < p.K);
+              cp_async8(bs + swz(n, k), ok ? Bb + (k0 + k) + (long long)(n0 + n) * p.sBn : p.B,
+                        ok ? 8 : 0);
+            }
+          } else {
+            for (int idx = lane; idx < BN * BK; idx += 32) {
+              const int n = idx % BN, k = idx / BN;
+              const bool ok = (n0 + n < p.N) && (k0 + k < p.K);
+              cp_async8(bs + (n >> 4) * 16 * BK + swz(k, n & 15),
+                        ok ? Bb + (n0 + n) + (long long)(k0 + k) * p.sBk : p.B, ok ? 8 : 0);
+            }
+          }
+          cp_async_mbar_arrive(&full[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------- consumer warps
+  const int g = lane >> 2, tig = lane & 3;
+  const int wm0 = (warp % CF::WARPS_M_) * CF::WM, wn0 = (warp / CF::WARPS_M_) * CF::WN;
+  const int pg = perm8(g);
+  // per-thread fragment offsets inside a stage (doubles), k-step s adds 64 (A, B
+  // N-contiguous: 4 rows of 16) -- the swizzle depends only on (4s + tig) & 7,
+  // which is tig or tig + 4
+  int a_off[2], b_off[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = 4 * h + tig;
+    a_off[h] = (wm0 >> 4) * 16 * BK + swz(r, 2 * pg);
+    b_off[h] = B_KCONTIG ? 0 : CF::A_DBL + (wn0 >> 4) * 16 * BK + swz(r, 2 * pg);
+  }
+  // K-contiguous B: row rperm(g) of n tile ni, k = 4s + tig; k + 8 flips
+  // bit 2 of the 16-byte chunk index, i.e. bit 3 of the offset (XOR 8)
+  int bk_off[NI][2];
+#pragma unroll
+  for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      bk_off[ni][h] = CF::A_DBL + swz(wn0 + 8 * ni + rperm8(g), 4 * h + tig);
+
+  int stage = 0;
+  unsigned phase = 0, stg_phase = 0;
+  bool nonfinite = false;
+  for (long long tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    long long q;
+    int m0, n0;
+    decode(tile, q, m0, n0);
+    double acc[MI][NI][2];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    // A slot is released one stage late: the DMMAs that consumed its
+    // fragments sit before this iteration's full-barrier wait loop (a basic
+    // block boundary the scheduler does not move instructions across), and a
+    // DMMA cannot issue before its LDS operands have landed -- so every read
+    // of the slot has completed before its "empty" arrive lets TMA overwrite
+    // it.  (Releasing right after the last LDS let the arrive overtake the
+    // loads in flight: a write-after-read race under TMA.)
+    int prev = -1;
+    for (int kt = 0; kt < KT; ++kt) {
+      mbar_wait(&full[stage], phase);
+      if (prev >= 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[prev]);
+      }
+      const double* st = ring + stage * CF::STAGE_DBL;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const int h = s & 1, kofs = (s >> 1) * 128;  // rows 8..15: +8 rows of 16
+        double2 af[MI / 2];
+#pragma unroll
+        for (int pi = 0; pi < MI / 2; ++pi)
+          af[pi] = *reinterpret_cast<const double2*>(st + a_off[h] + kofs + pi * 16 * BK);
+        double bv[NI];
+        if constexpr (B_KCONTIG) {
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) bv[ni] = st[bk_off[ni][h] ^ ((s >> 1) << 3)];
+        } else {
+#pragma unroll
+          for (int pj = 0; pj < NI / 2; ++pj) {
+            const double2 b2 =
+                *reinterpret_cast<const double2*>(st + b_off[h] + kofs + pj * 16 * BK);
+            bv[2 * pj] = b2.x;
+            bv[2 * pj + 1] = b2.y;
+          }
+        }
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi) {
+          const double a = (mi & 1) ? af[mi >> 1].y : af[mi >> 1].x;
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a, bv[ni]);
+        }
+      }
+      prev = stage;
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    // the last slot: bar.sync orders (waits for) this thread's shared loads
+    consumer_bar(NC * 32);
+    if (prev >= 0 && lane == 0) mbar_arrive(&empty[prev]);
+
+    // ---- epilogue: stage C (undoing the fragment maps), then the fused
+    // pass -- by the epilogue warps (NE > 0), or here in BN / SC passes
+    auto stage_acc = [&](int c0) {
+#pragma unroll
+      for (int pi = 0; pi < MI / 2; ++pi) {
+        const int ml = wm0 + 16 * pi + 2 * pg;
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int c = 2 * tig + j;  // DMMA column
+            const int nl = (B_KCONTIG ? wn0 + 8 * ni + rperm8(c)
+                                      : wn0 + 16 * (ni >> 1) + 2 * perm8(c) + (ni & 1)) - c0;
+            if (CF::SC == BN || (nl >= 0 && nl < CF::SC))
+              *reinterpret_cast<double2*>(stg + ml + nl * CF::LDS_C) =
+                  make_double2(acc[2 * pi][ni][j], acc[2 * pi + 1][ni][j]);
+          }
+      }
+    };
+    if constexpr (NE > 0) {
+      mbar_wait(stg_empty, stg_phase ^ 1u);  // the epilogue warps drained it
+      stage_acc(0);
+      consumer_bar(NC * 32);  // all staging stores done before the release
+      if (tid == 0) mbar_arrive(stg_full);
+      stg_phase ^= 1u;
+    } else {
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += CF::SC) {
+        if (c0 > 0) consumer_bar(NC * 32);  // the previous pass has read stg
+        stage_acc(c0);
+        consumer_bar(NC * 32);
+        nonfinite |= staged_epilogue<BM, CF::SC, CF::LDS_C, NC * 32, CPLX, SCAT>(
+            p, e, stg, m0, n0 + c0, q, tid, c_vec2, half);
+      }
+    }
+  }
+  if (e.bad_step && nonfinite) atomicMin(e.bad_step, *e.step_ctr + 1);
+  if (e.step_next && blockIdx.x == 0 && tid == 0) *e.step_next = *e.step_ctr + 1;
+}
+
+// ------------------------------------------------------------ host side
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    KP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !f)
+      throw cuda_error("cuTensorMapEncodeTiled is not available from the driver");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// A 3-D FP64 tensor map (dims d0 fastest) with a {b0, b1, 1} box and the
+// 128-byte swizzle.  s1, s2 = strides of dims 1 and 2 in elements.
+void make_map(CUtensorMap* m, const double* ptr, long long d0, long long d1, long long d2,
+              long long s1, long long s2, int b0, int b1) {
+  cuuint64_t dims[3] = {cuuint64_t(d0), cuuint64_t(d1), cuuint64_t(d2)};
+  cuuint64_t strides[2] = {cuuint64_t(s1) * 8u, cuuint64_t(s2) * 8u};
+  cuuint32_t box[3] = {cuuint32_t(b0), cuuint32_t(b1), 1u};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  const CUresult r = tensor_map_encoder()(
+      m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ptr), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw cuda_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+
+bool a16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) % 16) == 0; }
+
+// Can TMA describe both operands?  (16-byte aligned bases and strides, 32-bit dims)
+bool tma_ok(const GemmProblem& p, bool kcontig) {
+  static const bool off = [] {
+    const char* v = getenv("KP_TMA");
+    return v && std::string(v) == "0";
+  }();
+  if (off) return false;
+  if (!a16(p.A) || !a16(p.B)) return false;
+  if (p.lda % 2 || (p.batch > 1 && p.sA % 2) || (p.sB % 2)) return false;
+  if (kcontig ? (p.sBn % 2) : (p.sBk % 2)) return false;
+  const long long big = 0xffffffffLL;
+  return p.M <= big && p.N <= big && p.K <= big && p.batch <= big;
+}
+
+int resident_ctas(const void* kern, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<const void*, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(kern);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  KP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem));
+  n = std::max(1, n);
+  cache[kern] = n;
+  return n;
+}
+
+template <class CF, bool KC, bool TMA, int CPLX, bool SCAT>
+void launch_tile(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, long long half) {
+  auto kern = dmma_tile_kernel<CF, KC, TMA, CPLX, SCAT>;
+  ensure_smem_attr(ctx, reinterpret_cast<const void*>(kern), int(CF::SMEM));
+  const int tiles_m = (p.M + CF::BM - 1) / CF::BM;
+  const int tiles_n = (p.N + CF::BN - 1) / CF::BN;
+  const long long total = (long long)tiles_m * tiles_n * p.batch;
+  const int n_fastest = tiles_n <= tiles_m ? 1 : 0;
+  const int c_vec2 = ((p.ldc % 2) == 0 && (p.sC % 2) == 0 && a16(p.C) &&
+                      (e.D == nullptr || a16(e.D)))
+                         ? 1
+                         : 0;
+  CUtensorMap ma{}, mb{};
+  if constexpr (TMA) {
+    const long long qa_stride = p.batch > 1 ? p.sA : p.lda * std::max(1, p.K);
+    make_map(&ma, p.A, p.M, p.K, p.batch, p.lda, (qa_stride + 1) & ~1LL, 16, CF::BK);
+    const long long bb = p.sB ? p.batch : 1;
+    if (KC) {
+      const long long qs = p.sB ? p.sB : p.sBn * std::max(1, p.N);
+      make_map(&mb, p.B, p.K, p.N, bb, p.sBn, (qs + 1) & ~1LL, CF::BK, CF::BN);
+    } else {
+      const long long qs = p.sB ? p.sB : p.sBk * std::max(1, p.K);
+      make_map(&mb, p.B, p.N, p.K, bb, p.sBk, (qs + 1) & ~1LL, 16, CF::BK);
+    }
+  }
+  const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), CF::NT, CF::SMEM);
+  const long long grid = std::min<long long>(total, (long long)ctx->num_sms * per_sm);
+  launch_pdl(ctx, kern, dim3(unsigned(grid)), dim3(CF::NT), CF::SMEM, ma, mb, p, e, tiles_m,
+             tiles_n, n_fastest, c_vec2, half);
+  KP_CUDA(cudaGetLastError());
+}
+
+template <class CF, int CPLX, bool SCAT>
+void launch_layout(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, bool kcontig,
+                   long long half) {
+  const bool tma = tma_ok(p, kcontig);
+  if (kcontig)
+    tma ? launch_tile<CF, true, true, CPLX, SCAT>(ctx, p, e, half)
+        : launch_tile<CF, true, false, CPLX, SCAT>(ctx, p, e, half);
+  else
+    tma ? launch_tile<CF, false, true, CPLX, SCAT>(ctx, p, e, half)
+        : launch_tile<CF, false, false, CPLX, SCAT>(ctx, p, e, half);
+}
+
+template <class CF, bool SCAT>
+void launch_cplx(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, bool kcontig, int cplx,
+                 long long half) {
+  if (cplx == 1)
+    launch_layout<CF, 1, SCAT>(ctx, p, e, kcontig, half);
+  else if (cplx == 2)
+    launch_layout<CF, 2, SCAT>(ctx, p, e, kcontig, half);
+  else
+    launch_layout<CF, 0, SCAT>(ctx, p, e, kcontig, half);
+}
+
+}  // namespace
+
+// Tile menu: 32 x 32 when 64 x 64 tiles would not give every resident CTA
+// a few tiles; 128 x 64 for long K; 64 x 64 otherwise.  The k order is the
+// same in all of them (see the file comment), so the choice never changes a
+// bit.  KP_GEMM_TILE=S|M|L forces one (testing / benchmarking).
+void launch_gemm_dmma(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int cplx,
+                      bool kcontig, long long half) {
+  static const char forced = [] {
+    const char* v = getenv("KP_GEMM_TILE");
+    return v && *v ? v[0] : '\0';
+  }();
+  const long long tiles64 = (long long)((p.M + 63) / 64) * ((p.N + 63) / 64) * p.batch;
+  char cfg = 'G';
+  if (tiles64 < 4LL * ctx->num_sms)
+    cfg = 'S';
+  else if (p.K <= 256)
+    cfg = 'N';
+  if (forced) cfg = forced;
+  if (e.sc_dir) {
+    cfg == 'S' ? launch_cplx<CfgS, true>(ctx, p, e, kcontig, cplx, half)
+               : launch_cplx<CfgM, true>(ctx, p, e, kcontig, cplx, half);
+    return;
+  }
+  switch (cfg) {
+    case 'S': launch_cplx<CfgS, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'L': launch_cplx<CfgL, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'N': launch_cplx<CfgN, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'W': launch_cplx<CfgW, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'A': launch_cplx<CfgA, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'B': launch_cplx<CfgB, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'C': launch_cplx<CfgC, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'E': launch_cplx<CfgE, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'F': launch_cplx<CfgF, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'G': launch_cplx<CfgG, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'H': launch_cplx<CfgE5, false>(ctx, p, e, kcontig, cplx, half); break;
+    default: launch_cplx<CfgM, false>(ctx, p, e, kcontig, cplx, half); break;
+  }
+}
+
+}  // namespace kp

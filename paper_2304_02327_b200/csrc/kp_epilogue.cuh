@@ -66,21 +66,39 @@ __device__ __forceinline__ void store_pair(const Epilogue& e, double* c, unsigne
   }
 }
 
+// Finite test on the integer pipe (the FP64 datapath belongs to the DMMAs).
+__device__ __forceinline__ bool fin(double x) {
+  return (__double_as_longlong(x) & 0x7ff0000000000000LL) != 0x7ff0000000000000LL;
+}
+
+// Per-launch uniform facts of an Epilogue, evaluated once per thread instead
+// of per entry (a per-entry `beta != 0` is a DSETP that waits behind the
+// other warps' DMMAs on the shared FP64 datapath).
+struct EpiU {
+  bool beta;   // beta != 0: accumulate into C
+  bool one;    // alpha == 1: v = acc exactly
+  bool track;  // divergence tracking on
+};
+__device__ __forceinline__ EpiU epi_uniform(const Epilogue& e) {
+  return EpiU{e.beta != 0.0, e.alpha == 1.0, e.bad_step != nullptr};
+}
+
 // Epilogue on one output entry.  v = alpha*acc; idx = linear index into C
 // (and X/D, which share C's layout).
-__device__ __forceinline__ double epi_one(const Epilogue& e, double v, const double* C,
-                                          long long idx, long long half, double* dval) {
+__device__ __forceinline__ double epi_one(const Epilogue& e, const EpiU& u, double v,
+                                          const double* C, long long idx, long long half,
+                                          double* dval) {
   switch (e.kind) {
     case EPI_FMA_X:
       return __fma_rn(e.gamma, v, e.X[idx]);
     case EPI_ADD_G: {
-      const double base = (e.beta != 0.0) ? __fma_rn(e.beta, C[idx], v) : v;
+      const double base = u.beta ? __fma_rn(e.beta, C[idx], v) : v;
       const bool second = half > 0 && idx >= half;
       const double partner = half > 0 ? e.X[second ? idx - half : idx + half] : 0.0;
       return __dadd_rn(base, g_real(e.g, e.X[idx], partner, second, idx, e.t));
     }
     case EPI_ADD_X: {
-      const double base = (e.beta != 0.0) ? __fma_rn(e.beta, C[idx], v) : v;
+      const double base = u.beta ? __fma_rn(e.beta, C[idx], v) : v;
       return __dadd_rn(base, e.X[idx]);
     }
     case EPI_STAGE_D: {
@@ -90,25 +108,25 @@ __device__ __forceinline__ double epi_one(const Epilogue& e, double v, const dou
       return s;
     }
     default:
-      return (e.beta != 0.0) ? __fma_rn(e.beta, C[idx], v) : v;
+      return u.beta ? __fma_rn(e.beta, C[idx], v) : v;
   }
 }
 
 // Complex epilogue on one (re, im) pair; idx = real index of the re part.
-__device__ __forceinline__ double2 epi_pair_c(const Epilogue& e, double2 v, const double* C,
-                                              long long idx, double2* dval) {
+__device__ __forceinline__ double2 epi_pair_c(const Epilogue& e, const EpiU& u, double2 v,
+                                              const double* C, long long idx, double2* dval) {
   switch (e.kind) {
     case EPI_FMA_X:
       return make_double2(__fma_rn(e.gamma, v.x, e.X[idx]), __fma_rn(e.gamma, v.y, e.X[idx + 1]));
     case EPI_ADD_G: {
       double2 b = v;
-      if (e.beta != 0.0) b = make_double2(__fma_rn(e.beta, C[idx], v.x), __fma_rn(e.beta, C[idx + 1], v.y));
+      if (u.beta) b = make_double2(__fma_rn(e.beta, C[idx], v.x), __fma_rn(e.beta, C[idx + 1], v.y));
       const double2 gx = g_cplx(e.g, make_double2(e.X[idx], e.X[idx + 1]));
       return make_double2(__dadd_rn(b.x, gx.x), __dadd_rn(b.y, gx.y));
     }
     case EPI_ADD_X: {
       double2 b = v;
-      if (e.beta != 0.0) b = make_double2(__fma_rn(e.beta, C[idx], v.x), __fma_rn(e.beta, C[idx + 1], v.y));
+      if (u.beta) b = make_double2(__fma_rn(e.beta, C[idx], v.x), __fma_rn(e.beta, C[idx + 1], v.y));
       return make_double2(__dadd_rn(b.x, e.X[idx]), __dadd_rn(b.y, e.X[idx + 1]));
     }
     case EPI_STAGE_D: {
@@ -119,10 +137,121 @@ __device__ __forceinline__ double2 epi_pair_c(const Epilogue& e, double2 v, cons
       return st;
     }
     default:
-      if (e.beta != 0.0)
+      if (u.beta)
         return make_double2(__fma_rn(e.beta, C[idx], v.x), __fma_rn(e.beta, C[idx + 1], v.y));
       return v;
   }
+}
+
+}  // namespace
+}  // namespace kp
+
+namespace kp {
+namespace {
+
+// The fused epilogue of one output tile of C staged in shared memory as a
+// column-major TM x TN block (pitch LDS doubles; element (ml, nl) is
+// alpha-less acc of C(m0 + ml, n0 + nl) of batch q).  NTH threads walk (m,
+// m+1) pairs with consecutive threads on consecutive m: coalesced 16-byte
+// stores and one copy of the epilogue code.  CPLX: 0 real; 1 rows are (re,
+// im) pairs (complex mode 0); 2 rows 2p/2p+1 = re/im of the tensor, columns
+// 2i/2i+1 = re/im of the factor, combined as (rr - ii, ri + ir) at complex
+// offset p + i*P (complex modes >= 1).  Returns whether a non-finite value
+// was written (the divergence flag).
+template <int TM, int TN, int LDS, int NTH, int CPLX, bool SCAT>
+__device__ __forceinline__ bool staged_epilogue(const GemmProblem& p, const Epilogue& e,
+                                                const double* __restrict__ cs, int m0, int n0,
+                                                long long q, int tid, int c_vec2,
+                                                long long species_half) {
+  double* __restrict__ Cb = p.C + q * p.sC;
+  const long long cq = q * p.sC;
+  bool nonfinite = false;
+  const EpiU u = epi_uniform(e);
+  const double al = e.alpha;
+  if constexpr (CPLX == 0 && !SCAT) {
+    // plain store (a mode product of a Tucker operator): the decisions are
+    // uniform, so no per-entry FP64 compare -- the FP64 datapath is the
+    // DMMA's, and epilogue DSETP/DMUL stall behind the other warps' DMMAs
+    if (e.kind == EPI_STORE && !u.beta && !u.track) {
+      const bool one = u.one;
+#pragma unroll 2
+      for (int e2 = tid; e2 < TM * TN / 2; e2 += NTH) {
+        const int ml = 2 * (e2 % (TM / 2)), nl = e2 / (TM / 2);
+        const int mrow = m0 + ml, ncol = n0 + nl;
+        if (mrow >= p.M || ncol >= p.N) continue;
+        double2 a2 = *reinterpret_cast<const double2*>(cs + ml + nl * LDS);
+        if (!one) a2 = make_double2(al * a2.x, al * a2.y);
+        double* dst = Cb + mrow + (long long)ncol * p.ldc;
+        if (mrow + 1 < p.M) {
+          if (c_vec2)
+            *reinterpret_cast<double2*>(dst) = a2;
+          else {
+            dst[0] = a2.x;
+            dst[1] = a2.y;
+          }
+        } else {
+          dst[0] = a2.x;
+        }
+      }
+      return false;
+    }
+  }
+  if constexpr (CPLX == 2) {
+#pragma unroll 1
+    for (int e2 = tid; e2 < (TM / 2) * (TN / 2); e2 += NTH) {
+      const int pl = e2 % (TM / 2), il = e2 / (TM / 2);
+      const int mrow = m0 + 2 * pl, ncol = n0 + 2 * il;
+      if (mrow >= p.M || ncol >= p.N) continue;
+      const double* c0 = cs + 2 * pl + 2 * il * LDS;
+      const double c_rr = c0[0], c_ir = c0[1], c_ri = c0[LDS], c_ii = c0[LDS + 1];
+      double2 v = make_double2(__dsub_rn(c_rr, c_ii), __dadd_rn(c_ri, c_ir));
+      if (!u.one) v = make_double2(al * v.x, al * v.y);
+      const long long off = mrow + (long long)(ncol >> 1) * p.ldc;
+      double2 dv = make_double2(0.0, 0.0);
+      const double2 rr = epi_pair_c(e, u, v, p.C, cq + off, &dv);
+      double* dst = Cb + off;
+      if constexpr (SCAT) dst = scatter_ptr(e, unsigned((cq + off) >> 1), 2);
+      *reinterpret_cast<double2*>(dst) = rr;
+      if (u.track) nonfinite |= !fin(rr.x) || !fin(rr.y);
+      if (e.kind == EPI_STAGE_D) *reinterpret_cast<double2*>(e.D + cq + off) = dv;
+    }
+    return nonfinite;
+  }
+#pragma unroll 1
+  for (int e2 = tid; e2 < TM * TN / 2; e2 += NTH) {
+    const int ml = 2 * (e2 % (TM / 2)), nl = e2 / (TM / 2);
+    const int mrow = m0 + ml, ncol = n0 + nl;
+    if (mrow >= p.M || ncol >= p.N) continue;
+    const bool two = (mrow + 1 < p.M);
+    const long long off = mrow + (long long)ncol * p.ldc;
+    const double2 a2 = *reinterpret_cast<const double2*>(cs + ml + nl * LDS);
+    const double v0 = u.one ? a2.x : al * a2.x, v1 = u.one ? a2.y : al * a2.y;
+    if constexpr (CPLX == 1) {
+      double2 dv = make_double2(0.0, 0.0);
+      const double2 rr = epi_pair_c(e, u, make_double2(v0, v1), p.C, cq + off, &dv);
+      double* dst = Cb + off;
+      if constexpr (SCAT) dst = scatter_ptr(e, unsigned((cq + off) >> 1), 2);
+      *reinterpret_cast<double2*>(dst) = rr;
+      if (u.track) nonfinite |= !fin(rr.x) || !fin(rr.y);
+      if (e.kind == EPI_STAGE_D) *reinterpret_cast<double2*>(e.D + cq + off) = dv;
+      continue;
+    }
+    double d0 = 0.0, d1 = 0.0;
+    const double r0 = epi_one(e, u, v0, p.C, cq + off, species_half, &d0);
+    double r1 = 0.0;
+    if (two) r1 = epi_one(e, u, v1, p.C, cq + off + 1, species_half, &d1);
+    if (u.track) nonfinite |= !fin(r0) || (two && !fin(r1));
+    store_pair<SCAT>(e, Cb + off, (unsigned long long)(cq + off), r0, r1, two, c_vec2);
+    if (e.kind == EPI_STAGE_D) {
+      if (two && c_vec2) {
+        *reinterpret_cast<double2*>(e.D + cq + off) = make_double2(d0, d1);
+      } else {
+        e.D[cq + off] = d0;
+        if (two) e.D[cq + off + 1] = d1;
+      }
+    }
+  }
+  return nonfinite;
 }
 
 }  // namespace

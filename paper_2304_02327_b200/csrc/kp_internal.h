@@ -125,9 +125,9 @@ struct GemmProblem {
 // its kp_scatter destination (e.sc_*).
 void scatter_copy(kp_ctx* ctx, const double* x, long long n, int comps, const Epilogue& e);
 
-// The same GEMM on the CUTLASS mainloop (gemm_cutlass.cu); launch_gemm's default.
-void launch_gemm_cutlass(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int cplx,
-                         bool kcontig, long long half);
+// The hand-written warp-specialized TMA/DMMA GEMM (gemm_dmma.cu): launch_gemm's path.
+void launch_gemm_dmma(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int cplx,
+                      bool kcontig, long long half);
 
 // cplx: 0 real, 1 complex rows (mode 0), 2 complex combine (mode >= 1); see mode_product.cu
 void launch_gemm(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int cplx = 0);
