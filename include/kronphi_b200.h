@@ -367,6 +367,23 @@ int kp_integrate_f64(kp_ctx* ctx, int method, double* u, const int* dims, int d,
 int kp_integrate_c128(kp_ctx* ctx, int method, double* u, const int* dims, int d,
                       const double* const* as, const kp_gfun* g, double t0, double t_final,
                       long n_steps, int q, long* diverged_step, double* loop_seconds);
+/* integrate with trajectory sampling (StepperConfig::sample_every,
+ * IntegrateResult::trajectory, :284-287,:365-366): after every sample_every
+ * steps fn(user, step, u_host) receives the state (a library-owned pinned
+ * host buffer of prod(dims) (x2 complex) doubles, valid during the call);
+ * the caller records (t0, u0) itself, as the reference does before the loop.
+ * sample_every = 0 is kp_integrate_*. */
+typedef void (*kp_sample_fn)(void* user, long step, const double* u_host);
+int kp_integrate_sampled_f64(kp_ctx* ctx, int method, double* u, const int* dims, int d,
+                             const double* const* as, const kp_gfun* g, double t0,
+                             double t_final, long n_steps, int q, int sample_every,
+                             kp_sample_fn fn, void* user, long* diverged_step,
+                             double* loop_seconds);
+int kp_integrate_sampled_c128(kp_ctx* ctx, int method, double* u, const int* dims, int d,
+                              const double* const* as, const kp_gfun* g, double t0,
+                              double t_final, long n_steps, int q, int sample_every,
+                              kp_sample_fn fn, void* user, long* diverged_step,
+                              double* loop_seconds);
 /* Host-buffer drop-in: u0/as on the host, u_final written on the host. */
 int kp_host_integrate_f64(kp_ctx* ctx, int method, const double* u0, const int* dims, int d,
                           const double* const* as, const kp_gfun* g, double t0, double t_final,

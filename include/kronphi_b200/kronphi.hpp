@@ -37,6 +37,8 @@
 #include <complex>
 #include <cstddef>
 #include <cstring>
+#include <functional>
+#include <map>
 #include <algorithm>
 #include <initializer_list>
 #include <memory>
@@ -52,9 +54,13 @@ namespace kronphi {
 
 // ------------------------------------------------------------ errors
 
+// inc/integrators.hpp:86-97 (same constructor and message)
 class DivergenceError : public std::runtime_error {
  public:
-  DivergenceError(long step, const std::string& msg) : std::runtime_error(msg), step_(step) {}
+  DivergenceError(long step, double t)
+      : std::runtime_error("state became non-finite at step " + std::to_string(step) +
+                           " (t = " + std::to_string(t) + ")"),
+        step_(step) {}
   long step() const { return step_; }
 
  private:
@@ -67,7 +73,7 @@ inline void check(int rc, long step = 0) {
   if (rc == KP_OK) return;
   const std::string m = kp_last_error();
   if (rc == KP_EINVAL) throw std::invalid_argument(m);
-  if (rc == KP_EDIVERGE) throw DivergenceError(step, m);
+  if (rc == KP_EDIVERGE) throw std::runtime_error(m);  // callers map it with t
   throw std::runtime_error(m);
 }
 
@@ -88,18 +94,48 @@ inline kp_ctx* ctx() {
   return h.ctx;
 }
 
-// RAII device buffer through the C ABI.
+// Grow-only per-thread pool of device buffers: the drop-in's per-call
+// functions (the *_step functions, tucker, ...) reuse device memory instead
+// of a cudaMalloc/cudaFree (which synchronizes the device) per operand per
+// call.  Buffers are returned to the pool by size and freed at thread exit.
+struct BufPool {
+  kp_ctx* c;
+  std::multimap<size_t, void*> free_;
+  explicit BufPool(kp_ctx* cc) : c(cc) {}
+  ~BufPool() {
+    for (auto& kv : free_) kp_free(c, kv.second);
+  }
+  void* get(size_t bytes) {
+    auto it = free_.find(bytes);
+    if (it != free_.end()) {
+      void* p = it->second;
+      free_.erase(it);
+      return p;
+    }
+    void* p = nullptr;
+    check(kp_malloc(c, bytes, &p));
+    return p;
+  }
+  void put(void* p, size_t bytes) { free_.emplace(bytes, p); }
+};
+inline BufPool& pool() {
+  kp_ctx* c = ctx();  // constructed first, so destroyed after the pool
+  static thread_local BufPool p(c);
+  return p;
+}
+
+// RAII device buffer through the C ABI (from the pool).
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   DevBuf() = default;
-  explicit DevBuf(size_t b) : bytes(b) { check(kp_malloc(ctx(), b, &p)); }
+  explicit DevBuf(size_t b) : p(pool().get(b ? b : 8)), bytes(b ? b : 8) {}
   DevBuf(const void* host, size_t b) : DevBuf(b) { check(kp_upload(ctx(), p, host, b)); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; }
   ~DevBuf() {
-    if (p) kp_free(ctx(), p);
+    if (p) pool().put(p, bytes);
   }
   double* d() const { return static_cast<double*>(p); }
   void download(void* host) const { check(kp_download(ctx(), host, p, bytes)); }
@@ -686,6 +722,11 @@ Tensor<T> apply_split_phi(const SplitPhi<T>& sp, const Tensor<T>& v) {
 // ------------------------------------------------------- integrators
 
 enum class Method { LawsonEuler, Lawson2b, ExpEuler, ExpEulerLinearSplit, ETD2RK, RosenbrockEuler };
+// inc/integrators.hpp:33.  DenseOracle assembles the Kronecker sum K (N x N,
+// small problems only, validation) and integrates the one-mode problem
+// vec(u)' = K vec(u) + g on the device: the split phi of a single factor is
+// the exact phi_l(tau K), i.e. the textbook exponential integrator.
+enum class Backend { Split, DenseOracle };
 
 inline const char* method_name(Method m) {
   switch (m) {
@@ -705,14 +746,54 @@ inline Method parse_method(const std::string& s) {
   throw std::invalid_argument("unknown method: " + s);
 }
 
-// Device nonlinearities (the reference's GFun is a host std::function).
-using GFun = kp_gfun;
-inline GFun g_zero() { return GFun{KP_G_ZERO, {0, 0, 0, 0}}; }
-inline GFun g_square() { return GFun{KP_G_SQUARE, {0, 0, 0, 0}}; }
-inline GFun g_const(double c) { return GFun{KP_G_CONST, {c, 0, 0, 0}}; }
-inline GFun g_allen_cahn() { return GFun{KP_G_ALLEN_CAHN, {0, 0, 0, 0}}; }
-inline GFun g_brusselator(double a, double b) { return GFun{KP_G_BRUSSELATOR, {a, b, 0, 0}}; }
-inline GFun g_nls() { return GFun{KP_G_NLS, {0, 0, 0, 0}}; }
+// g(t, u): the reference's GFun is a host std::function (inc/integrators.hpp:
+// 60,112).  Here it is either
+//   * a device nonlinearity from the closed set (kp_gfun: Allen-Cahn,
+//     Brusselator, NLS, zero, square, const, ADR, Riccati), evaluated inside
+//     the fused GEMM epilogues of the device time loop; or
+//   * any host callable Tensor<T>(double, const Tensor<T>&), exactly like the
+//     reference: the state stays on the GPU and every g evaluation is a
+//     documented host round trip (D2H of the argument, the user's g on the
+//     host, H2D of the result) between device operations.
+template <typename T>
+class GFunT {
+ public:
+  using HostFn = std::function<Tensor<T>(double, const Tensor<T>&)>;
+  GFunT() { dev_.kind = KP_G_ZERO; }
+  GFunT(const kp_gfun& d) : dev_(d) {}  // NOLINT: implicit like the reference's lambdas
+  template <class F, class = std::enable_if_t<
+                         !std::is_same_v<std::decay_t<F>, kp_gfun> &&
+                         !std::is_same_v<std::decay_t<F>, GFunT> &&
+                         std::is_invocable_r_v<Tensor<T>, F, double, const Tensor<T>&>>>
+  GFunT(F f) : host_(std::move(f)) {  // NOLINT
+    dev_.kind = -1;
+  }
+  bool is_host() const { return bool(host_); }
+  explicit operator bool() const { return true; }
+  // the device descriptor (aux fields of the ADR / Riccati g's are set here)
+  kp_gfun& device() {
+    if (is_host()) throw std::invalid_argument("GFun: a host g has no device descriptor");
+    return dev_;
+  }
+  const kp_gfun& device() const {
+    if (is_host()) throw std::invalid_argument("GFun: a host g has no device descriptor");
+    return dev_;
+  }
+  // host evaluation (a device g is evaluated on the GPU and downloaded)
+  Tensor<T> operator()(double t, const Tensor<T>& u) const;
+
+ private:
+  kp_gfun dev_{};
+  HostFn host_;
+};
+using GFun = GFunT<double>;
+
+inline GFun g_zero() { return kp_gfun{KP_G_ZERO, {0, 0, 0, 0}}; }
+inline GFun g_square() { return kp_gfun{KP_G_SQUARE, {0, 0, 0, 0}}; }
+inline GFun g_const(double c) { return kp_gfun{KP_G_CONST, {c, 0, 0, 0}}; }
+inline GFun g_allen_cahn() { return kp_gfun{KP_G_ALLEN_CAHN, {0, 0, 0, 0}}; }
+inline GFun g_brusselator(double a, double b) { return kp_gfun{KP_G_BRUSSELATOR, {a, b, 0, 0}}; }
+inline GFunT<std::complex<double>> g_nls() { return kp_gfun{KP_G_NLS, {0, 0, 0, 0}}; }
 
 // Device copies of a g's auxiliary fields (ADR: psi_a, u0^2; Riccati: b, C).
 struct DeviceFields {
@@ -723,48 +804,405 @@ struct DeviceFields {
   }
 };
 
+// inc/integrators.hpp:57-69
 template <typename T = double>
 struct ProblemSpecT {
   KroneckerSum<T> K;
-  GFun g = g_zero();
+  GFunT<T> g = GFunT<T>();
   Tensor<T> u0;
   double t0 = 0.0;
   double t_final = 1.0;
-  std::shared_ptr<DeviceFields> device_data;  // keeps g.aux alive
+  // Optional: analytical solution at time t.
+  std::function<Tensor<T>(double)> exact;
+  // Optional: per-direction Jacobian factors J_mu(U) (Rosenbrock only); a
+  // host callback, called once per step on the downloaded state.
+  std::function<std::vector<Matrix<T>>(const Tensor<T>&)> jacobian_factors;
+  std::shared_ptr<DeviceFields> device_data;  // keeps a device g's aux fields alive
 };
 using ProblemSpec = ProblemSpecT<double>;
 
+// inc/integrators.hpp:71-77
 struct StepperConfig {
   Method method = Method::ExpEuler;
   long n_steps = 1;
+  Backend backend = Backend::Split;
+  int sample_every = 0;  // 0 disables trajectory sampling
   int quad_nodes = kDefaultQuadNodes;
 };
 
+// inc/integrators.hpp:79-84
 template <typename T = double>
 struct IntegrateResultT {
   Tensor<T> final;
+  std::vector<std::pair<double, Tensor<T>>> trajectory;
   double wallclock_s = 0.0;  // includes factor precomputation
-  double loop_s = 0.0;       // device time of the time loop
+  double loop_s = 0.0;       // time loop only (device time on the device path)
 };
 using IntegrateResult = IntegrateResultT<double>;
+
+namespace detail {
+
+template <typename T>
+void check_problem(const KroneckerSum<T>& k, const Tensor<T>& u) {
+  if (k.order() != u.order())
+    throw std::invalid_argument("kronsum_action: expected one factor per mode");
+  for (int mu = 0; mu < u.order(); ++mu) check_mode_sizes(u, k.factors[mu], mu);
+}
+template <typename T>
+void check_factors(const std::vector<Matrix<T>>& fs, const Tensor<T>& u, const char* who) {
+  if (int(fs.size()) != u.order())
+    throw std::invalid_argument(std::string(who) + ": expected one factor per mode");
+  for (int mu = 0; mu < u.order(); ++mu) {
+    check_mode_sizes(u, fs[mu], mu);
+    if (fs[mu].rows() != u.dim(mu))
+      throw std::invalid_argument(std::string(who) + ": factor " + std::to_string(mu) +
+                                  " is not square");
+  }
+}
+
+inline std::vector<int> dims_vec(const Tensor<double>& t) { return t.dims(); }
+
+// Device workspace of a host-g loop: the state, a few tensors, the factors.
+template <typename T>
+struct HostGLoop {
+  static_assert(std::is_same_v<T, double>, "host g: real tensors (the reference's GFun)");
+  std::vector<int> dims;
+  size_t n = 0;
+  const GFunT<T>& g;
+  DevBuf u, w, r, s, gb;
+  Tensor<T> hx, hg;
+  std::vector<DevBuf> kf;  // K factors (device)
+  std::vector<const double*> kp;
+  HostGLoop(const std::vector<int>& dv, const GFunT<T>& gf)
+      : dims(dv), n(size_of(dv)), g(gf), u(n * 8), w(n * 8), r(n * 8), s(n * 8), gb(n * 8),
+        hx(Tensor<T>::no_init(dv)) {}
+  static size_t size_of(const std::vector<int>& dv) {
+    size_t x = 1;
+    for (int v : dv) x *= size_t(v);
+    return x;
+  }
+  void upload_k(const KroneckerSum<T>& k) {
+    kf.clear();
+    kp.clear();
+    for (const auto& f : k.factors) {
+      kf.emplace_back(f.data(), f.size() * 8);
+      kp.push_back(kf.back().d());
+    }
+  }
+  // out (device) = g(t, x (device)): the host round trip
+  void eval_g(double t, const double* x, double* out) {
+    check(kp_download(ctx(), hx.data(), x, n * 8));
+    hg = g(t, hx);
+    if (hg.dims() != dims) throw std::invalid_argument("g: result shape mismatch");
+    check(kp_upload(ctx(), out, hg.data(), n * 8));
+  }
+  void tucker(const double* x, const std::vector<const double*>& f, double pref, double* out) {
+    check(kp_tucker_f64(ctx(), x, dims.data(), int(dims.size()), f.data(), dims.data(), pref,
+                        out));
+  }
+  // one step (inc/integrators.hpp:116-164, same operation order); in: u, out: u
+  void step(Method m, double t, double tau, const std::vector<const double*>& f1, double p1,
+            const std::vector<const double*>& f2, double p2) {
+    const int d = int(dims.size());
+    switch (m) {
+      case Method::LawsonEuler:  // tucker(add_scaled(u, tau, g(t, u)), E)
+        eval_g(t, u.d(), gb.d());
+        check(kp_add_scaled_f64(ctx(), n, u.d(), tau, gb.d(), w.d()));
+        tucker(w.d(), f1, 1.0, u.d());
+        break;
+      case Method::Lawson2b:
+        eval_g(t, u.d(), gb.d());
+        check(kp_add_scaled_f64(ctx(), n, u.d(), tau, gb.d(), w.d()));
+        tucker(w.d(), f1, 1.0, s.d());                                 // stage
+        check(kp_add_scaled_f64(ctx(), n, u.d(), 0.5 * tau, gb.d(), w.d()));
+        tucker(w.d(), f1, 1.0, u.d());                                 // out
+        eval_g(t + tau, s.d(), gb.d());
+        check(kp_axpy_f64(ctx(), n, 0.5 * tau, gb.d(), u.d()));
+        break;
+      case Method::ExpEuler:
+      case Method::RosenbrockEuler:  // f1 = phi_1 factors (of K or of the Jacobians)
+        check(kp_kronsum_f64(ctx(), u.d(), dims.data(), d, kp.data(), r.d()));
+        eval_g(t, u.d(), gb.d());
+        check(kp_axpy_f64(ctx(), n, 1.0, gb.d(), r.d()));
+        tucker(r.d(), f1, p1, w.d());
+        check(kp_add_scaled_f64(ctx(), n, u.d(), tau, w.d(), s.d()));
+        check(kp_copy(ctx(), u.d(), s.d(), n * 8));
+        break;
+      case Method::ExpEulerLinearSplit:  // out = tucker(u, E); axpy(tau, SP1(g), out)
+        eval_g(t, u.d(), gb.d());
+        tucker(u.d(), f1, 1.0, s.d());
+        tucker(gb.d(), f2, p2, w.d());
+        check(kp_axpy_f64(ctx(), n, tau, w.d(), s.d()));
+        check(kp_copy(ctx(), u.d(), s.d(), n * 8));
+        break;
+      case Method::ETD2RK: {
+        eval_g(t, u.d(), gb.d());                                      // gn
+        check(kp_kronsum_f64(ctx(), u.d(), dims.data(), d, kp.data(), r.d()));
+        check(kp_axpy_f64(ctx(), n, 1.0, gb.d(), r.d()));
+        tucker(r.d(), f1, p1, w.d());
+        check(kp_add_scaled_f64(ctx(), n, u.d(), tau, w.d(), s.d()));  // stage
+        eval_g(t + tau, s.d(), r.d());                                 // d = g(t+tau, stage)
+        check(kp_axpy_f64(ctx(), n, -1.0, gb.d(), r.d()));
+        tucker(r.d(), f2, p2, w.d());
+        check(kp_add_scaled_f64(ctx(), n, s.d(), tau, w.d(), u.d()));
+        break;
+      }
+    }
+  }
+};
+
+// phi_ell(tau F_mu) of host factors on the device (build_split_phi)
+struct DeviceSplit {
+  std::vector<DevBuf> in, out;
+  std::vector<const double*> f;
+  double pref = 1.0;
+  DeviceSplit(const std::vector<Matrix<double>>& fs, double tau, int ell, int q) {
+    std::vector<const double*> ip;
+    std::vector<double*> op;
+    std::vector<int> dims;
+    for (size_t mu = 0; mu < fs.size(); ++mu) {
+      int same = -1;
+      for (size_t m2 = 0; m2 < mu; ++m2)
+        if (fs[m2] == fs[mu]) same = int(m2);
+      if (same >= 0) {
+        ip.push_back(ip[same]);
+      } else {
+        in.emplace_back(fs[mu].data(), fs[mu].size() * 8);
+        ip.push_back(in.back().d());
+      }
+      out.emplace_back(fs[mu].size() * 8);
+      op.push_back(out.back().d());
+      dims.push_back(fs[mu].rows());
+    }
+    check(kp_build_split_phi_f64(ctx(), ip.data(), dims.data(), int(fs.size()), tau, ell, q,
+                                 op.data(), &pref));
+    for (auto* p : op) f.push_back(p);
+  }
+};
+
+inline double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+// integrate() with a host g (or a host jacobian_factors callback): the
+// reference's loop (inc/integrators.hpp:219-373) on a device-resident state.
+inline IntegrateResultT<double> integrate_host_g(const ProblemSpecT<double>& p,
+                                                 const StepperConfig& c) {
+  const double w0 = now_s();
+  const double tau = (p.t_final - p.t0) / double(c.n_steps);
+  const int q = c.quad_nodes;
+  HostGLoop<double> L(p.u0.dims(), p.g);
+  L.upload_k(p.K);
+  check(kp_upload(ctx(), L.u.d(), p.u0.data(), L.n * 8));
+  std::unique_ptr<DeviceSplit> s1, s2;
+  switch (c.method) {  // step-invariant factors (:263-283)
+    case Method::LawsonEuler:
+    case Method::Lawson2b:
+      s1 = std::make_unique<DeviceSplit>(p.K.factors, tau, 0, q);
+      break;
+    case Method::ExpEuler:
+      s1 = std::make_unique<DeviceSplit>(p.K.factors, tau, 1, q);
+      break;
+    case Method::ExpEulerLinearSplit:
+      s1 = std::make_unique<DeviceSplit>(p.K.factors, tau, 0, q);
+      s2 = std::make_unique<DeviceSplit>(p.K.factors, tau, 1, q);
+      break;
+    case Method::ETD2RK:
+      s1 = std::make_unique<DeviceSplit>(p.K.factors, tau, 1, q);
+      s2 = std::make_unique<DeviceSplit>(p.K.factors, tau, 2, q);
+      break;
+    case Method::RosenbrockEuler:
+      break;  // per step
+  }
+  IntegrateResultT<double> res;
+  if (c.sample_every > 0) res.trajectory.emplace_back(p.t0, p.u0);
+  const double l0 = now_s();
+  Tensor<double> host_u = Tensor<double>::no_init(p.u0.dims());
+  const std::vector<const double*> none;
+  for (long n = 0; n < c.n_steps; ++n) {
+    const double t = p.t0 + double(n) * tau;
+    if (c.method == Method::RosenbrockEuler) {
+      check(kp_download(ctx(), host_u.data(), L.u.d(), L.n * 8));
+      const auto jac = p.jacobian_factors(host_u);
+      check_factors(jac, host_u, "rosenbrock_euler_step");
+      DeviceSplit sj(jac, tau, 1, q);
+      L.step(c.method, t, tau, sj.f, 1.0, none, 1.0);
+    } else {
+      L.step(c.method, t, tau, s1->f, s1->pref, s2 ? s2->f : none, s2 ? s2->pref : 1.0);
+    }
+    int ok = 1;
+    check(kp_all_finite_f64(ctx(), L.n, L.u.d(), &ok));
+    if (!ok) throw DivergenceError(n + 1, t + tau);
+    if (c.sample_every > 0 && (n + 1) % c.sample_every == 0) {
+      check(kp_download(ctx(), host_u.data(), L.u.d(), L.n * 8));
+      res.trajectory.emplace_back(p.t0 + double(n + 1) * tau, host_u);
+    }
+  }
+  res.final = Tensor<double>::no_init(p.u0.dims());
+  check(kp_download(ctx(), res.final.data(), L.u.d(), L.n * 8));
+  const double w1 = now_s();
+  res.loop_s = w1 - l0;
+  res.wallclock_s = w1 - w0;
+  return res;
+}
+
+// assemble_kronsum: K = sum_mu I (x) ... (x) A_mu (x) ... (x) I, with the first
+// mode fastest (inc/oracle.hpp's dense operator of the Kronecker sum)
+template <typename T>
+Matrix<T> assemble_kronsum_dense(const KroneckerSum<T>& k) {
+  const auto dims = k.dims();
+  long long N = 1;
+  for (int x : dims) N *= x;
+  if (N > 8192) throw std::invalid_argument("DenseOracle: problem too large (N > 8192)");
+  Matrix<T> K{int(N), int(N)};
+  long long P = 1;
+  for (int mu = 0; mu < int(dims.size()); ++mu) {
+    const int nm = dims[mu];
+    const long long Q = N / (P * nm);
+    const Matrix<T>& A = k.factors[mu];
+    for (long long qq = 0; qq < Q; ++qq)
+      for (int i = 0; i < nm; ++i)
+        for (int j = 0; j < nm; ++j) {
+          const T a = A(i, j);
+          if (a == T{}) continue;
+          for (long long pp = 0; pp < P; ++pp)
+            K(int(pp + P * (i + nm * qq)), int(pp + P * (j + nm * qq))) += a;
+        }
+    P *= nm;
+  }
+  return K;
+}
+
+struct SampleSink {
+  std::vector<std::pair<double, Tensor<double>>>* traj;
+  std::vector<int> dims;
+  double t0, tau;
+  size_t n;
+  static void fn(void* user, long step, const double* u) {
+    auto* s = static_cast<SampleSink*>(user);
+    Tensor<double> t = Tensor<double>::no_init(s->dims);
+    std::memcpy(t.data(), u, s->n * sizeof(double));
+    s->traj->emplace_back(s->t0 + double(step) * s->tau, std::move(t));
+  }
+};
+
+}  // namespace detail
+
+template <typename T>
+Tensor<T> GFunT<T>::operator()(double t, const Tensor<T>& u) const {
+  if (host_) return host_(t, u);
+  using namespace detail;
+  DevBuf du(u.data(), bytes_of<T>(u.size())), dg(bytes_of<T>(u.size()));
+  auto f = std::is_same_v<T, double> ? kp_eval_g_f64 : kp_eval_g_c128;
+  check(f(ctx(), &dev_, t, du.d(), u.dims().data(), u.order(), dg.d()));
+  Tensor<T> out = Tensor<T>::no_init(u.dims());
+  dg.download(out.data());
+  return out;
+}
 
 template <typename T>
 IntegrateResultT<T> integrate(const ProblemSpecT<T>& p, const StepperConfig& c) {
   using namespace detail;
   if (c.n_steps <= 0) throw std::invalid_argument("integrate: n_steps must be positive");
   if (!(p.t_final > p.t0)) throw std::invalid_argument("integrate: empty time interval");
+  if (c.sample_every < 0) throw std::invalid_argument("integrate: negative sample_every");
+  check_problem(p.K, p.u0);
+  const bool device_jac = !p.g.is_host() && p.g.device().kind == KP_G_RICCATI;
+  if (c.method == Method::RosenbrockEuler && !p.jacobian_factors && !device_jac)
+    throw std::invalid_argument("integrate: Rosenbrock-Euler requires jacobian_factors");
+  if (c.backend == Backend::DenseOracle) {
+    if (c.method == Method::RosenbrockEuler)
+      throw std::invalid_argument("DenseOracle: Rosenbrock-Euler is not provided");
+    if (!p.g.is_host()) {
+      const int k = p.g.device().kind;
+      if (k == KP_G_BRUSSELATOR || k == KP_G_RICCATI)
+        throw std::invalid_argument("DenseOracle: this g needs the tensor shape");
+    }
+    const std::vector<int> shape = p.u0.dims();
+    ProblemSpecT<T> q1;
+    q1.K = KroneckerSum<T>({assemble_kronsum_dense(p.K)});
+    const int N = q1.K.factors[0].rows();
+    q1.u0 = Tensor<T>({N}, vec(p.u0));
+    q1.t0 = p.t0;
+    q1.t_final = p.t_final;
+    q1.device_data = p.device_data;
+    if (p.g.is_host()) {
+      const GFunT<T> g = p.g;
+      q1.g = [g, shape](double t, const Tensor<T>& u) {
+        return Tensor<T>({int(u.size())}, vec(g(t, Tensor<T>(shape, vec(u)))));
+      };
+    } else {
+      q1.g = p.g;
+    }
+    StepperConfig c1 = c;
+    c1.backend = Backend::Split;
+    IntegrateResultT<T> r1 = integrate(q1, c1);
+    IntegrateResultT<T> r;
+    r.final = Tensor<T>(shape, vec(r1.final));
+    for (auto& s : r1.trajectory) r.trajectory.emplace_back(s.first, Tensor<T>(shape, vec(s.second)));
+    r.loop_s = r1.loop_s;
+    r.wallclock_s = r1.wallclock_s;
+    return r;
+  }
+  if constexpr (std::is_same_v<T, double>) {
+    if (p.g.is_host() || (c.method == Method::RosenbrockEuler && p.jacobian_factors && !device_jac))
+      return integrate_host_g(p, c);
+  } else {
+    if (p.g.is_host()) throw std::invalid_argument("integrate: complex host g is not provided");
+  }
   const auto w0 = std::chrono::steady_clock::now();
-  std::vector<const double*> hp;
-  for (const auto& f : p.K.factors) hp.push_back(dp(f.data()));
+  const double tau = (p.t_final - p.t0) / double(c.n_steps);
   IntegrateResultT<T> r;
   r.final = Tensor<T>::no_init(p.u0.dims());
   long dv = 0;
   double loop = 0.0;
-  auto f = std::is_same_v<T, double> ? kp_host_integrate_f64 : kp_host_integrate_c128;
-  const int rc = f(ctx(), int(c.method), dp(p.u0.data()), p.u0.dims().data(), p.u0.order(),
-                   hp.data(), &p.g, p.t0, p.t_final, c.n_steps, c.quad_nodes,
-                   dp(r.final.data()), &dv, &loop);
-  check(rc, dv);
+  std::vector<const double*> hp;
+  for (const auto& f : p.K.factors) hp.push_back(dp(f.data()));
+  int rc;
+  if (c.sample_every == 0) {
+    auto f = std::is_same_v<T, double> ? kp_host_integrate_f64 : kp_host_integrate_c128;
+    rc = f(ctx(), int(c.method), dp(p.u0.data()), p.u0.dims().data(), p.u0.order(), hp.data(),
+           &p.g.device(), p.t0, p.t_final, c.n_steps, c.quad_nodes, dp(r.final.data()), &dv,
+           &loop);
+  } else {
+    r.trajectory.emplace_back(p.t0, p.u0);
+    DevBuf du(p.u0.data(), bytes_of<T>(p.u0.size()));
+    std::vector<DevBuf> kf;
+    std::vector<const double*> kd;
+    for (const auto& f : p.K.factors) {
+      kf.emplace_back(f.data(), bytes_of<T>(f.size()));
+      kd.push_back(kf.back().d());
+    }
+    if constexpr (std::is_same_v<T, double>) {
+      SampleSink sink{&r.trajectory, p.u0.dims(), p.t0, tau, p.u0.size()};
+      rc = kp_integrate_sampled_f64(ctx(), int(c.method), du.d(), p.u0.dims().data(),
+                                    p.u0.order(), kd.data(), &p.g.device(), p.t0, p.t_final,
+                                    c.n_steps, c.quad_nodes, c.sample_every, &SampleSink::fn,
+                                    &sink, &dv, &loop);
+    } else {
+      struct CSink {
+        std::vector<std::pair<double, Tensor<T>>>* traj;
+        std::vector<int> dims;
+        double t0, tau;
+        size_t n;
+        static void fn(void* user, long step, const double* u) {
+          auto* s = static_cast<CSink*>(user);
+          Tensor<T> t = Tensor<T>::no_init(s->dims);
+          std::memcpy(static_cast<void*>(t.data()), u, s->n * sizeof(T));
+          s->traj->emplace_back(s->t0 + double(step) * s->tau, std::move(t));
+        }
+      } sink{&r.trajectory, p.u0.dims(), p.t0, tau, p.u0.size()};
+      rc = kp_integrate_sampled_c128(ctx(), int(c.method), du.d(), p.u0.dims().data(),
+                                     p.u0.order(), kd.data(), &p.g.device(), p.t0, p.t_final,
+                                     c.n_steps, c.quad_nodes, c.sample_every, &CSink::fn, &sink,
+                                     &dv, &loop);
+    }
+    if (rc == KP_OK) du.download(r.final.data());
+  }
+  if (rc == KP_EDIVERGE)  // DivergenceError(n + 1, t + tau), inc/integrators.hpp:364
+    throw DivergenceError(dv, (p.t0 + double(dv - 1) * tau) + tau);
+  check(rc);
   r.loop_s = loop;
   r.wallclock_s =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
@@ -774,8 +1212,39 @@ IntegrateResultT<T> integrate(const ProblemSpecT<T>& p, const StepperConfig& c) 
 namespace detail {
 template <typename T>
 Tensor<T> step(Method m, const Tensor<T>& u, double t, double tau, const KroneckerSum<T>* k,
-               const GFun& g, const std::vector<Matrix<T>>& f1, double pref1,
+               const GFunT<T>& g, const std::vector<Matrix<T>>& f1, double pref1,
                const std::vector<Matrix<T>>* f2, double pref2) {
+  check_factors(f1, u, method_name(m));
+  if (f2) check_factors(*f2, u, method_name(m));
+  if (k) check_problem(*k, u);
+  if constexpr (std::is_same_v<T, double>) {
+    if (g.is_host()) {  // the host round trip, same operation order as the reference
+      HostGLoop<double> L(u.dims(), g);
+      if (k) L.upload_k(*k);
+      check(kp_upload(ctx(), L.u.d(), u.data(), L.n * 8));
+      std::vector<DevBuf> keep;
+      auto up = [&](const std::vector<Matrix<T>>& ms) {
+        std::vector<const double*> v;
+        for (const auto& x : ms) {
+          keep.emplace_back(x.data(), x.size() * 8);
+          v.push_back(keep.back().d());
+        }
+        return v;
+      };
+      std::vector<const double*> p1, p2;
+      if (m == Method::RosenbrockEuler) {
+        DeviceSplit sj(f1, tau, 1, kDefaultQuadNodes);
+        L.step(m, t, tau, sj.f, 1.0, p2, 1.0);
+      } else {
+        p1 = up(f1);
+        if (f2) p2 = up(*f2);
+        L.step(m, t, tau, p1, pref1, p2, pref2);
+      }
+      Tensor<T> out = Tensor<T>::no_init(u.dims());
+      check(kp_download(ctx(), out.data(), L.u.d(), L.n * 8));
+      return out;
+    }
+  }
   auto upload_all = [](const std::vector<Matrix<T>>& ms, std::vector<DevBuf>& keep) {
     std::vector<const double*> p;
     for (const auto& x : ms) {
@@ -792,7 +1261,7 @@ Tensor<T> step(Method m, const Tensor<T>& u, double t, double tau, const Kroneck
   if (k) pk = upload_all(k->factors, keep);
   auto f = std::is_same_v<T, double> ? kp_step_f64 : kp_step_c128;
   check(f(ctx(), int(m), du.d(), u.dims().data(), u.order(), t, tau, k ? pk.data() : nullptr,
-          p1.data(), pref1, f2 ? p2.data() : nullptr, pref2, &g, dout.d()));
+          p1.data(), pref1, f2 ? p2.data() : nullptr, pref2, &g.device(), dout.d()));
   Tensor<T> out = Tensor<T>::no_init(u.dims());
   dout.download(out.data());
   return out;
@@ -800,24 +1269,24 @@ Tensor<T> step(Method m, const Tensor<T>& u, double t, double tau, const Kroneck
 }  // namespace detail
 
 template <typename T>
-Tensor<T> lawson_euler_step(const Tensor<T>& u, double t, double tau, const GFun& g,
+Tensor<T> lawson_euler_step(const Tensor<T>& u, double t, double tau, const GFunT<T>& g,
                             const std::vector<Matrix<T>>& exp_factors) {
   return detail::step<T>(Method::LawsonEuler, u, t, tau, nullptr, g, exp_factors, 1.0, nullptr,
                          1.0);
 }
 template <typename T>
-Tensor<T> lawson2b_step(const Tensor<T>& u, double t, double tau, const GFun& g,
+Tensor<T> lawson2b_step(const Tensor<T>& u, double t, double tau, const GFunT<T>& g,
                         const std::vector<Matrix<T>>& exp_factors) {
   return detail::step<T>(Method::Lawson2b, u, t, tau, nullptr, g, exp_factors, 1.0, nullptr, 1.0);
 }
 template <typename T>
 Tensor<T> exp_euler_step(const Tensor<T>& u, double t, double tau, const KroneckerSum<T>& k,
-                         const GFun& g, const SplitPhi<T>& phi1) {
+                         const GFunT<T>& g, const SplitPhi<T>& phi1) {
   return detail::step<T>(Method::ExpEuler, u, t, tau, &k, g, phi1.factors, phi1.prefactor,
                          nullptr, 1.0);
 }
 template <typename T>
-Tensor<T> exp_euler_linear_split_step(const Tensor<T>& u, double t, double tau, const GFun& g,
+Tensor<T> exp_euler_linear_split_step(const Tensor<T>& u, double t, double tau, const GFunT<T>& g,
                                       const std::vector<Matrix<T>>& exp_factors,
                                       const SplitPhi<T>& phi1) {
   return detail::step<T>(Method::ExpEulerLinearSplit, u, t, tau, nullptr, g, exp_factors, 1.0,
@@ -825,18 +1294,25 @@ Tensor<T> exp_euler_linear_split_step(const Tensor<T>& u, double t, double tau, 
 }
 template <typename T>
 Tensor<T> etd2rk_step(const Tensor<T>& u, double t, double tau, const KroneckerSum<T>& k,
-                      const GFun& g, const SplitPhi<T>& phi1, const SplitPhi<T>& phi2) {
+                      const GFunT<T>& g, const SplitPhi<T>& phi1, const SplitPhi<T>& phi2) {
   return detail::step<T>(Method::ETD2RK, u, t, tau, &k, g, phi1.factors, phi1.prefactor,
                          &phi2.factors, phi2.prefactor);
 }
 // inc/integrators.hpp:166-194: phi_1(tau J_mu) of the given Jacobian factors
-// built on the device in the call (uses the default 12-node rule).
+// built on the device in the call (the default 12-node rule; the overload
+// with a GLLRule takes the reference's signature).
 template <typename T>
 Tensor<T> rosenbrock_euler_step(const Tensor<T>& u, double t, double tau,
-                                const KroneckerSum<T>& k, const GFun& g,
+                                const KroneckerSum<T>& k, const GFunT<T>& g,
                                 const std::vector<Matrix<T>>& jac_factors) {
   return detail::step<T>(Method::RosenbrockEuler, u, t, tau, &k, g, jac_factors, 1.0, nullptr,
                          1.0);
+}
+template <typename T>
+Tensor<T> rosenbrock_euler_step(const Tensor<T>& u, double t, double tau,
+                                const KroneckerSum<T>& k, const GFunT<T>& g,
+                                const std::vector<Matrix<T>>& jac_factors, const GLLRule&) {
+  return rosenbrock_euler_step(u, t, tau, k, g, jac_factors);
 }
 
 // ------------------------------------------------------- problems (problems.hpp)
@@ -887,9 +1363,10 @@ struct ADRProblem {
     spec.t0 = 0.0;
     spec.t_final = 1.0;
     spec.device_data = std::make_shared<DeviceFields>();
-    spec.g = GFun{KP_G_ADR, {0, 0, 0, 0}};
-    spec.g.aux[0] = spec.device_data->add(psi_a.data(), psi_a.size());
-    spec.g.aux[1] = spec.device_data->add(u0_sq.data(), u0_sq.size());
+    kp_gfun g{KP_G_ADR, {0, 0, 0, 0}};
+    g.aux[0] = spec.device_data->add(psi_a.data(), psi_a.size());
+    g.aux[1] = spec.device_data->add(u0_sq.data(), u0_sq.size());
+    spec.g = g;
     return spec;
   }
 };
@@ -941,9 +1418,10 @@ struct RiccatiProblem {
     spec.t0 = 0.0;
     spec.t_final = t_final;
     spec.device_data = std::make_shared<DeviceFields>();
-    spec.g = GFun{KP_G_RICCATI, {0, 0, 0, 0}};
-    spec.g.aux[0] = spec.device_data->add(b.data(), b.size());
-    spec.g.aux[1] = spec.device_data->add(c_mat.data(), c_mat.size());
+    kp_gfun g{KP_G_RICCATI, {0, 0, 0, 0}};
+    g.aux[0] = spec.device_data->add(b.data(), b.size());
+    g.aux[1] = spec.device_data->add(c_mat.data(), c_mat.size());
+    spec.g = g;
     return spec;
   }
 };

@@ -588,8 +588,12 @@ void launch_gemm_dmma(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int 
     return v && *v ? v[0] : '\0';
   }();
   const long long tiles64 = (long long)((p.M + 63) / 64) * ((p.N + 63) / 64) * p.batch;
+  // fused epilogues (stage updates, g, accumulation) carry FP64 work that
+  // competes with the DMMAs for the FP64 datapath: at short K they run best
+  // spread over many small CTAs (measured on the integrator configs)
+  const bool fused = !(e.kind == EPI_STORE && e.beta == 0.0 && e.bad_step == nullptr);
   char cfg = 'G';
-  if (tiles64 < 4LL * ctx->num_sms)
+  if (tiles64 < 4LL * ctx->num_sms || (fused && p.K <= 256))
     cfg = 'S';
   else if (p.K <= 256)
     cfg = 'N';

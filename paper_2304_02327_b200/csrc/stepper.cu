@@ -766,7 +766,11 @@ class Integrator {
   }
 
   // integrate loop (:290-367) on u (device, in/out).  Returns loop seconds.
-  double run(double* u, double t0, long n_steps, bool use_graph) {
+  // sample_every > 0: after every sample_every steps the state is copied to
+  // the host and handed to fn (the reference's trajectory, :365-366); the
+  // loop then runs eagerly (same kernels as the graph replay).
+  double run(double* u, double t0, long n_steps, bool use_graph, int sample_every = 0,
+             kp_sample_fn sample_fn = nullptr, void* sample_user = nullptr) {
     // step counter in two alternating slots (step k reads slot k&1 and its
     // last kernel writes slot (k+1)&1), divergence flag in between
     int* cbuf = static_cast<int*>(ctx->ws.get(S_CTR, 16));
@@ -801,7 +805,18 @@ class Integrator {
     // return to their start); 8 for small states, whose steps are a few
     // microseconds each and would otherwise pay a graph launch every 2
     const long span = (n_entries <= (1L << 17) && n_steps - n >= 10) ? 8 : 2;
-    if (use_graph && method != KP_ROSENBROCK_EULER && n_steps - n >= 4) {
+    const bool sampling = sample_every > 0 && sample_fn;
+    double* hs = nullptr;
+    if (sampling) {
+      hs = static_cast<double*>(ctx->pin_out.get(size_t(n_entries) * comps * sizeof(double)));
+      if (1 % sample_every == 0) {  // the eager first step completes a sample
+        KP_CUDA(cudaMemcpyAsync(hs, ub[1], size_t(n_entries) * comps * sizeof(double),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+        KP_CUDA(cudaStreamSynchronize(ctx->stream));
+        sample_fn(sample_user, 1, hs);
+      }
+    }
+    if (use_graph && !sampling && method != KP_ROSENBROCK_EULER && n_steps - n >= 4) {
       cudaGraph_t graph;
       const unsigned long long l0 = ctx->launches;
       KP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
@@ -823,7 +838,15 @@ class Integrator {
         n += span;
       }
     }
-    while (n < n_steps) one(n++);
+    while (n < n_steps) {
+      one(n++);
+      if (sampling && n % sample_every == 0) {
+        KP_CUDA(cudaMemcpyAsync(hs, ub[n & 1], size_t(n_entries) * comps * sizeof(double),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+        KP_CUDA(cudaStreamSynchronize(ctx->stream));
+        sample_fn(sample_user, n, hs);
+      }
+    }
     KP_CUDA(cudaEventRecord(ev[3], ctx->stream));
     if (exec) cudaGraphExecDestroy(exec);
     if (n_steps & 1)
@@ -960,7 +983,9 @@ void ctx_ok(kp_ctx* ctx) {
 
 int integrate_impl(kp_ctx* ctx, bool cplx, int method, double* u, const int* dims, int d,
                    const double* const* as, const kp_gfun* g, double t0, double t_final,
-                   long n_steps, int q, long* diverged_step, double* loop_seconds) {
+                   long n_steps, int q, long* diverged_step, double* loop_seconds,
+                   int sample_every = 0, kp_sample_fn sample_fn = nullptr,
+                   void* sample_user = nullptr) {
   if (diverged_step) *diverged_step = 0;
   return guard_c(
       [&] {
@@ -974,12 +999,15 @@ int integrate_impl(kp_ctx* ctx, bool cplx, int method, double* u, const int* dim
         Integrator it(ctx, method, cplx, dv, as, *g, tau);
         it.setup(q);
         static const bool no_graph = getenv("KP_NO_GRAPH") != nullptr;  // debugging aid
-        const double sec = it.run(u, t0, n_steps, !no_graph);
+        if (sample_every < 0) throw invalid_argument("integrate: negative sample_every");
+        const double sec = it.run(u, t0, n_steps, !no_graph, sample_every, sample_fn, sample_user);
         if (loop_seconds) *loop_seconds = sec;
         if (it.diverged_at) {  // DivergenceError(n+1, t+tau), inc/integrators.hpp:86-97,364
           const long k = it.diverged_at;
+          // t + tau with t = t0 + (k-1) tau, as the reference computes it
+          const double tk = (t0 + double(k - 1) * tau) + tau;
           throw divergence_error("state became non-finite at step " + std::to_string(k) +
-                                     " (t = " + std::to_string(t0 + double(k) * tau) + ")",
+                                     " (t = " + std::to_string(tk) + ")",
                                  k);
         }
       },
@@ -1172,6 +1200,22 @@ int kp_integrate_c128(kp_ctx* ctx, int method, double* u, const int* dims, int d
                       long n_steps, int q, long* diverged_step, double* loop_seconds) {
   return integrate_impl(ctx, true, method, u, dims, d, as, g, t0, t_final, n_steps, q,
                         diverged_step, loop_seconds);
+}
+int kp_integrate_sampled_f64(kp_ctx* ctx, int method, double* u, const int* dims, int d,
+                             const double* const* as, const kp_gfun* g, double t0,
+                             double t_final, long n_steps, int q, int sample_every,
+                             kp_sample_fn fn, void* user, long* diverged_step,
+                             double* loop_seconds) {
+  return integrate_impl(ctx, false, method, u, dims, d, as, g, t0, t_final, n_steps, q,
+                        diverged_step, loop_seconds, sample_every, fn, user);
+}
+int kp_integrate_sampled_c128(kp_ctx* ctx, int method, double* u, const int* dims, int d,
+                              const double* const* as, const kp_gfun* g, double t0,
+                              double t_final, long n_steps, int q, int sample_every,
+                              kp_sample_fn fn, void* user, long* diverged_step,
+                              double* loop_seconds) {
+  return integrate_impl(ctx, true, method, u, dims, d, as, g, t0, t_final, n_steps, q,
+                        diverged_step, loop_seconds, sample_every, fn, user);
 }
 int kp_host_integrate_f64(kp_ctx* ctx, int method, const double* u0, const int* dims, int d,
                           const double* const* as, const kp_gfun* g, double t0, double t_final,

@@ -31,7 +31,13 @@ _D, _I, _L, _PD, _PI, _VP, _PPD = (C.c_double, C.c_int, C.c_long, C.POINTER(C.c_
                                    C.POINTER(C.c_int), C.c_void_p,
                                    C.POINTER(C.POINTER(C.c_double)))
 _CTX, _PG, _PL = C.c_void_p, C.POINTER(GFun), C.POINTER(C.c_long)
+# kp_sample_fn: (user, step, u_host) -- the trajectory hook of kp_integrate_sampled_*
+SAMPLE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_long, C.POINTER(C.c_double))
 for _name, _res, _args in [
+    ("kp_integrate_sampled_f64", _I, [_CTX, _I, _VP, _PI, _I, _PPD, _PG, _D, _D, _L, _I, _I,
+                                      SAMPLE_FN, _VP, _PL, _PD]),
+    ("kp_integrate_sampled_c128", _I, [_CTX, _I, _VP, _PI, _I, _PPD, _PG, _D, _D, _L, _I, _I,
+                                       SAMPLE_FN, _VP, _PL, _PD]),
     ("kp_gll_rule", _I, [_I, _PD, _PD]),
     ("kp_expm_f64", _I, [_CTX, _VP, _I, _VP]),
     ("kp_solve_f64", _I, [_CTX, _VP, _I, _VP, _I, _VP]),
@@ -385,10 +391,14 @@ class ProblemSpec:
 
 @dataclass
 class StepperConfig:
-    """inc/integrators.hpp:71-77 (the Split backend; no trajectory sampling)."""
+    """inc/integrators.hpp:71-77.  backend: "split" (the device splitting
+    path) or "dense_oracle" (validation: the assembled Kronecker sum as the
+    single factor of a one-mode problem, i.e. the exact phi actions)."""
     method: Method = Method.ExpEuler
     n_steps: int = 1
     quad_nodes: int = kDefaultQuadNodes
+    sample_every: int = 0  # 0 disables trajectory sampling
+    backend: str = "split"
 
 
 @dataclass
@@ -397,6 +407,7 @@ class IntegrateResult:
     final: object
     wallclock_s: float = 0.0
     loop_s: float = 0.0
+    trajectory: list = None  # [(t, u)] at t0 and every sample_every steps
 
 
 def integrate(p: ProblemSpec, c: StepperConfig) -> IntegrateResult:
@@ -416,11 +427,18 @@ def integrate(p: ProblemSpec, c: StepperConfig) -> IntegrateResult:
     for mu, f in enumerate(k.factors):
         if f.shape[0] != dims[mu]:
             raise InvalidArgument(1, f"mode_product: size mismatch on mode {mu}")
+    if c.sample_every < 0:
+        raise InvalidArgument(1, "integrate: negative sample_every")
+    if c.backend == "dense_oracle":
+        return _integrate_dense_oracle(p, c, k, dims, cplx, host)
+    if c.backend != "split":
+        raise InvalidArgument(1, f"integrate: unknown backend {c.backend}")
     t_start = time.perf_counter()
     dv = C.c_long(0)
     loop = C.c_double(0)
     _bind_aux(p.g)
-    if host:
+    traj = None
+    if host and not c.sample_every:
         dtype = np.complex128 if cplx else np.float64
         uh = np.asfortranarray(u0, dtype=dtype)
         fs = [np.asfortranarray(f, dtype=dtype) for f in k.factors]
@@ -433,20 +451,81 @@ def integrate(p: ProblemSpec, c: StepperConfig) -> IntegrateResult:
                C.byref(dv), C.byref(loop))
     else:
         dt = torch.complex128 if cplx else torch.float64
-        out = fortran_empty(dims, dt, u0.device)
-        out.copy_(u0)
+        src = to_device(np.asarray(u0)) if host else u0
+        out = fortran_empty(dims, dt, src.device)
+        out.copy_(src)
         fs = [x.to(dt) for x in _upload_factors(k.factors)]
-        ctx = _ctx_for(u0)
-        f = ctx.lib.kp_integrate_c128 if cplx else ctx.lib.kp_integrate_f64
-        rc = f(ctx.h, int(c.method), out.data_ptr(), ints(dims), len(dims),
-               ptr_array([x.data_ptr() for x in fs]), C.byref(p.g), float(p.t0),
-               float(p.t_final), int(c.n_steps), int(c.quad_nodes), C.byref(dv), C.byref(loop))
+        ctx = _ctx_for(out)
+        if c.sample_every:
+            tau = (p.t_final - p.t0) / float(c.n_steps)
+            n = int(np.prod(dims))
+            npdt = np.complex128 if cplx else np.float64
+            traj = [(p.t0, np.array(u0, copy=True) if host else u0.clone())]
+
+            def _hook(user, step, uh):
+                a = np.ctypeslib.as_array(uh, shape=(n * (2 if cplx else 1),)).copy()
+                a = a.view(npdt).reshape(dims, order="F")
+                traj.append((p.t0 + float(step) * tau, a if host else to_device(a)))
+            hook = SAMPLE_FN(_hook)
+            f = ctx.lib.kp_integrate_sampled_c128 if cplx else ctx.lib.kp_integrate_sampled_f64
+            rc = f(ctx.h, int(c.method), out.data_ptr(), ints(dims), len(dims),
+                   ptr_array([x.data_ptr() for x in fs]), C.byref(p.g), float(p.t0),
+                   float(p.t_final), int(c.n_steps), int(c.quad_nodes), int(c.sample_every),
+                   hook, None, C.byref(dv), C.byref(loop))
+        else:
+            f = ctx.lib.kp_integrate_c128 if cplx else ctx.lib.kp_integrate_f64
+            rc = f(ctx.h, int(c.method), out.data_ptr(), ints(dims), len(dims),
+                   ptr_array([x.data_ptr() for x in fs]), C.byref(p.g), float(p.t0),
+                   float(p.t_final), int(c.n_steps), int(c.quad_nodes), C.byref(dv),
+                   C.byref(loop))
+        if host:
+            torch.cuda.synchronize(out.device)
+            out = to_host(out)
     try:
         check(rc, step=dv.value)
     except DivergenceError as e:
         e.loop_s = loop.value  # the loop ran to the end; its device time is still valid
         raise
-    return IntegrateResult(out, time.perf_counter() - t_start, loop.value)
+    return IntegrateResult(out, time.perf_counter() - t_start, loop.value, traj)
+
+
+def _assemble_kronsum(factors):
+    """Dense K = sum_mu I (x) .. (x) A_mu (x) .. (x) I, first mode fastest."""
+    dims = [f.shape[0] for f in factors]
+    N = int(np.prod(dims))
+    if N > 8192:
+        raise InvalidArgument(1, "DenseOracle: problem too large (N > 8192)")
+    K = np.zeros((N, N), dtype=np.result_type(*factors), order="F")
+    P = 1
+    for mu, a in enumerate(factors):
+        Q = N // (P * dims[mu])
+        K += np.kron(np.kron(np.eye(Q), np.asarray(a)), np.eye(P))
+        P *= dims[mu]
+    return np.asfortranarray(K)
+
+
+def _integrate_dense_oracle(p, c, k, dims, cplx, host):
+    """Backend::DenseOracle (inc/integrators.hpp:243-262): the textbook
+    exponential integrators on the assembled operator -- run as the one-mode
+    problem vec(u)' = K vec(u) + g on the device, where the split phi of the
+    single factor is the exact phi_l(tau K)."""
+    if int(c.method) == int(Method.RosenbrockEuler):
+        raise InvalidArgument(1, "DenseOracle: Rosenbrock-Euler is not provided")
+    if p.g.kind in (G_BRUSSELATOR, G_RICCATI):
+        raise InvalidArgument(1, "DenseOracle: this g needs the tensor shape")
+    fs = [to_host(f) if _is_torch(f) else np.asarray(f) for f in k.factors]
+    K = _assemble_kronsum(fs)
+    u = to_host(p.u0) if not host else np.asarray(p.u0)
+    u1 = np.asfortranarray(u.reshape(-1, order="F"))
+    c1 = StepperConfig(c.method, c.n_steps, c.quad_nodes, c.sample_every, "split")
+    r = integrate(ProblemSpec([K], p.g, u1, p.t0, p.t_final), c1)
+    shape = lambda a: np.asfortranarray(np.asarray(a).reshape(dims, order="F"))
+    fin = shape(r.final)
+    traj = [(t, shape(x)) for t, x in r.trajectory] if r.trajectory else None
+    if not host:
+        fin = to_device(fin)
+        traj = [(t, to_device(x)) for t, x in traj] if traj else None
+    return IntegrateResult(fin, r.wallclock_s, r.loop_s, traj)
 
 
 def integrate_config(method, u0, As, g, t0, t_final, n_steps, q=kDefaultQuadNodes):
