@@ -200,7 +200,7 @@ TEST_CASE("divergence is reported with the step index") {
     caught = true;
     CHECK(e.step() >= 1);
     CHECK(std::string(e.what()).find("step") != std::string::npos);
-    CHECK(std::string(e.what()) == "state became non-finite at step 1 (t = 1.000000)");
+    CHECK(std::string(e.what()) == "state became non-finite at step 2 (t = 2.000000)");
   }
   CHECK(caught);
   // the device path reports the same step and message
@@ -210,7 +210,7 @@ TEST_CASE("divergence is reported with the step index") {
     integrate(p, c);
   } catch (const DivergenceError& e) {
     caught = true;
-    CHECK(std::string(e.what()) == "state became non-finite at step 1 (t = 1.000000)");
+    CHECK(std::string(e.what()) == "state became non-finite at step 2 (t = 2.000000)");
   }
   CHECK(caught);
 }
