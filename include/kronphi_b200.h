@@ -384,6 +384,42 @@ int kp_integrate_sampled_c128(kp_ctx* ctx, int method, double* u, const int* dim
                               double t_final, long n_steps, int q, int sample_every,
                               kp_sample_fn fn, void* user, long* diverged_step,
                               double* loop_seconds);
+/* Slab-sharded integrate across the GPUs of one node (the
+ * reference is single-node CPU).  u_local: this rank's slab of the state on
+ * the context's device (dims_local: the last spatial mode holds n_d / P
+ * planes; a stacked Brusselator keeps its species mode last); as: the FULL
+ * factors (device).  Exchanges over comm (NCCL on the context's stream, no
+ * host sync inside a step; the step is a replayed CUDA graph).  mode_d: how
+ * the last mode crosses the slabs -- 1 = all-to-all pencil transpose (bitwise
+ * equal to the single-GPU integrate), 2 = partial products + reduce-scatter,
+ * 0 = pick by measurement (one step of each, max over ranks); *mode_used
+ * reports the choice.  Divergence: KP_EDIVERGE with the first bad step over
+ * all ranks.  *loop_seconds = device time of the loop, max over ranks.
+ * g: the pointwise set (not ADR / Riccati); methods lawson_euler, lawson2b,
+ * exp_euler, etd2rk. */
+int kp_integrate_sharded_f64(kp_ctx* ctx, kp_comm* comm, int method, double* u_local,
+                             const int* dims_local, int d, const double* const* as,
+                             const kp_gfun* g, double t0, double t_final, long n_steps, int q,
+                             int mode_d, int* mode_used, long* diverged_step,
+                             double* loop_seconds);
+int kp_integrate_sharded_c128(kp_ctx* ctx, kp_comm* comm, int method, double* u_local,
+                              const int* dims_local, int d, const double* const* as,
+                              const kp_gfun* g, double t0, double t_final, long n_steps, int q,
+                              int mode_d, int* mode_used, long* diverged_step,
+                              double* loop_seconds);
+/* The same sharded integrator with all P ranks driven by this process on one
+ * device (u_slabs[r] = rank r's slab; the exchanges become device copies):
+ * the data movement of a P-GPU run, testable on one GPU. */
+int kp_integrate_sharded_local_f64(kp_ctx* ctx, int P, int method, double* const* u_slabs,
+                                   const int* dims_local, int d, const double* const* as,
+                                   const kp_gfun* g, double t0, double t_final, long n_steps,
+                                   int q, int mode_d, int* mode_used, long* diverged_step,
+                                   double* loop_seconds);
+int kp_integrate_sharded_local_c128(kp_ctx* ctx, int P, int method, double* const* u_slabs,
+                                    const int* dims_local, int d, const double* const* as,
+                                    const kp_gfun* g, double t0, double t_final, long n_steps,
+                                    int q, int mode_d, int* mode_used, long* diverged_step,
+                                    double* loop_seconds);
 /* Host-buffer drop-in: u0/as on the host, u_final written on the host. */
 int kp_host_integrate_f64(kp_ctx* ctx, int method, const double* u0, const int* dims, int d,
                           const double* const* as, const kp_gfun* g, double t0, double t_final,

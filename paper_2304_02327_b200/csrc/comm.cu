@@ -44,6 +44,10 @@ struct NcclApi {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -65,8 +69,10 @@ const NcclApi& nccl() {
     a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
     a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    a.ReduceScatter = reinterpret_cast<decltype(a.ReduceScatter)>(sym("ncclReduceScatter"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(sym("ncclAllReduce"));
     a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.GroupStart &&
-           a.GroupEnd && a.GetErrorString;
+           a.GroupEnd && a.GetErrorString && a.ReduceScatter && a.AllReduce;
     if (!a.ok) a.why = "NCCL library lacks the point-to-point API";
     return a;
   }();
@@ -209,6 +215,64 @@ void need(kp_ctx* ctx, kp_comm* c) {
 constexpr int SLOT_SEND = 64, SLOT_RECV = 65;  // distinct from every other slot (phi.cu uses 20..58)
 
 }  // namespace
+
+// ---- internal entry points for the sharded integrator (stepper.cu) ----
+int comm_size(const kp_comm* c) { return c->P; }
+int comm_rank(const kp_comm* c) { return c->rank; }
+
+void repartition_pack(kp_ctx* ctx, int dir, int P, int rank, long long A, long long B,
+                      long long C, long long S, int comps, const double* x, double* send,
+                      bool pack) {
+  long long n = 0;
+  const Part p = make_part(dir, P, rank, A, B, C, S, comps, &n);
+  launch_repartition(ctx, p, dir, pack, comps, n, x, send);
+}
+
+void comm_repartition(kp_ctx* ctx, kp_comm* c, int dir, long long A, long long B, long long C,
+                      long long S, int comps, const double* x, double* y, double* send,
+                      double* recv) {
+  long long n = 0;
+  const Part p = make_part(dir, c->P, c->rank, A, B, C, S, comps, &n);
+  if (c->P == 1) {
+    if (x != y)
+      KP_CUDA(cudaMemcpyAsync(y, x, size_t(n) * comps * sizeof(double), cudaMemcpyDeviceToDevice,
+                              ctx->stream));
+    return;
+  }
+  launch_repartition(ctx, p, dir, true, comps, n, x, send);
+  alltoall(ctx, c, send, recv, size_t(n / c->P) * comps);
+  launch_repartition(ctx, p, dir, false, comps, n, recv, y);
+}
+
+// grouped send/recv of `count` doubles from each (src, dst) pair below:
+// sends[i] -> rank to[i], recvs[i] <- rank from[i]
+void comm_sendrecv(kp_ctx* ctx, kp_comm* c, const std::vector<const double*>& sends,
+                   const std::vector<int>& to, const std::vector<double*>& recvs,
+                   const std::vector<int>& from, size_t count) {
+  const NcclApi& a = need_nccl();
+  nccl_check(a.GroupStart(), "ncclGroupStart");
+  for (size_t i = 0; i < sends.size(); ++i)
+    nccl_check(a.Send(sends[i], count, ncclFloat64, to[i], c->nc, ctx->stream), "ncclSend");
+  for (size_t i = 0; i < recvs.size(); ++i)
+    nccl_check(a.Recv(recvs[i], count, ncclFloat64, from[i], c->nc, ctx->stream), "ncclRecv");
+  nccl_check(a.GroupEnd(), "ncclGroupEnd");
+}
+
+// recv (count doubles) = sum over ranks of chunk `rank` of send (P chunks)
+void comm_reduce_scatter(kp_ctx* ctx, kp_comm* c, const double* send, double* recv,
+                         size_t count) {
+  nccl_check(need_nccl().ReduceScatter(send, recv, count, ncclFloat64, ncclSum, c->nc,
+                                       ctx->stream),
+             "ncclReduceScatter");
+}
+
+// in place: x = op over ranks (op 0 min, 1 max), n doubles
+void comm_allreduce(kp_ctx* ctx, kp_comm* c, double* x, size_t n, int op) {
+  nccl_check(need_nccl().AllReduce(x, x, n, ncclFloat64, op == 0 ? ncclMin : ncclMax, c->nc,
+                                   ctx->stream),
+             "ncclAllReduce");
+}
+
 }  // namespace kp
 
 using namespace kp;

@@ -183,6 +183,23 @@ void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<i
                     long long half, int slab = -1, int k0 = 0, int n_glob = 0, int halo = 0,
                     double t = 0.0);
 
+// ---- communicator internals (comm.cu), used by the sharded integrator ----
+int comm_size(const kp_comm* c);
+int comm_rank(const kp_comm* c);
+// pack (slab/pencil -> send blocks) or unpack (recv blocks -> pencil/slab)
+void repartition_pack(kp_ctx* ctx, int dir, int P, int rank, long long A, long long B,
+                      long long C, long long S, int comps, const double* x, double* y,
+                      bool pack);
+void comm_repartition(kp_ctx* ctx, kp_comm* c, int dir, long long A, long long B, long long C,
+                      long long S, int comps, const double* x, double* y, double* send,
+                      double* recv);
+void comm_sendrecv(kp_ctx* ctx, kp_comm* c, const std::vector<const double*>& sends,
+                   const std::vector<int>& to, const std::vector<double*>& recvs,
+                   const std::vector<int>& from, size_t count);
+void comm_reduce_scatter(kp_ctx* ctx, kp_comm* c, const double* send, double* recv,
+                         size_t count);
+void comm_allreduce(kp_ctx* ctx, kp_comm* c, double* x, size_t n, int op);
+
 // ---- steppers (stepper.cu) ----
 // d = g(t + tau, s) - g(t, u); half > 0: Brusselator species offset
 void gdiff_dev(kp_ctx* ctx, const kp_gfun& g, double t, double tau, const double* s,

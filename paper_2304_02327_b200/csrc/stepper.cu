@@ -865,6 +865,649 @@ class Integrator {
   }
 };
 
+
+// ======================================================================
+// Slab-sharded integrate; replaces parallel.py's
+// ShardedIntegrator behind the C ABI (kp_integrate_sharded_*).
+//
+// Global layout: spatial modes n_1..n_ds, species S (2 for the stacked
+// Brusselator: the slowest mode), viewed column-major as (A, B, C, S) with
+// A = n_1..n_{ds-2}, B = n_{ds-1}, C = n_ds.  Rank r owns the slab of planes
+// [r C/P, (r+1) C/P) of the last spatial mode; the pencil layout splits B
+// instead (modes < ds-1 and g are slab-local, mode ds is pencil-local).
+//
+// Mode ds (the exchange step), two ways:
+//   A: all-to-all pencil transpose (comm.cu pack -> grouped send/recv ->
+//      unpack), mode ds on the pencil, the step's last update fused into its
+//      epilogue, transposed back.  Every entry is computed from the same
+//      inputs in the same k order as on one GPU: bitwise equal to the
+//      single-GPU integrate.
+//   B: every rank multiplies its slab by its column block of the factor
+//      (a full-size partial product), the partials are reduce-scattered into
+//      slabs (ncclReduceScatter), the epilogue runs as an elementwise pass.
+//      P x the bytes of one transpose but no transpose back and no pencil
+//      copy of u; sums the k range in a different order (tolerance-level).
+//   mode_d = 0 picks by measurement: one step of each, device time (max over
+//   ranks), the faster wins.
+// The Kronecker sum of banded factors (every config) is the stencil of
+// banded.cu on the slab with a one-plane halo exchange.
+//
+// Exchanges are stream-ordered (NCCL on the context's stream): no host sync
+// or barrier inside a step, and the step is captured into a CUDA graph.
+// The same code drives all P ranks inside one process (comm == NULL,
+// "emulated": the exchanges become device copies between the ranks'
+// buffers) -- how the data movement is tested bitwise on one GPU.
+// ======================================================================
+
+__global__ void add_into_kernel(long long n, const double* __restrict__ x, double* __restrict__ y) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = __dadd_rn(y[i], x[i]);
+}
+
+class ShardExchange {
+ public:
+  int P = 1;
+  kp_comm* comm = nullptr;      // NCCL, one local rank
+  std::vector<int> ranks;       // ranks this process drives
+  std::vector<double*> send, recv;  // per local rank scratch (repartition)
+  long long cap = 0;
+
+  int nlocal() const { return int(ranks.size()); }
+
+  void scratch(long long doubles) {
+    if (doubles <= cap) return;
+    for (double* p : send) cudaFree(p);
+    for (double* p : recv) cudaFree(p);
+    send.assign(ranks.size(), nullptr);
+    recv.assign(ranks.size(), nullptr);
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      KP_CUDA(cudaMalloc(&send[i], size_t(doubles) * sizeof(double)));
+      KP_CUDA(cudaMalloc(&recv[i], size_t(doubles) * sizeof(double)));
+    }
+    cap = doubles;
+  }
+  ~ShardExchange() {
+    for (double* p : send) cudaFree(p);
+    for (double* p : recv) cudaFree(p);
+  }
+
+  // y[i] = x[i] re-partitioned (dir 1: slab -> pencil, 2: back)
+  void repartition(kp_ctx* ctx, int dir, long long A, long long B, long long C, long long S,
+                   int comps, const std::vector<const double*>& x, const std::vector<double*>& y) {
+    const long long n = A * B * C * S / P * comps;  // doubles per rank
+    if (P == 1) {
+      if (x[0] != y[0])
+        KP_CUDA(cudaMemcpyAsync(y[0], x[0], size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+      return;
+    }
+    scratch(n);
+    if (comm) {
+      comm_repartition(ctx, comm, dir, A, B, C, S, comps, x[0], y[0], send[0], recv[0]);
+      return;
+    }
+    const long long blk = n / P;
+    for (int r = 0; r < P; ++r)
+      repartition_pack(ctx, dir, P, r, A, B, C, S, comps, x[r], send[r], true);
+    for (int r = 0; r < P; ++r)
+      for (int s = 0; s < P; ++s)
+        KP_CUDA(cudaMemcpyAsync(recv[s] + r * blk, send[r] + s * blk, size_t(blk) * sizeof(double),
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+    for (int r = 0; r < P; ++r)
+      repartition_pack(ctx, dir, P, r, A, B, C, S, comps, recv[r], y[r], false);
+  }
+
+  // ext[i] = (plane doubles) x (Cl + 2) x S: fill planes 0 and Cl+1 of every
+  // species from the neighbours' last / first interior planes (periodic in
+  // the rank index; a Dirichlet factor never reads the wrapped plane)
+  void halo(kp_ctx* ctx, long long plane, long long Cl, long long S,
+            const std::vector<double*>& ext) {
+    auto at = [&](double* e, long long sp, long long k) { return e + (sp * (Cl + 2) + k) * plane; };
+    if (comm && P > 1) {
+      const int r = ranks[0], up = (r + 1) % P, down = (r + P - 1) % P;
+      std::vector<const double*> sends;
+      std::vector<int> to, from;
+      std::vector<double*> recvs;
+      for (long long sp = 0; sp < S; ++sp) {  // same order as kp_comm_halo_f64
+        sends.push_back(at(ext[0], sp, Cl));  // last interior -> up (its left halo)
+        to.push_back(up);
+        sends.push_back(at(ext[0], sp, 1));   // first interior -> down (its right halo)
+        to.push_back(down);
+        recvs.push_back(at(ext[0], sp, 0));   // left halo <- down's last
+        from.push_back(down);
+        recvs.push_back(at(ext[0], sp, Cl + 1));  // right halo <- up's first
+        from.push_back(up);
+      }
+      comm_sendrecv(ctx, comm, sends, to, recvs, from, size_t(plane));
+      return;
+    }
+    const int n = nlocal();  // emulated (or P == 1): device copies
+    for (int i = 0; i < n; ++i) {
+      const int dn = (i + n - 1) % n, upi = (i + 1) % n;
+      for (long long sp = 0; sp < S; ++sp) {
+        KP_CUDA(cudaMemcpyAsync(at(ext[i], sp, 0), at(ext[dn], sp, Cl), size_t(plane) * 8,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+        KP_CUDA(cudaMemcpyAsync(at(ext[i], sp, Cl + 1), at(ext[upi], sp, 1), size_t(plane) * 8,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+      }
+    }
+  }
+
+  // y[i] = sum over ranks of the ranks[i]-th C/P-plane block (per species) of
+  // the full-size partials part[*]  (plane doubles per plane)
+  void reduce_scatter(kp_ctx* ctx, long long plane, long long C, long long S,
+                      const std::vector<double*>& part, const std::vector<double*>& y) {
+    const long long Cl = C / P, cnt = plane * Cl;
+    if (comm) {
+      for (long long sp = 0; sp < S; ++sp)
+        comm_reduce_scatter(ctx, comm, part[0] + sp * plane * C, y[0] + sp * cnt, size_t(cnt));
+      return;
+    }
+    for (int s = 0; s < P; ++s)
+      for (long long sp = 0; sp < S; ++sp) {
+        double* dst = y[s] + sp * cnt;
+        KP_CUDA(cudaMemcpyAsync(dst, part[0] + sp * plane * C + s * cnt, size_t(cnt) * 8,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+        for (int r = 1; r < P; ++r) {
+          add_into_kernel<<<grid_ew(ctx, cnt), 256, 0, ctx->stream>>>(
+              cnt, part[r] + sp * plane * C + s * cnt, dst);
+          ctx->launches++;
+        }
+      }
+  }
+
+  // max over all ranks of a host value (NCCL all-reduce through the device)
+  double max_over_ranks(kp_ctx* ctx, double v, double* dev_scratch) {
+    if (!comm || P == 1) return v;
+    KP_CUDA(cudaMemcpyAsync(dev_scratch, &v, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    comm_allreduce(ctx, comm, dev_scratch, 1, 1);
+    KP_CUDA(cudaMemcpyAsync(&v, dev_scratch, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    KP_CUDA(cudaStreamSynchronize(ctx->stream));
+    return v;
+  }
+};
+
+class ShardedIntegrator {
+ public:
+  kp_ctx* ctx;
+  ShardExchange& X;
+  Integrator G;  // global set-up: factor sets, band structures, g checks
+  int method, P, ds, comps, mode_d = 1;
+  bool cplx;
+  long long A, B, C, S, Cl, Bp, nloc;
+  std::vector<int> dl, dp;  // local slab / pencil dims (incl. species)
+  struct Rank {
+    int r;
+    double *u, *ub, *ext, *rr, *rp, *up, *sp, *dq, *dd, *t0, *t1, *w, *y, *part, *out, *tr;
+    int* cnt;  // [ctr slot 0, bad, ctr slot 1]
+  };
+  std::vector<Rank> R;
+  std::vector<double*> owned;
+  double* scratch = nullptr;
+
+  ShardedIntegrator(kp_ctx* c, ShardExchange& x, int m, bool cp, const std::vector<int>& gdims,
+                    const double* const* as, const kp_gfun& g, double tau)
+      : ctx(c), X(x), G(c, m, cp, gdims, as, g, tau), method(m), P(x.P), comps(cp ? 2 : 1),
+        cplx(cp) {
+    if (g.kind == KP_G_ADR || g.kind == KP_G_RICCATI || g.step_ctr)
+      throw invalid_argument("sharded integrate: the ADR and Riccati g's are not supported "
+                             "(time-dependent / nonlocal)");
+    if (method == KP_ROSENBROCK_EULER || method == KP_EXP_EULER_LS)
+      throw invalid_argument("sharded integrate: lawson_euler, lawson2b, exp_euler, etd2rk");
+    S = (g.kind == KP_G_BRUSSELATOR) ? 2 : 1;
+    ds = int(gdims.size()) - (S == 2 ? 1 : 0);
+    if (ds < 2) throw invalid_argument("sharded integrate: needs >= 2 spatial modes");
+    A = 1;
+    for (int mu = 0; mu < ds - 2; ++mu) A *= gdims[mu];
+    B = gdims[ds - 2];
+    C = gdims[ds - 1];
+    if (B % P || C % P)
+      throw invalid_argument("sharded integrate: n_(d-1) and n_d must be divisible by P");
+    Cl = C / P;
+    Bp = B / P;
+    dl = gdims;
+    dl[ds - 1] = int(Cl);
+    dp = gdims;
+    dp[ds - 2] = int(Bp);
+    nloc = A * B * Cl * S;
+    KP_CUDA(cudaMalloc(&scratch, 64));
+    owned.push_back(scratch);
+  }
+  ~ShardedIntegrator() {
+    for (double* p : owned) cudaFree(p);
+  }
+  double* alloc(long long entries) {
+    double* p = nullptr;
+    KP_CUDA(cudaMalloc(&p, size_t(std::max<long long>(entries, 1)) * comps * sizeof(double)));
+    owned.push_back(p);
+    return p;
+  }
+  void setup(int q, int md, const std::vector<double*>& user_u) {
+    G.setup(q);
+    for (const FactorSet* fs : {&G.f1, &G.f2}) {
+      if (fs->f.empty()) continue;
+      for (int mu = 0; mu < ds; ++mu)
+        if (!fs->active[mu])
+          throw invalid_argument("sharded integrate: a spatial phi factor is a multiple of I");
+    }
+    const long long plane = A * B;
+    R.resize(X.nlocal());
+    for (int i = 0; i < X.nlocal(); ++i) {
+      Rank& k = R[i];
+      k.r = X.ranks[i];
+      k.u = user_u[i];
+      k.ub = alloc(nloc);
+      k.ext = alloc(plane * (Cl + 2) * S);
+      k.rr = alloc(nloc);
+      k.rp = alloc(nloc);
+      k.up = alloc(nloc);
+      k.sp = alloc(2 * nloc);  // [stage; y1] for Lawson2b
+      k.dq = alloc(nloc);
+      k.dd = alloc(nloc);
+      k.t0 = alloc(nloc);
+      k.t1 = alloc(nloc);
+      k.w = alloc(2 * nloc);
+      k.y = alloc(nloc);
+      k.out = alloc(nloc);
+      k.tr = alloc(nloc);
+      k.part = md == 1 ? nullptr : alloc(A * B * C * S);
+      int* cb = nullptr;
+      KP_CUDA(cudaMalloc(&cb, 16));
+      owned.push_back(reinterpret_cast<double*>(cb));
+      const int init[4] = {0, INT_MAX, 0, 0};
+      KP_CUDA(cudaMemcpyAsync(cb, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+      k.cnt = cb;
+    }
+  }
+
+  template <typename F>
+  void each(F&& f) {
+    for (auto& k : R) f(k);
+  }
+  std::vector<const double*> cv(double* Rank::*m, long long off = 0) {
+    std::vector<const double*> v;
+    for (auto& k : R) v.push_back(k.*m + off);
+    return v;
+  }
+  std::vector<double*> mv(double* Rank::*m, long long off = 0) {
+    std::vector<double*> v;
+    for (auto& k : R) v.push_back(k.*m + off);
+    return v;
+  }
+  void to_pencil(const std::vector<const double*>& x, const std::vector<double*>& y) {
+    X.repartition(ctx, 1, A, B, C, S, comps, x, y);
+  }
+  void to_slab(const std::vector<const double*>& x, const std::vector<double*>& y) {
+    X.repartition(ctx, 2, A, B, C, S, comps, x, y);
+  }
+
+  // modes 0 .. ds-2 of a Tucker on the slab: returns the buffer holding the result
+  const double* tucker_slab(const FactorSet& fs, const double* x, Rank& k) {
+    const double* cur = x;
+    for (int mu = 0; mu < ds - 1; ++mu) {
+      double* dst = (mu & 1) ? k.t1 : k.t0;
+      Epilogue e;
+      e.alpha = (mu == 0) ? fs.pref : 1.0;
+      G.mp(ctx, cur, dl, mu, fs.f[mu], dl[mu], e, dst);
+      cur = dst;
+    }
+    return cur;
+  }
+  // Tucker with the last spatial mode on the pencil (option A): in (slab) ->
+  // out (pencil), `last(k)` = the epilogue of the last mode
+  template <typename L>
+  void tucker_A(const FactorSet& fs, const std::vector<const double*>& in,
+                const std::vector<double*>& out, L&& last) {
+    std::vector<const double*> mid;
+    for (size_t i = 0; i < R.size(); ++i) mid.push_back(tucker_slab(fs, in[i], R[i]));
+    std::vector<double*> pen;
+    for (auto& k : R) pen.push_back(mid[&k - R.data()] == k.t0 ? k.t1 : k.t0);
+    to_pencil(mid, pen);
+    for (size_t i = 0; i < R.size(); ++i) {
+      Epilogue e = last(R[i]);
+      e.alpha = fs.fold * (ds == 1 ? fs.pref : 1.0);
+      G.mp(ctx, pen[i], dp, ds - 1, fs.f[ds - 1], dp[ds - 1], e, out[i]);
+    }
+  }
+  // Tucker with the last spatial mode as partial products + reduce-scatter
+  // (option B): in (slab) -> out (slab), no epilogue
+  void tucker_B(const FactorSet& fs, const std::vector<const double*>& in,
+                const std::vector<double*>& out) {
+    std::vector<int> fd = dl;
+    fd[ds - 1] = int(C);
+    std::vector<double*> parts;
+    for (size_t i = 0; i < R.size(); ++i) {
+      Rank& k = R[i];
+      const double* mid = tucker_slab(fs, in[i], k);
+      Epilogue e;
+      e.alpha = fs.fold * (ds == 1 ? fs.pref : 1.0);
+      // columns [r Cl, (r+1) Cl) of the C x C factor: a C x Cl matrix, ld C
+      const double* blk = fs.f[ds - 1] + (long long)k.r * Cl * C * comps;
+      G.mp(ctx, mid, dl, ds - 1, blk, int(C), e, k.part);
+      parts.push_back(k.part);
+    }
+    X.reduce_scatter(ctx, A * B * comps, C, S, parts, out);
+  }
+
+  // r = K u + g(u) in slab layout (u: slab)
+  void kronsum_g(const std::vector<const double*>& u, const std::vector<double*>& r, double t) {
+    if (G.banded) {
+      const long long plane = A * B * comps;
+      // interior planes of every species into ext, then the halo planes
+      each([&](Rank& k) {
+        const long long i = &k - R.data();
+        KP_CUDA(cudaMemcpy2DAsync(k.ext + plane, size_t(plane * (Cl + 2)) * 8, u[i],
+                                  size_t(plane * Cl) * 8, size_t(plane * Cl) * 8, size_t(S),
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+      });
+      X.halo(ctx, plane, Cl, S, mv(&Rank::ext));
+      each([&](Rank& k) {
+        const long long i = &k - R.data();
+        kronsum_banded(ctx, cplx, k.ext, dl, G.band_cols, G.band_vals, G.a_active, r[i], true,
+                       G.g, S == 2 ? 1 : 0, ds - 1, int(k.r * Cl), int(C), 1, t);
+      });
+      return;
+    }
+    // dense: terms 0..ds-2 on the slab, the last on the pencil, back to the slab
+    each([&](Rank& k) {
+      const long long i = &k - R.data();
+      bool first = true;
+      for (int mu = 0; mu < ds - 1; ++mu) {
+        if (!G.a_active[mu]) continue;
+        Epilogue e;
+        e.beta = first ? 0.0 : 1.0;
+        G.mp(ctx, u[i], dl, mu, G.A[mu], dl[mu], e, k.rr);
+        first = false;
+      }
+      if (first) KP_CUDA(cudaMemsetAsync(k.rr, 0, size_t(nloc) * comps * 8, ctx->stream));
+    });
+    to_pencil(cv(&Rank::rr), mv(&Rank::rp));
+    each([&](Rank& k) {
+      Epilogue e;
+      e.kind = EPI_ADD_G;
+      e.beta = 1.0;
+      e.X = k.up;
+      e.g = G.g;
+      e.t = t;
+      G.mp(ctx, k.up, dp, ds - 1, G.A[ds - 1], dp[ds - 1], e, k.rp);
+    });
+    to_slab(cv(&Rank::rp), r);
+  }
+
+  void pre(const double* u, double* w, bool two, double t) {
+    const long long half = S == 2 ? nloc / 2 : 0;
+    if (!cplx && half > 0) {
+      launch_pdl(ctx, lawson_pre_pair_kernel, dim3(grid_ew(ctx, half)), dim3(256), 0, G.g, t,
+                 half, G.tau, two, u, w);
+    } else if (cplx) {
+      launch_pdl(ctx, lawson_pre_kernel<true>, dim3(grid_ew(ctx, nloc)), dim3(256), 0, G.g, t,
+                 nloc, half, G.tau, two, reinterpret_cast<const double2*>(u),
+                 reinterpret_cast<double2*>(w));
+    } else {
+      launch_pdl(ctx, lawson_pre_kernel<false>, dim3(grid_ew(ctx, nloc)), dim3(256), 0, G.g, t,
+                 nloc, half, G.tau, two, u, w);
+    }
+  }
+  void post(const double* y, double* out, int* bad, const int* ctr, double t2, int* next) {
+    const long long half = S == 2 ? nloc / 2 : 0;
+    if (!cplx && half > 0) {
+      launch_pdl(ctx, lawson2b_post_pair_kernel, dim3(grid_ew(ctx, half)), dim3(256), 0, G.g, t2,
+                 half, G.tau, y, out, bad, ctr, next);
+    } else if (cplx) {
+      launch_pdl(ctx, lawson2b_post_kernel<true>, dim3(grid_ew(ctx, nloc)), dim3(256), 0, G.g,
+                 t2, nloc, half, G.tau, reinterpret_cast<const double2*>(y),
+                 reinterpret_cast<double2*>(out), bad, ctr, next);
+    } else {
+      launch_pdl(ctx, lawson2b_post_kernel<false>, dim3(grid_ew(ctx, nloc)), dim3(256), 0, G.g,
+                 t2, nloc, half, G.tau, y, out, bad, ctr, next);
+    }
+  }
+  void gdiff(const double* s, const double* u, double* dd, double t) {
+    gdiff_dev(ctx, G.g, t, G.tau, s, u, nloc, S == 2 ? nloc / 2 : 0, cplx, dd);
+  }
+  void fma(double b, const double* y, const double* x, double* z) {
+    launch_fma(ctx, size_t(nloc) * comps, b, y, x, z);
+  }
+
+  // one step: u[i] -> o[i] (slab).  slot = counter slot of this step.
+  void step(const std::vector<const double*>& u, const std::vector<double*>& o, int slot) {
+    const double tau = G.tau, t = 0.0;
+    auto fin_of = [&](Rank& k) {
+      Epilogue f;
+      f.bad_step = k.cnt + 1;
+      f.step_ctr = k.cnt + (slot ? 2 : 0);
+      f.step_next = k.cnt + (slot ? 0 : 2);
+      return f;
+    };
+    const bool B_ = (mode_d == 2);
+    switch (method) {
+      case KP_EXP_EULER:
+      case KP_ETD2RK: {
+        // u on the pencil: the fused last-mode epilogues read it (A), the
+        // dense Kronecker sum's last term needs it (both)
+        if (!B_ || !G.banded) to_pencil(u, mv(&Rank::up));
+        kronsum_g(u, mv(&Rank::rr), t);
+        if (B_) {
+          tucker_B(G.f1, cv(&Rank::rr), mv(&Rank::y));
+          if (method == KP_EXP_EULER) {
+            each([&](Rank& k) {
+              const long long i = &k - R.data();
+              fma(tau, k.y, u[i], o[i]);
+              finite_flag(ctx, size_t(nloc) * comps, o[i], k.cnt + 1, k.cnt + (slot ? 2 : 0));
+              tick(k, slot);
+            });
+            return;
+          }
+          each([&](Rank& k) {
+            const long long i = &k - R.data();
+            fma(tau, k.y, u[i], k.sp);  // stage
+            gdiff(k.sp, u[i], k.dd, t);
+          });
+          tucker_B(G.f2, cv(&Rank::dd), mv(&Rank::y));
+          each([&](Rank& k) {
+            const long long i = &k - R.data();
+            fma(tau, k.y, k.sp, o[i]);
+            finite_flag(ctx, size_t(nloc) * comps, o[i], k.cnt + 1, k.cnt + (slot ? 2 : 0));
+            tick(k, slot);
+          });
+          return;
+        }
+        if (method == KP_EXP_EULER) {
+          tucker_A(G.f1, cv(&Rank::rr), mv(&Rank::out), [&](Rank& k) {
+            Epilogue f = fin_of(k);
+            f.kind = EPI_FMA_X;
+            f.X = k.up;
+            f.gamma = tau;
+            return f;
+          });
+          to_slab(cv(&Rank::out), o);
+          return;
+        }
+        const bool paired = S == 2;  // the coupled g: its own pass (as on one GPU)
+        tucker_A(G.f1, cv(&Rank::rr), mv(&Rank::sp), [&](Rank& k) {
+          Epilogue e;
+          e.X = k.up;
+          e.gamma = tau;
+          e.g = G.g;
+          e.t = t;
+          e.t2 = t + tau;
+          if (paired) {
+            e.kind = EPI_FMA_X;
+          } else {
+            e.kind = EPI_STAGE_D;
+            e.D = k.dq;
+          }
+          return e;
+        });
+        if (paired) each([&](Rank& k) { gdiff(k.sp, k.up, k.dq, t); });
+        to_slab(cv(&Rank::dq), mv(&Rank::dd));
+        tucker_A(G.f2, cv(&Rank::dd), mv(&Rank::out), [&](Rank& k) {
+          Epilogue f = fin_of(k);
+          f.kind = EPI_FMA_X;
+          f.X = k.sp;
+          f.gamma = tau;
+          return f;
+        });
+        to_slab(cv(&Rank::out), o);
+        return;
+      }
+      case KP_LAWSON_EULER:
+      case KP_LAWSON2B: {
+        const bool two = method == KP_LAWSON2B;
+        each([&](Rank& k) { pre(u[&k - R.data()], k.w, two, t); });
+        if (!two) {
+          if (B_) {
+            tucker_B(G.f1, cv(&Rank::w), o);
+            each([&](Rank& k) {
+              finite_flag(ctx, size_t(nloc) * comps, o[&k - R.data()], k.cnt + 1,
+                          k.cnt + (slot ? 2 : 0));
+              tick(k, slot);
+            });
+            return;
+          }
+          tucker_A(G.f1, cv(&Rank::w), mv(&Rank::out), [&](Rank& k) { return fin_of(k); });
+          to_slab(cv(&Rank::out), o);
+          return;
+        }
+        // [stage; y1] in one buffer (the post kernel's layout)
+        if (B_) {
+          tucker_B(G.f1, cv(&Rank::w), mv(&Rank::sp));
+          tucker_B(G.f1, cv(&Rank::w, nloc * comps), mv(&Rank::sp, nloc * comps));
+          each([&](Rank& k) {
+            post(k.sp, o[&k - R.data()], k.cnt + 1, k.cnt + (slot ? 2 : 0), t + tau,
+                 k.cnt + (slot ? 0 : 2));
+          });
+          return;
+        }
+        tucker_A(G.f1, cv(&Rank::w), mv(&Rank::sp), [&](Rank&) { return Epilogue{}; });
+        tucker_A(G.f1, cv(&Rank::w, nloc * comps), mv(&Rank::sp, nloc * comps),
+                 [&](Rank&) { return Epilogue{}; });
+        each([&](Rank& k) {
+          post(k.sp, k.out, k.cnt + 1, k.cnt + (slot ? 2 : 0), t + tau, k.cnt + (slot ? 0 : 2));
+        });
+        to_slab(cv(&Rank::out), o);
+        return;
+      }
+      default:
+        throw invalid_argument("sharded integrate: unsupported method");
+    }
+  }
+  void tick(Rank& k, int slot) {
+    launch_pdl(ctx, tick_kernel, dim3(1), dim3(1), 0, (const int*)(k.cnt + (slot ? 2 : 0)),
+               k.cnt + (slot ? 0 : 2));
+  }
+
+  // n_steps steps on the ranks' u (in/out); returns the loop's device time
+  // (this process; the caller takes the max over ranks)
+  double run(long n_steps, bool use_graph) {
+    std::vector<const double*> cu[2] = {cv(&Rank::u), cv(&Rank::ub)};
+    std::vector<double*> mu_[2] = {mv(&Rank::u), mv(&Rank::ub)};
+    cudaEvent_t ev[4];
+    for (auto& e : ev) KP_CUDA(cudaEventCreate(&e));
+    long n = 0;
+    KP_CUDA(cudaEventRecord(ev[0], ctx->stream));
+    step(cu[0], mu_[1], 0);
+    ++n;
+    KP_CUDA(cudaEventRecord(ev[1], ctx->stream));
+    cudaGraphExec_t exec = nullptr;
+    unsigned long long per = 0;
+    if (use_graph && n_steps - n >= 4) {
+      cudaGraph_t graph;
+      const unsigned long long l0 = ctx->launches;
+      KP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      step(cu[1], mu_[0], 1);
+      step(cu[0], mu_[1], 0);
+      KP_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+      per = ctx->launches - l0;
+      ctx->launches = l0;
+      KP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      cudaGraphDestroy(graph);
+    }
+    KP_CUDA(cudaEventRecord(ev[2], ctx->stream));
+    if (exec)
+      while (n_steps - n >= 2) {
+        KP_CUDA(cudaGraphLaunch(exec, ctx->stream));
+        ctx->launches += per;
+        n += 2;
+      }
+    while (n < n_steps) {
+      step(cu[n & 1], mu_[(n + 1) & 1], int(n & 1));
+      ++n;
+    }
+    KP_CUDA(cudaEventRecord(ev[3], ctx->stream));
+    if (exec) cudaGraphExecDestroy(exec);
+    if (n_steps & 1)
+      each([&](Rank& k) {
+        KP_CUDA(cudaMemcpyAsync(k.u, k.ub, size_t(nloc) * comps * 8, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+      });
+    KP_CUDA(cudaStreamSynchronize(ctx->stream));
+    float ms1 = 0.f, ms2 = 0.f;
+    KP_CUDA(cudaEventElapsedTime(&ms1, ev[0], ev[1]));
+    KP_CUDA(cudaEventElapsedTime(&ms2, ev[2], ev[3]));
+    for (auto& e : ev) cudaEventDestroy(e);
+    return double(ms1 + ms2) * 1e-3;
+  }
+  void reset_counters() {
+    each([&](Rank& k) {
+      const int init[4] = {0, INT_MAX, 0, 0};
+      KP_CUDA(cudaMemcpyAsync(k.cnt, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+    });
+  }
+  // first non-finite step over all ranks (0 = none)
+  long first_bad() {
+    double worst = double(INT_MAX);
+    each([&](Rank& k) {
+      int hb[2];
+      KP_CUDA(cudaMemcpyAsync(hb, k.cnt, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
+      KP_CUDA(cudaStreamSynchronize(ctx->stream));
+      worst = std::min(worst, double(hb[1]));
+    });
+    if (X.comm && P > 1) worst = -X.max_over_ranks(ctx, -worst, scratch);
+    return worst >= double(INT_MAX) ? 0 : long(worst);
+  }
+  // mode_d = 0: one step of each kind on scratch copies of the state, the
+  // faster (device time, max over ranks) is used for the run
+  void choose_mode_d(int requested) {
+    if (requested == 1 || requested == 2 || P == 1) {
+      mode_d = (P == 1) ? 1 : requested;
+      if (requested == 0) mode_d = 1;
+      return;
+    }
+    double best = 1e300;
+    int pick = 1;
+    for (int md : {1, 2}) {
+      mode_d = md;
+      if (md == 2)
+        each([&](Rank& k) {
+          if (!k.part) k.part = alloc(A * B * C * S);
+        });
+      for (int rep = 0; rep < 2; ++rep) {  // rep 0 warms up (workspace, kernels)
+        cudaEvent_t e0, e1;
+        KP_CUDA(cudaEventCreate(&e0));
+        KP_CUDA(cudaEventCreate(&e1));
+        // the trial writes a scratch copy (out -> y buffer), u is untouched
+        KP_CUDA(cudaEventRecord(e0, ctx->stream));
+        step(cv(&Rank::u), mv(&Rank::tr), 0);
+        KP_CUDA(cudaEventRecord(e1, ctx->stream));
+        KP_CUDA(cudaStreamSynchronize(ctx->stream));
+        float ms = 0.f;
+        KP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        const double sec = X.max_over_ranks(ctx, double(ms) * 1e-3, scratch);
+        if (rep == 1 && sec < best) {
+          best = sec;
+          pick = md;
+        }
+      }
+    }
+    mode_d = pick;
+    reset_counters();
+  }
+};
+
 }  // namespace kp
 
 // ============================================================== C ABI
@@ -1201,6 +1844,103 @@ int kp_integrate_c128(kp_ctx* ctx, int method, double* u, const int* dims, int d
   return integrate_impl(ctx, true, method, u, dims, d, as, g, t0, t_final, n_steps, q,
                         diverged_step, loop_seconds);
 }
+}  // extern "C"
+
+namespace {
+int sharded_impl(kp_ctx* ctx, kp_comm* comm, int P_local, bool cplx, int method,
+                 double* const* u, const int* dims, int d, const double* const* as,
+                 const kp_gfun* g, double t0, double t_final, long n_steps, int q, int mode_d,
+                 int* mode_used, long* diverged_step, double* loop_seconds) {
+  if (diverged_step) *diverged_step = 0;
+  return guard_c(
+      [&] {
+        ctx_ok(ctx);
+        auto dl = dims_of(dims, d, "integrate_sharded");
+        if (n_steps <= 0) throw invalid_argument("integrate: n_steps must be positive");
+        if (!(t_final > t0)) throw invalid_argument("integrate: empty time interval");
+        if (!as || !g || !u) throw invalid_argument("integrate_sharded: null argument");
+        if (mode_d < 0 || mode_d > 2) throw invalid_argument("integrate_sharded: mode_d 0/1/2");
+        StreamScope scope(ctx);
+        ShardExchange X;
+        if (comm) {
+          X.comm = comm;
+          X.P = comm_size(comm);
+          X.ranks = {comm_rank(comm)};
+        } else {
+          if (P_local < 1) throw invalid_argument("integrate_sharded: P must be >= 1");
+          X.P = P_local;
+          for (int r = 0; r < P_local; ++r) X.ranks.push_back(r);
+        }
+        const int S = (g->kind == KP_G_BRUSSELATOR) ? 2 : 1;
+        const int ds = d - (S == 2 ? 1 : 0);
+        if (ds < 2) throw invalid_argument("sharded integrate: needs >= 2 spatial modes");
+        std::vector<int> gd = dl;
+        gd[ds - 1] *= X.P;
+        const double tau = (t_final - t0) / double(n_steps);
+        kp_gfun gg = *g;
+        ShardedIntegrator it(ctx, X, method, cplx, gd, as, gg, tau);
+        std::vector<double*> us(u, u + X.nlocal());
+        it.setup(q, mode_d == 1 ? 1 : 2, us);
+        it.choose_mode_d(mode_d);
+        if (mode_used) *mode_used = it.mode_d;
+        static const bool no_graph = getenv("KP_NO_GRAPH") != nullptr;
+        const double sec = it.run(n_steps, !no_graph);
+        if (loop_seconds) *loop_seconds = it.X.max_over_ranks(ctx, sec, it.scratch);
+        const long k = it.first_bad();
+        if (k) {
+          const double tk = (t0 + double(k - 1) * tau) + tau;
+          throw divergence_error("state became non-finite at step " + std::to_string(k) +
+                                     " (t = " + std::to_string(tk) + ")",
+                                 k);
+        }
+      },
+      diverged_step);
+}
+}  // namespace
+
+extern "C" {
+
+int kp_integrate_sharded_f64(kp_ctx* ctx, kp_comm* comm, int method, double* u_local,
+                             const int* dims_local, int d, const double* const* as,
+                             const kp_gfun* g, double t0, double t_final, long n_steps, int q,
+                             int mode_d, int* mode_used, long* diverged_step,
+                             double* loop_seconds) {
+  if (!comm) {
+    kp_set_last_error("integrate_sharded: null communicator");
+    return KP_EINVAL;
+  }
+  return sharded_impl(ctx, comm, 1, false, method, &u_local, dims_local, d, as, g, t0, t_final,
+                      n_steps, q, mode_d, mode_used, diverged_step, loop_seconds);
+}
+int kp_integrate_sharded_c128(kp_ctx* ctx, kp_comm* comm, int method, double* u_local,
+                              const int* dims_local, int d, const double* const* as,
+                              const kp_gfun* g, double t0, double t_final, long n_steps, int q,
+                              int mode_d, int* mode_used, long* diverged_step,
+                              double* loop_seconds) {
+  if (!comm) {
+    kp_set_last_error("integrate_sharded: null communicator");
+    return KP_EINVAL;
+  }
+  return sharded_impl(ctx, comm, 1, true, method, &u_local, dims_local, d, as, g, t0, t_final,
+                      n_steps, q, mode_d, mode_used, diverged_step, loop_seconds);
+}
+int kp_integrate_sharded_local_f64(kp_ctx* ctx, int P, int method, double* const* u_slabs,
+                                   const int* dims_local, int d, const double* const* as,
+                                   const kp_gfun* g, double t0, double t_final, long n_steps,
+                                   int q, int mode_d, int* mode_used, long* diverged_step,
+                                   double* loop_seconds) {
+  return sharded_impl(ctx, nullptr, P, false, method, u_slabs, dims_local, d, as, g, t0, t_final,
+                      n_steps, q, mode_d, mode_used, diverged_step, loop_seconds);
+}
+int kp_integrate_sharded_local_c128(kp_ctx* ctx, int P, int method, double* const* u_slabs,
+                                    const int* dims_local, int d, const double* const* as,
+                                    const kp_gfun* g, double t0, double t_final, long n_steps,
+                                    int q, int mode_d, int* mode_used, long* diverged_step,
+                                    double* loop_seconds) {
+  return sharded_impl(ctx, nullptr, P, true, method, u_slabs, dims_local, d, as, g, t0, t_final,
+                      n_steps, q, mode_d, mode_used, diverged_step, loop_seconds);
+}
+
 int kp_integrate_sampled_f64(kp_ctx* ctx, int method, double* u, const int* dims, int d,
                              const double* const* as, const kp_gfun* g, double t0,
                              double t_final, long n_steps, int q, int sample_every,

@@ -34,6 +34,15 @@ _CTX, _PG, _PL = C.c_void_p, C.POINTER(GFun), C.POINTER(C.c_long)
 # kp_sample_fn: (user, step, u_host) -- the trajectory hook of kp_integrate_sampled_*
 SAMPLE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_long, C.POINTER(C.c_double))
 for _name, _res, _args in [
+    # the native slab-sharded integrator (stepper.cu; parallel.native_sharded_integrate)
+    ("kp_integrate_sharded_f64", _I, [_CTX, _VP, _I, _VP, _PI, _I, _PPD, _PG, _D, _D, _L, _I,
+                                      _I, _PI, _PL, _PD]),
+    ("kp_integrate_sharded_c128", _I, [_CTX, _VP, _I, _VP, _PI, _I, _PPD, _PG, _D, _D, _L, _I,
+                                       _I, _PI, _PL, _PD]),
+    ("kp_integrate_sharded_local_f64", _I, [_CTX, _I, _I, _VP, _PI, _I, _PPD, _PG, _D, _D, _L,
+                                            _I, _I, _PI, _PL, _PD]),
+    ("kp_integrate_sharded_local_c128", _I, [_CTX, _I, _I, _VP, _PI, _I, _PPD, _PG, _D, _D, _L,
+                                             _I, _I, _PI, _PL, _PD]),
     ("kp_integrate_sampled_f64", _I, [_CTX, _I, _VP, _PI, _I, _PPD, _PG, _D, _D, _L, _I, _I,
                                       SAMPLE_FN, _VP, _PL, _PD]),
     ("kp_integrate_sampled_c128", _I, [_CTX, _I, _VP, _PI, _I, _PPD, _PG, _D, _D, _L, _I, _I,

@@ -770,3 +770,51 @@ def sharded_integrate(kp, backend, comm, method, u_local, dims_local, K, g, t0, 
         rel = getattr(backend, "release_bands", None)
         if rel is not None:
             rel()
+
+
+# ------------------------------------------- the native sharded integrator
+
+MODE_D = {"auto": 0, "alltoall": 1, "reduce_scatter": 2}
+
+
+def native_sharded_integrate(kp, method, u_slabs, dims_local, K, g, t0, t_final, n_steps,
+                             comm=None, mode_d="alltoall", q=12):
+    """The C++ slab-sharded integrator (stepper.cu ShardedIntegrator,
+    kp_integrate_sharded_*).  u_slabs: list of this process's slabs (flat or
+    shaped CUDA tensors, column-major data, updated in place) -- one slab
+    with `comm` (a NcclComm over the job's ranks), or all P slabs with
+    comm=None (the P ranks emulated in this process on one GPU).  K: the full
+    factors (device tensors).  Returns (mode_used, loop_seconds); raises
+    DivergenceError like integrate()."""
+    import ctypes as C
+    from ._lib import check, ints, ptr_array
+    from .integrators import _upload_factors, parse_method
+    cplx = torch.is_complex(u_slabs[0])
+    ctx = kp.default_context(u_slabs[0].device.index or 0)
+    fs = _upload_factors(K)
+    fs = [f.to(torch.complex128 if cplx else torch.float64) for f in fs]
+    m = parse_method(method) if isinstance(method, str) else int(method)
+    used = C.c_int(0)
+    dv = C.c_long(0)
+    loop = C.c_double(0.0)
+    md = MODE_D.get(mode_d, mode_d)
+    torch.cuda.current_stream(u_slabs[0].device).synchronize()
+    if comm is not None:
+        f = ctx.lib.kp_integrate_sharded_c128 if cplx else ctx.lib.kp_integrate_sharded_f64
+        rc = f(ctx.h, comm.h, int(m), u_slabs[0].data_ptr(), ints(dims_local), len(dims_local),
+               ptr_array([x.data_ptr() for x in fs]), C.byref(g), float(t0), float(t_final),
+               int(n_steps), int(q), int(md), C.byref(used), C.byref(dv), C.byref(loop))
+    else:
+        f = ctx.lib.kp_integrate_sharded_local_c128 if cplx else \
+            ctx.lib.kp_integrate_sharded_local_f64
+        arr = (C.c_void_p * len(u_slabs))(*[x.data_ptr() for x in u_slabs])
+        rc = f(ctx.h, len(u_slabs), int(m), C.cast(arr, C.c_void_p), ints(dims_local),
+               len(dims_local), ptr_array([x.data_ptr() for x in fs]), C.byref(g), float(t0),
+               float(t_final), int(n_steps), int(q), int(md), C.byref(used), C.byref(dv),
+               C.byref(loop))
+    try:
+        check(rc, step=dv.value)
+    except Exception as e:
+        e.loop_s = loop.value
+        raise
+    return used.value, loop.value

@@ -1,0 +1,143 @@
+"""The native (C++) slab-sharded integrator, kp_integrate_sharded_* (stepper.cu
+ShardedIntegrator).  On one GPU its P ranks run emulated in
+one process (kp_integrate_sharded_local_*: the exchanges become device copies
+between the ranks' buffers -- the same step sequence and data movement as a
+P-GPU run); the NCCL communicator path runs at world size 1.
+  * mode d by all-to-all pencil transposes: BITWISE equal to the single-GPU
+    integrate (same inputs, same k order per entry);
+  * mode d by partial products + reduce-scatter: rel-l2 <= 1e-12."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import rel2, rng
+
+pytestmark = pytest.mark.gpu
+
+
+def config(name, method):
+    from paper_2304_02327_b200 import problems
+    if name == "ac3d":
+        c = problems.ac3d(n=32, n_steps=12)
+    elif name == "bru":
+        c = problems.brusselator(n=16, n_steps=10, method=method)
+    elif name == "nls":
+        c = problems.nls(n=16, n_steps=8, method=method)
+    elif name == "dense":  # non-banded factors: the dense Kronecker sum path
+        r = rng(17)
+        K = []
+        for n in (12, 10, 8):
+            a = r.uniform(-1, 1, (n, n))
+            a -= np.abs(a).sum(0).max() * np.eye(n)
+            K.append(np.asfortranarray(a))
+        c = problems.ac3d(n=8, n_steps=6)
+        c.u0 = np.asfortranarray(r.uniform(-1, 1, (12, 10, 8)))
+        c.K = K
+    c.method = method
+    return c
+
+
+def slabs_of(u0, P, species):
+    ax = u0.ndim - (2 if species else 1)
+    n = u0.shape[ax] // P
+    return [np.asfortranarray(np.take(u0, range(r * n, (r + 1) * n), axis=ax)) for r in range(P)]
+
+
+def run_native(kp, c, P, mode_d, comm=None):
+    from paper_2304_02327_b200 import parallel
+    species = c.g.kind == kp.G_BRUSSELATOR
+    hs = slabs_of(c.u0, P, species)
+    ds = [kp.to_device(h) for h in hs]
+    used, loop = parallel.native_sharded_integrate(
+        kp, c.method, ds, list(hs[0].shape), [kp.to_device(np.asarray(k)) for k in c.K], c.g,
+        0.0, c.t_final, c.n_steps, comm=comm, mode_d=mode_d)
+    ax = c.u0.ndim - (2 if species else 1)
+    return np.concatenate([kp.to_host(x) for x in ds], axis=ax), used, loop
+
+
+CASES = [("ac3d", "etd2rk"), ("ac3d", "exp_euler"), ("ac3d", "lawson2b"),
+         ("ac3d", "lawson_euler"), ("bru", "etd2rk"), ("bru", "lawson2b"),
+         ("nls", "etd2rk"), ("nls", "exp_euler"), ("dense", "etd2rk")]
+
+
+@pytest.mark.parametrize("name,method", CASES)
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_native_sharded_alltoall_bitwise(kp, name, method, P):
+    c = config(name, method)
+    want = kp.integrate_config(c.method, c.u0, c.K, c.g, 0.0, c.t_final, c.n_steps)
+    got, used, loop = run_native(kp, c, P, "alltoall")
+    assert used == 1 and loop > 0
+    assert np.array_equal(got, want), rel2(got, want)
+
+
+@pytest.mark.parametrize("name,method", [("ac3d", "etd2rk"), ("bru", "etd2rk"),
+                                         ("nls", "etd2rk"), ("ac3d", "lawson2b"),
+                                         ("ac3d", "exp_euler"), ("dense", "etd2rk")])
+@pytest.mark.parametrize("P", [2, 4])
+def test_native_sharded_reduce_scatter(kp, name, method, P):
+    c = config(name, method)
+    want = kp.integrate_config(c.method, c.u0, c.K, c.g, 0.0, c.t_final, c.n_steps)
+    got, used, _ = run_native(kp, c, P, "reduce_scatter")
+    assert used == 2
+    assert rel2(got, want) < 1e-12
+
+
+def test_native_sharded_auto_picks_one(kp):
+    c = config("ac3d", "etd2rk")
+    want = kp.integrate_config(c.method, c.u0, c.K, c.g, 0.0, c.t_final, c.n_steps)
+    got, used, _ = run_native(kp, c, 2, "auto")
+    assert used in (1, 2)
+    assert rel2(got, want) < 1e-12
+
+
+def test_native_sharded_divergence_step(kp):
+    """The 2-D NLS analogue of configs[4] diverges: the sharded
+    run reports the single-GPU run's first non-finite step."""
+    import pyoracle
+    n = 64
+    h = 2.0 / n
+    A = np.asfortranarray(0.5j * pyoracle.periodic_laplacian_1d(n, h))
+    r = rng(11)
+    x = -1.0 + h * np.arange(n)
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    u0 = np.asfortranarray(np.exp(-(X * X + Y * Y) * 8.0) + 0.01 * (r.standard_normal((n, n)) +
+                                                                    1j * r.standard_normal((n, n))))
+    with pytest.raises(kp.DivergenceError) as e1:
+        kp.integrate_config("exp_euler", u0, [A, A], kp.G.nls(), 0.0, 0.2, 200)
+    from paper_2304_02327_b200 import problems
+    c = problems.nls(n=8)
+    c.u0, c.K, c.method, c.t_final, c.n_steps = u0, [A, A], "exp_euler", 0.2, 200
+    with pytest.raises(kp.DivergenceError) as e2:
+        run_native(kp, c, 2, "alltoall")
+    assert e2.value.step == e1.value.step
+
+
+class _OneRankComm:
+    """kp_comm over NCCL at world size 1 (kp_comm_unique_id + kp_comm_create)."""
+
+    def __init__(self, kp):
+        ctx = kp.default_context(0)
+        self.lib = ctx.lib
+        uid = (C.c_char * 128)()
+        assert self.lib.kp_comm_unique_id(uid) == 0
+        h = C.c_void_p()
+        assert self.lib.kp_comm_create(ctx.h, 1, 0, uid, C.byref(h)) == 0, \
+            kp.last_error() if hasattr(kp, "last_error") else ""
+        self.h = h
+
+    def close(self):
+        self.lib.kp_comm_destroy(self.h)
+
+
+@pytest.mark.parametrize("name,method", [("ac3d", "etd2rk"), ("bru", "lawson2b"),
+                                         ("nls", "etd2rk")])
+def test_native_sharded_nccl_world1_bitwise(kp, name, method):
+    c = config(name, method)
+    want = kp.integrate_config(c.method, c.u0, c.K, c.g, 0.0, c.t_final, c.n_steps)
+    comm = _OneRankComm(kp)
+    try:
+        got, used, _ = run_native(kp, c, 1, "auto", comm=comm)
+    finally:
+        comm.close()
+    assert np.array_equal(got, want)
