@@ -27,12 +27,12 @@ def config(name, method):
     elif name == "dense":  # non-banded factors: the dense Kronecker sum path
         r = rng(17)
         K = []
-        for n in (12, 10, 8):
+        for n in (12, 8, 8):
             a = r.uniform(-1, 1, (n, n))
             a -= np.abs(a).sum(0).max() * np.eye(n)
             K.append(np.asfortranarray(a))
         c = problems.ac3d(n=8, n_steps=6)
-        c.u0 = np.asfortranarray(r.uniform(-1, 1, (12, 10, 8)))
+        c.u0 = np.asfortranarray(r.uniform(-1, 1, (12, 8, 8)))
         c.K = K
     c.method = method
     return c
@@ -107,7 +107,7 @@ def test_native_sharded_divergence_step(kp):
         kp.integrate_config("exp_euler", u0, [A, A], kp.G.nls(), 0.0, 0.2, 200)
     from paper_2304_02327_b200 import problems
     c = problems.nls(n=8)
-    c.u0, c.K, c.method, c.t_final, c.n_steps = u0, [A, A], "exp_euler", 0.2, 200
+    c.u0, c.K, c.method, c.t_end, c.n_steps = u0, [A, A], "exp_euler", 0.2, 200
     with pytest.raises(kp.DivergenceError) as e2:
         run_native(kp, c, 2, "alltoall")
     assert e2.value.step == e1.value.step
