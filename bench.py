@@ -54,9 +54,9 @@ def parse():
                     help="skip the integrator-config block (steps/s of configs 0,2,3,4)")
     ap.add_argument("--no-paper", action="store_true",
                     help="skip the paper's ADR wall-clock runs")
-    ap.add_argument("--exchange", choices=["peer", "nccl", "kpnccl"], default="peer",
-                    help="N>1 sharded integrators: fused peer stores, torch NCCL all-to-all, "
-                         "or the C ABI's own NCCL communicator (kp_comm_*)")
+    ap.add_argument("--exchange", choices=["native", "python"], default="native",
+                    help="N>1 sharded integrators: the native C++ sharded integrator "
+                         "(kp_integrate_sharded_*) or the round-1 Python one (parallel.py)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the sharded integrator block even at N=1 (testing)")
     return ap.parse_args()
@@ -256,31 +256,16 @@ def run_paper_experiments(kp):
     return out
 
 
-def run_sharded_integrators(kp, peak, world, rank, local, exchange="peer"):
-    """N > 1: configs 3 and 4 slab-sharded along mode 3 (paper_2304_02327_b200/
-    parallel.py).  exchange "peer": the re-partitions are peer stores from the
-    GEMM epilogues / scatter kernels into CUDA-IPC-mapped buffers over NVLink
-    (PeerComm); "nccl": all-to-all collectives (Comm).  Loop time = max over
-    ranks (CUDA events on each rank's stream)."""
+def run_sharded_integrators(kp, peak, world, rank, local, comm, exchange="native"):
+    """N > 1: configs 3 and 4 slab-sharded along mode 3 by the native sharded
+    integrator (stepper.cu ShardedIntegrator through kp_integrate_sharded_*:
+    stream-ordered NCCL exchanges, the step a replayed CUDA graph, mode d by
+    all-to-all or by partial products + reduce-scatter, picked by measuring
+    one step of each).  exchange "python": the round-1 Python ShardedIntegrator
+    (parallel.py) with the fused peer stores.  Loop time = max over ranks."""
     import torch
-    import torch.distributed as dist
     from paper_2304_02327_b200 import parallel, problems
     from paper_2304_02327_b200.integrators import _upload_factors
-    be = parallel.CudaBackend(local)
-    comm = parallel.NcclComm(be) if exchange == "kpnccl" else parallel.Comm()
-    if exchange == "peer":  # probe the IPC mappings on every rank first
-        ok = 1.0
-        try:
-            pc = parallel.PeerComm(be)
-            pc._slot("probe", 4096)
-        except Exception:
-            ok = 0.0
-        t = torch.tensor([ok], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        if float(t.item()) == 1.0:
-            comm = pc
-        else:
-            exchange = "nccl (peer mappings unavailable)"
     out = {}
     for tag, builder, kw in INTEGRATOR_CONFIGS:
         if builder not in ("brusselator", "nls"):
@@ -289,29 +274,50 @@ def run_sharded_integrators(kp, peak, world, rank, local, exchange="peer"):
         nl = n_full // world
         c = getattr(problems, builder)(planes=(rank * nl, (rank + 1) * nl), **kw)
         ud = kp.to_device(c.u0)
-        flat = ud.permute(*reversed(range(ud.ndim))).reshape(-1)
         K = _upload_factors(c.K)
         note = None
         try:
-            it = parallel.make_sharded_integrator(kp, be, comm, c.method, list(c.u0.shape), K,
-                                                  c.g, 0.0, c.t_final, c.n_steps)
-            try:  # warm-up (untimed)
-                it.run(flat.clone(), 2)
-            except kp.DivergenceError:
-                pass
-            dist.barrier()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            try:
-                it.run(flat, c.n_steps)
-            except kp.DivergenceError as e:
-                note = f"diverged at step {e.step} (as on one GPU; DESIGN.md 9)"
-            e1.record()
-            torch.cuda.synchronize()
-            t = torch.tensor([e0.elapsed_time(e1) * 1e-3], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            loop = float(t.item())
+            if exchange == "python":
+                be = parallel.CudaBackend(local)
+                flat = ud.permute(*reversed(range(ud.ndim))).reshape(-1)
+                it = parallel.make_sharded_integrator(kp, be, parallel.Comm(), c.method,
+                                                      list(c.u0.shape), K, c.g, 0.0, c.t_final,
+                                                      c.n_steps)
+                try:
+                    it.run(flat.clone(), 2)
+                except kp.DivergenceError:
+                    pass
+                import torch.distributed as dist
+                dist.barrier()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                try:
+                    it.run(flat, c.n_steps)
+                except kp.DivergenceError as e:
+                    note = f"diverged at step {e.step} (as on one GPU; DESIGN.md 9)"
+                e1.record()
+                torch.cuda.synchronize()
+                t = torch.tensor([e0.elapsed_time(e1) * 1e-3], device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                loop, used = float(t.item()), "python peer/nccl"
+            else:
+                warm = ud.clone()
+                try:  # warm-up: 2 steps (graph instantiation, workspace, NCCL channels)
+                    parallel.native_sharded_integrate(kp, c.method, [warm], list(c.u0.shape), K,
+                                                      c.g, 0.0, 2 * c.tau, 2, comm=comm,
+                                                      mode_d="auto")
+                except kp.DivergenceError:
+                    pass
+                try:
+                    used, loop = parallel.native_sharded_integrate(
+                        kp, c.method, [ud], list(c.u0.shape), K, c.g, 0.0, c.t_final,
+                        c.n_steps, comm=comm, mode_d="auto")
+                except kp.DivergenceError as e:
+                    loop, used = e.loop_s, "auto"
+                    note = f"diverged at step {e.step} (as on one GPU; DESIGN.md 9)"
+                used = {1: "all-to-all pencil transpose", 2: "partial products + reduce-scatter"}.get(
+                    used, used)
         except Exception as ex:  # reported, never fatal for the headline
             out[tag + "_sharded"] = {"error": str(ex)[:300]}
             continue
@@ -320,21 +326,17 @@ def run_sharded_integrators(kp, peak, world, rank, local, exchange="peer"):
         species = 2 if builder == "brusselator" else 1
         per_tucker = species * (8.0 if cplx else 2.0) * float(np.prod(spatial)) * sum(spatial)
         fl = tucker_equivalents(c.method) * per_tucker
-        # the banded Kronecker sum (a stencil, not a Tucker) is not dense work:
-        # the roofline fraction counts the GEMMs actually executed
         fl_run = dense_tuckers_executed(c.method) * per_tucker
         sps = c.n_steps / loop
         out[tag + "_sharded"] = {"method": c.method, "global_dims": spatial + (
             [2] if species == 2 else []), "ranks": world, "steps": c.n_steps,
-            "exchange": exchange,
+            "exchange": exchange, "mode_d": used,
             "steps_per_s": sps, "loop_ms": loop * 1e3,
             "tflops_tucker_equivalent": fl * sps / 1e12,
             "tflops_dense_executed": fl_run * sps / 1e12,
             "frac_of_fp64_peak_per_gpu": fl_run * sps / 1e12 / (peak * world), "note": note}
-        del ud, flat, K
+        del ud, K
         torch.cuda.empty_cache()
-    if isinstance(comm, (parallel.PeerComm, parallel.NcclComm)):
-        comm.close()
     return out
 
 
@@ -503,6 +505,123 @@ def emit(line):
     os.write(fd, (json.dumps(line) + "\n").encode())
 
 
+def main_sharded(args, rank, world, local, dist, kp, ctx, stream):
+    """N > 1 (or --force-sharded): the headline workload is the SAME n = 512
+    Tucker operator, slab-sharded along mode 3 across the N GPUs (strong
+    scaling): modes 1, 2 on the slab, mode 3 across the slabs by the exchange
+    the run measures faster -- all-to-all pencil transpose (NCCL grouped
+    send/recv) or partial products + ncclReduceScatter
+    (kp_tucker_sharded_f64).  value = 412.3 GFLOP / (device time, max over
+    ranks)."""
+    import torch
+    from paper_2304_02327_b200 import parallel
+    from paper_2304_02327_b200._lib import check, ints, ptr_array
+    n, P = args.n, world
+    if n % P:
+        raise SystemExit(f"n={n} not divisible by {P} GPUs")
+    be = parallel.CudaBackend(local)
+    comm = parallel.NcclComm(be)  # kp_comm over all ranks (id shared via torch.distributed)
+    v_h, a_h = make_inputs(n)
+    nl = n // P
+    slab_h = np.asfortranarray(v_h[:, :, rank * nl:(rank + 1) * nl])
+    del v_h
+    a_d = kp.to_device(a_h)
+    fs_d = kp.build_split_phi([a_d, a_d, a_d], 1e-3, 1).factors
+    slab_d = kp.to_device(slab_h)
+    out_d = torch.empty_like(slab_d)
+    dims_l = [n, n, nl]
+    lib = ctx.lib
+    mptr = ptr_array([f.data_ptr() for f in fs_d])
+
+    def step(md):
+        check(lib.kp_tucker_sharded_f64(ctx.h, comm.h, slab_d.data_ptr(), ints(dims_l), 3, mptr,
+                                        1.0, md, out_d.data_ptr()))
+
+    def max_ranks(x):
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    peak = ctx.fp64_peak_tflops()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed(md, k, pre=None, post=None):
+        for _ in range(args.warmup):
+            if pre:
+                pre()
+            step(md)
+            if post:
+                post()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record(stream)
+        for _ in range(k):
+            if pre:
+                pre()
+            step(md)
+            if post:
+                post()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return max_ranks(e0.elapsed_time(e1) / k)
+
+    l0 = ctx.launches
+    with ClockSampler(local) as clk:
+        ms_a = timed(1, args.steps)
+        ms_b = timed(2, args.steps)
+    md_best = 1 if ms_a <= ms_b else 2
+    l0 = ctx.launches
+    step(md_best)
+    torch.cuda.synchronize()
+    launches = (ctx.launches - l0) * args.steps
+    ms = min(ms_a, ms_b)
+    fl = flops_per_tucker(n)
+    value = fl / (ms * 1e-3) / 1e9
+    achieved = fl / P / (ms * 1e-3) / 1e12  # per GPU
+
+    e2e = None
+    if not args.no_e2e:  # pinned host slab in, result out, every step
+        pin_in = torch.empty(slab_d.numel(), dtype=torch.float64, pin_memory=True)
+        pin_out = torch.empty(slab_d.numel(), dtype=torch.float64, pin_memory=True)
+        pin_in.copy_(torch.from_numpy(slab_h.reshape(-1, order="F")))
+        flat_in = slab_d.permute(2, 1, 0).reshape(-1)
+        flat_out = out_d.permute(2, 1, 0).reshape(-1)
+        sec = timed(md_best, max(4, args.steps),
+                    pre=lambda: flat_in.copy_(pin_in, non_blocking=True),
+                    post=lambda: pin_out.copy_(flat_out, non_blocking=True)) * 1e-3
+        e2e = {"value": fl / sec / 1e9, "unit": "GFLOP/s", "ms_per_step": sec * 1e3,
+               "h2d_bytes_per_step": int(slab_h.nbytes) * P,
+               "d2h_bytes_per_step": int(slab_h.nbytes) * P,
+               "api": "kp_tucker_sharded_f64 per step with the rank's slab copied in from "
+                      "pinned host memory and its result copied out (all ranks)"}
+
+    integ = None
+    if not args.no_integrators:
+        del slab_d, out_d
+        torch.cuda.empty_cache()
+        integ = run_sharded_integrators(kp, peak, world, rank, local, comm,
+                                        "python" if args.exchange == "python" else "native")
+    comm.close()
+    if rank == 0:
+        line = {"metric": f"FP64 Tucker-op GFLOP/s (d=3, n={n})", "value": value,
+                "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": dict(config(n, world), parallelism=f"slab{P} (mode 3 sharded)",
+                               workload=f"tucker_d3_n{n}_sharded"),
+                "sharded": {"mode_d_alltoall_ms": ms_a, "mode_d_reduce_scatter_ms": ms_b,
+                            "chosen": "all-to-all pencil transpose" if md_best == 1 else
+                            "partial products + reduce-scatter",
+                            "output_layout": "pencil" if md_best == 1 else "slab"},
+                "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
+                             "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                             "peak_source": "live DMMA m8n8k4 micro-benchmark on this GPU",
+                             "algorithmic": "2*N*sum(n_mu) / P per GPU"},
+                "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary(), "integrators": integ}
+        emit(line)
+
+
 def main():
     _claim_stdout()
     _omp_env()
@@ -528,6 +647,10 @@ def main():
     ctx = kp.default_context(local)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
+    if dist:
+        main_sharded(args, rank, world, local, dist, kp, ctx, stream)
+        dist.destroy_process_group()
+        return
 
     n = args.n
     v_h, a_h = make_inputs(n)
@@ -639,8 +762,7 @@ def main():
     if not args.no_integrators:
         del v_d, out_d
         torch.cuda.empty_cache()
-        integ = run_integrators(kp, peak) if (world == 1 and not args.force_sharded) else \
-            run_sharded_integrators(kp, peak, world, rank, local, args.exchange)
+        integ = run_integrators(kp, peak)
 
     paper = None
     if world == 1 and not args.no_paper:

@@ -420,6 +420,18 @@ int kp_integrate_sharded_local_c128(kp_ctx* ctx, int P, int method, double* cons
                                     const kp_gfun* g, double t0, double t_final, long n_steps,
                                     int q, int mode_d, int* mode_used, long* diverged_step,
                                     double* loop_seconds);
+/* The mode-d-sharded Tucker operator (real): V x_1 M_1 ... x_d M_d with V
+ * slab-sharded along mode d (t_slab: this rank's n_1 x .. x n_d/P slab;
+ * square, full factors).  Modes 1..d-1 on the slab; mode d across the slabs:
+ * mode_d 1 = all-to-all, result in the PENCIL layout (n_1 .. n_(d-1)/P x n_d,
+ * bitwise the rank's block of the single-GPU result); 2 = partial products +
+ * reduce-scatter, result in the SLAB layout. */
+int kp_tucker_sharded_f64(kp_ctx* ctx, kp_comm* comm, const double* t_slab,
+                          const int* dims_local, int d, const double* const* ms,
+                          double prefactor, int mode_d, double* out);
+int kp_tucker_sharded_local_f64(kp_ctx* ctx, int P, const double* const* t_slabs,
+                                const int* dims_local, int d, const double* const* ms,
+                                double prefactor, int mode_d, double* const* outs);
 /* Host-buffer drop-in: u0/as on the host, u_final written on the host. */
 int kp_host_integrate_f64(kp_ctx* ctx, int method, const double* u0, const int* dims, int d,
                           const double* const* as, const kp_gfun* g, double t0, double t_final,

@@ -915,21 +915,17 @@ class ShardExchange {
 
   int nlocal() const { return int(ranks.size()); }
 
+  // send/recv scratch of local rank i: grow-only workspace slots 80+i / 96+i
+  // (no cudaMalloc / cudaFree per call)
+  kp_ctx* wctx = nullptr;
   void scratch(long long doubles) {
-    if (doubles <= cap) return;
-    for (double* p : send) cudaFree(p);
-    for (double* p : recv) cudaFree(p);
-    send.assign(ranks.size(), nullptr);
-    recv.assign(ranks.size(), nullptr);
+    send.resize(ranks.size());
+    recv.resize(ranks.size());
     for (size_t i = 0; i < ranks.size(); ++i) {
-      KP_CUDA(cudaMalloc(&send[i], size_t(doubles) * sizeof(double)));
-      KP_CUDA(cudaMalloc(&recv[i], size_t(doubles) * sizeof(double)));
+      if (i >= 16) throw invalid_argument("sharded: at most 16 emulated ranks");
+      send[i] = static_cast<double*>(wctx->ws.get(80 + int(i), size_t(doubles) * 8));
+      recv[i] = static_cast<double*>(wctx->ws.get(96 + int(i), size_t(doubles) * 8));
     }
-    cap = doubles;
-  }
-  ~ShardExchange() {
-    for (double* p : send) cudaFree(p);
-    for (double* p : recv) cudaFree(p);
   }
 
   // y[i] = x[i] re-partitioned (dir 1: slab -> pencil, 2: back)
@@ -942,6 +938,7 @@ class ShardExchange {
                                 ctx->stream));
       return;
     }
+    wctx = ctx;
     scratch(n);
     if (comm) {
       comm_repartition(ctx, comm, dir, A, B, C, S, comps, x[0], y[0], send[0], recv[0]);
@@ -1161,9 +1158,13 @@ class ShardedIntegrator {
                 const std::vector<double*>& out, L&& last) {
     std::vector<const double*> mid;
     for (size_t i = 0; i < R.size(); ++i) mid.push_back(tucker_slab(fs, in[i], R[i]));
-    std::vector<double*> pen;
-    for (auto& k : R) pen.push_back(mid[&k - R.data()] == k.t0 ? k.t1 : k.t0);
-    to_pencil(mid, pen);
+    std::vector<const double*> pen = mid;  // P = 1: the pencil is the slab
+    if (P > 1) {
+      std::vector<double*> pb;
+      for (size_t i = 0; i < R.size(); ++i) pb.push_back(mid[i] == R[i].t0 ? R[i].t1 : R[i].t0);
+      to_pencil(mid, pb);
+      pen.assign(pb.begin(), pb.end());
+    }
     for (size_t i = 0; i < R.size(); ++i) {
       Epilogue e = last(R[i]);
       e.alpha = fs.fold * (ds == 1 ? fs.pref : 1.0);
@@ -1192,6 +1193,13 @@ class ShardedIntegrator {
 
   // r = K u + g(u) in slab layout (u: slab)
   void kronsum_g(const std::vector<const double*>& u, const std::vector<double*>& r, double t) {
+    if (G.banded && P == 1) {  // one rank: the plain stencil on u, no halo planes
+      each([&](Rank& k) {
+        kronsum_banded(ctx, cplx, u[&k - R.data()], dl, G.band_cols, G.band_vals, G.a_active,
+                       r[&k - R.data()], true, G.g, S == 2 ? 1 : 0, -1, 0, 0, 0, t);
+      });
+      return;
+    }
     if (G.banded) {
       const long long plane = A * B * comps;
       // interior planes of every species into ext, then the halo planes
@@ -1286,7 +1294,12 @@ class ShardedIntegrator {
       case KP_ETD2RK: {
         // u on the pencil: the fused last-mode epilogues read it (A), the
         // dense Kronecker sum's last term needs it (both)
-        if (!B_ || !G.banded) to_pencil(u, mv(&Rank::up));
+        if (!B_ || !G.banded) {
+          if (P == 1)
+            each([&](Rank& k) { k.up = const_cast<double*>(u[&k - R.data()]); });
+          else
+            to_pencil(u, mv(&Rank::up));
+        }
         kronsum_g(u, mv(&Rank::rr), t);
         if (B_) {
           tucker_B(G.f1, cv(&Rank::rr), mv(&Rank::y));
@@ -1314,14 +1327,14 @@ class ShardedIntegrator {
           return;
         }
         if (method == KP_EXP_EULER) {
-          tucker_A(G.f1, cv(&Rank::rr), mv(&Rank::out), [&](Rank& k) {
+          tucker_A(G.f1, cv(&Rank::rr), outs(o), [&](Rank& k) {
             Epilogue f = fin_of(k);
             f.kind = EPI_FMA_X;
             f.X = k.up;
             f.gamma = tau;
             return f;
           });
-          to_slab(cv(&Rank::out), o);
+          back(o);
           return;
         }
         const bool paired = S == 2;  // the coupled g: its own pass (as on one GPU)
@@ -1341,15 +1354,15 @@ class ShardedIntegrator {
           return e;
         });
         if (paired) each([&](Rank& k) { gdiff(k.sp, k.up, k.dq, t); });
-        to_slab(cv(&Rank::dq), mv(&Rank::dd));
-        tucker_A(G.f2, cv(&Rank::dd), mv(&Rank::out), [&](Rank& k) {
+        if (P > 1) to_slab(cv(&Rank::dq), mv(&Rank::dd));
+        tucker_A(G.f2, P > 1 ? cv(&Rank::dd) : cv(&Rank::dq), outs(o), [&](Rank& k) {
           Epilogue f = fin_of(k);
           f.kind = EPI_FMA_X;
           f.X = k.sp;
           f.gamma = tau;
           return f;
         });
-        to_slab(cv(&Rank::out), o);
+        back(o);
         return;
       }
       case KP_LAWSON_EULER:
@@ -1366,8 +1379,8 @@ class ShardedIntegrator {
             });
             return;
           }
-          tucker_A(G.f1, cv(&Rank::w), mv(&Rank::out), [&](Rank& k) { return fin_of(k); });
-          to_slab(cv(&Rank::out), o);
+          tucker_A(G.f1, cv(&Rank::w), outs(o), [&](Rank& k) { return fin_of(k); });
+          back(o);
           return;
         }
         // [stage; y1] in one buffer (the post kernel's layout)
@@ -1383,15 +1396,26 @@ class ShardedIntegrator {
         tucker_A(G.f1, cv(&Rank::w), mv(&Rank::sp), [&](Rank&) { return Epilogue{}; });
         tucker_A(G.f1, cv(&Rank::w, nloc * comps), mv(&Rank::sp, nloc * comps),
                  [&](Rank&) { return Epilogue{}; });
-        each([&](Rank& k) {
-          post(k.sp, k.out, k.cnt + 1, k.cnt + (slot ? 2 : 0), t + tau, k.cnt + (slot ? 0 : 2));
-        });
-        to_slab(cv(&Rank::out), o);
+        {
+          const auto ov = outs(o);
+          each([&](Rank& k) {
+            post(k.sp, ov[&k - R.data()], k.cnt + 1, k.cnt + (slot ? 2 : 0), t + tau,
+                 k.cnt + (slot ? 0 : 2));
+          });
+        }
+        back(o);
         return;
       }
       default:
         throw invalid_argument("sharded integrate: unsupported method");
     }
+  }
+  // where the last (pencil) result of a step goes: straight into o at P = 1
+  std::vector<double*> outs(const std::vector<double*>& o) {
+    return P == 1 ? o : mv(&Rank::out);
+  }
+  void back(const std::vector<double*>& o) {
+    if (P > 1) to_slab(cv(&Rank::out), o);
   }
   void tick(Rank& k, int slot) {
     launch_pdl(ctx, tick_kernel, dim3(1), dim3(1), 0, (const int*)(k.cnt + (slot ? 2 : 0)),
@@ -1939,6 +1963,100 @@ int kp_integrate_sharded_local_c128(kp_ctx* ctx, int P, int method, double* cons
                                     double* loop_seconds) {
   return sharded_impl(ctx, nullptr, P, true, method, u_slabs, dims_local, d, as, g, t0, t_final,
                       n_steps, q, mode_d, mode_used, diverged_step, loop_seconds);
+}
+
+}  // extern "C"
+
+namespace {
+// mode-d-sharded Tucker operator (the headline op of bench.py at N > 1)
+int tucker_sharded_impl(kp_ctx* ctx, kp_comm* comm, int P_local, const double* const* t,
+                        const int* dims, int d, const double* const* ms, double pref, int mode_d,
+                        double* const* out) {
+  return guard_c([&] {
+    ctx_ok(ctx);
+    auto dl = dims_of(dims, d, "tucker_sharded");
+    if (d < 2) throw invalid_argument("tucker_sharded: needs order >= 2");
+    if (!t || !ms || !out) throw invalid_argument("tucker_sharded: null argument");
+    if (mode_d != 1 && mode_d != 2) throw invalid_argument("tucker_sharded: mode_d 1 or 2");
+    ShardExchange X;
+    X.wctx = ctx;
+    if (comm) {
+      X.comm = comm;
+      X.P = comm_size(comm);
+      X.ranks = {comm_rank(comm)};
+    } else {
+      if (P_local < 1 || P_local > 16) throw invalid_argument("tucker_sharded: P in 1..16");
+      X.P = P_local;
+      for (int r = 0; r < P_local; ++r) X.ranks.push_back(r);
+    }
+    const int P = X.P;
+    long long A = 1;
+    for (int mu = 0; mu < d - 2; ++mu) A *= dl[mu];
+    const long long B = dl[d - 2], Cl = dl[d - 1], C = Cl * P;
+    if (B % P) throw invalid_argument("tucker_sharded: n_(d-1) must be divisible by P");
+    const long long n = A * B * Cl;
+    std::vector<int> dp = dl;
+    dp[d - 2] = int(B / P);
+    dp[d - 1] = int(C);
+    std::vector<const double*> mid;
+    for (int i = 0; i < X.nlocal(); ++i) {
+      const double* cur = t[i];
+      for (int mu = 0; mu < d - 1; ++mu) {
+        double* dst = static_cast<double*>(ctx->ws.get(112 + 2 * i + (mu & 1), size_t(n) * 8));
+        Epilogue e;
+        e.alpha = (mu == 0) ? pref : 1.0;
+        mode_product_f64(ctx, cur, dl, mu, ms[mu], dl[mu], e, dst);
+        cur = dst;
+      }
+      mid.push_back(cur);
+    }
+    if (mode_d == 1) {
+      std::vector<const double*> pen = mid;
+      if (P > 1) {
+        std::vector<double*> pb;
+        for (int i = 0; i < X.nlocal(); ++i)
+          pb.push_back(static_cast<double*>(ctx->ws.get(144 + i, size_t(n) * 8)));
+        X.repartition(ctx, 1, A, B, C, 1, 1, mid, pb);
+        pen.assign(pb.begin(), pb.end());
+      }
+      for (int i = 0; i < X.nlocal(); ++i) {
+        Epilogue e;
+        mode_product_f64(ctx, pen[i], P > 1 ? dp : dl, d - 1, ms[d - 1], int(C), e, out[i]);
+      }
+      return;
+    }
+    std::vector<int> fd = dl;
+    fd[d - 1] = int(C);
+    std::vector<double*> parts;
+    for (int i = 0; i < X.nlocal(); ++i) {
+      double* part = static_cast<double*>(ctx->ws.get(160 + i, size_t(n) * P * 8));
+      Epilogue e;
+      mode_product_f64(ctx, mid[i], dl, d - 1, ms[d - 1] + (long long)X.ranks[i] * Cl * C,
+                       int(C), e, part);
+      parts.push_back(part);
+    }
+    std::vector<double*> ov(out, out + X.nlocal());
+    X.reduce_scatter(ctx, A * B, C, 1, parts, ov);
+  });
+}
+}  // namespace
+
+extern "C" {
+
+int kp_tucker_sharded_f64(kp_ctx* ctx, kp_comm* comm, const double* t_slab,
+                          const int* dims_local, int d, const double* const* ms,
+                          double prefactor, int mode_d, double* out) {
+  if (!comm) {
+    kp_set_last_error("tucker_sharded: null communicator");
+    return KP_EINVAL;
+  }
+  return tucker_sharded_impl(ctx, comm, 1, &t_slab, dims_local, d, ms, prefactor, mode_d, &out);
+}
+int kp_tucker_sharded_local_f64(kp_ctx* ctx, int P, const double* const* t_slabs,
+                                const int* dims_local, int d, const double* const* ms,
+                                double prefactor, int mode_d, double* const* outs) {
+  return tucker_sharded_impl(ctx, nullptr, P, t_slabs, dims_local, d, ms, prefactor, mode_d,
+                             outs);
 }
 
 int kp_integrate_sampled_f64(kp_ctx* ctx, int method, double* u, const int* dims, int d,

@@ -43,6 +43,8 @@ for _name, _res, _args in [
                                             _I, _I, _PI, _PL, _PD]),
     ("kp_integrate_sharded_local_c128", _I, [_CTX, _I, _I, _VP, _PI, _I, _PPD, _PG, _D, _D, _L,
                                              _I, _I, _PI, _PL, _PD]),
+    ("kp_tucker_sharded_f64", _I, [_CTX, _VP, _VP, _PI, _I, _PPD, _D, _I, _VP]),
+    ("kp_tucker_sharded_local_f64", _I, [_CTX, _I, _VP, _PI, _I, _PPD, _D, _I, _VP]),
     ("kp_integrate_sampled_f64", _I, [_CTX, _I, _VP, _PI, _I, _PPD, _PG, _D, _D, _L, _I, _I,
                                       SAMPLE_FN, _VP, _PL, _PD]),
     ("kp_integrate_sampled_c128", _I, [_CTX, _I, _VP, _PI, _I, _PPD, _PG, _D, _D, _L, _I, _I,

@@ -141,3 +141,38 @@ def test_native_sharded_nccl_world1_bitwise(kp, name, method):
     finally:
         comm.close()
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+@pytest.mark.parametrize("mode_d", [1, 2])
+def test_tucker_sharded_local(kp, P, mode_d):
+    """kp_tucker_sharded_local_f64: mode 1 (all-to-all) gives each rank its
+    pencil block of the single-GPU Tucker bitwise; mode 2 (reduce-scatter)
+    its slab block within 1e-12."""
+    import torch
+    from paper_2304_02327_b200._lib import check, ints, ptr_array
+    r = rng(99)
+    n1, n2, n3 = 24, 16, 32
+    v = np.asfortranarray(r.standard_normal((n1, n2, n3)))
+    ms = [np.asfortranarray(r.standard_normal((n, n)) / n) for n in (n1, n2, n3)]
+    want = kp.tucker(v, ms)
+    ctx = kp.default_context(0)
+    slabs = [kp.to_device(np.asfortranarray(v[:, :, k * n3 // P:(k + 1) * n3 // P]))
+             for k in range(P)]
+    outs = [kp.to_device(np.zeros_like(kp.to_host(s))) for s in slabs]
+    md = [kp.to_device(m) for m in ms]
+    arr = (C.c_void_p * P)(*[s.data_ptr() for s in slabs])
+    oarr = (C.c_void_p * P)(*[o.data_ptr() for o in outs])
+    check(ctx.lib.kp_tucker_sharded_local_f64(ctx.h, P, C.cast(arr, C.c_void_p),
+                                              ints([n1, n2, n3 // P]), 3,
+                                              ptr_array([m.data_ptr() for m in md]), 1.0,
+                                              mode_d, C.cast(oarr, C.c_void_p)))
+    torch.cuda.synchronize()
+    for k, o in enumerate(outs):
+        flat = kp.to_host(o).reshape(-1, order="F")
+        if mode_d == 1:  # pencil: (n1, n2/P, n3)
+            blk = np.asfortranarray(want[:, k * n2 // P:(k + 1) * n2 // P, :])
+            assert np.array_equal(flat, blk.reshape(-1, order="F"))
+        else:            # slab: (n1, n2, n3/P)
+            blk = np.asfortranarray(want[:, :, k * n3 // P:(k + 1) * n3 // P])
+            assert rel2(flat, blk.reshape(-1, order="F")) < 1e-12
