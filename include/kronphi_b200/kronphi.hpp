@@ -1514,4 +1514,55 @@ class Communicator {
   int P_ = 1, rank_ = 0;
 };
 
+// How the last mode crosses the slabs in a sharded integrate (kp_integrate_sharded_*).
+enum class ModeD { Measure = 0, AllToAll = 1, ReduceScatter = 2 };
+
+// integrate() slab-sharded over `comm`'s ranks: p.u0 is this
+// rank's slab (the last spatial mode holds n_d / P planes, a stacked
+// Brusselator keeps its species mode last), p.K the FULL factors; returns
+// this rank's slab of the final state.  Mode d by all-to-all (bitwise equal
+// to the single-GPU integrate), by partial products + reduce-scatter, or by
+// whichever one step of each measures faster.  loop_s is the device time of
+// the loop, max over ranks.  Methods LawsonEuler, Lawson2b, ExpEuler, ETD2RK
+// with a pointwise device g.
+template <typename T>
+IntegrateResultT<T> integrate(const ProblemSpecT<T>& p, const StepperConfig& c,
+                              Communicator& comm, ModeD mode_d = ModeD::Measure,
+                              ModeD* used = nullptr) {
+  using namespace detail;
+  if (c.n_steps <= 0) throw std::invalid_argument("integrate: n_steps must be positive");
+  if (!(p.t_final > p.t0)) throw std::invalid_argument("integrate: empty time interval");
+  if (p.g.is_host()) throw std::invalid_argument("sharded integrate: needs a device g");
+  if (c.sample_every != 0 || c.backend != Backend::Split)
+    throw std::invalid_argument("sharded integrate: Split backend, no trajectory sampling");
+  if (p.K.order() != p.u0.order())
+    throw std::invalid_argument("kronsum_action: expected one factor per mode");
+  const auto w0 = std::chrono::steady_clock::now();
+  DevBuf du(p.u0.data(), bytes_of<T>(p.u0.size()));
+  std::vector<DevBuf> kf;
+  std::vector<const double*> kd;
+  for (const auto& f : p.K.factors) {
+    kf.emplace_back(f.data(), bytes_of<T>(f.size()));
+    kd.push_back(kf.back().d());
+  }
+  long dv = 0;
+  double loop = 0.0;
+  int md = 0;
+  auto f = std::is_same_v<T, double> ? kp_integrate_sharded_f64 : kp_integrate_sharded_c128;
+  const int rc = f(ctx(), comm.handle(), int(c.method), du.d(), p.u0.dims().data(),
+                   p.u0.order(), kd.data(), &p.g.device(), p.t0, p.t_final, c.n_steps,
+                   c.quad_nodes, int(mode_d), &md, &dv, &loop);
+  const double tau = (p.t_final - p.t0) / double(c.n_steps);
+  if (rc == KP_EDIVERGE) throw DivergenceError(dv, (p.t0 + double(dv - 1) * tau) + tau);
+  check(rc);
+  if (used) *used = ModeD(md);
+  IntegrateResultT<T> r;
+  r.final = Tensor<T>::no_init(p.u0.dims());
+  du.download(r.final.data());
+  r.loop_s = loop;
+  r.wallclock_s =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+  return r;
+}
+
 }  // namespace kronphi

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "kronphi/integrators.hpp"
+#include "kronphi/problems.hpp"
 #include "mini_doctest.h"
 
 using namespace kronphi;
@@ -275,6 +276,24 @@ TEST_CASE("problem spec carries the exact solution") {
   ProblemSpec p = small_problem();
   p.exact = [](double t) { return Tensor<double>({1}, {std::exp(t)}); };
   CHECK(p.exact(0.0)[0] == 1.0);
+}
+
+TEST_CASE("sharded integrate through a Communicator (world size 1) equals integrate") {
+  ProblemSpec p;
+  p.K = KroneckerSum<double>({fd_operator_1d(16, 0.01, 0.0), fd_operator_1d(12, 0.01, 0.0),
+                              fd_operator_1d(8, 0.01, 0.0)});
+  p.g = g_allen_cahn();
+  p.u0 = random_tensor({16, 12, 8});
+  p.t_final = 0.02;
+  StepperConfig c;
+  c.method = Method::ETD2RK;
+  c.n_steps = 10;
+  const auto single = integrate(p, c);
+  Communicator comm(1, 0, Communicator::unique_id());
+  ModeD used = ModeD::Measure;
+  const auto sh = integrate(p, c, comm, ModeD::Measure, &used);
+  CHECK(used == ModeD::AllToAll);  // one rank: the identity exchange
+  CHECK(diff_norm_inf(sh.final, single.final) == 0.0);
 }
 
 int main() { return mini_doctest::run_all(); }
