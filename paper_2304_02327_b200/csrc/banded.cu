@@ -18,6 +18,9 @@
 // Band detection (once per factor): a device scan collects, per row, up to
 // three (column, value) pairs in increasing column order; more nonzeros =>
 // not banded (dense path).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <string>
@@ -447,6 +450,260 @@ __global__ void __launch_bounds__(256, (CPLX || PAIR) ? 3 : 4)
   }
 }
 
+
+// ---- v3: TMA plane ring (d = 3 + optional species; the configs' shapes) ----
+// A block owns a 32 x 8 tile of (i0, i1) lines and marches a chunk of planes
+// z.  The (32+2) x (8+2) input tile of every plane it needs (the +-1 halo in
+// i0 and i1 included, zero-filled outside the tensor) arrives by TMA
+// (cp.async.bulk.tensor) into a ring of D3 plane slots, each with its own
+// mbarrier: D3 - 3 planes stay in flight ahead of the one being computed, so
+// the march is no longer one dependent HBM round trip per plane.  Each
+// entry's neighbours are read from shared memory (row deltas of -1 / 0 / +1;
+// a periodic wrap-around column falls back to a global load), then the same
+// row_combine as v2 -- bit-identical results.
+constexpr int D3 = 8, TX = 32, TY = 8, PX = TX + 2, PY = TY + 2;
+
+template <bool CPLX>
+struct BandRow3 : BandRow<CPLX> {
+  int dl[3];  // column - row (mode units); |dl| > 1: a wrap-around, read from global
+};
+
+template <bool CPLX>
+__device__ __forceinline__ void load_row3(const BandArgs& b, int mu, int i, BandRow3<CPLX>& rw) {
+  load_row(b, mu, i, static_cast<BandRow<CPLX>&>(rw));
+  const int ig = (mu == b.slab) ? i + b.k0 : i;
+  const int* cs = b.cols[mu] + ig * 3;
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    rw.dl[s] = 0;
+    if (s < rw.n) rw.dl[s] = int(col_off(b, mu, ig, __ldg(cs + s)));
+  }
+}
+
+__device__ __forceinline__ unsigned s3_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void s3_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(s3_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <bool CPLX, bool PAIR>
+__global__ void __launch_bounds__(256)
+    kronsum_band3_kernel(const __grid_constant__ CUtensorMap map, BandArgs b, int nz,
+                         int zchunk, const double* __restrict__ u, double* __restrict__ r,
+                         bool with_g, kp_gfun g, double t) {
+  pdl_wait();
+  using T = typename std::conditional<CPLX, double2, double>::type;
+  constexpr int NSP = PAIR ? 2 : 1;
+  constexpr unsigned TILE_B = PX * PY * sizeof(T);  // bytes of one plane tile (a TMA box)
+  // tiles start on 128-byte boundaries (the TMA destination alignment)
+  constexpr unsigned TILE = ((TILE_B + 127) / 128 * 128) / sizeof(T);  // padded, in elements
+  constexpr unsigned SLOT_BYTES = TILE_B * NSP;  // bytes landing per slot
+  constexpr unsigned SLOT_PAD = TILE * sizeof(T) * NSP;
+  extern __shared__ __align__(128) unsigned char s3raw[];
+  T* ring = reinterpret_cast<T*>(s3raw);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(s3raw + D3 * SLOT_PAD);
+  __shared__ BandRow3<CPLX> rows2[ZMAX];
+  const T* __restrict__ ut = reinterpret_cast<const T*>(u);
+  T* __restrict__ rt = reinterpret_cast<T*>(r);
+
+  const int z0 = blockIdx.z * zchunk;
+  const int z1 = min(nz, z0 + zchunk);
+  const int tid = threadIdx.x + 32 * threadIdx.y;
+  const int t0 = blockIdx.x * TX, t1 = blockIdx.y * TY;
+  const int h2 = b.slab == 2 ? b.halo : 0;
+  // input planes z0-1 .. z1 (with the slab halo offset h2); plane j of the
+  // march (j = p - (z0 - 1)) lives in slot j % D3, phase (j / D3) & 1
+  const int jmax = z1 - z0 + 1;
+  auto issue = [&](int j) {
+    const int slot = j % D3;
+    const int zin = z0 - 1 + j + h2;
+    unsigned long long* bar = &full[slot];
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(s3_u32(bar)),
+                 "r"(SLOT_BYTES)
+                 : "memory");
+#pragma unroll
+    for (int sp = 0; sp < NSP; ++sp) {
+      T* dst = ring + (size_t(slot) * NSP + sp) * TILE;
+      const int c0 = CPLX ? 2 * (t0 - 1) : t0 - 1;
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(s3_u32(dst)),
+          "l"(reinterpret_cast<unsigned long long>(&map)), "r"(c0), "r"(t1 - 1), "r"(zin),
+          "r"(sp), "r"(s3_u32(bar))
+          : "memory");
+    }
+  };
+  if (tid == 0) {
+    for (int s = 0; s < D3; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s3_u32(&full[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  if (b.active[2] && tid < z1 - z0) load_row3(b, 2, PAIR ? z0 + tid : (z0 + tid) % b.n[2], rows2[tid]);
+  __syncthreads();
+  if (tid == 0)
+    for (int j = 0; j < min(D3, jmax + 1); ++j) issue(j);
+
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const int i0 = t0 + lx, i1 = t1 + ly;
+  const bool live = i0 < b.n[0] && i1 < b.n[1];
+  BandRow3<CPLX> r0, r1;
+  if (live && b.active[0]) load_row3(b, 0, i0, r0);
+  if (live && b.active[1]) load_row3(b, 1, i1, r1);
+  const unsigned in01 = unsigned(i0) * unsigned(b.stride[0]) + unsigned(i1) * unsigned(b.stride[1]);
+  const unsigned plane = unsigned(b.n[0]) * unsigned(b.n[1]);
+  const unsigned out01 = unsigned(i0) + unsigned(i1) * unsigned(b.n[0]);
+  const unsigned st2 = unsigned(b.stride[2]), st3 = unsigned(b.stride[3]);
+  const unsigned n2 = unsigned(b.n[2]);
+  const bool a0 = b.active[0], a1 = b.active[1], a2 = b.active[2];
+  const int cen = (ly + 1) * PX + (lx + 1);  // the entry's offset in a plane tile
+
+  for (int z = z0; z < z1; ++z) {
+    const int jc = z - z0 + 1;  // the centre plane's march index
+#pragma unroll
+    for (int k = -1; k <= 1; ++k) {
+      const int j = jc + k;
+      s3_wait(&full[j % D3], unsigned((j / D3) & 1));
+    }
+    if (live) {
+      const BandRow3<CPLX>& q2 = rows2[z - z0];
+      const T* tc[NSP];
+#pragma unroll
+      for (int sp = 0; sp < NSP; ++sp) tc[sp] = ring + (size_t(jc % D3) * NSP + sp) * TILE;
+      const unsigned iz = unsigned(z);
+      unsigned in_base;
+      if constexpr (PAIR) {
+        in_base = in01 + (iz + h2) * st2;
+      } else {
+        const unsigned i3 = iz / n2, i2 = iz - i3 * n2;
+        in_base = in01 + (i2 + h2) * st2 + i3 * st3;
+      }
+#pragma unroll
+      for (int sp = 0; sp < NSP; ++sp) {
+        const T* tp = tc[sp];
+        const unsigned in = in_base + unsigned(sp) * st3;
+        T x0[3], x1[3], x2[3];
+        if (a0) {
+#pragma unroll
+          for (int s = 0; s < 3; ++s)
+            x0[s] = (r0.dl[s] >= -1 && r0.dl[s] <= 1) ? tp[cen + r0.dl[s]]
+                                                      : ut[in + unsigned(r0.off[s])];
+        }
+        if (a1) {
+#pragma unroll
+          for (int s = 0; s < 3; ++s)
+            x1[s] = (r1.dl[s] >= -1 && r1.dl[s] <= 1) ? tp[cen + r1.dl[s] * PX]
+                                                      : ut[in + unsigned(r1.off[s])];
+        }
+        if (a2) {
+#pragma unroll
+          for (int s = 0; s < 3; ++s) {
+            const int dz = q2.dl[s];
+            x2[s] = (dz >= -1 && dz <= 1)
+                        ? ring[(size_t((jc + dz) % D3) * NSP + sp) * TILE + cen]
+                        : ut[in + unsigned(q2.off[s])];
+          }
+        }
+        T c;
+        if constexpr (CPLX)
+          c = make_double2(0.0, 0.0);
+        else
+          c = 0.0;
+        if (a0) row_combine(static_cast<const BandRow<CPLX>&>(r0), x0, c);
+        if (a1) row_combine(static_cast<const BandRow<CPLX>&>(r1), x1, c);
+        if (a2) row_combine(static_cast<const BandRow<CPLX>&>(q2), x2, c);
+        const unsigned idx = out01 + (PAIR ? iz + unsigned(sp) * n2 : iz) * plane;
+        if (!with_g) {
+          rt[idx] = c;
+        } else if constexpr (CPLX) {
+          const double2 gg = g_cplx(g, tp[cen]);
+          rt[idx] = make_double2(__dadd_rn(c.x, gg.x), __dadd_rn(c.y, gg.y));
+        } else if constexpr (PAIR) {
+          const double uc = tp[cen], upart = tc[1 - sp][cen];
+          rt[idx] = __dadd_rn(c, g_real(g, uc, upart, sp == 1, idx, t));
+        } else {
+          rt[idx] = __dadd_rn(c, g_real(g, tp[cen], 0.0, false, idx, t));
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with plane z-1's slot
+    if (tid == 0 && jc - 1 + D3 <= jmax) issue(jc - 1 + D3);
+  }
+}
+
+// v3 launcher; false = not applicable (the v2 kernel runs)
+bool launch_band3(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz,
+                  const double* u, double* r, bool with_g, const kp_gfun& g, double t) {
+  static const bool off = [] {
+    const char* v = getenv("KP_BAND");
+    return v && (std::string(v) == "v2" || std::string(v) == "v1");
+  }();
+  if (off || b2.active[3] || b2.d < 3 || (!pair && b2.n[3] != 1)) return false;
+  if (b2.slab >= 0 && b2.slab != 2) return false;
+  if (b2.stride[0] != 1 || b2.stride[1] != b2.n[0] ||
+      b2.stride[2] != (long long)b2.n[0] * b2.n[1])
+    return false;
+  const int esz = cplx ? 16 : 8;
+  if ((long long)b2.n[0] * esz % 16 || (reinterpret_cast<uintptr_t>(u) % 16)) return false;
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  if (!enc) return false;
+  const long long h2 = b2.slab == 2 ? b2.halo : 0;
+  const long long planes = pair ? b2.n[2] + 2 * h2 : (long long)b2.n[2] * b2.n[3] + 2 * h2;
+  const long long nsp = pair ? 2 : 1;
+  const int ce = cplx ? 2 : 1;  // doubles per element
+  cuuint64_t dims[4] = {cuuint64_t(b2.n[0]) * ce, cuuint64_t(b2.n[1]), cuuint64_t(planes),
+                        cuuint64_t(nsp)};
+  const long long sp_stride = pair ? b2.stride[3] : planes * b2.n[0] * b2.n[1];
+  cuuint64_t strides[3] = {cuuint64_t(b2.n[0]) * esz, cuuint64_t(b2.n[0]) * b2.n[1] * esz,
+                           cuuint64_t(sp_stride) * esz};
+  cuuint32_t box[4] = {cuuint32_t(PX * ce), cuuint32_t(PY), 1u, 1u};
+  cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+  CUtensorMap map;
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(u), dims, strides, box,
+          es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  const long long bxy = (long long)((b2.n[0] + TX - 1) / TX) * ((b2.n[1] + TY - 1) / TY);
+  const long long want = ctx->num_sms * 6LL;  // resident blocks per wave (smem-bound)
+  const int zchunk = int(std::min<long long>(ZMAX, std::max<long long>(4, (nz * bxy + want - 1) / want)));
+  if ((nz + zchunk - 1) / zchunk > 65535) return false;
+  dim3 grid(unsigned((b2.n[0] + TX - 1) / TX), unsigned((b2.n[1] + TY - 1) / TY),
+            unsigned((nz + zchunk - 1) / zchunk));
+  const size_t tile_pad = (size_t(PX) * PY * esz + 127) / 128 * 128;
+  const size_t smem = size_t(D3) * tile_pad * nsp + D3 * 8;
+  auto go = [&](auto kern) {
+    ensure_smem_attr(ctx, reinterpret_cast<const void*>(kern), int(smem));
+    launch_pdl(ctx, kern, grid, dim3(32, 8), smem, map, b2, nz, zchunk, u, r, with_g, g, t);
+    ctx->launches--;  // counted once by the caller
+  };
+  if (cplx)
+    go(kronsum_band3_kernel<true, false>);
+  else if (pair)
+    go(kronsum_band3_kernel<false, true>);
+  else
+    go(kronsum_band3_kernel<false, false>);
+  return true;
+}
+
 }  // namespace
 
 // forward (defined below)
@@ -606,6 +863,11 @@ void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<i
     for (int mu = 0; mu < d; ++mu) ext *= dims[mu] + (mu == slab ? 2 * b.halo : 0);
     if (ext > 0x7fffffffLL) throw invalid_argument("kronsum: tensor too large for the stencil path");
     const bool m3 = b2.active[3] != 0;
+    if (launch_band3(ctx, b2, cplx, pair, nz, u, r, with_g, g, t)) {
+      ctx->launches++;
+      KP_CUDA(cudaGetLastError());
+      return;
+    }
     auto go = [&](auto kern) {
       launch_pdl(ctx, kern, grid, dim3(32, 8), 0, b2, nz, zchunk, u, r, with_g, g, t);
       ctx->launches--;  // counted once below
