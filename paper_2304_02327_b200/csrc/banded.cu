@@ -461,7 +461,14 @@ __global__ void __launch_bounds__(256, (CPLX || PAIR) ? 3 : 4)
 // entry's neighbours are read from shared memory (row deltas of -1 / 0 / +1;
 // a periodic wrap-around column falls back to a global load), then the same
 // row_combine as v2 -- bit-identical results.
-constexpr int D3 = 8, TX = 32, TY = 8, PX = TX + 2, PY = TY + 2;
+constexpr int D3 = 8, TX = 32, TY = 8, PY = TY + 2;
+// tile width and the centre's x offset: a TMA box must start on a 16-byte
+// boundary, so a real tile starts 2 entries left of the block (t0 - 2, even)
+// and is TX + 4 wide; a complex entry is 16 bytes, so t0 - 1 works
+template <bool CPLX>
+constexpr int tile_px() { return CPLX ? TX + 2 : TX + 4; }
+template <bool CPLX>
+constexpr int tile_xo() { return CPLX ? 1 : 2; }
 
 template <bool CPLX>
 struct BandRow3 : BandRow<CPLX> {
@@ -505,6 +512,7 @@ __global__ void __launch_bounds__(256)
   pdl_wait();
   using T = typename std::conditional<CPLX, double2, double>::type;
   constexpr int NSP = PAIR ? 2 : 1;
+  constexpr int PX = tile_px<CPLX>(), XO = tile_xo<CPLX>();
   constexpr unsigned TILE_B = PX * PY * sizeof(T);  // bytes of one plane tile (a TMA box)
   // tiles start on 128-byte boundaries (the TMA destination alignment)
   constexpr unsigned TILE = ((TILE_B + 127) / 128 * 128) / sizeof(T);  // padded, in elements
@@ -535,7 +543,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int sp = 0; sp < NSP; ++sp) {
       T* dst = ring + (size_t(slot) * NSP + sp) * TILE;
-      const int c0 = CPLX ? 2 * (t0 - 1) : t0 - 1;
+      const int c0 = CPLX ? 2 * (t0 - XO) : t0 - XO;
       asm volatile(
           "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
           " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(s3_u32(dst)),
@@ -567,7 +575,7 @@ __global__ void __launch_bounds__(256)
   const unsigned st2 = unsigned(b.stride[2]), st3 = unsigned(b.stride[3]);
   const unsigned n2 = unsigned(b.n[2]);
   const bool a0 = b.active[0], a1 = b.active[1], a2 = b.active[2];
-  const int cen = (ly + 1) * PX + (lx + 1);  // the entry's offset in a plane tile
+  const int cen = (ly + 1) * PX + (lx + XO);  // the entry's offset in a plane tile
 
   for (int z = z0; z < z1; ++z) {
     const int jc = z - z0 + 1;  // the centre plane's march index
@@ -675,7 +683,8 @@ bool launch_band3(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz,
   const long long sp_stride = pair ? b2.stride[3] : planes * b2.n[0] * b2.n[1];
   cuuint64_t strides[3] = {cuuint64_t(b2.n[0]) * esz, cuuint64_t(b2.n[0]) * b2.n[1] * esz,
                            cuuint64_t(sp_stride) * esz};
-  cuuint32_t box[4] = {cuuint32_t(PX * ce), cuuint32_t(PY), 1u, 1u};
+  const int px = cplx ? tile_px<true>() : tile_px<false>();
+  cuuint32_t box[4] = {cuuint32_t(px * ce), cuuint32_t(PY), 1u, 1u};
   cuuint32_t es[4] = {1u, 1u, 1u, 1u};
   CUtensorMap map;
   if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(u), dims, strides, box,
@@ -688,7 +697,7 @@ bool launch_band3(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz,
   if ((nz + zchunk - 1) / zchunk > 65535) return false;
   dim3 grid(unsigned((b2.n[0] + TX - 1) / TX), unsigned((b2.n[1] + TY - 1) / TY),
             unsigned((nz + zchunk - 1) / zchunk));
-  const size_t tile_pad = (size_t(PX) * PY * esz + 127) / 128 * 128;
+  const size_t tile_pad = (size_t(px) * PY * esz + 127) / 128 * 128;
   const size_t smem = size_t(D3) * tile_pad * nsp + D3 * 8;
   auto go = [&](auto kern) {
     ensure_smem_attr(ctx, reinterpret_cast<const void*>(kern), int(smem));
