@@ -653,9 +653,12 @@ __global__ void __launch_bounds__(256)
 // v3 launcher; false = not applicable (the v2 kernel runs)
 bool launch_band3(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz,
                   const double* u, double* r, bool with_g, const kp_gfun& g, double t) {
+  // opt-in (KP_BAND=v3): measured slower than v2 on the configs (AC3D 29.6
+  // vs 27.9 us, NLS 512^3 2.14 vs 1.71 ms): the per-plane block barrier and
+  // the single issuing thread cost more than the latency the ring hides
   static const bool off = [] {
     const char* v = getenv("KP_BAND");
-    return v && (std::string(v) == "v2" || std::string(v) == "v1");
+    return !(v && std::string(v) == "v3");
   }();
   if (off || b2.active[3] || b2.d < 3 || (!pair && b2.n[3] != 1)) return false;
   if (b2.slab >= 0 && b2.slab != 2) return false;
