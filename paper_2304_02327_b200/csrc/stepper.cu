@@ -1437,16 +1437,30 @@ class ShardedIntegrator {
     cudaGraphExec_t exec = nullptr;
     unsigned long long per = 0;
     if (use_graph && n_steps - n >= 4) {
-      cudaGraph_t graph;
+      // two steps (ping-pong) as one graph; if capturing the exchanges fails
+      // (a transport that cannot be captured), the loop runs eagerly
+      cudaGraph_t graph = nullptr;
       const unsigned long long l0 = ctx->launches;
-      KP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-      step(cu[1], mu_[0], 1);
-      step(cu[0], mu_[1], 0);
-      KP_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
-      per = ctx->launches - l0;
+      try {
+        KP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        step(cu[1], mu_[0], 1);
+        step(cu[0], mu_[1], 0);
+        KP_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+        KP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        per = ctx->launches - l0;
+      } catch (const std::exception&) {
+        cudaStreamCaptureStatus st;
+        if (cudaStreamIsCapturing(ctx->stream, &st) == cudaSuccess &&
+            st != cudaStreamCaptureStatusNone) {
+          cudaGraph_t g2 = nullptr;
+          cudaStreamEndCapture(ctx->stream, &g2);
+          if (g2) cudaGraphDestroy(g2);
+        }
+        cudaGetLastError();
+        exec = nullptr;
+      }
       ctx->launches = l0;
-      KP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-      cudaGraphDestroy(graph);
+      if (graph) cudaGraphDestroy(graph);
     }
     KP_CUDA(cudaEventRecord(ev[2], ctx->stream));
     if (exec)
