@@ -18,6 +18,7 @@
 // Band detection (once per factor): a device scan collects, per row, up to
 // three (column, value) pairs in increasing column order; more nonzeros =>
 // not banded (dense path).
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -716,6 +717,148 @@ bool launch_band3(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz,
   return true;
 }
 
+
+// ---- the whole exp-Euler time loop of a small 2-D state in ONE launch ----
+// (AC2D, configs[0]: 128 x 128, 100 steps; the regular loop is launch-bound
+// at ~14 us per step for three ~2 us kernels.)  A cluster of SJ = 16 CTAs
+// (distributed shared memory) holds the whole problem on chip: the phi_1
+// factor L (128 x 128, 128 KiB) in every CTA's shared memory, the state in
+// column blocks (CTA j owns columns [8j, 8j+8)).  Per step:
+//   1  r = K u + g(u) on the column block (the banded row chains of v2; the
+//      mode-1 neighbours of the block's edge columns are read from the
+//      neighbour CTAs' shared memory);
+//   2  y = L r (mode 0): each column block is independent (DMMA);
+//   3  gather the row block [8j, 8j+8) of y and of u from all 16 CTAs;
+//   4  u' = fma(tau, y L^T, u) (mode 1 + the exp-Euler update) on the rows;
+//   5  scatter u' back into column blocks.
+// Cluster barriers separate the phases; the loop never leaves the SMs.  The
+// arithmetic is the regular path's (same row chains, same DMMA k order, the
+// same FMA epilogue), so results are bit-identical to it.
+constexpr int SN = 128, SJ = 16, SB = SN / SJ;
+
+__device__ __forceinline__ void sdmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128, 1)
+    small2d_expeuler_kernel(BandArgs b, const double* __restrict__ L, kp_gfun g, double tau,
+                            long n_steps, double* __restrict__ u, int* bad) {
+  namespace cgx = cooperative_groups;
+  cgx::cluster_group cluster = cgx::this_cluster();
+  const int j = int(cluster.block_rank());
+  constexpr int HB = SB + 2;           // column block with a halo column each side
+  extern __shared__ __align__(16) double sm[];
+  double* Ls = sm;                     // L, column-major 128 x 128
+  double* ub = Ls + SN * SN;           // u(:, 8j-1 .. 8j+8)   128 x 10 (halo columns 0, 9)
+  double* rb = ub + SN * HB;           // r(:, block)          128 x 8
+  double* yr = rb + SN * SB;           // y(rows 8j.., :)      8 x 128 (p fastest)
+  double* ur = yr + SB * SN;           // u(rows 8j.., :)      8 x 128
+  BandRow<false>* rows = reinterpret_cast<BandRow<false>*>(ur + SB * SN);  // [2][128]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
+  for (int i = tid; i < SN * SN; i += 128) Ls[i] = L[i];
+  for (int i = tid; i < SN * HB; i += 128) {
+    const int i0 = i % SN, h = i / SN;
+    const int c = (j * SB + h - 1 + SN) % SN;  // halo columns wrap (periodic rows read them)
+    ub[i] = u[i0 + (long long)SN * c];
+  }
+  for (int i = tid; i < 2 * SN; i += 128) load_row(b, i / SN, i % SN, rows[i]);
+  cluster.sync();
+  // push targets: the row owner of row i is CTA i / 8; the column owner of
+  // column c is CTA c / 8, which also holds c as a halo column of its neighbours
+  bool nonfinite = false;
+  int first_bad = 0;
+  for (long step = 0; step < n_steps; ++step) {
+    // ---- 1: r = K u + g(u) on the column block (local: the halo columns)
+#pragma unroll
+    for (int it = 0; it < SN * SB / 128; ++it) {
+      const int e = tid + 128 * it;
+      const int i0 = e % SN, cl = e / SN, c = j * SB + cl;
+      const BandRow<false>& r0 = rows[i0];
+      const BandRow<false>& r1 = rows[SN + c];
+      double x0[3], x1[3];
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        x0[s] = ub[i0 + r0.off[s] + SN * (cl + 1)];
+        int dc = r1.off[s] / SN;  // column delta, -1 / 0 / +1 modulo n (checked)
+        if (dc > 1) dc -= SN;
+        if (dc < -1) dc += SN;
+        x1[s] = ub[i0 + SN * (cl + 1 + dc)];
+      }
+      double acc = 0.0;
+      row_combine(r0, x0, acc);
+      row_combine(r1, x1, acc);
+      rb[e] = __dadd_rn(acc, g_real(g, ub[i0 + SN * (cl + 1)], 0.0, false, i0 + SN * c, 0.0));
+    }
+    __syncthreads();
+    // ---- 2: y = L r (M = 128: warp w rows 32w.., N = 8, K = 128); push y and
+    // u into the row owners' yr / ur
+    {
+      double acc[4][2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) acc[mi][0] = acc[mi][1] = 0.0;
+#pragma unroll 4
+      for (int ks = 0; ks < SN / 4; ++ks) {
+        const int k = 4 * ks + tq;
+        const double bv = rb[k + SN * gq];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+          sdmma(acc[mi][0], acc[mi][1], Ls[(32 * warp + 8 * mi + gq) + SN * k], bv);
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int row = 32 * warp + 8 * mi + gq, owner = row / SB, p = row - owner * SB;
+        double* dy = cluster.map_shared_rank(yr, owner);
+        double* du = cluster.map_shared_rank(ur, owner);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = j * SB + 2 * tq + h;
+          dy[p + SB * c] = acc[mi][h];
+          du[p + SB * c] = ub[row + SN * (2 * tq + h + 1)];
+        }
+      }
+    }
+    cluster.sync();
+    // ---- 3: u' = fma(tau, y L^T, u) on the rows (M = 8, N = 128: warp w cols
+    // 32w.., K = 128); push u' into the column owners' blocks and halos
+    {
+      double acc[4][2];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) acc[ni][0] = acc[ni][1] = 0.0;
+#pragma unroll 4
+      for (int ks = 0; ks < SN / 4; ++ks) {
+        const int k = 4 * ks + tq;
+        const double av = yr[gq + SB * k];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+          sdmma(acc[ni][0], acc[ni][1], av, Ls[(32 * warp + 8 * ni + gq) + SN * k]);
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = 32 * warp + 8 * ni + 2 * tq + h, row = j * SB + gq;
+          const double v = __fma_rn(tau, acc[ni][h], ur[gq + SB * col]);
+          if (!isfinite(v) && !nonfinite) {
+            nonfinite = true;
+            first_bad = int(step) + 1;
+          }
+          const int owner = col / SB, cl = col - owner * SB;
+          cluster.map_shared_rank(ub, owner)[row + SN * (cl + 1)] = v;
+          if (cl == 0)  // right halo of the left neighbour (wrapping)
+            cluster.map_shared_rank(ub, (owner + SJ - 1) % SJ)[row + SN * (SB + 1)] = v;
+          if (cl == SB - 1)  // left halo of the right neighbour
+            cluster.map_shared_rank(ub, (owner + 1) % SJ)[row] = v;
+        }
+    }
+    cluster.sync();
+  }
+  for (int i = tid; i < SN * SB; i += 128)
+    u[(i % SN) + (long long)SN * (j * SB + i / SN)] = ub[(i % SN) + SN * (i / SN + 1)];
+  if (nonfinite) atomicMin(bad, first_bad);
+}
+
 }  // namespace
 
 // forward (defined below)
@@ -762,6 +905,74 @@ bool band_of(kp_ctx* ctx, const double* a, int n, bool cplx, int** cols, double*
   }
   *cols = dc;
   *vals = dv;
+  return true;
+}
+
+// The whole exp-Euler loop of a 128 x 128 real state in one cluster launch
+// (small2d_expeuler_kernel); false = not applicable.  u: device, in/out;
+// L: the phi_1 factor of both modes (prefactor and fold 1); cols/vals: the
+// band rows of A_0 and A_1; *bad: the first non-finite step (atomicMin).
+bool small2d_expeuler(kp_ctx* ctx, const std::vector<int>& dims,
+                      const std::vector<const int*>& cols, const std::vector<const double*>& vals,
+                      const double* L, const kp_gfun& g, double tau, long n_steps, double* u,
+                      int* bad) {
+  static const bool off = getenv("KP_SMALL_LOOP") && std::string(getenv("KP_SMALL_LOOP")) == "0";
+  if (off || dims.size() != 2 || dims[0] != SN || dims[1] != SN) return false;
+  if (!(g.kind == KP_G_ZERO || g.kind == KP_G_SQUARE || g.kind == KP_G_CONST ||
+        g.kind == KP_G_ALLEN_CAHN))
+    return false;
+  BandArgs b{};
+  b.d = 2;
+  for (int mu = 0; mu < 4; ++mu) {
+    b.n[mu] = mu < 2 ? SN : 1;
+    b.stride[mu] = mu == 0 ? 1 : (mu == 1 ? SN : 0);
+    b.cols[mu] = mu < 2 ? cols[mu] : nullptr;
+    b.vals[mu] = mu < 2 ? vals[mu] : nullptr;
+    b.active[mu] = mu < 2 ? 1 : 0;
+  }
+  b.slab = -1;
+  b.species = -1;
+  auto kern = small2d_expeuler_kernel;
+  // mode-1 rows must reach only the neighbour columns (mod n): the halo
+  std::vector<int> hc(3 * SN);
+  KP_CUDA(cudaMemcpyAsync(hc.data(), cols[1], hc.size() * sizeof(int), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  KP_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < SN; ++i)
+    for (int s = 0; s < 3; ++s) {
+      const int c = hc[3 * i + s];
+      if (c < 0) continue;
+      const int dlt = ((c - i) % SN + SN) % SN;
+      if (!(dlt == 0 || dlt == 1 || dlt == SN - 1)) return false;
+    }
+  const size_t smem = sizeof(double) * (size_t(SN) * SN + size_t(SN) * (SB + 2) +
+                                        size_t(SN) * SB + 2ull * SB * SN) +
+                      2 * SN * sizeof(BandRow<false>);
+  static bool attr = false;
+  if (!attr) {
+    KP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    KP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(SJ);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = SJ;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess || nclusters < 1) {
+    cudaGetLastError();
+    return false;
+  }
+  KP_CUDA(cudaLaunchKernelEx(&cfg, kern, b, L, g, tau, n_steps, u, bad));
+  ctx->launches++;
   return true;
 }
 

@@ -200,6 +200,13 @@ void comm_reduce_scatter(kp_ctx* ctx, kp_comm* c, const double* send, double* re
                          size_t count);
 void comm_allreduce(kp_ctx* ctx, kp_comm* c, double* x, size_t n, int op);
 
+// the whole exp-Euler loop of a 128 x 128 real state in one cluster launch
+// (banded.cu small2d_expeuler_kernel); false = not applicable
+bool small2d_expeuler(kp_ctx* ctx, const std::vector<int>& dims,
+                      const std::vector<const int*>& cols, const std::vector<const double*>& vals,
+                      const double* L, const kp_gfun& g, double tau, long n_steps, double* u,
+                      int* bad);
+
 // ---- steppers (stepper.cu) ----
 // d = g(t + tau, s) - g(t, u); half > 0: Brusselator species offset
 void gdiff_dev(kp_ctx* ctx, const kp_gfun& g, double t, double tau, const double* s,
