@@ -735,6 +735,7 @@ bool launch_band3(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz,
 // arithmetic is the regular path's (same row chains, same DMMA k order, the
 // same FMA epilogue), so results are bit-identical to it.
 constexpr int SN = 128, SJ = 16, SB = SN / SJ;
+constexpr int SNT = 256, SW = SNT / 32, WR = SN / SW, MT = WR / 8;  // 8 warps, 16 rows each
 
 __device__ __forceinline__ void sdmma(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -742,7 +743,7 @@ __device__ __forceinline__ void sdmma(double& d0, double& d1, double a, double b
       : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(SNT, 1)
     small2d_expeuler_kernel(BandArgs b, const double* __restrict__ L, kp_gfun g, double tau,
                             long n_steps, double* __restrict__ u, int* bad) {
   namespace cgx = cooperative_groups;
@@ -757,13 +758,13 @@ __global__ void __launch_bounds__(128, 1)
   double* ur = yr + SB * SN;           // u(rows 8j.., :)      8 x 128
   BandRow<false>* rows = reinterpret_cast<BandRow<false>*>(ur + SB * SN);  // [2][128]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
-  for (int i = tid; i < SN * SN; i += 128) Ls[i] = L[i];
-  for (int i = tid; i < SN * HB; i += 128) {
+  for (int i = tid; i < SN * SN; i += SNT) Ls[i] = L[i];
+  for (int i = tid; i < SN * HB; i += SNT) {
     const int i0 = i % SN, h = i / SN;
     const int c = (j * SB + h - 1 + SN) % SN;  // halo columns wrap (periodic rows read them)
     ub[i] = u[i0 + (long long)SN * c];
   }
-  for (int i = tid; i < 2 * SN; i += 128) load_row(b, i / SN, i % SN, rows[i]);
+  for (int i = tid; i < 2 * SN; i += SNT) load_row(b, i / SN, i % SN, rows[i]);
   cluster.sync();
   // push targets: the row owner of row i is CTA i / 8; the column owner of
   // column c is CTA c / 8, which also holds c as a halo column of its neighbours
@@ -772,8 +773,8 @@ __global__ void __launch_bounds__(128, 1)
   for (long step = 0; step < n_steps; ++step) {
     // ---- 1: r = K u + g(u) on the column block (local: the halo columns)
 #pragma unroll
-    for (int it = 0; it < SN * SB / 128; ++it) {
-      const int e = tid + 128 * it;
+    for (int it = 0; it < SN * SB / SNT; ++it) {
+      const int e = tid + SNT * it;
       const int i0 = e % SN, cl = e / SN, c = j * SB + cl;
       const BandRow<false>& r0 = rows[i0];
       const BandRow<false>& r1 = rows[SN + c];
@@ -792,23 +793,23 @@ __global__ void __launch_bounds__(128, 1)
       rb[e] = __dadd_rn(acc, g_real(g, ub[i0 + SN * (cl + 1)], 0.0, false, i0 + SN * c, 0.0));
     }
     __syncthreads();
-    // ---- 2: y = L r (M = 128: warp w rows 32w.., N = 8, K = 128); push y and
-    // u into the row owners' yr / ur
+    // ---- 2: y = L r (M = 128: warp w rows WR w.., N = 8, K = 128); push y
+    // and u into the row owners' yr / ur
     {
-      double acc[4][2];
+      double acc[MT][2];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) acc[mi][0] = acc[mi][1] = 0.0;
-#pragma unroll 4
+      for (int mi = 0; mi < MT; ++mi) acc[mi][0] = acc[mi][1] = 0.0;
+#pragma unroll 8
       for (int ks = 0; ks < SN / 4; ++ks) {
         const int k = 4 * ks + tq;
         const double bv = rb[k + SN * gq];
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-          sdmma(acc[mi][0], acc[mi][1], Ls[(32 * warp + 8 * mi + gq) + SN * k], bv);
+        for (int mi = 0; mi < MT; ++mi)
+          sdmma(acc[mi][0], acc[mi][1], Ls[(WR * warp + 8 * mi + gq) + SN * k], bv);
       }
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
-        const int row = 32 * warp + 8 * mi + gq, owner = row / SB, p = row - owner * SB;
+      for (int mi = 0; mi < MT; ++mi) {
+        const int row = WR * warp + 8 * mi + gq, owner = row / SB, p = row - owner * SB;
         double* dy = cluster.map_shared_rank(yr, owner);
         double* du = cluster.map_shared_rank(ur, owner);
 #pragma unroll
@@ -821,24 +822,24 @@ __global__ void __launch_bounds__(128, 1)
     }
     cluster.sync();
     // ---- 3: u' = fma(tau, y L^T, u) on the rows (M = 8, N = 128: warp w cols
-    // 32w.., K = 128); push u' into the column owners' blocks and halos
+    // WR w.., K = 128); push u' into the column owners' blocks and halos
     {
-      double acc[4][2];
+      double acc[MT][2];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) acc[ni][0] = acc[ni][1] = 0.0;
-#pragma unroll 4
+      for (int ni = 0; ni < MT; ++ni) acc[ni][0] = acc[ni][1] = 0.0;
+#pragma unroll 8
       for (int ks = 0; ks < SN / 4; ++ks) {
         const int k = 4 * ks + tq;
         const double av = yr[gq + SB * k];
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
-          sdmma(acc[ni][0], acc[ni][1], av, Ls[(32 * warp + 8 * ni + gq) + SN * k]);
+        for (int ni = 0; ni < MT; ++ni)
+          sdmma(acc[ni][0], acc[ni][1], av, Ls[(WR * warp + 8 * ni + gq) + SN * k]);
       }
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
+      for (int ni = 0; ni < MT; ++ni)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int col = 32 * warp + 8 * ni + 2 * tq + h, row = j * SB + gq;
+          const int col = WR * warp + 8 * ni + 2 * tq + h, row = j * SB + gq;
           const double v = __fma_rn(tau, acc[ni][h], ur[gq + SB * col]);
           if (!isfinite(v) && !nonfinite) {
             nonfinite = true;
@@ -854,7 +855,7 @@ __global__ void __launch_bounds__(128, 1)
     }
     cluster.sync();
   }
-  for (int i = tid; i < SN * SB; i += 128)
+  for (int i = tid; i < SN * SB; i += SNT)
     u[(i % SN) + (long long)SN * (j * SB + i / SN)] = ub[(i % SN) + SN * (i / SN + 1)];
   if (nonfinite) atomicMin(bad, first_bad);
 }
@@ -956,7 +957,7 @@ bool small2d_expeuler(kp_ctx* ctx, const std::vector<int>& dims,
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(SJ);
-  cfg.blockDim = dim3(128);
+  cfg.blockDim = dim3(SNT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx->stream;
   cudaLaunchAttribute at[1];
