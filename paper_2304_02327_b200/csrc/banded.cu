@@ -736,6 +736,7 @@ bool launch_band3(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz,
 // same FMA epilogue), so results are bit-identical to it.
 constexpr int SN = 128, SJ = 16, SB = SN / SJ;
 constexpr int SNT = 256, SW = SNT / 32, WR = SN / SW, MT = WR / 8;  // 8 warps, 16 rows each
+constexpr int LP = SN + 8, RP = SN + 4;  // smem pitches of L and r (bank-conflict free)
 
 __device__ __forceinline__ void sdmma(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -751,14 +752,16 @@ __global__ void __launch_bounds__(SNT, 1)
   const int j = int(cluster.block_rank());
   constexpr int HB = SB + 2;           // column block with a halo column each side
   extern __shared__ __align__(16) double sm[];
-  double* Ls = sm;                     // L, column-major 128 x 128
-  double* ub = Ls + SN * SN;           // u(:, 8j-1 .. 8j+8)   128 x 10 (halo columns 0, 9)
-  double* rb = ub + SN * HB;           // r(:, block)          128 x 8
-  double* yr = rb + SN * SB;           // y(rows 8j.., :)      8 x 128 (p fastest)
+  // pitches chosen so the DMMA fragment loads are bank-conflict free:
+  // L(row, k) at row + LP k (LP = 8 mod 32), r(k, c) at k + RP c (RP = 4 mod 32)
+  double* Ls = sm;                     // L, column-major 128 x 128, pitch LP
+  double* ub = Ls + LP * SN;           // u(:, 8j-1 .. 8j+8)   128 x 10 (halo columns 0, 9)
+  double* rb = ub + SN * HB;           // r(:, block)          128 x 8, pitch RP
+  double* yr = rb + RP * SB;           // y(rows 8j.., :)      8 x 128 (p fastest)
   double* ur = yr + SB * SN;           // u(rows 8j.., :)      8 x 128
   BandRow<false>* rows = reinterpret_cast<BandRow<false>*>(ur + SB * SN);  // [2][128]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
-  for (int i = tid; i < SN * SN; i += SNT) Ls[i] = L[i];
+  for (int i = tid; i < SN * SN; i += SNT) Ls[(i % SN) + LP * (i / SN)] = L[i];
   for (int i = tid; i < SN * HB; i += SNT) {
     const int i0 = i % SN, h = i / SN;
     const int c = (j * SB + h - 1 + SN) % SN;  // halo columns wrap (periodic rows read them)
@@ -790,7 +793,8 @@ __global__ void __launch_bounds__(SNT, 1)
       double acc = 0.0;
       row_combine(r0, x0, acc);
       row_combine(r1, x1, acc);
-      rb[e] = __dadd_rn(acc, g_real(g, ub[i0 + SN * (cl + 1)], 0.0, false, i0 + SN * c, 0.0));
+      rb[i0 + RP * cl] =
+          __dadd_rn(acc, g_real(g, ub[i0 + SN * (cl + 1)], 0.0, false, i0 + SN * c, 0.0));
     }
     __syncthreads();
     // ---- 2: y = L r (M = 128: warp w rows WR w.., N = 8, K = 128); push y
@@ -802,10 +806,10 @@ __global__ void __launch_bounds__(SNT, 1)
 #pragma unroll 8
       for (int ks = 0; ks < SN / 4; ++ks) {
         const int k = 4 * ks + tq;
-        const double bv = rb[k + SN * gq];
+        const double bv = rb[k + RP * gq];
 #pragma unroll
         for (int mi = 0; mi < MT; ++mi)
-          sdmma(acc[mi][0], acc[mi][1], Ls[(WR * warp + 8 * mi + gq) + SN * k], bv);
+          sdmma(acc[mi][0], acc[mi][1], Ls[(WR * warp + 8 * mi + gq) + LP * k], bv);
       }
 #pragma unroll
       for (int mi = 0; mi < MT; ++mi) {
@@ -833,7 +837,7 @@ __global__ void __launch_bounds__(SNT, 1)
         const double av = yr[gq + SB * k];
 #pragma unroll
         for (int ni = 0; ni < MT; ++ni)
-          sdmma(acc[ni][0], acc[ni][1], av, Ls[(WR * warp + 8 * ni + gq) + SN * k]);
+          sdmma(acc[ni][0], acc[ni][1], av, Ls[(WR * warp + 8 * ni + gq) + LP * k]);
       }
 #pragma unroll
       for (int ni = 0; ni < MT; ++ni)
@@ -946,8 +950,8 @@ bool small2d_expeuler(kp_ctx* ctx, const std::vector<int>& dims,
       const int dlt = ((c - i) % SN + SN) % SN;
       if (!(dlt == 0 || dlt == 1 || dlt == SN - 1)) return false;
     }
-  const size_t smem = sizeof(double) * (size_t(SN) * SN + size_t(SN) * (SB + 2) +
-                                        size_t(SN) * SB + 2ull * SB * SN) +
+  const size_t smem = sizeof(double) * (size_t(LP) * SN + size_t(SN) * (SB + 2) +
+                                        size_t(RP) * SB + 2ull * SB * SN) +
                       2 * SN * sizeof(BandRow<false>);
   static bool attr = false;
   if (!attr) {

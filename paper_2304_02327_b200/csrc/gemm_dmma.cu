@@ -180,6 +180,9 @@ using CfgF = TileCfg<64, 128, 2, 4, 4, 1, 128, 3>;
 using CfgG = TileCfg<64, 64, 2, 2, 4, 2, 64, 2>;
 // CfgE with a 5-deep ring
 using CfgE5 = TileCfg<128, 64, 4, 2, 5, 1, 64, 3>;
+// 64 x 32 / 32 x 64 tiles, 3-stage ring, 4 CTAs per SM (16 DMMA warps per SM)
+using CfgQ = TileCfg<64, 32, 2, 2, 3, 4>;
+using CfgR = TileCfg<32, 64, 2, 2, 3, 4>;
 
 // ------------------------------------------------------------ the kernel
 
@@ -615,6 +618,8 @@ void launch_gemm_dmma(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int 
     case 'F': launch_cplx<CfgF, false>(ctx, p, e, kcontig, cplx, half); break;
     case 'G': launch_cplx<CfgG, false>(ctx, p, e, kcontig, cplx, half); break;
     case 'H': launch_cplx<CfgE5, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'Q': launch_cplx<CfgQ, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'R': launch_cplx<CfgR, false>(ctx, p, e, kcontig, cplx, half); break;
     default: launch_cplx<CfgM, false>(ctx, p, e, kcontig, cplx, half); break;
   }
 }
