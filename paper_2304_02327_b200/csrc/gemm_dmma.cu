@@ -183,6 +183,9 @@ using CfgE5 = TileCfg<128, 64, 4, 2, 5, 1, 64, 3>;
 // 64 x 32 / 32 x 64 tiles, 3-stage ring, 4 CTAs per SM (16 DMMA warps per SM)
 using CfgQ = TileCfg<64, 32, 2, 2, 3, 4>;
 using CfgR = TileCfg<32, 64, 2, 2, 3, 4>;
+// 32 x 32 tiles with 2 epilogue warps, 3 CTAs per SM: small fused problems
+using CfgT = TileCfg<32, 32, 2, 2, 4, 3, 32, 2>;
+using CfgU = TileCfg<32, 64, 2, 2, 4, 3, 64, 2>;
 
 // ------------------------------------------------------------ the kernel
 
@@ -620,6 +623,8 @@ void launch_gemm_dmma(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int 
     case 'H': launch_cplx<CfgE5, false>(ctx, p, e, kcontig, cplx, half); break;
     case 'Q': launch_cplx<CfgQ, false>(ctx, p, e, kcontig, cplx, half); break;
     case 'R': launch_cplx<CfgR, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'T': launch_cplx<CfgT, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'U': launch_cplx<CfgU, false>(ctx, p, e, kcontig, cplx, half); break;
     default: launch_cplx<CfgM, false>(ctx, p, e, kcontig, cplx, half); break;
   }
 }
