@@ -48,6 +48,8 @@ struct NcclApi {
                                 cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -71,8 +73,9 @@ const NcclApi& nccl() {
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
     a.ReduceScatter = reinterpret_cast<decltype(a.ReduceScatter)>(sym("ncclReduceScatter"));
     a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(sym("ncclAllReduce"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(sym("ncclAllGather"));
     a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.GroupStart &&
-           a.GroupEnd && a.GetErrorString && a.ReduceScatter && a.AllReduce;
+           a.GroupEnd && a.GetErrorString && a.ReduceScatter && a.AllReduce && a.AllGather;
     if (!a.ok) a.why = "NCCL library lacks the point-to-point API";
     return a;
   }();
@@ -264,6 +267,12 @@ void comm_reduce_scatter(kp_ctx* ctx, kp_comm* c, const double* send, double* re
   nccl_check(need_nccl().ReduceScatter(send, recv, count, ncclFloat64, ncclSum, c->nc,
                                        ctx->stream),
              "ncclReduceScatter");
+}
+
+// recv = the P ranks' `bytes`-long send blocks, rank order (device buffers)
+void comm_allgather_bytes(kp_ctx* ctx, kp_comm* c, const void* send, void* recv, size_t bytes) {
+  nccl_check(need_nccl().AllGather(send, recv, bytes, ncclUint8, c->nc, ctx->stream),
+             "ncclAllGather");
 }
 
 // in place: x = op over ranks (op 0 min, 1 max), n doubles

@@ -199,6 +199,7 @@ void comm_sendrecv(kp_ctx* ctx, kp_comm* c, const std::vector<const double*>& se
 void comm_reduce_scatter(kp_ctx* ctx, kp_comm* c, const double* send, double* recv,
                          size_t count);
 void comm_allreduce(kp_ctx* ctx, kp_comm* c, double* x, size_t n, int op);
+void comm_allgather_bytes(kp_ctx* ctx, kp_comm* c, const void* send, void* recv, size_t bytes);
 
 // the whole exp-Euler loop of a 128 x 128 real state in one cluster launch
 // (banded.cu small2d_expeuler_kernel); false = not applicable

@@ -1040,6 +1040,65 @@ class ShardExchange {
       }
   }
 
+  // Peer mappings for the fused exchange (mode_d 3): all[r] = rank r's copy
+  // of a per-rank buffer as seen from this process.  Emulated: the local
+  // buffers themselves; NCCL: CUDA IPC handles all-gathered over the
+  // communicator and opened (NVLink P2P).  false = not mappable.
+  std::vector<void*> opened;
+  bool map(kp_ctx* ctx, const std::vector<double*>& local, std::vector<double*>& all,
+           void* dev_scratch) {
+    all.assign(P, nullptr);
+    if (!comm) {
+      for (int i = 0; i < nlocal(); ++i) all[ranks[i]] = local[i];
+      return true;
+    }
+    if (P == 1) {
+      all[0] = local[0];
+      return true;
+    }
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, local[0]) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    const size_t hb = sizeof(h);
+    unsigned char* d = static_cast<unsigned char*>(dev_scratch);
+    KP_CUDA(cudaMemcpyAsync(d, &h, hb, cudaMemcpyHostToDevice, ctx->stream));
+    comm_allgather_bytes(ctx, comm, d, d + hb, hb);
+    std::vector<unsigned char> hs(hb * P);
+    KP_CUDA(cudaMemcpyAsync(hs.data(), d + hb, hb * P, cudaMemcpyDeviceToHost, ctx->stream));
+    KP_CUDA(cudaStreamSynchronize(ctx->stream));
+    bool ok = true;
+    for (int r = 0; r < P; ++r) {
+      if (r == ranks[0]) {
+        all[r] = local[0];
+        continue;
+      }
+      cudaIpcMemHandle_t hr;
+      std::memcpy(&hr, hs.data() + hb * r, hb);
+      void* ptr = nullptr;
+      if (cudaIpcOpenMemHandle(&ptr, hr, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = false;
+        continue;
+      }
+      opened.push_back(ptr);
+      all[r] = static_cast<double*>(ptr);
+    }
+    // every rank must have mapped every peer (a max over ranks of "failed")
+    double bad = ok ? 0.0 : 1.0;
+    bad = max_over_ranks(ctx, bad, static_cast<double*>(dev_scratch));
+    return bad == 0.0;
+  }
+  // after peer stores: every rank's stores have landed before anyone reads
+  // (a one-double NCCL all-reduce, stream-ordered: no host sync)
+  void fence(kp_ctx* ctx, double* scratch) {
+    if (comm && P > 1) comm_allreduce(ctx, comm, scratch, 1, 1);
+  }
+  ~ShardExchange() {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+  }
+
   // max over all ranks of a host value (NCCL all-reduce through the device)
   double max_over_ranks(kp_ctx* ctx, double v, double* dev_scratch) {
     if (!comm || P == 1) return v;
@@ -1063,6 +1122,17 @@ class ShardedIntegrator {
   struct Rank {
     int r;
     double *u, *ub, *ext, *rr, *rp, *up, *sp, *dq, *dd, *t0, *t1, *w, *y, *part, *out, *tr;
+    // fused exchange (mode_d 3): state ping-pong, receive buffers per site
+    // and step parity, and the device arrays of the P ranks' copies
+    double* S[2] = {nullptr, nullptr};
+    double* pen[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    double* upb[2] = {nullptr, nullptr};
+    double* ddb[2] = {nullptr, nullptr};
+    double* const* pS[2] = {nullptr, nullptr};
+    double* const* ppen[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    double* const* pupb[2] = {nullptr, nullptr};
+    double* const* pddb[2] = {nullptr, nullptr};
+    double* const* part_arr = nullptr;  // staging for setup_fused
     int* cnt;  // [ctr slot 0, bad, ctr slot 1]
   };
   std::vector<Rank> R;
@@ -1106,6 +1176,53 @@ class ShardedIntegrator {
     owned.push_back(p);
     return p;
   }
+  bool fused_ready = false;
+  // allocate and map the fused exchange's buffers (all ranks must succeed)
+  bool setup_fused() {
+    if (fused_ready) return true;
+    if (!G.banded) return false;
+    double* scratch2 = nullptr;
+    KP_CUDA(cudaMalloc(&scratch2, 4096));
+    owned.push_back(scratch2);
+    auto site = [&](double* Rank::*one, double* const* Rank::*arr) -> bool {
+      std::vector<double*> loc;
+      for (auto& k : R) loc.push_back(k.*one);
+      std::vector<double*> all;
+      if (!X.map(ctx, loc, all, scratch2)) return false;
+      double** dev = nullptr;
+      KP_CUDA(cudaMalloc(&dev, sizeof(double*) * all.size()));
+      owned.push_back(reinterpret_cast<double*>(dev));
+      KP_CUDA(cudaMemcpyAsync(dev, all.data(), sizeof(double*) * all.size(),
+                              cudaMemcpyHostToDevice, ctx->stream));
+      for (auto& k : R) k.*arr = dev;
+      return true;
+    };
+    // member pointers cannot name array elements: map through staging members
+    bool ok = true;
+    for (int a = 0; a < 2 && ok; ++a) {
+      each([&](Rank& k) { k.S[a] = alloc(nloc); });
+      each([&](Rank& k) { k.tr = k.S[a]; });
+      ok = site(&Rank::tr, &Rank::part_arr);
+      each([&](Rank& k) { k.pS[a] = k.part_arr; });
+      for (int t = 0; t < 2 && ok; ++t) {
+        each([&](Rank& k) { k.pen[t][a] = alloc(nloc); k.tr = k.pen[t][a]; });
+        ok = site(&Rank::tr, &Rank::part_arr);
+        each([&](Rank& k) { k.ppen[t][a] = k.part_arr; });
+      }
+      if (!ok) break;
+      each([&](Rank& k) { k.upb[a] = alloc(nloc); k.tr = k.upb[a]; });
+      ok = site(&Rank::tr, &Rank::part_arr);
+      each([&](Rank& k) { k.pupb[a] = k.part_arr; });
+      if (!ok) break;
+      each([&](Rank& k) { k.ddb[a] = alloc(nloc); k.tr = k.ddb[a]; });
+      ok = site(&Rank::tr, &Rank::part_arr);
+      each([&](Rank& k) { k.pddb[a] = k.part_arr; });
+    }
+    each([&](Rank& k) { k.tr = alloc(nloc); });
+    fused_ready = ok;
+    return ok;
+  }
+
   void setup(int q, int md, const std::vector<double*>& user_u) {
     G.setup(q);
     for (const FactorSet* fs : {&G.f1, &G.f2}) {
@@ -1304,8 +1421,149 @@ class ShardedIntegrator {
     launch_fma(ctx, size_t(nloc) * comps, b, y, x, z);
   }
 
+  // ---- fused exchange (mode_d 3): the GEMM epilogues store every entry
+  // straight into its owner's buffer (peer memory over NVLink), so the
+  // re-partition overlaps the mode product tile by tile; plain re-partitions
+  // are a scatter kernel; a one-double NCCL all-reduce fences each exchange
+  // (emulated ranks: stream order).  Receive buffers alternate by step parity,
+  // so one fence per exchange also orders the next step's stores after this
+  // step's reads.
+  Epilogue scat(const Rank& k, int dir, double* const* peers) const {
+    Epilogue e;
+    e.sc_dir = dir;
+    e.sc_P = P;
+    e.sc_rank = k.r;
+    e.sc_A = unsigned(A);
+    e.sc_B = unsigned(B);
+    e.sc_C = unsigned(C);
+    e.sc_peers = peers;
+    return e;
+  }
+  void fence() { X.fence(ctx, scratch); }
+  // modes 0..ds-2 of a Tucker, the last of them scattering into the ranks'
+  // pencil buffers pen[t][par]
+  void tucker_to_pencil(const FactorSet& fs, int t, int par, const std::vector<const double*>& in) {
+    each([&](Rank& k) {
+      const double* cur = in[&k - R.data()];
+      for (int mu = 0; mu < ds - 1; ++mu) {
+        const bool last = (mu == ds - 2);
+        double* dst = (mu & 1) ? k.t1 : k.t0;
+        Epilogue e = last ? scat(k, 1, k.ppen[t][par]) : Epilogue{};
+        e.alpha = (mu == 0) ? fs.pref : 1.0;
+        G.mp(ctx, cur, dl, mu, fs.f[mu], dl[mu], e, dst);
+        cur = dst;
+      }
+    });
+    fence();
+  }
+  void step_fused(const std::vector<const double*>& u, int slot) {
+    const double tau = G.tau, t = 0.0;
+    const int par = slot, nxt = 1 - slot;
+    auto fin_of = [&](Rank& k) {
+      Epilogue f;
+      f.bad_step = k.cnt + 1;
+      f.step_ctr = k.cnt + (slot ? 2 : 0);
+      f.step_next = k.cnt + (slot ? 0 : 2);
+      return f;
+    };
+    auto last_mode = [&](const FactorSet& fs, int tk, Rank& k, Epilogue e, double* out) {
+      e.alpha = fs.fold * (ds == 1 ? fs.pref : 1.0);
+      G.mp(ctx, k.pen[tk][par], dp, ds - 1, fs.f[ds - 1], dp[ds - 1], e, out);
+    };
+    auto with_scat = [&](Epilogue e, Rank& k) {
+      const Epilogue sc = scat(k, 2, k.pS[nxt]);
+      e.sc_dir = sc.sc_dir;
+      e.sc_P = sc.sc_P;
+      e.sc_rank = sc.sc_rank;
+      e.sc_A = sc.sc_A;
+      e.sc_B = sc.sc_B;
+      e.sc_C = sc.sc_C;
+      e.sc_peers = sc.sc_peers;
+      return e;
+    };
+    switch (method) {
+      case KP_EXP_EULER:
+      case KP_ETD2RK: {
+        kronsum_g(u, mv(&Rank::rr), t);
+        each([&](Rank& k) {
+          scatter_copy(ctx, u[&k - R.data()], nloc, comps, scat(k, 1, k.pupb[par]));
+        });
+        tucker_to_pencil(G.f1, 0, par, cv(&Rank::rr));  // (fences the u scatter too)
+        if (method == KP_EXP_EULER) {
+          each([&](Rank& k) {
+            Epilogue f = fin_of(k);
+            f.kind = EPI_FMA_X;
+            f.X = k.upb[par];
+            f.gamma = tau;
+            last_mode(G.f1, 0, k, with_scat(f, k), k.out);
+          });
+          fence();
+          return;
+        }
+        const bool paired = S == 2;
+        each([&](Rank& k) {
+          Epilogue e;
+          e.X = k.upb[par];
+          e.gamma = tau;
+          e.g = G.g;
+          e.t = t;
+          e.t2 = t + tau;
+          if (paired) {
+            e.kind = EPI_FMA_X;
+          } else {
+            e.kind = EPI_STAGE_D;
+            e.D = k.dq;
+          }
+          last_mode(G.f1, 0, k, e, k.sp);
+          if (paired) gdiff(k.sp, k.upb[par], k.dq, t);
+          scatter_copy(ctx, k.dq, nloc, comps, scat(k, 2, k.pddb[par]));
+        });
+        fence();
+        std::vector<const double*> dd;
+        for (auto& k : R) dd.push_back(k.ddb[par]);
+        tucker_to_pencil(G.f2, 1, par, dd);
+        each([&](Rank& k) {
+          Epilogue f = fin_of(k);
+          f.kind = EPI_FMA_X;
+          f.X = k.sp;
+          f.gamma = tau;
+          last_mode(G.f2, 1, k, with_scat(f, k), k.out);
+        });
+        fence();
+        return;
+      }
+      case KP_LAWSON_EULER:
+      case KP_LAWSON2B: {
+        const bool two = method == KP_LAWSON2B;
+        each([&](Rank& k) { pre(u[&k - R.data()], k.w, two, t); });
+        if (!two) {
+          tucker_to_pencil(G.f1, 0, par, cv(&Rank::w));
+          each([&](Rank& k) { last_mode(G.f1, 0, k, with_scat(fin_of(k), k), k.out); });
+          fence();
+          return;
+        }
+        tucker_to_pencil(G.f1, 0, par, cv(&Rank::w));
+        tucker_to_pencil(G.f1, 1, par, cv(&Rank::w, nloc * comps));
+        each([&](Rank& k) {
+          last_mode(G.f1, 0, k, Epilogue{}, k.sp);
+          last_mode(G.f1, 1, k, Epilogue{}, k.sp + nloc * comps);
+          post(k.sp, k.out, k.cnt + 1, k.cnt + (slot ? 2 : 0), t + tau, k.cnt + (slot ? 0 : 2));
+          scatter_copy(ctx, k.out, nloc, comps, scat(k, 2, k.pS[nxt]));
+        });
+        fence();
+        return;
+      }
+      default:
+        throw invalid_argument("sharded integrate: unsupported method");
+    }
+  }
+
   // one step: u[i] -> o[i] (slab).  slot = counter slot of this step.
   void step(const std::vector<const double*>& u, const std::vector<double*>& o, int slot) {
+    if (mode_d == 3) {  // the output lands in the ranks' S[1 - slot] (o is S[1 - slot])
+      step_fused(u, slot);
+      return;
+    }
     const double tau = G.tau, t = 0.0;
     auto fin_of = [&](Rank& k) {
       Epilogue f;
@@ -1453,6 +1711,21 @@ class ShardedIntegrator {
   double run(long n_steps, bool use_graph) {
     std::vector<const double*> cu[2] = {cv(&Rank::u), cv(&Rank::ub)};
     std::vector<double*> mu_[2] = {mv(&Rank::u), mv(&Rank::ub)};
+    if (mode_d == 3) {  // the state lives in the peer-mapped S buffers
+      each([&](Rank& k) {
+        KP_CUDA(cudaMemcpyAsync(k.S[0], k.u, size_t(nloc) * comps * 8, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+      });
+      fence();
+      for (int a = 0; a < 2; ++a) {
+        cu[a].clear();
+        mu_[a].clear();
+        for (auto& k : R) {
+          cu[a].push_back(k.S[a]);
+          mu_[a].push_back(k.S[a]);
+        }
+      }
+    }
     cudaEvent_t ev[4];
     for (auto& e : ev) KP_CUDA(cudaEventCreate(&e));
     long n = 0;
@@ -1501,7 +1774,12 @@ class ShardedIntegrator {
     }
     KP_CUDA(cudaEventRecord(ev[3], ctx->stream));
     if (exec) cudaGraphExecDestroy(exec);
-    if (n_steps & 1)
+    if (mode_d == 3)
+      each([&](Rank& k) {
+        KP_CUDA(cudaMemcpyAsync(k.u, k.S[n_steps & 1], size_t(nloc) * comps * 8,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+      });
+    else if (n_steps & 1)
       each([&](Rank& k) {
         KP_CUDA(cudaMemcpyAsync(k.u, k.ub, size_t(nloc) * comps * 8, cudaMemcpyDeviceToDevice,
                                 ctx->stream));
@@ -1534,14 +1812,19 @@ class ShardedIntegrator {
   // mode_d = 0: one step of each kind on scratch copies of the state, the
   // faster (device time, max over ranks) is used for the run
   void choose_mode_d(int requested) {
-    if (requested == 1 || requested == 2 || P == 1) {
-      mode_d = (P == 1) ? 1 : requested;
+    if (requested == 3 && !setup_fused())
+      throw invalid_argument("sharded integrate: the fused exchange needs peer-mappable "
+                             "buffers and banded factors");
+    if (requested == 1 || requested == 2 || requested == 3 || P == 1) {
+      mode_d = (P == 1 && requested != 3) ? 1 : requested;
       if (requested == 0) mode_d = 1;
       return;
     }
     double best = 1e300;
     int pick = 1;
-    for (int md : {1, 2}) {
+    std::vector<int> cand = {1, 2};
+    if (setup_fused()) cand.push_back(3);
+    for (int md : cand) {
       mode_d = md;
       if (md == 2)
         each([&](Rank& k) {
@@ -1923,7 +2206,7 @@ int sharded_impl(kp_ctx* ctx, kp_comm* comm, int P_local, bool cplx, int method,
         if (n_steps <= 0) throw invalid_argument("integrate: n_steps must be positive");
         if (!(t_final > t0)) throw invalid_argument("integrate: empty time interval");
         if (!as || !g || !u) throw invalid_argument("integrate_sharded: null argument");
-        if (mode_d < 0 || mode_d > 2) throw invalid_argument("integrate_sharded: mode_d 0/1/2");
+        if (mode_d < 0 || mode_d > 3) throw invalid_argument("integrate_sharded: mode_d 0..3");
         StreamScope scope(ctx);
         ShardExchange X;
         if (comm) {

@@ -774,7 +774,7 @@ def sharded_integrate(kp, backend, comm, method, u_local, dims_local, K, g, t0, 
 
 # ------------------------------------------- the native sharded integrator
 
-MODE_D = {"auto": 0, "alltoall": 1, "reduce_scatter": 2}
+MODE_D = {"auto": 0, "alltoall": 1, "reduce_scatter": 2, "fused": 3}
 
 
 def native_sharded_integrate(kp, method, u_slabs, dims_local, K, g, t0, t_final, n_steps,
