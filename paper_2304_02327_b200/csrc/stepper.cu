@@ -1180,7 +1180,8 @@ class ShardedIntegrator {
   // allocate and map the fused exchange's buffers (all ranks must succeed)
   bool setup_fused() {
     if (fused_ready) return true;
-    if (!G.banded) return false;
+    // the Kronecker sum's last mode runs as the halo stencil (no pencil term)
+    if ((method == KP_EXP_EULER || method == KP_ETD2RK) && !G.banded) return false;
     double* scratch2 = nullptr;
     KP_CUDA(cudaMalloc(&scratch2, 4096));
     owned.push_back(scratch2);
