@@ -572,12 +572,17 @@ def main_sharded(args, rank, world, local, dist, kp, ctx, stream):
     with ClockSampler(local) as clk:
         ms_a = timed(1, args.steps)
         ms_b = timed(2, args.steps)
-    md_best = 1 if ms_a <= ms_b else 2
+        try:  # fused: mode 2's epilogue stores straight into the owners' pencils
+            ms_f = timed(3, args.steps)
+        except Exception as ex:
+            sys.stderr.write(f"fused exchange unavailable: {ex!r}\n")
+            ms_f = float("inf")
+    md_best = min(((ms_a, 1), (ms_b, 2), (ms_f, 3)))[1]
     l0 = ctx.launches
     step(md_best)
     torch.cuda.synchronize()
     launches = (ctx.launches - l0) * args.steps
-    ms = min(ms_a, ms_b)
+    ms = min(ms_a, ms_b, ms_f)
     fl = flops_per_tucker(n)
     value = fl / (ms * 1e-3) / 1e9
     achieved = fl / P / (ms * 1e-3) / 1e12  # per GPU
@@ -613,9 +618,12 @@ def main_sharded(args, rank, world, local, dist, kp, ctx, stream):
                 "config": dict(config(n, world), parallelism=f"slab{P} (mode 3 sharded)",
                                workload=f"tucker_d3_n{n}_sharded"),
                 "sharded": {"mode_d_alltoall_ms": ms_a, "mode_d_reduce_scatter_ms": ms_b,
-                            "chosen": "all-to-all pencil transpose" if md_best == 1 else
-                            "partial products + reduce-scatter",
-                            "output_layout": "pencil" if md_best == 1 else "slab"},
+                            "mode_d_fused_peer_store_ms": ms_f if ms_f != float("inf") else None,
+                            "chosen": {1: "all-to-all pencil transpose (NCCL)",
+                                       2: "partial products + reduce-scatter (NCCL)",
+                                       3: "fused: GEMM epilogue stores into the owners' "
+                                          "pencils over peer memory"}[md_best],
+                            "output_layout": "slab" if md_best == 2 else "pencil"},
                 "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                              "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
                              "peak_source": "live DMMA m8n8k4 micro-benchmark on this GPU",

@@ -425,7 +425,9 @@ int kp_integrate_sharded_local_c128(kp_ctx* ctx, int P, int method, double* cons
  * square, full factors).  Modes 1..d-1 on the slab; mode d across the slabs:
  * mode_d 1 = all-to-all, result in the PENCIL layout (n_1 .. n_(d-1)/P x n_d,
  * bitwise the rank's block of the single-GPU result); 2 = partial products +
- * reduce-scatter, result in the SLAB layout. */
+ * reduce-scatter, result in the SLAB layout; 3 = fused: mode d-1's GEMM
+ * epilogue stores every entry straight into its owner's pencil buffer (peer
+ * memory, CUDA IPC over NVLink; mappings cached), result as for 1. */
 int kp_tucker_sharded_f64(kp_ctx* ctx, kp_comm* comm, const double* t_slab,
                           const int* dims_local, int d, const double* const* ms,
                           double prefactor, int mode_d, double* out);

@@ -23,6 +23,9 @@
 // divergence is detected on the device (epilogue atomicMin of the step
 // counter) and reported with the reference's message and step index.
 #include <climits>
+#include <map>
+#include <memory>
+#include <tuple>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -2301,7 +2304,7 @@ int tucker_sharded_impl(kp_ctx* ctx, kp_comm* comm, int P_local, const double* c
     auto dl = dims_of(dims, d, "tucker_sharded");
     if (d < 2) throw invalid_argument("tucker_sharded: needs order >= 2");
     if (!t || !ms || !out) throw invalid_argument("tucker_sharded: null argument");
-    if (mode_d != 1 && mode_d != 2) throw invalid_argument("tucker_sharded: mode_d 1 or 2");
+    if (mode_d < 1 || mode_d > 3) throw invalid_argument("tucker_sharded: mode_d 1, 2 or 3");
     ShardExchange X;
     X.wctx = ctx;
     if (comm) {
@@ -2322,17 +2325,72 @@ int tucker_sharded_impl(kp_ctx* ctx, kp_comm* comm, int P_local, const double* c
     std::vector<int> dp = dl;
     dp[d - 2] = int(B / P);
     dp[d - 1] = int(C);
+    // mode_d 3 (fused): mode d-1's epilogue stores every entry straight into
+    // its owner's pencil buffer (peer memory); the mappings are cached per
+    // (context, communicator, buffer)
+    double* const* peers = nullptr;
+    std::vector<double*> pbuf;
+    if (mode_d == 3) {
+      for (int i = 0; i < X.nlocal(); ++i)
+        pbuf.push_back(static_cast<double*>(ctx->ws.get(144 + i, size_t(n) * 8)));
+      struct Key {
+        kp_ctx* c;
+        kp_comm* m;
+        double* p;
+        size_t n;
+        bool operator<(const Key& o) const {
+          return std::tie(c, m, p, n) < std::tie(o.c, o.m, o.p, o.n);
+        }
+      };
+      static std::map<Key, std::pair<double**, std::shared_ptr<ShardExchange>>> cache;
+      const Key key{ctx, comm, pbuf[0], size_t(n)};
+      auto it = cache.find(key);
+      if (it == cache.end()) {
+        auto keep = std::make_shared<ShardExchange>();
+        keep->P = X.P;
+        keep->comm = X.comm;
+        keep->ranks = X.ranks;
+        double* scr = static_cast<double*>(ctx->ws.get(176, 4096));
+        std::vector<double*> all;
+        if (!keep->map(ctx, pbuf, all, scr))
+          throw invalid_argument("tucker_sharded: peer buffers cannot be mapped");
+        double** dev = nullptr;
+        KP_CUDA(cudaMalloc(&dev, sizeof(double*) * all.size()));
+        KP_CUDA(cudaMemcpyAsync(dev, all.data(), sizeof(double*) * all.size(),
+                                cudaMemcpyHostToDevice, ctx->stream));
+        it = cache.emplace(key, std::make_pair(dev, keep)).first;
+      }
+      peers = it->second.first;
+    }
     std::vector<const double*> mid;
     for (int i = 0; i < X.nlocal(); ++i) {
       const double* cur = t[i];
       for (int mu = 0; mu < d - 1; ++mu) {
         double* dst = static_cast<double*>(ctx->ws.get(112 + 2 * i + (mu & 1), size_t(n) * 8));
         Epilogue e;
+        if (mode_d == 3 && mu == d - 2) {
+          e.sc_dir = 1;
+          e.sc_P = P;
+          e.sc_rank = X.ranks[i];
+          e.sc_A = unsigned(A);
+          e.sc_B = unsigned(B);
+          e.sc_C = unsigned(C);
+          e.sc_peers = peers;
+        }
         e.alpha = (mu == 0) ? pref : 1.0;
         mode_product_f64(ctx, cur, dl, mu, ms[mu], dl[mu], e, dst);
         cur = dst;
       }
       mid.push_back(cur);
+    }
+    if (mode_d == 3) {
+      double* scr = static_cast<double*>(ctx->ws.get(177, 64));
+      X.fence(ctx, scr);
+      for (int i = 0; i < X.nlocal(); ++i) {
+        Epilogue e;
+        mode_product_f64(ctx, pbuf[i], P > 1 ? dp : dl, d - 1, ms[d - 1], int(C), e, out[i]);
+      }
+      return;
     }
     if (mode_d == 1) {
       std::vector<const double*> pen = mid;

@@ -158,7 +158,7 @@ def test_native_sharded_nccl_world1_bitwise(kp, name, method):
 
 
 @pytest.mark.parametrize("P", [1, 2, 4])
-@pytest.mark.parametrize("mode_d", [1, 2])
+@pytest.mark.parametrize("mode_d", [1, 2, 3])
 def test_tucker_sharded_local(kp, P, mode_d):
     """kp_tucker_sharded_local_f64: mode 1 (all-to-all) gives each rank its
     pencil block of the single-GPU Tucker bitwise; mode 2 (reduce-scatter)
@@ -184,7 +184,7 @@ def test_tucker_sharded_local(kp, P, mode_d):
     torch.cuda.synchronize()
     for k, o in enumerate(outs):
         flat = kp.to_host(o).reshape(-1, order="F")
-        if mode_d == 1:  # pencil: (n1, n2/P, n3)
+        if mode_d in (1, 3):  # pencil: (n1, n2/P, n3)
             blk = np.asfortranarray(want[:, k * n2 // P:(k + 1) * n2 // P, :])
             assert np.array_equal(flat, blk.reshape(-1, order="F"))
         else:            # slab: (n1, n2, n3/P)
