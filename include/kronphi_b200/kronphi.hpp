@@ -1515,7 +1515,9 @@ class Communicator {
 };
 
 // How the last mode crosses the slabs in a sharded integrate (kp_integrate_sharded_*).
-enum class ModeD { Measure = 0, AllToAll = 1, ReduceScatter = 2 };
+// Fused: the mode products' epilogues store each entry straight into its
+// owner's buffer over peer memory (CUDA IPC mappings exchanged over NCCL).
+enum class ModeD { Measure = 0, AllToAll = 1, ReduceScatter = 2, Fused = 3 };
 
 // integrate() slab-sharded over `comm`'s ranks: p.u0 is this
 // rank's slab (the last spatial mode holds n_d / P planes, a stacked
