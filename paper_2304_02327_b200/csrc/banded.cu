@@ -339,8 +339,10 @@ __device__ __forceinline__ void row_combine(const BandRow<true>& rw, const doubl
 // (z-chunk <= ZMAX) are decoded once into shared memory.
 constexpr int ZMAX = 32;
 
-template <bool CPLX, bool PAIR, bool M3>
-__global__ void __launch_bounds__(256, (CPLX || PAIR) ? 3 : 4)
+// SMR (v5, KP_BAND=v5): the block's mode-0 / mode-1 rows in shared memory
+// instead of registers (fewer registers per thread, more resident warps)
+template <bool CPLX, bool PAIR, bool M3, bool SMR = false>
+__global__ void __launch_bounds__(256, SMR ? ((CPLX || PAIR) ? 4 : 6) : ((CPLX || PAIR) ? 3 : 4))
     kronsum_band2_kernel(BandArgs b, int nz, int zchunk, const double* __restrict__ u,
                          double* __restrict__ r, bool with_g, kp_gfun g, double t) {
   pdl_wait();
@@ -355,13 +357,20 @@ __global__ void __launch_bounds__(256, (CPLX || PAIR) ? 3 : 4)
     const int z = z0 + tid;
     load_row(b, 2, PAIR ? z : z % b.n[2], rows2[tid]);
   }
-  __syncthreads();
   const int i0 = blockIdx.x * 32 + threadIdx.x;
   const int i1 = blockIdx.y * 8 + threadIdx.y;
+  __shared__ BandRow<CPLX> rows0s[SMR ? 32 : 1], rows1s[SMR ? 8 : 1];
+  if constexpr (SMR) {
+    if (threadIdx.y == 0 && b.active[0] && i0 < b.n[0]) load_row(b, 0, i0, rows0s[threadIdx.x]);
+    if (threadIdx.x == 0 && b.active[1] && i1 < b.n[1]) load_row(b, 1, i1, rows1s[threadIdx.y]);
+  }
+  __syncthreads();
   if (i0 >= b.n[0] || i1 >= b.n[1]) return;
-  BandRow<CPLX> r0, r1;
-  if (b.active[0]) load_row(b, 0, i0, r0);
-  if (b.active[1]) load_row(b, 1, i1, r1);
+  BandRow<CPLX> r0l, r1l;
+  if (!SMR && b.active[0]) load_row(b, 0, i0, r0l);
+  if (!SMR && b.active[1]) load_row(b, 1, i1, r1l);
+  const BandRow<CPLX>& r0 = SMR ? rows0s[threadIdx.x] : r0l;
+  const BandRow<CPLX>& r1 = SMR ? rows1s[threadIdx.y] : r1l;
   const int h2 = b.slab == 2 ? b.halo : 0, h3 = b.slab == 3 ? b.halo : 0;
   const unsigned in01 = unsigned(i0 + (b.slab == 0 ? b.halo : 0)) * unsigned(b.stride[0]) +
                         unsigned(i1 + (b.slab == 1 ? b.halo : 0)) * unsigned(b.stride[1]);
@@ -1080,12 +1089,8 @@ bool small2d_expeuler(kp_ctx* ctx, const std::vector<int>& dims,
   const size_t smem = sizeof(double) * (size_t(LP) * SN + size_t(SN) * (SB + 2) +
                                         size_t(RP) * SB + 2ull * SB * SN) +
                       2 * SN * sizeof(BandRow<false>);
-  static bool attr = false;
-  if (!attr) {
-    KP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    KP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr = true;
-  }
+  ensure_smem_attr(ctx, reinterpret_cast<const void*>(kern), int(smem));  // per device
+  KP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(SJ);
   cfg.blockDim = dim3(SNT);
@@ -1232,7 +1237,18 @@ void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<i
       launch_pdl(ctx, kern, grid, dim3(32, 8), 0, b2, nz, zchunk, u, r, with_g, g, t);
       ctx->launches--;  // counted once below
     };
-    if (cplx) {
+    static const bool v5 = [] {
+      const char* v = getenv("KP_BAND");
+      return v && std::string(v) == "v5";
+    }();
+    if (v5 && !m3) {
+      if (cplx)
+        go(kronsum_band2_kernel<true, false, false, true>);
+      else if (pair)
+        go(kronsum_band2_kernel<false, true, false, true>);
+      else
+        go(kronsum_band2_kernel<false, false, false, true>);
+    } else if (cplx) {
       m3 ? go(kronsum_band2_kernel<true, false, true>) : go(kronsum_band2_kernel<true, false, false>);
     } else if (pair) {
       m3 ? go(kronsum_band2_kernel<false, true, true>) : go(kronsum_band2_kernel<false, true, false>);

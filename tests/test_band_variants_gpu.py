@@ -1,5 +1,6 @@
 """The banded Kronecker-sum kernels (banded.cu): the default v2 line march,
-the TMA plane ring v3 and the register z line v4 (opt-in, KP_BAND) give
+the TMA plane ring v3, the register z line v4 and v2 with its rows in shared
+memory v5 (opt-in, KP_BAND) give
 BIT-IDENTICAL Kronecker sums and integrations (same values into the same row
 chains).  One process per variant (the switch is read once)."""
 import os
@@ -21,6 +22,6 @@ def probe(env_extra):
     return r.stdout.split()
 
 
-@pytest.mark.parametrize("variant", ["v3", "v4"])
+@pytest.mark.parametrize("variant", ["v3", "v4", "v5"])
 def test_band_variant_bitwise(variant):
     assert probe({"KP_BAND": variant}) == probe({})
