@@ -154,38 +154,24 @@ struct TileCfg {
   static_assert(NE == 0 || SC == BN, "epilogue warps take the whole staged tile");
 };
 
-// 64 x 64 tiles, 4 consumer warps of 32 x 32, 2 CTAs per SM: the default
-using CfgM = TileCfg<64, 64, 2, 2, 4, 2>;
-// 64 x 64 tiles, 3-stage ring, the epilogue staged in two 32-column passes:
-// 3 CTAs per SM (12 consumer warps)
-using CfgN = TileCfg<64, 64, 2, 2, 3, 3, 32>;
-// 128 x 64 tiles, 8 consumer warps of 32 x 32, one CTA per SM
-using CfgW = TileCfg<128, 64, 4, 2, 4, 1>;
-// 64 x 64 tiles, 8 consumer warps of 32 x 16 / 16 x 32, 2 CTAs per SM (4
-// consumer warps per SM sub-partition)
-using CfgA = TileCfg<64, 64, 2, 4, 4, 2>;
-using CfgB = TileCfg<64, 64, 4, 2, 4, 2>;
-// 32 x 64 tiles, 4 warps of 16 x 32
-using CfgC = TileCfg<32, 64, 2, 2, 4, 4>;
-// 32 x 32 tiles, 4 warps of 16 x 16: problems that would leave SMs idle
-using CfgS = TileCfg<32, 32, 2, 2, 4, 3>;
-// 128 x 64 tiles, 4 warps of 64 x 32: long-K problems (d = 2, n >= 1024)
-using CfgL = TileCfg<128, 64, 2, 2, 4, 1>;
-// one CTA per SM, 8 DMMA warps of 32 x 32 + 3 epilogue warps + the producer:
-// the fused epilogue of tile t runs on its own warps while the DMMA warps
-// already compute tile t+1
-using CfgE = TileCfg<128, 64, 4, 2, 4, 1, 64, 3>;
-using CfgF = TileCfg<64, 128, 2, 4, 4, 1, 128, 3>;
-// two CTAs per SM of 4 DMMA warps + 2 epilogue warps + the producer
+// The tile menu (measured; profiles/ncu_r02_summary.md).
+// G: 64 x 64 tiles, 4 DMMA warps of 32 x 32 + 2 epilogue warps + the
+//    producer, 2 CTAs per SM -- plain products with K > 256 (the headline)
 using CfgG = TileCfg<64, 64, 2, 2, 4, 2, 64, 2>;
-// CfgE with a 5-deep ring
-using CfgE5 = TileCfg<128, 64, 4, 2, 5, 1, 64, 3>;
-// 64 x 32 / 32 x 64 tiles, 3-stage ring, 4 CTAs per SM (16 DMMA warps per SM)
-using CfgQ = TileCfg<64, 32, 2, 2, 3, 4>;
-using CfgR = TileCfg<32, 64, 2, 2, 3, 4>;
-// 32 x 32 tiles with 2 epilogue warps, 3 CTAs per SM: small fused problems
-using CfgT = TileCfg<32, 32, 2, 2, 4, 3, 32, 2>;
-using CfgU = TileCfg<32, 64, 2, 2, 4, 3, 64, 2>;
+// N: 64 x 64, 3-stage ring, inline epilogue in two 32-column passes, 3 CTAs
+//    per SM -- plain products with K <= 256
+using CfgN = TileCfg<64, 64, 2, 2, 3, 3, 32>;
+// M: 64 x 64, 4 stages, inline epilogue, 2 CTAs per SM -- the fused-scatter
+//    (peer store) epilogues of the sharded path
+using CfgM = TileCfg<64, 64, 2, 2, 4, 2>;
+// S: 32 x 32, 4 warps of 16 x 16 -- small problems and FP64-heavy fused
+//    epilogues at short K (the integrators)
+using CfgS = TileCfg<32, 32, 2, 2, 4, 3>;
+// L: 128 x 64, 4 warps of 64 x 32, one CTA per SM (KP_GEMM_TILE=L)
+using CfgL = TileCfg<128, 64, 2, 2, 4, 1>;
+// (measured and dropped: 128x64 / 64x128 with 8 DMMA + 3 epilogue warps at 1
+// CTA/SM, 64x64 with 8 DMMA warps of 32x16 / 16x32, 64x32 / 32x64 at 4
+// CTAs/SM, 32x32 / 32x64 with epilogue warps: all at or below G / N / S)
 
 // ------------------------------------------------------------ the kernel
 
@@ -611,21 +597,10 @@ void launch_gemm_dmma(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int 
   }
   switch (cfg) {
     case 'S': launch_cplx<CfgS, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'L': launch_cplx<CfgL, false>(ctx, p, e, kcontig, cplx, half); break;
     case 'N': launch_cplx<CfgN, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'W': launch_cplx<CfgW, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'A': launch_cplx<CfgA, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'B': launch_cplx<CfgB, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'C': launch_cplx<CfgC, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'E': launch_cplx<CfgE, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'F': launch_cplx<CfgF, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'G': launch_cplx<CfgG, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'H': launch_cplx<CfgE5, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'Q': launch_cplx<CfgQ, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'R': launch_cplx<CfgR, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'T': launch_cplx<CfgT, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'U': launch_cplx<CfgU, false>(ctx, p, e, kcontig, cplx, half); break;
-    default: launch_cplx<CfgM, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'M': launch_cplx<CfgM, false>(ctx, p, e, kcontig, cplx, half); break;
+    case 'L': launch_cplx<CfgL, false>(ctx, p, e, kcontig, cplx, half); break;
+    default: launch_cplx<CfgG, false>(ctx, p, e, kcontig, cplx, half); break;
   }
 }
 
