@@ -53,6 +53,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "kp_epilogue.cuh"
 #include "kp_launch.cuh"
@@ -590,18 +591,22 @@ void launch_gemm_dmma(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int 
   else if (p.K <= 256)
     cfg = 'N';
   if (forced) cfg = forced;
-  if (e.sc_dir) {
-    cfg == 'S' ? launch_cplx<CfgS, true>(ctx, p, e, kcontig, cplx, half)
-               : launch_cplx<CfgM, true>(ctx, p, e, kcontig, cplx, half);
-    return;
-  }
-  switch (cfg) {
-    case 'S': launch_cplx<CfgS, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'N': launch_cplx<CfgN, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'M': launch_cplx<CfgM, false>(ctx, p, e, kcontig, cplx, half); break;
-    case 'L': launch_cplx<CfgL, false>(ctx, p, e, kcontig, cplx, half); break;
-    default: launch_cplx<CfgG, false>(ctx, p, e, kcontig, cplx, half); break;
-  }
+  // the fused exchange's peer-store epilogues take the same menu (the
+  // epilogue warps of G overlap the scattered stores with the mainloop)
+  auto go = [&](auto scat) {
+    constexpr bool SC = decltype(scat)::value;
+    switch (cfg) {
+      case 'S': launch_cplx<CfgS, SC>(ctx, p, e, kcontig, cplx, half); break;
+      case 'N': launch_cplx<CfgN, SC>(ctx, p, e, kcontig, cplx, half); break;
+      case 'M': launch_cplx<CfgM, SC>(ctx, p, e, kcontig, cplx, half); break;
+      case 'L': launch_cplx<CfgL, SC>(ctx, p, e, kcontig, cplx, half); break;
+      default: launch_cplx<CfgG, SC>(ctx, p, e, kcontig, cplx, half); break;
+    }
+  };
+  if (e.sc_dir)
+    go(std::true_type{});
+  else
+    go(std::false_type{});
 }
 
 }  // namespace kp
