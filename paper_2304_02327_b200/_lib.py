@@ -11,7 +11,9 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libkronphi_b200.so")
+# KP_LIB: another build of the same library (A/B measurements of two builds
+# on one GPU box); the default is the in-tree build
+LIB_PATH = os.environ.get("KP_LIB") or os.path.join(HERE, "lib", "libkronphi_b200.so")
 
 KP_OK, KP_EINVAL, KP_ERUNTIME, KP_EDIVERGE, KP_ECUDA = range(5)
 LAWSON_EULER, LAWSON2B, EXP_EULER, EXP_EULER_LS, ETD2RK = range(5)

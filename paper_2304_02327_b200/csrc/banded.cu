@@ -765,6 +765,117 @@ __global__ void __launch_bounds__(256, (CPLX || PAIR) ? 2 : 3)
   }
 }
 
+// ---- v6: v2's march with a lean per-plane loop (the default) ----
+// v2's traversal and arithmetic exactly (bit-identical), restricted to the
+// configs' shapes -- z runs over mode 2 only (order <= 3, or the 2-species
+// pair in slot 3 with no factor on it) -- so the per-plane loop carries no
+// index division, no mode-3 row, and its rows by value (v2's conditional
+// row references cost local-memory round trips and shared-memory address
+// rebuilds every plane: 116 SASS instructions per entry on AC3D, ncu
+// source page).  Two planes per iteration keep both planes' loads in flight.
+template <bool CPLX, bool PAIR>
+__global__ void __launch_bounds__(256, (CPLX || PAIR) ? 2 : 4)
+    kronsum_band6_kernel(BandArgs b, int nz, int zchunk, const double* __restrict__ u,
+                         double* __restrict__ r, bool with_g, kp_gfun g, double t) {
+  pdl_wait();
+  using T = typename std::conditional<CPLX, double2, double>::type;
+  __shared__ BandRow<CPLX> rows2[ZMAX];
+  const T* __restrict__ ut = reinterpret_cast<const T*>(u);
+  T* __restrict__ rt = reinterpret_cast<T*>(r);
+  const int z0 = blockIdx.z * zchunk;
+  const int z1 = min(nz, z0 + zchunk);
+  const int tid = threadIdx.x + 32 * threadIdx.y;
+  const bool a0 = b.active[0], a1 = b.active[1], a2 = b.active[2];
+  if (a2 && tid < z1 - z0) load_row(b, 2, z0 + tid, rows2[tid]);
+  __syncthreads();
+  const int i0 = blockIdx.x * 32 + threadIdx.x;
+  const int i1 = blockIdx.y * 8 + threadIdx.y;
+  if (i0 >= b.n[0] || i1 >= b.n[1]) return;
+  BandRow<CPLX> r0, r1;
+  if (a0) load_row(b, 0, i0, r0);
+  if (a1) load_row(b, 1, i1, r1);
+  const int h2 = b.slab == 2 ? b.halo : 0, h3 = b.slab == 3 ? b.halo : 0;
+  const unsigned st2 = unsigned(b.stride[2]), st3 = unsigned(b.stride[3]);
+  const unsigned in01 = unsigned(i0 + (b.slab == 0 ? b.halo : 0)) * unsigned(b.stride[0]) +
+                        unsigned(i1 + (b.slab == 1 ? b.halo : 0)) * unsigned(b.stride[1]) +
+                        unsigned(h2) * st2 + unsigned(h3) * st3;
+  const unsigned plane = unsigned(b.n[0]) * unsigned(b.n[1]);
+  const unsigned out01 = unsigned(i0) + unsigned(i1) * unsigned(b.n[0]);
+  const unsigned sp_out = unsigned(b.n[2]) * plane;  // species 1 output offset (PAIR)
+  auto entry = [&](unsigned in, const BandRow<CPLX>& q2) -> T {
+    T x0[3], x1[3], x2[3];
+    if (a0) row_gather(r0, ut, in, x0);
+    if (a1) row_gather(r1, ut, in, x1);
+    if (a2) row_gather(q2, ut, in, x2);
+    T c;
+    if constexpr (CPLX)
+      c = make_double2(0.0, 0.0);
+    else
+      c = 0.0;
+    if (a0) row_combine(r0, x0, c);
+    if (a1) row_combine(r1, x1, c);
+    if (a2) row_combine(q2, x2, c);
+    return c;
+  };
+#pragma unroll 1
+  for (int z = z0; z < z1; ++z) {
+    const BandRow<CPLX> q2 = rows2[z - z0];
+    const unsigned in0 = in01 + unsigned(z) * st2;
+    const unsigned idx0 = out01 + unsigned(z) * plane;
+    if constexpr (PAIR) {
+      const unsigned in1 = in0 + st3, idx1 = idx0 + sp_out;
+      const T c0 = entry(in0, q2);
+      const T c1 = entry(in1, q2);
+      if (with_g) {
+        const double u0 = ut[in0], u1 = ut[in1];
+        rt[idx0] = __dadd_rn(c0, g_real(g, u0, u1, false, idx0, t));
+        rt[idx1] = __dadd_rn(c1, g_real(g, u1, u0, true, idx1, t));
+      } else {
+        rt[idx0] = c0;
+        rt[idx1] = c1;
+      }
+    } else {
+      const T c = entry(in0, q2);
+      if (!with_g) {
+        rt[idx0] = c;
+      } else if constexpr (CPLX) {
+        const double2 gg = g_cplx(g, ut[in0]);
+        rt[idx0] = make_double2(__dadd_rn(c.x, gg.x), __dadd_rn(c.y, gg.y));
+      } else {
+        rt[idx0] = __dadd_rn(c, g_real(g, ut[in0], 0.0, false, idx0, t));
+      }
+    }
+  }
+}
+
+// v6 launcher; false = not applicable (KP_BAND=v2 forces the v2 kernel)
+bool launch_band6(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz, int zchunk,
+                  dim3 grid, const double* u, double* r, bool with_g, const kp_gfun& g,
+                  double t) {
+  // default for real single-species tensors; the complex and species-pair
+  // forms are opt-in (KP_BAND=v6): at the register budget their two-value
+  // entries need (2 blocks/SM) they measured slower than v2 (NLS 512^3 1.85
+  // vs 1.63 ms)
+  static const int mode = [] {
+    const char* v = getenv("KP_BAND");
+    if (!v || !*v) return 1;
+    return std::string(v) == "v6" ? 2 : 0;
+  }();
+  if (mode == 0 || b2.active[3] || (!pair && b2.n[3] != 1)) return false;
+  if (mode == 1 && (cplx || pair)) return false;
+  auto go = [&](auto kern) {
+    launch_pdl(ctx, kern, grid, dim3(32, 8), 0, b2, nz, zchunk, u, r, with_g, g, t);
+    ctx->launches--;  // counted once by the caller
+  };
+  if (cplx)
+    go(kronsum_band6_kernel<true, false>);
+  else if (pair)
+    go(kronsum_band6_kernel<false, true>);
+  else
+    go(kronsum_band6_kernel<false, false>);
+  return true;
+}
+
 bool launch_band4(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz, int zchunk,
                   dim3 grid, const double* u, double* r, bool with_g, const kp_gfun& g,
                   double t) {
@@ -1212,7 +1323,13 @@ void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<i
     }
     const int nz = pair ? b2.n[2] : b2.n[2] * b2.n[3];
     const long long bxy = (long long)((b2.n[0] + 31) / 32) * ((b2.n[1] + 7) / 8);
-    const long long want = ctx->num_sms * 16LL;  // ~2 waves of 8 resident blocks
+    static const long long per_sm = [] {
+      const char* v = getenv("KP_BAND_BLOCKS");
+      return v && *v ? std::max(1LL, atoll(v)) : 4LL;
+    }();
+    // z chunks long enough to amortise a thread's row set-up (AC3D: 13 planes;
+    // measured best at 4 blocks per SM, KP_BAND_BLOCKS overrides)
+    const long long want = ctx->num_sms * per_sm;
     int zchunk = int(std::min<long long>(ZMAX, std::max<long long>(1, (nz * bxy + want - 1) / want)));
     if ((nz + zchunk - 1) / zchunk > 65535)
       throw invalid_argument("kronsum: modes 2-3 too large for the stencil path");
@@ -1229,6 +1346,11 @@ void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<i
       return;
     }
     if (!m3 && launch_band4(ctx, b2, cplx, pair, nz, zchunk, grid, u, r, with_g, g, t)) {
+      ctx->launches++;
+      KP_CUDA(cudaGetLastError());
+      return;
+    }
+    if (launch_band6(ctx, b2, cplx, pair, nz, zchunk, grid, u, r, with_g, g, t)) {
       ctx->launches++;
       KP_CUDA(cudaGetLastError());
       return;

@@ -149,6 +149,10 @@ struct TileCfg {
   static constexpr size_t SMEM =
       1024 + size_t(STAGES) * STAGE_BYTES + size_t(STG_DBL) * 8 + (2 * STAGES + 2) * 8;
   static constexpr int kMinBlocks = MINB;
+  // entries per thread batched in the inline epilogue (kp_epilogue.cuh):
+  // 1 for the 32 x 32 tiles, whose latency is hidden by 5 resident CTAs per
+  // SM (a batch's registers would cost two of them); 2 for 64 x 64
+  static constexpr int EU = (MI * NI <= 4) ? 1 : 2;
   static_assert(WM % 16 == 0 && WN % 16 == 0, "warp tiles are pairs of 8x8 DMMA tiles");
   static_assert(BM % 16 == 0 && BN % 16 == 0 && BN <= 256, "TMA boxes");
   static_assert(BN % SC == 0, "staging passes");
@@ -167,7 +171,7 @@ using CfgN = TileCfg<64, 64, 2, 2, 3, 3, 32>;
 using CfgM = TileCfg<64, 64, 2, 2, 4, 2>;
 // S: 32 x 32, 4 warps of 16 x 16 -- small problems and FP64-heavy fused
 //    epilogues at short K (the integrators)
-using CfgS = TileCfg<32, 32, 2, 2, 4, 3>;
+using CfgS = TileCfg<32, 32, 2, 2, 4, 5>;
 // L: 128 x 64, 4 warps of 64 x 32, one CTA per SM (KP_GEMM_TILE=L)
 using CfgL = TileCfg<128, 64, 2, 2, 4, 1>;
 // (measured and dropped: 128x64 / 64x128 with 8 DMMA + 3 epilogue warps at 1
@@ -239,7 +243,7 @@ __global__ void __launch_bounds__(CF::NT, CF::kMinBlocks)
       int m0, n0;
       decode(tile, q, m0, n0);
       mbar_wait(stg_full, ph);
-      nonfinite |= staged_epilogue<BM, BN, CF::LDS_C, NE * 32, CPLX, SCAT>(
+      nonfinite |= staged_epilogue<BM, BN, CF::LDS_C, NE * 32, CPLX, SCAT, 4>(
           p, e, stg, m0, n0, q, etid, c_vec2, half);
       // bar.sync completes this group's shared loads before the release
       asm volatile("bar.sync 2, %0;\n" ::"r"(NE * 32) : "memory");
@@ -445,7 +449,7 @@ __global__ void __launch_bounds__(CF::NT, CF::kMinBlocks)
         if (c0 > 0) consumer_bar(NC * 32);  // the previous pass has read stg
         stage_acc(c0);
         consumer_bar(NC * 32);
-        nonfinite |= staged_epilogue<BM, CF::SC, CF::LDS_C, NC * 32, CPLX, SCAT>(
+        nonfinite |= staged_epilogue<BM, CF::SC, CF::LDS_C, NC * 32, CPLX, SCAT, CF::EU>(
             p, e, stg, m0, n0 + c0, q, tid, c_vec2, half);
       }
     }
@@ -573,7 +577,8 @@ void launch_cplx(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, bool kcon
 // Tile menu: 32 x 32 when 64 x 64 tiles would not give every resident CTA
 // a few tiles; 128 x 64 for long K; 64 x 64 otherwise.  The k order is the
 // same in all of them (see the file comment), so the choice never changes a
-// bit.  KP_GEMM_TILE=S|M|L forces one (testing / benchmarking).
+// bit.  KP_GEMM_TILE=G|N|M|S|L forces one, KP_GEMM_TILE_FUSED one for the
+// fused-epilogue launches only (testing / benchmarking).
 void launch_gemm_dmma(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int cplx,
                       bool kcontig, long long half) {
   static const char forced = [] {
@@ -591,6 +596,11 @@ void launch_gemm_dmma(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int 
   else if (p.K <= 256)
     cfg = 'N';
   if (forced) cfg = forced;
+  static const char forced_fused = [] {
+    const char* v = getenv("KP_GEMM_TILE_FUSED");
+    return v && *v ? v[0] : '\0';
+  }();
+  if (fused && forced_fused) cfg = forced_fused;
   // the fused exchange's peer-store epilogues take the same menu (the
   // epilogue warps of G overlap the scattered stores with the mainloop)
   auto go = [&](auto scat) {

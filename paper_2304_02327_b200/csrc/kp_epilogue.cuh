@@ -83,8 +83,66 @@ __device__ __forceinline__ EpiU epi_uniform(const Epilogue& e) {
   return EpiU{e.beta != 0.0, e.alpha == 1.0, e.bad_step != nullptr};
 }
 
-// Epilogue on one output entry.  v = alpha*acc; idx = linear index into C
-// (and X/D, which share C's layout).
+// The global inputs an epilogue kind reads for one output entry, loaded
+// ahead of the arithmetic: the staged loops below issue the loads of several
+// entries before the first use, so each thread has several HBM reads in
+// flight instead of one dependent load per entry.
+struct EpiIn {
+  double c = 0.0, x = 0.0, p = 0.0;  // beta * C operand, X, species partner of X
+};
+__device__ __forceinline__ EpiIn epi_load(const Epilogue& e, const EpiU& u, const double* C,
+                                          long long idx, long long half) {
+  EpiIn in;
+  switch (e.kind) {
+    case EPI_FMA_X:
+    case EPI_STAGE_D:
+      in.x = e.X[idx];
+      break;
+    case EPI_ADD_G:
+      if (u.beta) in.c = C[idx];
+      in.x = e.X[idx];
+      if (half > 0) in.p = e.X[idx >= half ? idx - half : idx + half];
+      break;
+    case EPI_ADD_X:
+      if (u.beta) in.c = C[idx];
+      in.x = e.X[idx];
+      break;
+    default:
+      if (u.beta) in.c = C[idx];
+  }
+  return in;
+}
+
+// Epilogue arithmetic on one output entry.  v = alpha*acc; idx = linear
+// index into C (and X/D, which share C's layout).
+__device__ __forceinline__ double epi_apply(const Epilogue& e, const EpiU& u, double v,
+                                            const EpiIn& in, long long idx, long long half,
+                                            double* dval) {
+  switch (e.kind) {
+    case EPI_FMA_X:
+      return __fma_rn(e.gamma, v, in.x);
+    case EPI_ADD_G: {
+      const double base = u.beta ? __fma_rn(e.beta, in.c, v) : v;
+      const bool second = half > 0 && idx >= half;
+      return __dadd_rn(base, g_real(e.g, in.x, in.p, second, idx, e.t));
+    }
+    case EPI_ADD_X: {
+      const double base = u.beta ? __fma_rn(e.beta, in.c, v) : v;
+      return __dadd_rn(base, in.x);
+    }
+    case EPI_STAGE_D: {
+      const double s = __fma_rn(e.gamma, v, in.x);
+      *dval = __dsub_rn(g_real(e.g, s, 0.0, false, idx, e.t2), g_real(e.g, in.x, 0.0, false, idx, e.t));
+      return s;
+    }
+    default:
+      return u.beta ? __fma_rn(e.beta, in.c, v) : v;
+  }
+}
+
+// epi_load + epi_apply in one switch (the per-entry form of fused01.cu; the
+// same operations in the same order, so the two forms agree bit for bit --
+// one switch keeps that kernel's epilogue branch-light).
 __device__ __forceinline__ double epi_one(const Epilogue& e, const EpiU& u, double v,
                                           const double* C, long long idx, long long half,
                                           double* dval) {
@@ -112,33 +170,43 @@ __device__ __forceinline__ double epi_one(const Epilogue& e, const EpiU& u, doub
   }
 }
 
-// Complex epilogue on one (re, im) pair; idx = real index of the re part.
-__device__ __forceinline__ double2 epi_pair_c(const Epilogue& e, const EpiU& u, double2 v,
-                                              const double* C, long long idx, double2* dval) {
+// Complex entry (re, im at idx, idx + 1; idx even, so 16-byte loads).
+struct EpiInC {
+  double2 c = make_double2(0.0, 0.0), x = make_double2(0.0, 0.0);
+};
+__device__ __forceinline__ EpiInC epi_load_c(const Epilogue& e, const EpiU& u, const double* C,
+                                             long long idx) {
+  EpiInC in;
+  if (e.kind != EPI_FMA_X && e.kind != EPI_STAGE_D && u.beta)
+    in.c = *reinterpret_cast<const double2*>(C + idx);
+  if (e.kind != EPI_STORE) in.x = *reinterpret_cast<const double2*>(e.X + idx);
+  return in;
+}
+__device__ __forceinline__ double2 epi_apply_c(const Epilogue& e, const EpiU& u, double2 v,
+                                               const EpiInC& in, double2* dval) {
   switch (e.kind) {
     case EPI_FMA_X:
-      return make_double2(__fma_rn(e.gamma, v.x, e.X[idx]), __fma_rn(e.gamma, v.y, e.X[idx + 1]));
+      return make_double2(__fma_rn(e.gamma, v.x, in.x.x), __fma_rn(e.gamma, v.y, in.x.y));
     case EPI_ADD_G: {
       double2 b = v;
-      if (u.beta) b = make_double2(__fma_rn(e.beta, C[idx], v.x), __fma_rn(e.beta, C[idx + 1], v.y));
-      const double2 gx = g_cplx(e.g, make_double2(e.X[idx], e.X[idx + 1]));
+      if (u.beta) b = make_double2(__fma_rn(e.beta, in.c.x, v.x), __fma_rn(e.beta, in.c.y, v.y));
+      const double2 gx = g_cplx(e.g, in.x);
       return make_double2(__dadd_rn(b.x, gx.x), __dadd_rn(b.y, gx.y));
     }
     case EPI_ADD_X: {
       double2 b = v;
-      if (u.beta) b = make_double2(__fma_rn(e.beta, C[idx], v.x), __fma_rn(e.beta, C[idx + 1], v.y));
-      return make_double2(__dadd_rn(b.x, e.X[idx]), __dadd_rn(b.y, e.X[idx + 1]));
+      if (u.beta) b = make_double2(__fma_rn(e.beta, in.c.x, v.x), __fma_rn(e.beta, in.c.y, v.y));
+      return make_double2(__dadd_rn(b.x, in.x.x), __dadd_rn(b.y, in.x.y));
     }
     case EPI_STAGE_D: {
-      const double2 x = make_double2(e.X[idx], e.X[idx + 1]);
-      const double2 st = make_double2(__fma_rn(e.gamma, v.x, x.x), __fma_rn(e.gamma, v.y, x.y));
-      const double2 gs = g_cplx(e.g, st), gx = g_cplx(e.g, x);
+      const double2 st = make_double2(__fma_rn(e.gamma, v.x, in.x.x), __fma_rn(e.gamma, v.y, in.x.y));
+      const double2 gs = g_cplx(e.g, st), gx = g_cplx(e.g, in.x);
       *dval = make_double2(__dsub_rn(gs.x, gx.x), __dsub_rn(gs.y, gx.y));
       return st;
     }
     default:
       if (u.beta)
-        return make_double2(__fma_rn(e.beta, C[idx], v.x), __fma_rn(e.beta, C[idx + 1], v.y));
+        return make_double2(__fma_rn(e.beta, in.c.x, v.x), __fma_rn(e.beta, in.c.y, v.y));
       return v;
   }
 }
@@ -158,7 +226,7 @@ namespace {
 // 2i/2i+1 = re/im of the factor, combined as (rr - ii, ri + ir) at complex
 // offset p + i*P (complex modes >= 1).  Returns whether a non-finite value
 // was written (the divergence flag).
-template <int TM, int TN, int LDS, int NTH, int CPLX, bool SCAT>
+template <int TM, int TN, int LDS, int NTH, int CPLX, bool SCAT, int EU = 4>
 __device__ __forceinline__ bool staged_epilogue(const GemmProblem& p, const Epilogue& e,
                                                 const double* __restrict__ cs, int m0, int n0,
                                                 long long q, int tid, int c_vec2,
@@ -196,58 +264,100 @@ __device__ __forceinline__ bool staged_epilogue(const GemmProblem& p, const Epil
       return false;
     }
   }
+  // Batches of EU entries per thread: all global loads of a batch are issued
+  // before its arithmetic and stores (program order keeps them ahead), so a
+  // thread has EU x (1-3) reads in flight rather than one dependent read.
+  // (EU is smaller where the DMMA accumulators leave few registers.)
   if constexpr (CPLX == 2) {
+    constexpr int TOT = (TM / 2) * (TN / 2);
 #pragma unroll 1
-    for (int e2 = tid; e2 < (TM / 2) * (TN / 2); e2 += NTH) {
-      const int pl = e2 % (TM / 2), il = e2 / (TM / 2);
-      const int mrow = m0 + 2 * pl, ncol = n0 + 2 * il;
-      if (mrow >= p.M || ncol >= p.N) continue;
-      const double* c0 = cs + 2 * pl + 2 * il * LDS;
-      const double c_rr = c0[0], c_ir = c0[1], c_ri = c0[LDS], c_ii = c0[LDS + 1];
-      double2 v = make_double2(__dsub_rn(c_rr, c_ii), __dadd_rn(c_ri, c_ir));
-      if (!u.one) v = make_double2(al * v.x, al * v.y);
-      const long long off = mrow + (long long)(ncol >> 1) * p.ldc;
-      double2 dv = make_double2(0.0, 0.0);
-      const double2 rr = epi_pair_c(e, u, v, p.C, cq + off, &dv);
-      double* dst = Cb + off;
-      if constexpr (SCAT) dst = scatter_ptr(e, unsigned((cq + off) >> 1), 2);
-      *reinterpret_cast<double2*>(dst) = rr;
-      if (u.track) nonfinite |= !fin(rr.x) || !fin(rr.y);
-      if (e.kind == EPI_STAGE_D) *reinterpret_cast<double2*>(e.D + cq + off) = dv;
+    for (int b0 = tid; b0 < TOT; b0 += EU * NTH) {
+      EpiInC in[EU];
+      long long off[EU];
+      bool ok[EU];
+#pragma unroll
+      for (int j = 0; j < EU; ++j) {
+        const int e2 = b0 + j * NTH;
+        const int pl = e2 % (TM / 2), il = e2 / (TM / 2);
+        const int mrow = m0 + 2 * pl, ncol = n0 + 2 * il;
+        ok[j] = e2 < TOT && mrow < p.M && ncol < p.N;
+        off[j] = mrow + (long long)(ncol >> 1) * p.ldc;
+        if (ok[j]) in[j] = epi_load_c(e, u, p.C, cq + off[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < EU; ++j) {
+        if (!ok[j]) continue;
+        const int e2 = b0 + j * NTH;
+        const int pl = e2 % (TM / 2), il = e2 / (TM / 2);
+        const double* c0 = cs + 2 * pl + 2 * il * LDS;
+        const double c_rr = c0[0], c_ir = c0[1], c_ri = c0[LDS], c_ii = c0[LDS + 1];
+        double2 v = make_double2(__dsub_rn(c_rr, c_ii), __dadd_rn(c_ri, c_ir));
+        if (!u.one) v = make_double2(al * v.x, al * v.y);
+        double2 dv = make_double2(0.0, 0.0);
+        const double2 rr = epi_apply_c(e, u, v, in[j], &dv);
+        double* dst = Cb + off[j];
+        if constexpr (SCAT) dst = scatter_ptr(e, unsigned((cq + off[j]) >> 1), 2);
+        *reinterpret_cast<double2*>(dst) = rr;
+        if (u.track) nonfinite |= !fin(rr.x) || !fin(rr.y);
+        if (e.kind == EPI_STAGE_D) *reinterpret_cast<double2*>(e.D + cq + off[j]) = dv;
+      }
     }
     return nonfinite;
   }
+  constexpr int TOT = TM * TN / 2;
 #pragma unroll 1
-  for (int e2 = tid; e2 < TM * TN / 2; e2 += NTH) {
-    const int ml = 2 * (e2 % (TM / 2)), nl = e2 / (TM / 2);
-    const int mrow = m0 + ml, ncol = n0 + nl;
-    if (mrow >= p.M || ncol >= p.N) continue;
-    const bool two = (mrow + 1 < p.M);
-    const long long off = mrow + (long long)ncol * p.ldc;
-    const double2 a2 = *reinterpret_cast<const double2*>(cs + ml + nl * LDS);
-    const double v0 = u.one ? a2.x : al * a2.x, v1 = u.one ? a2.y : al * a2.y;
-    if constexpr (CPLX == 1) {
-      double2 dv = make_double2(0.0, 0.0);
-      const double2 rr = epi_pair_c(e, u, make_double2(v0, v1), p.C, cq + off, &dv);
-      double* dst = Cb + off;
-      if constexpr (SCAT) dst = scatter_ptr(e, unsigned((cq + off) >> 1), 2);
-      *reinterpret_cast<double2*>(dst) = rr;
-      if (u.track) nonfinite |= !fin(rr.x) || !fin(rr.y);
-      if (e.kind == EPI_STAGE_D) *reinterpret_cast<double2*>(e.D + cq + off) = dv;
-      continue;
-    }
-    double d0 = 0.0, d1 = 0.0;
-    const double r0 = epi_one(e, u, v0, p.C, cq + off, species_half, &d0);
-    double r1 = 0.0;
-    if (two) r1 = epi_one(e, u, v1, p.C, cq + off + 1, species_half, &d1);
-    if (u.track) nonfinite |= !fin(r0) || (two && !fin(r1));
-    store_pair<SCAT>(e, Cb + off, (unsigned long long)(cq + off), r0, r1, two, c_vec2);
-    if (e.kind == EPI_STAGE_D) {
-      if (two && c_vec2) {
-        *reinterpret_cast<double2*>(e.D + cq + off) = make_double2(d0, d1);
+  for (int b0 = tid; b0 < TOT; b0 += EU * NTH) {
+    long long off[EU];
+    bool ok[EU], two[EU];
+    EpiIn in0[EU], in1[EU];
+    EpiInC inc[EU];
+#pragma unroll
+    for (int j = 0; j < EU; ++j) {
+      const int e2 = b0 + j * NTH;
+      const int ml = 2 * (e2 % (TM / 2)), nl = e2 / (TM / 2);
+      const int mrow = m0 + ml, ncol = n0 + nl;
+      ok[j] = e2 < TOT && mrow < p.M && ncol < p.N;
+      two[j] = mrow + 1 < p.M;
+      off[j] = mrow + (long long)ncol * p.ldc;
+      if (!ok[j]) continue;
+      if constexpr (CPLX == 1) {
+        inc[j] = epi_load_c(e, u, p.C, cq + off[j]);
       } else {
-        e.D[cq + off] = d0;
-        if (two) e.D[cq + off + 1] = d1;
+        in0[j] = epi_load(e, u, p.C, cq + off[j], species_half);
+        if (two[j]) in1[j] = epi_load(e, u, p.C, cq + off[j] + 1, species_half);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < EU; ++j) {
+      if (!ok[j]) continue;
+      const int e2 = b0 + j * NTH;
+      const int ml = 2 * (e2 % (TM / 2)), nl = e2 / (TM / 2);
+      const long long o = cq + off[j];
+      const double2 a2 = *reinterpret_cast<const double2*>(cs + ml + nl * LDS);
+      const double v0 = u.one ? a2.x : al * a2.x, v1 = u.one ? a2.y : al * a2.y;
+      if constexpr (CPLX == 1) {
+        double2 dv = make_double2(0.0, 0.0);
+        const double2 rr = epi_apply_c(e, u, make_double2(v0, v1), inc[j], &dv);
+        double* dst = Cb + off[j];
+        if constexpr (SCAT) dst = scatter_ptr(e, unsigned(o >> 1), 2);
+        *reinterpret_cast<double2*>(dst) = rr;
+        if (u.track) nonfinite |= !fin(rr.x) || !fin(rr.y);
+        if (e.kind == EPI_STAGE_D) *reinterpret_cast<double2*>(e.D + o) = dv;
+      } else {
+        double d0 = 0.0, d1 = 0.0;
+        const double r0 = epi_apply(e, u, v0, in0[j], o, species_half, &d0);
+        double r1 = 0.0;
+        if (two[j]) r1 = epi_apply(e, u, v1, in1[j], o + 1, species_half, &d1);
+        if (u.track) nonfinite |= !fin(r0) || (two[j] && !fin(r1));
+        store_pair<SCAT>(e, Cb + off[j], (unsigned long long)o, r0, r1, two[j], c_vec2);
+        if (e.kind == EPI_STAGE_D) {
+          if (two[j] && c_vec2) {
+            *reinterpret_cast<double2*>(e.D + o) = make_double2(d0, d1);
+          } else {
+            e.D[o] = d0;
+            if (two[j]) e.D[o + 1] = d1;
+          }
+        }
       }
     }
   }

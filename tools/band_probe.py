@@ -13,7 +13,8 @@ from paper_2304_02327_b200 import problems
 
 out = []
 r = np.random.default_rng(77)
-for dims in [(64, 40, 30), (36, 24, 16), (130, 10, 9)]:
+# (300 / 260 / 270: rows straddling the reference's KC = 256 slice boundary)
+for dims in [(64, 40, 30), (36, 24, 16), (130, 10, 9), (300, 6, 5), (8, 260, 3), (4, 4, 270)]:
     u = np.asfortranarray(r.standard_normal(dims))
     out.append(kp.kronsum_action(u, [problems.fd_operator_1d(n, 0.01) for n in dims]))
 z = np.asfortranarray(r.standard_normal((32, 16, 24)) + 1j * r.standard_normal((32, 16, 24)))
