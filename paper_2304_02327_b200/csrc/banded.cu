@@ -765,6 +765,9 @@ __global__ void __launch_bounds__(256, (CPLX || PAIR) ? 2 : 3)
   }
 }
 
+#ifndef KP_B6_PAIR_BLOCKS
+#define KP_B6_PAIR_BLOCKS 3  // measured: 2 -> NLS 1.85 ms, 3 -> 1.60 ms (v2 1.63)
+#endif
 // ---- v6: v2's march with a lean per-plane loop (the default) ----
 // v2's traversal and arithmetic exactly (bit-identical), restricted to the
 // configs' shapes -- z runs over mode 2 only (order <= 3, or the 2-species
@@ -774,7 +777,7 @@ __global__ void __launch_bounds__(256, (CPLX || PAIR) ? 2 : 3)
 // rebuilds every plane: 116 SASS instructions per entry on AC3D, ncu
 // source page).  Two planes per iteration keep both planes' loads in flight.
 template <bool CPLX, bool PAIR>
-__global__ void __launch_bounds__(256, (CPLX || PAIR) ? 2 : 4)
+__global__ void __launch_bounds__(256, (CPLX || PAIR) ? KP_B6_PAIR_BLOCKS : 4)
     kronsum_band6_kernel(BandArgs b, int nz, int zchunk, const double* __restrict__ u,
                          double* __restrict__ r, bool with_g, kp_gfun g, double t) {
   pdl_wait();
@@ -852,17 +855,16 @@ __global__ void __launch_bounds__(256, (CPLX || PAIR) ? 2 : 4)
 bool launch_band6(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz, int zchunk,
                   dim3 grid, const double* u, double* r, bool with_g, const kp_gfun& g,
                   double t) {
-  // default for real single-species tensors; the complex and species-pair
-  // forms are opt-in (KP_BAND=v6): at the register budget their two-value
-  // entries need (2 blocks/SM) they measured slower than v2 (NLS 512^3 1.85
-  // vs 1.63 ms)
+  // default for single-species tensors (AC3D 14.3 vs v2 20.2 us; NLS 512^3
+  // 1.60 vs 1.63 ms); the species-pair form is opt-in (KP_BAND=v6): it
+  // measured no faster than v2 on the Brusselator
   static const int mode = [] {
     const char* v = getenv("KP_BAND");
     if (!v || !*v) return 1;
     return std::string(v) == "v6" ? 2 : 0;
   }();
   if (mode == 0 || b2.active[3] || (!pair && b2.n[3] != 1)) return false;
-  if (mode == 1 && (cplx || pair)) return false;
+  if (mode == 1 && pair) return false;
   auto go = [&](auto kern) {
     launch_pdl(ctx, kern, grid, dim3(32, 8), 0, b2, nz, zchunk, u, r, with_g, g, t);
     ctx->launches--;  // counted once by the caller
