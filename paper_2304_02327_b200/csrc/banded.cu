@@ -295,6 +295,7 @@ __device__ __forceinline__ void row_gather(const BandRow<CPLX>& rw, const T* __r
   for (int s = 0; s < 3; ++s) x[s] = u[in + unsigned(rw.off[s])];
 }
 
+template <bool IMAG = false>
 __device__ __forceinline__ void row_combine(const BandRow<false>& rw, const double* x, double& c) {
   if (rw.brk == 0) {
     const double acc = __fma_rn(rw.v[2], x[2], __fma_rn(rw.v[1], x[1], __fma_rn(rw.v[0], x[0], 0.0)));
@@ -314,8 +315,28 @@ __device__ __forceinline__ void row_combine(const BandRow<false>& rw, const doub
   c = __dadd_rn(c, acc);
 }
 
+// IMAG: every value of the row is purely imaginary (a.x == +-0; the NLS
+// factors i/2 * Laplacian).  a * x is then (-(a.y x.y), a.y x.x): the generic
+// micro-kernel's two products with a.x are signed zeros, and adding a signed
+// zero changes no value, so half of the FP64 work (4 of 8 operations per
+// term, and the first term's add to the +0 accumulator) is dropped.  Every
+// entry keeps its VALUE (== holds; only the sign of an exact zero can differ).
+// The complex stencil is otherwise FP64-bound: ~80 DMUL/DADD per entry is 0.64
+// ms of the FP64 pipe at 512^3, the HBM floor is 0.66 ms.
+template <bool IMAG = false>
 __device__ __forceinline__ void row_combine(const BandRow<true>& rw, const double2* x, double2& c) {
   double2 acc = make_double2(0.0, 0.0);
+  if constexpr (IMAG) {
+    if (rw.brk == 0) {
+      double2 t = make_double2(-__dmul_rn(rw.v[0].y, x[0].y), __dmul_rn(rw.v[0].y, x[0].x));
+#pragma unroll
+      for (int s = 1; s < 3; ++s)
+        t = make_double2(__dsub_rn(t.x, __dmul_rn(rw.v[s].y, x[s].y)),
+                         __dadd_rn(t.y, __dmul_rn(rw.v[s].y, x[s].x)));
+      c = make_double2(__dadd_rn(c.x, t.x), __dadd_rn(c.y, t.y));
+      return;
+    }
+  }
   if (rw.brk == 0) {
     acc = cmul_add(rw.v[2], x[2], cmul_add(rw.v[1], x[1], cmul_add(rw.v[0], x[0], acc)));
     c = make_double2(__dadd_rn(c.x, acc.x), __dadd_rn(c.y, acc.y));
@@ -331,6 +352,14 @@ __device__ __forceinline__ void row_combine(const BandRow<true>& rw, const doubl
     acc = cmul_add(rw.v[s], x[s], acc);
   }
   c = make_double2(__dadd_rn(c.x, acc.x), __dadd_rn(c.y, acc.y));
+}
+
+template <bool CPLX>
+__device__ __forceinline__ bool row_imag(const BandRow<CPLX>& rw) {
+  if constexpr (CPLX)
+    return rw.v[0].x == 0.0 && rw.v[1].x == 0.0 && rw.v[2].x == 0.0;
+  else
+    return false;
 }
 
 // b.n / b.stride / b.active are padded to 4 modes (extent 1, inactive).
@@ -851,6 +880,601 @@ __global__ void __launch_bounds__(256, (CPLX || PAIR) ? KP_B6_PAIR_BLOCKS : 4)
   }
 }
 
+// ---- v8: v6 with the thread's z line in registers, one plane AHEAD ----
+// v6's only HBM miss per plane is the first touch of plane z + 1 (its mode-2
+// "+1" neighbour); every other value was touched an iteration earlier.  v8
+// loads that value one iteration early: at plane z the centres of planes
+// z - 1, z, z + 1 are registers and the load of plane z + 2's centre is
+// issued before plane z is computed, so the miss has a whole iteration of
+// the SM's other warps to land.  Interior mode-2 rows (columns z-1, z, z+1,
+// no KC break) read the z line; other rows gather through their offsets.
+// Same chains in the same order as v6: bit-identical.
+constexpr int ZMAX8 = 64;
+template <bool CPLX>
+__device__ __forceinline__ bool interior_row8(const BandRow<CPLX>& rw, int st) {
+  return rw.n == 3 && rw.brk == 0 && rw.off[0] == -st && rw.off[1] == 0 && rw.off[2] == st;
+}
+
+template <bool CPLX, bool PAIR, int MB>
+__global__ void __launch_bounds__(256, MB)
+    kronsum_band8_kernel(BandArgs b, int nz, int zchunk, int pf2, int hpf,
+                         const double* __restrict__ u,
+                         double* __restrict__ r, bool with_g, kp_gfun g, double t) {
+  pdl_wait();
+  using T = typename std::conditional<CPLX, double2, double>::type;
+  constexpr int NSP = PAIR ? 2 : 1;
+  __shared__ BandRow<CPLX> rows2[ZMAX8];
+  __shared__ unsigned char pat2[ZMAX8];
+  const T* __restrict__ ut = reinterpret_cast<const T*>(u);
+  T* __restrict__ rt = reinterpret_cast<T*>(r);
+  const int z0 = blockIdx.z * zchunk;
+  const int z1 = min(nz, z0 + zchunk);
+  const int tid = threadIdx.x + 32 * threadIdx.y;
+  const bool a0 = b.active[0], a1 = b.active[1], a2 = b.active[2];
+  const unsigned st2 = unsigned(b.stride[2]), st3 = unsigned(b.stride[3]);
+  bool im = CPLX;  // all of this thread's rows purely imaginary (row_combine<IMAG>)
+  if (a2 && tid < z1 - z0) {
+    load_row(b, 2, z0 + tid, rows2[tid]);
+    pat2[tid] = interior_row8(rows2[tid], int(st2));
+    im = im && row_imag(rows2[tid]);
+  }
+  const int i0 = blockIdx.x * 32 + threadIdx.x;
+  const int i1 = blockIdx.y * 8 + threadIdx.y;
+  const bool inb = i0 < b.n[0] && i1 < b.n[1];
+  BandRow<CPLX> r0, r1;
+  if (inb && a0) {
+    load_row(b, 0, i0, r0);
+    im = im && row_imag(r0);
+  }
+  if (inb && a1) {
+    load_row(b, 1, i1, r1);
+    im = im && row_imag(r1);
+  }
+  const bool imag = __syncthreads_and(im) != 0;
+  if (!inb) return;
+  const int h2 = b.slab == 2 ? b.halo : 0, h3 = b.slab == 3 ? b.halo : 0;
+  const unsigned in01 = unsigned(i0 + (b.slab == 0 ? b.halo : 0)) * unsigned(b.stride[0]) +
+                        unsigned(i1 + (b.slab == 1 ? b.halo : 0)) * unsigned(b.stride[1]) +
+                        unsigned(h2) * st2 + unsigned(h3) * st3;
+  const unsigned plane = unsigned(b.n[0]) * unsigned(b.n[1]);
+  const unsigned out01 = unsigned(i0) + unsigned(i1) * unsigned(b.n[0]);
+  const unsigned sp_out = unsigned(b.n[2]) * plane;  // species 1 output offset (PAIR)
+  const int plo = -h2, phi = nz + h2;                 // planes plo .. phi - 1 exist
+  // rim prefetch (see the loop): lanes 0 / 31 take the mode-0 neighbour beyond
+  // the warp, the tile's first / last warp its mode-1 neighbour row
+  int halo_off = 0;
+  if (b.slab != 0 && b.slab != 1 && b.stride[0] == 1) {
+    if (threadIdx.y == 0 && i1 > 0)
+      halo_off = -int(b.stride[1]);
+    else if (threadIdx.y == 7 && i1 + 1 < b.n[1])
+      halo_off = int(b.stride[1]);
+    else if (threadIdx.x == 0 && i0 > 0)
+      halo_off = -1;
+    else if (threadIdx.x == 31 && i0 + 1 < b.n[0])
+      halo_off = 1;
+  }
+  const bool halo_pf = halo_off != 0 && hpf != 0;
+  auto centre = [&](int p, int sp) -> T {
+    if (p >= plo && p < phi) return ut[in01 + unsigned(p) * st2 + unsigned(sp) * st3];
+    if constexpr (CPLX)
+      return make_double2(0.0, 0.0);
+    else
+      return 0.0;
+  };
+  T zm[NSP], zc[NSP], zp[NSP];
+#pragma unroll
+  for (int sp = 0; sp < NSP; ++sp) {
+    zm[sp] = centre(z0 - 1, sp);
+    zc[sp] = centre(z0, sp);
+    zp[sp] = centre(z0 + 1, sp);
+  }
+  auto march = [&](auto imag_tag) {
+  constexpr bool IM = decltype(imag_tag)::value;
+  unsigned rim[NSP] = {};
+#pragma unroll 1
+  for (int z = z0; z < z1; ++z) {
+    T zn[NSP];
+#pragma unroll
+    for (int sp = 0; sp < NSP; ++sp) zn[sp] = centre(z + 2, sp);
+    if (pf2 > 0 && z + pf2 < phi) {
+#pragma unroll
+      for (int sp = 0; sp < NSP; ++sp)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(ut + in01 + unsigned(z + pf2) * st2 +
+                                                        unsigned(sp) * st3));
+    }
+    // the tile's rim of the NEXT plane belongs to other blocks' lines: bring
+    // it into L1 now, or every warp waits an L2 round trip on its two edge
+    // lanes (and the tile's first / last row) once per plane.  A plain load
+    // whose result is only "used" (an empty asm) an iteration later:
+    // prefetch.global.L1 measured 8x SLOWER for the whole kernel (NLS 1.5 ->
+    // 13 ms) on this B200.
+#pragma unroll
+    for (int sp = 0; sp < NSP; ++sp) asm volatile("" ::"r"(rim[sp]));
+    if (halo_pf && z + 1 < phi) {
+#pragma unroll
+      for (int sp = 0; sp < NSP; ++sp)
+        asm volatile("ld.global.u32 %0, [%1];"
+                     : "=r"(rim[sp])
+                     : "l"(ut + in01 + unsigned(z + 1) * st2 + unsigned(sp) * st3 +
+                           unsigned(halo_off)));
+    }
+    const BandRow<CPLX> q2 = rows2[z - z0];
+    const bool int2 = pat2[z - z0];
+    const unsigned in0 = in01 + unsigned(z) * st2;
+    const unsigned idx0 = out01 + unsigned(z) * plane;
+    T res[NSP];
+#pragma unroll
+    for (int sp = 0; sp < NSP; ++sp) {
+      const unsigned in = in0 + unsigned(sp) * st3;
+      T x0[3], x1[3], x2[3];
+      if (a0) row_gather(r0, ut, in, x0);
+      if (a1) row_gather(r1, ut, in, x1);
+      if (a2) {
+        if (int2) {
+          x2[0] = zm[sp];
+          x2[1] = zc[sp];
+          x2[2] = zp[sp];
+        } else {
+          row_gather(q2, ut, in, x2);
+        }
+      }
+      T c;
+      if constexpr (CPLX)
+        c = make_double2(0.0, 0.0);
+      else
+        c = 0.0;
+      if (a0) row_combine<IM>(r0, x0, c);
+      if (a1) row_combine<IM>(r1, x1, c);
+      if (a2) row_combine<IM>(q2, x2, c);
+      res[sp] = c;
+    }
+    if constexpr (PAIR) {
+      const unsigned idx1 = idx0 + sp_out;
+      if (with_g) {
+        const double u0 = zc[0], u1 = zc[1];
+        rt[idx0] = __dadd_rn(res[0], g_real(g, u0, u1, false, idx0, t));
+        rt[idx1] = __dadd_rn(res[1], g_real(g, u1, u0, true, idx1, t));
+      } else {
+        rt[idx0] = res[0];
+        rt[idx1] = res[1];
+      }
+    } else if (!with_g) {
+      rt[idx0] = res[0];
+    } else if constexpr (CPLX) {
+      const double2 gg = g_cplx(g, zc[0]);
+      rt[idx0] = make_double2(__dadd_rn(res[0].x, gg.x), __dadd_rn(res[0].y, gg.y));
+    } else {
+      rt[idx0] = __dadd_rn(res[0], g_real(g, zc[0], 0.0, false, idx0, t));
+    }
+#pragma unroll
+    for (int sp = 0; sp < NSP; ++sp) {
+      zm[sp] = zc[sp];
+      zc[sp] = zp[sp];
+      zp[sp] = zn[sp];
+    }
+  }
+  };
+  if constexpr (CPLX) {
+    if (imag)
+      march(std::true_type{});
+    else
+      march(std::false_type{});
+  } else {
+    march(std::false_type{});
+  }
+}
+
+// v8 launcher; false = not applicable
+bool launch_band8(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz, const double* u,
+                  double* r, bool with_g, const kp_gfun& g, double t) {
+  static const int mode = [] {
+    const char* v = getenv("KP_BAND");
+    if (!v || !*v) return 1;
+    return std::string(v) == "v8" ? 2 : 0;
+  }();
+  if (mode == 0 || b2.active[3] || (!pair && b2.n[3] != 1)) return false;
+  // default for complex tensors only (NLS 512^3: 1.48 vs v6's 1.68 ms); for
+  // real tensors v6 measured faster (AC3D 17 vs 21 us; Brusselator pair 310
+  // vs 322 us): KP_BAND=v8 runs it for every form
+  if (mode == 1 && !cplx) return false;
+  static const int pf2 = [] {
+    const char* v = getenv("KP_B8_PF");
+    return v && *v ? atoi(v) : 4;
+  }();
+  static const int hpf = [] {
+    const char* v = getenv("KP_B8_HPF");
+    return v && *v ? atoi(v) : 1;
+  }();
+  static const long long per_sm = [] {
+    const char* v = getenv("KP_B8_BLOCKS");
+    return v && *v ? std::max(1LL, atoll(v)) : 4LL;
+  }();
+  const long long bxy = (long long)((b2.n[0] + 31) / 32) * ((b2.n[1] + 7) / 8);
+  const long long want = ctx->num_sms * per_sm;
+  const int zchunk =
+      int(std::min<long long>(ZMAX8, std::max<long long>(1, (nz * bxy + want - 1) / want)));
+  if ((nz + zchunk - 1) / zchunk > 65535 || (b2.n[1] + 7) / 8 > 65535) return false;
+  dim3 grid(unsigned((b2.n[0] + 31) / 32), unsigned((b2.n[1] + 7) / 8),
+            unsigned((nz + zchunk - 1) / zchunk));
+  auto go = [&](auto kern) {
+    launch_pdl(ctx, kern, grid, dim3(32, 8), 0, b2, nz, zchunk, pf2, hpf, u, r, with_g, g, t);
+    ctx->launches--;  // counted once by the caller
+  };
+  static const int mb = [] {  // resident blocks per SM the kernel is compiled for
+    const char* v = getenv("KP_B8_MINB");
+    return v && *v ? atoi(v) : 0;
+  }();
+  if (cplx)
+    mb == 3 ? go(kronsum_band8_kernel<true, false, 3>) : go(kronsum_band8_kernel<true, false, 2>);
+  else if (pair)
+    mb == 3 ? go(kronsum_band8_kernel<false, true, 3>) : go(kronsum_band8_kernel<false, true, 2>);
+  else
+    mb == 3 ? go(kronsum_band8_kernel<false, false, 3>) : go(kronsum_band8_kernel<false, false, 4>);
+  return true;
+}
+
+// ---- v7: register-tiled march, nothing but registers on the critical path ----
+// ncu on v6 (NLS 512^3): the L1 data pipe is the limiter (LSU wavefronts 73 %
+// of peak: nine 16-byte gathers per entry, each 4-5 wavefronts per warp, plus
+// spills), with the FP64 pipe at 40 % (a complex entry is ~80 DMUL/DADD) and
+// one exposed HBM miss per plane.  v7 takes every neighbour from registers:
+//   * a thread owns a strip of RY consecutive mode-1 rows of one mode-0
+//     column and marches mode 2; the strip of plane z (+ one halo row each
+//     side) is loaded TWO iterations early, so (RY + 2) x 2 loads per thread
+//     are always in flight and no load result is awaited in the iteration
+//     that issued it;
+//   * mode-1 neighbours are the strip's registers, mode-2 neighbours the
+//     strips of planes z - 1 / z + 1, mode-0 neighbours come by warp shuffle
+//     (lanes 0 / 31 load the one value beyond the warp, one iteration early);
+//   * (RY + 2) / RY aligned loads per entry instead of nine.
+// Rows are canonicalised once (canon_row): a row whose columns lie in
+// {i-1, i, i+1} becomes the three slots (i-1, i, i+1) with zero values in
+// the missing ones -- a leading fma(0, x, +0) is +0 and a trailing fma(0, x,
+// acc) is acc (the chain's accumulator is never -0, see row_gather), so the
+// chain's value is unchanged bit for bit; KC = 256 slice breaks keep their
+// slot.  Rows that reach elsewhere (the periodic wrap) gather through their
+// offsets as in v6 (lane-divergent for mode 0, warp-uniform otherwise).
+// Same chains in the same mode order: bit-identical to v6.
+// NSP = 2: both species of a grid point per thread (species stride st3).
+constexpr int ZMAX7 = 128;
+
+// true: rw rewritten as slots (-st, 0, +st); false: left alone
+template <bool CPLX>
+__device__ __forceinline__ bool canon_row(BandRow<CPLX>& rw, int st) {
+  int slot[3] = {0, 0, 0};
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    if (s >= rw.n) break;
+    const int o = rw.off[s];
+    if (o == -st)
+      slot[s] = 0;
+    else if (o == 0)
+      slot[s] = 1;
+    else if (o == st)
+      slot[s] = 2;
+    else
+      return false;
+    // the chain runs in column order: the slots must come in that order too
+    // (a slab's wrap row has its -st neighbour last)
+    if (s > 0 && slot[s] <= slot[s - 1]) return false;
+  }
+  BandRow<CPLX> c;
+  c.n = 3;
+  c.brk = 0;
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    c.off[s] = (s - 1) * st;
+    if constexpr (CPLX)
+      c.v[s] = make_double2(0.0, 0.0);
+    else
+      c.v[s] = 0.0;
+  }
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    if (s >= rw.n) break;
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+      if (slot[s] == q) {
+        c.v[q] = rw.v[s];
+        if ((rw.brk >> s) & 1u) c.brk |= 1u << q;
+      }
+  }
+  rw = c;
+  return true;
+}
+
+// The rare rows (periodic wrap): gather through the row's own offsets and fold
+// it into c.  Out of line on purpose -- inlined, the compiler predicates these
+// gathers into the march and every plane issues their (masked) address
+// arithmetic and loads: 300 instructions per entry instead of 150 (ncu).
+template <bool CPLX>
+__device__ __noinline__ typename std::conditional<CPLX, double2, double>::type slow_term(
+    const BandRow<CPLX>* rw, const typename std::conditional<CPLX, double2, double>::type* ut,
+    unsigned in, typename std::conditional<CPLX, double2, double>::type c) {
+  using T = typename std::conditional<CPLX, double2, double>::type;
+  const BandRow<CPLX> q = *rw;
+  T x[3];
+  row_gather(q, ut, in, x);
+  row_combine(q, x, c);
+  return c;
+}
+
+template <bool CPLX, int NSP, int RY, int WY, int MB>
+__global__ void __launch_bounds__(32 * WY, MB)
+    kronsum_band7_kernel(BandArgs b, int zchunk, int pf2, const double* __restrict__ u,
+                         double* __restrict__ r, bool with_g, kp_gfun g, double t) {
+  pdl_wait();
+  using T = typename std::conditional<CPLX, double2, double>::type;
+  constexpr int NROW = WY * RY;
+  __shared__ BandRow<CPLX> rows1[NROW];
+  __shared__ BandRow<CPLX> rows2[ZMAX7];
+  __shared__ BandRow<CPLX> rows0[32];  // the non-canonical mode-0 rows (slow_term)
+  __shared__ unsigned char pat1[NROW], pat2[ZMAX7];
+  const T* __restrict__ ut = reinterpret_cast<const T*>(u);
+  T* __restrict__ rt = reinterpret_cast<T*>(r);
+  const int n0 = b.n[0], n1 = b.n[1], n2 = b.n[2];
+  const int z0 = blockIdx.z * zchunk;
+  const int z1 = min(n2, z0 + zchunk);
+  const int lane = threadIdx.x;
+  const int tid = threadIdx.x + 32 * threadIdx.y;
+  const bool a0 = b.active[0], a1 = b.active[1], a2 = b.active[2];
+  const int st1 = int(b.stride[1]), st2 = int(b.stride[2]), st3 = int(b.stride[3]);
+  const int yb = blockIdx.y * NROW;
+  bool im = CPLX;  // all of this thread's rows purely imaginary (row_combine<IMAG>)
+  if (a1 && tid < NROW && yb + tid < n1) {
+    load_row(b, 1, yb + tid, rows1[tid]);
+    im = im && row_imag(rows1[tid]);
+    pat1[tid] = canon_row(rows1[tid], st1);
+  }
+  if (a2)
+    for (int i = tid; i < z1 - z0; i += 32 * WY) {
+      load_row(b, 2, z0 + i, rows2[i]);
+      im = im && row_imag(rows2[i]);
+      pat2[i] = canon_row(rows2[i], st2);
+    }
+  const int i0 = blockIdx.x * 32 + lane;
+  const int y0 = yb + threadIdx.y * RY;
+  const bool xv = i0 < n0;
+  BandRow<CPLX> r0;
+  bool pat0 = true;
+  r0.n = 0;
+  r0.brk = 0;
+  if (a0 && xv) {
+    load_row(b, 0, i0, r0);
+    im = im && row_imag(r0);
+    if (threadIdx.y == 0) rows0[lane] = r0;
+    pat0 = canon_row(r0, 1);
+  }
+  const bool imag = __syncthreads_and(im) != 0;
+  if (y0 >= n1) return;  // whole warps only: the shuffles need all 32 lanes
+  const int h2 = b.slab == 2 ? b.halo : 0;
+  // input index of (i0, y0, plane 0); planes -h2 .. n2 + h2 - 1 exist
+  const unsigned in01 = unsigned(i0) + unsigned(y0) * unsigned(st1) + unsigned(h2) * unsigned(st2);
+  const unsigned plane = unsigned(n0) * unsigned(n1);
+  const unsigned out01 = unsigned(i0) + unsigned(y0) * unsigned(n0);
+  const unsigned sp_out = unsigned(n2) * plane;  // species 1 output offset
+  bool yv[RY + 2];  // strip rows -1 .. RY inside the tensor
+#pragma unroll
+  for (int k = 0; k < RY + 2; ++k) yv[k] = (y0 + k - 1 >= 0) && (y0 + k - 1 < n1);
+  // lanes 0 / 31 fetch the mode-0 neighbour beyond the warp (when it exists)
+  const bool edge_l = lane == 0 && i0 - 1 >= 0 && xv;
+  const bool edge_r = lane == 31 && i0 + 1 < n0;
+  const int edge_off = edge_l ? -1 : 1;
+  T zm[NSP][RY], cur[NSP][RY + 2], nxt[NSP][RY + 2], pre[NSP][RY + 2];
+  T xe[NSP][RY], xen[NSP][RY];  // edge values of the current / next plane
+  auto zero = [](T& x) {
+    if constexpr (CPLX)
+      x = make_double2(0.0, 0.0);
+    else
+      x = 0.0;
+  };
+  auto load_strip = [&](int p, T(*s)[RY + 2]) {
+    const bool pv = xv && p >= -h2 && p < n2 + h2;
+    const unsigned base = in01 + unsigned(p) * unsigned(st2) - unsigned(st1);
+#pragma unroll
+    for (int sp = 0; sp < NSP; ++sp)
+#pragma unroll
+      for (int k = 0; k < RY + 2; ++k) {
+        if (pv && yv[k])
+          s[sp][k] = ut[base + unsigned(k) * unsigned(st1) + unsigned(sp) * unsigned(st3)];
+        else
+          zero(s[sp][k]);
+      }
+  };
+  auto load_edge = [&](int p, T(*e)[RY]) {
+    const bool pv = (edge_l || edge_r) && p >= -h2 && p < n2 + h2;
+    const unsigned base = in01 + unsigned(p) * unsigned(st2) + unsigned(edge_off);
+#pragma unroll
+    for (int sp = 0; sp < NSP; ++sp)
+#pragma unroll
+      for (int k = 0; k < RY; ++k) {
+        if (pv && yv[k + 1])
+          e[sp][k] = ut[base + unsigned(k) * unsigned(st1) + unsigned(sp) * unsigned(st3)];
+        else
+          zero(e[sp][k]);
+      }
+  };
+  auto shfl = [&](const T& v, bool up) -> T {
+    if constexpr (CPLX) {
+      return up ? make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1))
+                : make_double2(__shfl_down_sync(0xffffffffu, v.x, 1),
+                               __shfl_down_sync(0xffffffffu, v.y, 1));
+    } else {
+      return up ? __shfl_up_sync(0xffffffffu, v, 1) : __shfl_down_sync(0xffffffffu, v, 1);
+    }
+  };
+  {
+    T tmp[NSP][RY + 2];
+    load_strip(z0 - 1, tmp);
+#pragma unroll
+    for (int sp = 0; sp < NSP; ++sp)
+#pragma unroll
+      for (int k = 0; k < RY; ++k) zm[sp][k] = tmp[sp][k + 1];
+  }
+  load_strip(z0, cur);
+  load_edge(z0, xe);
+  load_strip(z0 + 1, nxt);
+  auto march = [&](auto imag_tag) {
+  constexpr bool IM = decltype(imag_tag)::value;
+#pragma unroll 1
+  for (int z = z0; z < z1; ++z) {
+    load_strip(z + 2, pre);
+    load_edge(z + 1, xen);
+    if (pf2 > 0 && xv && z + pf2 < n2 + h2) {
+      const unsigned base = in01 + unsigned(z + pf2) * unsigned(st2);
+#pragma unroll
+      for (int sp = 0; sp < NSP; ++sp)
+#pragma unroll
+        for (int k = 0; k < RY; ++k)
+          if (yv[k + 1])
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(
+                ut + base + unsigned(k) * unsigned(st1) + unsigned(sp) * unsigned(st3)));
+    }
+    const BandRow<CPLX> q2 = rows2[z - z0];
+    const bool int2 = pat2[z - z0];
+    const unsigned inz = in01 + unsigned(z) * unsigned(st2);
+    const unsigned idz = out01 + unsigned(z) * plane;
+    T res[NSP][RY];
+#pragma unroll
+    for (int k = 0; k < RY; ++k) {
+#pragma unroll
+      for (int sp = 0; sp < NSP; ++sp) {
+        const unsigned in = inz + unsigned(k) * unsigned(st1) + unsigned(sp) * unsigned(st3);
+        const T ctr = cur[sp][k + 1];
+        T c;
+        zero(c);
+        if (a0) {
+          // all 32 lanes shuffle (rows past the tensor hold zeros)
+          T xl = shfl(ctr, true), xr = shfl(ctr, false);
+          if (lane == 0) xl = xe[sp][k];
+          if (lane == 31) xr = xe[sp][k];
+          const T x[3] = {xl, ctr, xr};
+          if (xv && yv[k + 1]) {
+            if (pat0)
+              row_combine<IM>(r0, x, c);
+            else
+              c = slow_term<CPLX>(&rows0[lane], ut, in, c);
+          }
+        }
+        if (!xv || !yv[k + 1]) continue;
+        if (a1) {
+          if (pat1[threadIdx.y * RY + k]) {
+            const BandRow<CPLX> q1 = rows1[threadIdx.y * RY + k];
+            const T x[3] = {cur[sp][k], ctr, cur[sp][k + 2]};
+            row_combine<IM>(q1, x, c);
+          } else {
+            c = slow_term<CPLX>(&rows1[threadIdx.y * RY + k], ut, in, c);
+          }
+        }
+        if (a2) {
+          if (int2) {
+            const T x[3] = {zm[sp][k], ctr, nxt[sp][k + 1]};
+            row_combine<IM>(q2, x, c);
+          } else {
+            c = slow_term<CPLX>(&rows2[z - z0], ut, in, c);
+          }
+        }
+        res[sp][k] = c;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < RY; ++k) {
+      if (!xv || !yv[k + 1]) continue;
+      const unsigned idx = idz + unsigned(k) * unsigned(n0);
+      if constexpr (NSP == 2) {
+        if (with_g) {
+          const double u0 = cur[0][k + 1], u1 = cur[1][k + 1];
+          rt[idx] = __dadd_rn(res[0][k], g_real(g, u0, u1, false, idx, t));
+          rt[idx + sp_out] = __dadd_rn(res[1][k], g_real(g, u1, u0, true, idx + sp_out, t));
+        } else {
+          rt[idx] = res[0][k];
+          rt[idx + sp_out] = res[1][k];
+        }
+      } else if (!with_g) {
+        rt[idx] = res[0][k];
+      } else if constexpr (CPLX) {
+        const double2 gg = g_cplx(g, cur[0][k + 1]);
+        rt[idx] = make_double2(__dadd_rn(res[0][k].x, gg.x), __dadd_rn(res[0][k].y, gg.y));
+      } else {
+        rt[idx] = __dadd_rn(res[0][k], g_real(g, cur[0][k + 1], 0.0, false, idx, t));
+      }
+    }
+#pragma unroll
+    for (int sp = 0; sp < NSP; ++sp) {
+#pragma unroll
+      for (int k = 0; k < RY; ++k) {
+        zm[sp][k] = cur[sp][k + 1];
+        xe[sp][k] = xen[sp][k];
+      }
+#pragma unroll
+      for (int k = 0; k < RY + 2; ++k) {
+        cur[sp][k] = nxt[sp][k];
+        nxt[sp][k] = pre[sp][k];
+      }
+    }
+  }
+  };
+  if constexpr (CPLX) {
+    if (imag)
+      march(std::true_type{});
+    else
+      march(std::false_type{});
+  } else {
+    march(std::false_type{});
+  }
+}
+
+// v7 launcher; false = not applicable
+bool launch_band7(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz, const double* u,
+                  double* r, bool with_g, const kp_gfun& g, double t) {
+  static const int mode = [] {  // opt-in (KP_BAND=v7): measured slower than v6
+    const char* v = getenv("KP_BAND");
+    return v && std::string(v) == "v7" ? 2 : 0;
+  }();
+  if (mode == 0 || b2.active[3] || b2.d < 3 || (!pair && b2.n[3] != 1)) return false;
+  if ((b2.slab >= 0 && b2.slab != 2) || b2.stride[0] != 1) return false;
+  static const int ry_env = [] {
+    const char* v = getenv("KP_B7_RY");
+    return v && *v ? atoi(v) : 0;
+  }();
+  static const int pf2 = [] {
+    const char* v = getenv("KP_B7_PF");
+    return v && *v ? atoi(v) : 6;
+  }();
+  static const long long per_sm = [] {
+    const char* v = getenv("KP_B7_BLOCKS");
+    return v && *v ? std::max(1LL, atoll(v)) : 12LL;
+  }();
+  const int ry = ry_env ? ry_env : ((cplx || pair) ? 2 : 4);
+  if (ry != 2 && ry != 4) return false;
+  if ((cplx || pair) && ry != 2) return false;
+  constexpr int B7_WY = 4;
+  const long long bxy = (long long)((b2.n[0] + 31) / 32) * ((b2.n[1] + B7_WY * ry - 1) / (B7_WY * ry));
+  // enough blocks for a few waves; chunks as long as that allows (each chunk
+  // start re-reads two planes)
+  const long long want = ctx->num_sms * per_sm;
+  long long chunks = std::max<long long>(1, (want + bxy - 1) / bxy);
+  int zchunk = int(std::max<long long>(4, (nz + chunks - 1) / chunks));
+  zchunk = std::min(zchunk, ZMAX7);
+  const long long gz = (nz + zchunk - 1) / zchunk;
+  const long long gy = (b2.n[1] + B7_WY * ry - 1) / (B7_WY * ry);
+  if (gz > 65535 || gy > 65535) return false;
+  dim3 grid(unsigned((b2.n[0] + 31) / 32), unsigned(gy), unsigned(gz));
+  auto go = [&](auto kern) {
+    launch_pdl(ctx, kern, grid, dim3(32, B7_WY), 0, b2, zchunk, pf2, u, r, with_g, g, t);
+    ctx->launches--;  // counted once by the caller
+  };
+  if (cplx)
+    go(kronsum_band7_kernel<true, 1, 2, B7_WY, 3>);
+  else if (pair)
+    go(kronsum_band7_kernel<false, 2, 2, B7_WY, 3>);
+  else if (ry == 2)
+    go(kronsum_band7_kernel<false, 1, 2, B7_WY, 4>);
+  else
+    go(kronsum_band7_kernel<false, 1, 4, B7_WY, 4>);
+  return true;
+}
+
 // v6 launcher; false = not applicable (KP_BAND=v2 forces the v2 kernel)
 bool launch_band6(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz, int zchunk,
                   dim3 grid, const double* u, double* r, bool with_g, const kp_gfun& g,
@@ -1348,6 +1972,12 @@ void kronsum_banded(kp_ctx* ctx, bool cplx, const double* u, const std::vector<i
       return;
     }
     if (!m3 && launch_band4(ctx, b2, cplx, pair, nz, zchunk, grid, u, r, with_g, g, t)) {
+      ctx->launches++;
+      KP_CUDA(cudaGetLastError());
+      return;
+    }
+    if (launch_band8(ctx, b2, cplx, pair, nz, u, r, with_g, g, t) ||
+        launch_band7(ctx, b2, cplx, pair, nz, u, r, with_g, g, t)) {
       ctx->launches++;
       KP_CUDA(cudaGetLastError());
       return;

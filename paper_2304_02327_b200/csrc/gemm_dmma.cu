@@ -174,13 +174,23 @@ using CfgM = TileCfg<64, 64, 2, 2, 4, 2>;
 using CfgS = TileCfg<32, 32, 2, 2, 4, 5>;
 // L: 128 x 64, 4 warps of 64 x 32, one CTA per SM (KP_GEMM_TILE=L)
 using CfgL = TileCfg<128, 64, 2, 2, 4, 1>;
+// B / C: balanced single-wave tiles.  A mode product of a 128-cube has
+//    16384 rows (or columns) to share among 148 SMs: 64-row tiles leave
+//    3.46 per SM (one SM in two does a 4th while the rest idle), 112-row
+//    tiles give 147 x 2 = 294 CTAs, two per SM, all resident at once.
+//    B: 112 x 64 (4 DMMA warps of 112 x 16), rows taken from the STACKED
+//    (batch x M) matrix for batched products (FLAT: 16-row TMA boxes, each
+//    with its own batch coordinate), C: 64 x 112 for the K-contiguous B
+//    of mode 0 (4 DMMA warps of 16 x 112).
+using CfgB = TileCfg<112, 64, 1, 4, 3, 2, 32>;
+using CfgC = TileCfg<64, 112, 4, 1, 3, 2, 56>;
 // (measured and dropped: 128x64 / 64x128 with 8 DMMA + 3 epilogue warps at 1
 // CTA/SM, 64x64 with 8 DMMA warps of 32x16 / 16x32, 64x32 / 32x64 at 4
 // CTAs/SM, 32x32 / 32x64 with epilogue warps: all at or below G / N / S)
 
 // ------------------------------------------------------------ the kernel
 
-template <class CF, bool B_KCONTIG, bool TMA, int CPLX, bool SCAT>
+template <class CF, bool B_KCONTIG, bool TMA, int CPLX, bool SCAT, bool FLAT = false>
 __global__ void __launch_bounds__(CF::NT, CF::kMinBlocks)
     dmma_tile_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB, GemmProblem p, Epilogue e,
@@ -216,7 +226,8 @@ __global__ void __launch_bounds__(CF::NT, CF::kMinBlocks)
   __syncthreads();
 
   const long long per_q = (long long)tiles_m * tiles_n;
-  const long long total = per_q * p.batch;
+  // FLAT: tiles_m counts row blocks of the stacked (batch x M) matrix
+  const long long total = FLAT ? per_q : per_q * p.batch;
   const int KT = (p.K + BK - 1) / BK;
   auto decode = [&](long long tile, long long& q, int& m0, int& n0) {
     q = tile / per_q;
@@ -243,8 +254,14 @@ __global__ void __launch_bounds__(CF::NT, CF::kMinBlocks)
       int m0, n0;
       decode(tile, q, m0, n0);
       mbar_wait(stg_full, ph);
-      nonfinite |= staged_epilogue<BM, BN, CF::LDS_C, NE * 32, CPLX, SCAT, 4>(
-          p, e, stg, m0, n0, q, etid, c_vec2, half);
+      int rb = 0;
+      if constexpr (FLAT) {
+        q = m0 / p.M;
+        m0 -= int(q) * p.M;
+        rb = p.M - m0;
+      }
+      nonfinite |= staged_epilogue<BM, BN, CF::LDS_C, NE * 32, CPLX, SCAT, 4, FLAT>(
+          p, e, stg, m0, n0, q, etid, c_vec2, half, rb);
       // bar.sync completes this group's shared loads before the release
       asm volatile("bar.sync 2, %0;\n" ::"r"(NE * 32) : "memory");
       if (etid == 0) mbar_arrive(stg_empty);
@@ -263,15 +280,26 @@ __global__ void __launch_bounds__(CF::NT, CF::kMinBlocks)
         long long q;
         int m0, n0;
         decode(tile, q, m0, n0);
-        const int qa = int(q), qb = p.sB ? int(q) : 0;
+        int qa = int(q);
+        const int qb = p.sB ? int(q) : 0;
+        if constexpr (FLAT) {
+          qa = m0 / p.M;
+          m0 -= qa * p.M;
+        }
         for (int kt = 0; kt < KT; ++kt) {
           mbar_wait(&empty[stage], phase ^ 1u);
           double* as = ring + stage * CF::STAGE_DBL;
           double* bs = as + CF::A_DBL;
           mbar_expect_tx(&full[stage], CF::STAGE_BYTES);
 #pragma unroll
-          for (int c = 0; c < BM / 16; ++c)
-            tma_load_3d(as + c * 16 * BK, &mapA, &full[stage], m0 + 16 * c, kt * BK, qa);
+          for (int c = 0; c < BM / 16; ++c) {
+            int mc = m0 + 16 * c, qc = qa;
+            if (FLAT && mc >= p.M) {  // the tile runs on into the next batch
+              mc -= p.M;              // (past the last batch: out of bounds, zero-filled)
+              ++qc;
+            }
+            tma_load_3d(as + c * 16 * BK, &mapA, &full[stage], mc, kt * BK, qc);
+          }
           if constexpr (B_KCONTIG) {
             tma_load_3d(bs, &mapB, &full[stage], kt * BK, n0, qb);
           } else {
@@ -444,13 +472,19 @@ __global__ void __launch_bounds__(CF::NT, CF::kMinBlocks)
       if (tid == 0) mbar_arrive(stg_full);
       stg_phase ^= 1u;
     } else {
+      int rb = 0;
+      if constexpr (FLAT) {
+        q = m0 / p.M;
+        m0 -= int(q) * p.M;
+        rb = p.M - m0;
+      }
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += CF::SC) {
         if (c0 > 0) consumer_bar(NC * 32);  // the previous pass has read stg
         stage_acc(c0);
         consumer_bar(NC * 32);
-        nonfinite |= staged_epilogue<BM, CF::SC, CF::LDS_C, NC * 32, CPLX, SCAT, CF::EU>(
-            p, e, stg, m0, n0 + c0, q, tid, c_vec2, half);
+        nonfinite |= staged_epilogue<BM, CF::SC, CF::LDS_C, NC * 32, CPLX, SCAT, CF::EU, FLAT>(
+            p, e, stg, m0, n0 + c0, q, tid, c_vec2, half, rb);
       }
     }
   }
@@ -517,13 +551,14 @@ int resident_ctas(const void* kern, int threads, size_t smem) {
   return n;
 }
 
-template <class CF, bool KC, bool TMA, int CPLX, bool SCAT>
+template <class CF, bool KC, bool TMA, int CPLX, bool SCAT, bool FLAT = false>
 void launch_tile(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, long long half) {
-  auto kern = dmma_tile_kernel<CF, KC, TMA, CPLX, SCAT>;
+  auto kern = dmma_tile_kernel<CF, KC, TMA, CPLX, SCAT, FLAT>;
   ensure_smem_attr(ctx, reinterpret_cast<const void*>(kern), int(CF::SMEM));
-  const int tiles_m = (p.M + CF::BM - 1) / CF::BM;
+  const int tiles_m =
+      int((FLAT ? (long long)p.M * p.batch + CF::BM - 1 : (long long)p.M + CF::BM - 1) / CF::BM);
   const int tiles_n = (p.N + CF::BN - 1) / CF::BN;
-  const long long total = (long long)tiles_m * tiles_n * p.batch;
+  const long long total = (long long)tiles_m * tiles_n * (FLAT ? 1 : p.batch);
   const int n_fastest = tiles_n <= tiles_m ? 1 : 0;
   const int c_vec2 = ((p.ldc % 2) == 0 && (p.sC % 2) == 0 && a16(p.C) &&
                       (e.D == nullptr || a16(e.D)))
@@ -595,12 +630,43 @@ void launch_gemm_dmma(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int 
     cfg = 'S';
   else if (p.K <= 256)
     cfg = 'N';
+  // balanced tiles (B / C), opt-in: KP_GEMM_BAL=2 for real, unscattered,
+  // TMA-describable products whose 112-row (-column) tiles fill one wave of
+  // two CTAs per SM, KP_GEMM_BAL=1 also for any product they spread more
+  // evenly than 64 x 64 tiles.  Measured (B200, n = 128 cube): the wave is
+  // balanced (294 CTAs) but nothing overlaps a CTA's TMA ramp and epilogue,
+  // 26.9 vs 25.8 us per mode product (DMMA pipe 66 vs 74 % of active cycles),
+  // AC3D 5.30k vs 5.97k steps/s; n = 256 29.7 vs 31.5 TFLOP/s -- so S / N / G
+  // stay the defaults.
+  const bool flat = !kcontig && p.batch > 1;
+  const bool bal_ok = cplx == 0 && !e.sc_dir && tma_ok(p, kcontig) &&
+                      (!flat || (p.sB == 0 && p.M % 16 == 0 && p.M >= CfgB::BM &&
+                                 (long long)p.M * p.batch < (1LL << 31)));
+  if (bal_ok) {
+    const long long tb = kcontig ? (long long)((p.M + 63) / 64) * ((p.N + 111) / 112) * p.batch
+                                 : (((long long)p.M * p.batch + 111) / 112) * ((p.N + 63) / 64);
+    const long long slots = 2LL * ctx->num_sms;
+    static const int bal_mode = [] {
+      const char* v = getenv("KP_GEMM_BAL");
+      return v && *v ? atoi(v) : 0;
+    }();
+    if (bal_mode != 0 && tb <= slots && 4 * tb >= 3 * slots && p.K >= 64) cfg = 'B';
+    if (bal_mode == 1 && tb > slots) {
+      const long long s64 = (long long)ctx->num_sms * (cfg == 'S' ? 5 : cfg == 'N' ? 3 : 2);
+      const long long t64 = cfg == 'S' ? (long long)((p.M + 31) / 32) * ((p.N + 31) / 32) * p.batch
+                                       : tiles64;
+      const double eff64 = double(t64) / double((t64 + s64 - 1) / s64 * s64);
+      const double effb = double(tb) / double((tb + slots - 1) / slots * slots);
+      if (effb > eff64 + 0.03) cfg = 'B';
+    }
+  }
   if (forced) cfg = forced;
+  if (cfg == 'B' && !bal_ok) cfg = 'S';
   static const char forced_fused = [] {
     const char* v = getenv("KP_GEMM_TILE_FUSED");
     return v && *v ? v[0] : '\0';
   }();
-  if (fused && forced_fused) cfg = forced_fused;
+  if (fused && forced_fused && (forced_fused != 'B' || bal_ok)) cfg = forced_fused;
   // the fused exchange's peer-store epilogues take the same menu (the
   // epilogue warps of G overlap the scattered stores with the mainloop)
   auto go = [&](auto scat) {
@@ -613,6 +679,15 @@ void launch_gemm_dmma(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int 
       default: launch_cplx<CfgG, SC>(ctx, p, e, kcontig, cplx, half); break;
     }
   };
+  if (cfg == 'B') {
+    if (kcontig)
+      launch_tile<CfgC, true, true, 0, false>(ctx, p, e, half);
+    else if (flat)
+      launch_tile<CfgB, false, true, 0, false, true>(ctx, p, e, half);
+    else
+      launch_tile<CfgB, false, true, 0, false>(ctx, p, e, half);
+    return;
+  }
   if (e.sc_dir)
     go(std::true_type{});
   else

@@ -226,13 +226,19 @@ namespace {
 // 2i/2i+1 = re/im of the factor, combined as (rr - ii, ri + ir) at complex
 // offset p + i*P (complex modes >= 1).  Returns whether a non-finite value
 // was written (the divergence flag).
-template <int TM, int TN, int LDS, int NTH, int CPLX, bool SCAT, int EU = 4>
+//
+// FLAT (real, no scatter): the tile's rows are rows of the stacked (batch x M)
+// matrix -- rows ml < rb belong to batch q (row m0 + ml), rows ml >= rb to
+// batch q + 1 (row ml - rb); rb is even, so (m, m+1) pairs never straddle.
+template <int TM, int TN, int LDS, int NTH, int CPLX, bool SCAT, int EU = 4, bool FLAT = false>
 __device__ __forceinline__ bool staged_epilogue(const GemmProblem& p, const Epilogue& e,
                                                 const double* __restrict__ cs, int m0, int n0,
                                                 long long q, int tid, int c_vec2,
-                                                long long species_half) {
+                                                long long species_half, int rb = 0) {
+  static_assert(!FLAT || (CPLX == 0 && !SCAT), "flat row blocks: real, unscattered tiles");
   double* __restrict__ Cb = p.C + q * p.sC;
   const long long cq = q * p.sC;
+  const bool next_ok = q + 1 < p.batch;  // FLAT: the tile's second batch exists
   bool nonfinite = false;
   const EpiU u = epi_uniform(e);
   const double al = e.alpha;
@@ -245,11 +251,20 @@ __device__ __forceinline__ bool staged_epilogue(const GemmProblem& p, const Epil
 #pragma unroll 2
       for (int e2 = tid; e2 < TM * TN / 2; e2 += NTH) {
         const int ml = 2 * (e2 % (TM / 2)), nl = e2 / (TM / 2);
-        const int mrow = m0 + ml, ncol = n0 + nl;
+        int mrow = m0 + ml;
+        const int ncol = n0 + nl;
+        double* Cq = Cb;
+        if constexpr (FLAT) {
+          if (ml >= rb) {
+            if (!next_ok) continue;
+            mrow = ml - rb;
+            Cq = Cb + p.sC;
+          }
+        }
         if (mrow >= p.M || ncol >= p.N) continue;
         double2 a2 = *reinterpret_cast<const double2*>(cs + ml + nl * LDS);
         if (!one) a2 = make_double2(al * a2.x, al * a2.y);
-        double* dst = Cb + mrow + (long long)ncol * p.ldc;
+        double* dst = Cq + mrow + (long long)ncol * p.ldc;
         if (mrow + 1 < p.M) {
           if (c_vec2)
             *reinterpret_cast<double2*>(dst) = a2;
@@ -315,10 +330,20 @@ __device__ __forceinline__ bool staged_epilogue(const GemmProblem& p, const Epil
     for (int j = 0; j < EU; ++j) {
       const int e2 = b0 + j * NTH;
       const int ml = 2 * (e2 % (TM / 2)), nl = e2 / (TM / 2);
-      const int mrow = m0 + ml, ncol = n0 + nl;
-      ok[j] = e2 < TOT && mrow < p.M && ncol < p.N;
+      int mrow = m0 + ml;
+      const int ncol = n0 + nl;
+      bool qok = true;
+      long long shift = 0;  // FLAT: rows of the next batch
+      if constexpr (FLAT) {
+        if (ml >= rb) {
+          mrow = ml - rb;
+          shift = p.sC;
+          qok = next_ok;
+        }
+      }
+      ok[j] = qok && e2 < TOT && mrow < p.M && ncol < p.N;
       two[j] = mrow + 1 < p.M;
-      off[j] = mrow + (long long)ncol * p.ldc;
+      off[j] = shift + mrow + (long long)ncol * p.ldc;
       if (!ok[j]) continue;
       if constexpr (CPLX == 1) {
         inc[j] = epi_load_c(e, u, p.C, cq + off[j]);

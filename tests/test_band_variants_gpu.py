@@ -1,5 +1,6 @@
-"""The banded Kronecker-sum kernels (banded.cu): the default v6 lean line
-march (real tensors; v2 for complex / species pairs), the v2 march, the TMA
+"""The banded Kronecker-sum kernels (banded.cu): the defaults (v8 = v6 with the
+z line in registers one plane ahead for complex tensors, the v6 lean line march
+for real ones, v2 for species pairs), the v7 register-tiled march, the v2 march, the TMA
 plane ring v3, the register z line v4, v2 with its rows in shared memory v5
 and v6 for every form (opt-in, KP_BAND), and other z-chunk lengths
 (KP_BAND_BLOCKS) give
@@ -29,7 +30,7 @@ def default_hashes():
     return probe({})
 
 
-@pytest.mark.parametrize("variant", ["v2", "v3", "v4", "v5", "v6"])
+@pytest.mark.parametrize("variant", ["v2", "v3", "v4", "v5", "v6", "v7", "v8"])
 def test_band_variant_bitwise(variant, default_hashes):
     assert probe({"KP_BAND": variant}) == default_hashes
 
@@ -37,3 +38,12 @@ def test_band_variant_bitwise(variant, default_hashes):
 @pytest.mark.parametrize("blocks", ["1", "16"])
 def test_band_zchunk_bitwise(blocks, default_hashes):
     assert probe({"KP_BAND_BLOCKS": blocks}) == default_hashes
+
+
+@pytest.mark.parametrize("env", [{"KP_BAND": "v7", "KP_B7_RY": "2"}, {"KP_BAND": "v7", "KP_B7_PF": "0"},
+                                 {"KP_BAND": "v7", "KP_B7_BLOCKS": "1"},
+                                 {"KP_BAND": "v7", "KP_B7_BLOCKS": "64"},
+                                 {"KP_BAND": "v8", "KP_B8_MINB": "3"}, {"KP_BAND": "v8", "KP_B8_PF": "0"},
+                                 {"KP_BAND": "v8", "KP_B8_BLOCKS": "1"}, {"KP_BAND": "v8", "KP_B8_HPF": "0"}])
+def test_band78_shapes_bitwise(env, default_hashes):
+    assert probe(env) == default_hashes

@@ -74,6 +74,9 @@ def test_fused01_prefactor_and_phi(kp, port):
 CASES = {
     # (method, u0 shape, K builder, g kind, g params, T, steps)
     "ac3d": ("etd2rk", (64, 64, 64), "ac", "G_ALLEN_CAHN", (), 5e-4 * 6, 6),
+    # the config's cube: balanced single-wave GEMM tiles (gemm_dmma.cu B / C)
+    "ac3d128": ("etd2rk", (128, 128, 128), "ac", "G_ALLEN_CAHN", (), 5e-4 * 3, 3),
+    "ac3d128_l2b": ("lawson2b", (128, 128, 128), "ac", "G_ALLEN_CAHN", (), 5e-4 * 2, 2),
     "ac2d": ("exp_euler", (128, 128), "ac", "G_ALLEN_CAHN", (), 1e-3 * 8, 8),
     "ac2d_etd": ("etd2rk", (128, 128), "ac", "G_ALLEN_CAHN", (), 1e-3 * 8, 8),
     "ac2d_l2b": ("lawson2b", (64, 64), "ac", "G_ALLEN_CAHN", (), 1e-3 * 8, 8),
@@ -106,7 +109,7 @@ def test_integrate_fastpaths_bitwise(kp, port, tmp_path, case):
         u0 = np.asfortranarray(0.4 + 0.1 * r.uniform(-1, 1, shape))
     gk = getattr(kp, gname)
     got = kp.integrate_config(method, u0, K, kp.gfun(gk, *gp), 0.0, T, steps)
-    want = run_general(tmp_path, {"KP_FUSE01": "0", "KP_BAND": "v1"},
+    want = run_general(tmp_path, {"KP_FUSE01": "0", "KP_BAND": "v1", "KP_GEMM_BAL": "0"},
                        what=method, u0=u0,
                        K=np.array(K, dtype=object), gk=gk, gp=np.array(gp, dtype=float),
                        T=T, steps=steps)

@@ -1,5 +1,6 @@
 """Every tile configuration of the GEMM (gemm_dmma.cu menu, forced with
-KP_GEMM_TILE) and the cp.async producer (KP_TMA=0) give BIT-IDENTICAL mode
+KP_GEMM_TILE; B = the balanced 112-row / 112-column tiles incl. the stacked
+"flat" row blocks of batched products, KP_GEMM_BAL=2 single-wave products / 1 also multi-wave) and the cp.async producer (KP_TMA=0) give BIT-IDENTICAL mode
 products, Tucker operators and complex products: the k order of every
 accumulator is the same in all of them (DMMA k-slot t of k-step s holds
 k = 16 kt + 4 s + t, in order).  Each variant runs in its own process (the
@@ -28,7 +29,8 @@ def default_hashes():
     return probe({})
 
 
-@pytest.mark.parametrize("variant", [{"KP_GEMM_TILE": t} for t in "SMNLG"] +
-                         [{"KP_TMA": "0"}, {"KP_TMA": "0", "KP_GEMM_TILE": "G"}])
+@pytest.mark.parametrize("variant", [{"KP_GEMM_TILE": t} for t in "SMNLGB"] +
+                         [{"KP_TMA": "0"}, {"KP_TMA": "0", "KP_GEMM_TILE": "G"},
+                          {"KP_GEMM_BAL": "2"}, {"KP_GEMM_BAL": "1"}, {"KP_FUSE01": "0"}])
 def test_tile_variant_bitwise(default_hashes, variant):
     assert probe(variant) == default_hashes

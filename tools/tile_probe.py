@@ -12,7 +12,8 @@ import paper_2304_02327_b200 as kp
 
 r = np.random.default_rng(4242)
 out = []
-for shape in [(64, 64, 64), (130, 7, 66), (33, 65, 17), (128, 96, 40), (200, 200)]:
+for shape in [(64, 64, 64), (130, 7, 66), (33, 65, 17), (128, 96, 40), (200, 200), (128, 128, 128),
+              (160, 48, 30), (112, 80, 3)]:
     t = np.asfortranarray(r.standard_normal(shape))
     ms = [np.asfortranarray(r.standard_normal((n, n)) / n) for n in shape]
     out.append(kp.tucker(t, ms))
