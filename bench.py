@@ -365,7 +365,38 @@ class ClockSampler:
         self.stop = threading.Event()
         self.th = threading.Thread(target=self.run, daemon=True)
 
+    def _nvml(self):
+        """NVML handle (nvidia_ml_py): ~1 ms per sample instead of a ~150 ms nvidia-smi
+        process, so a 0.1 s timed region still gets dozens of samples."""
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            idx = self.index
+            if vis and all(t.strip().isdigit() for t in vis.split(",")):
+                idx = int(vis.split(",")[self.index])
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx)
+        except Exception:
+            return None, None
+
     def run(self):
+        nv, h = self._nvml()
+        if nv is not None:
+            try:
+                get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                bits = [0x8, 0x40, 0x20, 0x4]  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                while not self.stop.is_set():
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    r = int(get_reasons(h))
+                    pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                    self.rows.append([str(sm), str(mx), f"{pw:.1f}", hex(r)] +
+                                     ["Active" if r & b else "Not Active" for b in bits])
+                    self.stop.wait(0.005)
+                return
+            except Exception:
+                pass  # fall back to nvidia-smi below
         while not self.stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", f"--id={self.index}",
