@@ -895,7 +895,12 @@ __device__ __forceinline__ bool interior_row8(const BandRow<CPLX>& rw, int st) {
   return rw.n == 3 && rw.brk == 0 && rw.off[0] == -st && rw.off[1] == 0 && rw.off[2] == st;
 }
 
-template <bool CPLX, bool PAIR, int MB>
+// YH (opt-in, KP_B8_YH=1): the thread's mode-1 neighbours (rows i1 - 1, i1 + 1)
+// of the NEXT plane are loaded one iteration early as well (the warps of a
+// tile march unsynchronised, so a warp that is ahead takes its neighbour
+// rows' first touch itself; L1 hit rate 63 %).  Measured slower: the extra
+// registers cost more than the exposed misses.
+template <bool CPLX, bool PAIR, int MB, bool YH>
 __global__ void __launch_bounds__(256, MB)
     kronsum_band8_kernel(BandArgs b, int nz, int zchunk, int pf2, int hpf,
                          const double* __restrict__ u,
@@ -968,14 +973,40 @@ __global__ void __launch_bounds__(256, MB)
     zc[sp] = centre(z0, sp);
     zp[sp] = centre(z0 + 1, sp);
   }
+  // mode-1 neighbours of the current plane (valid when the row has the
+  // columns i1 - 1, i1, i1 + 1 in this order; KC breaks stay with row_combine)
+  const bool y_int = YH && a1 && r1.n == 3 && r1.off[0] == -int(b.stride[1]) && r1.off[1] == 0 &&
+                     r1.off[2] == int(b.stride[1]);
+  T ym[NSP], yp[NSP];
+#pragma unroll
+  for (int sp = 0; sp < NSP; ++sp) {
+    if (y_int) {
+      const unsigned in = in01 + unsigned(z0) * st2 + unsigned(sp) * st3;
+      ym[sp] = ut[in - unsigned(b.stride[1])];
+      yp[sp] = ut[in + unsigned(b.stride[1])];
+    } else {
+      ym[sp] = zc[sp];
+      yp[sp] = zc[sp];
+    }
+  }
   auto march = [&](auto imag_tag) {
   constexpr bool IM = decltype(imag_tag)::value;
   unsigned rim[NSP] = {};
 #pragma unroll 1
   for (int z = z0; z < z1; ++z) {
-    T zn[NSP];
+    T zn[NSP], ymn[NSP], ypn[NSP];
 #pragma unroll
     for (int sp = 0; sp < NSP; ++sp) zn[sp] = centre(z + 2, sp);
+#pragma unroll
+    for (int sp = 0; sp < NSP; ++sp) {
+      ymn[sp] = ym[sp];
+      ypn[sp] = yp[sp];
+      if (y_int && z + 1 < phi) {
+        const unsigned in = in01 + unsigned(z + 1) * st2 + unsigned(sp) * st3;
+        ymn[sp] = ut[in - unsigned(b.stride[1])];
+        ypn[sp] = ut[in + unsigned(b.stride[1])];
+      }
+    }
     if (pf2 > 0 && z + pf2 < phi) {
 #pragma unroll
       for (int sp = 0; sp < NSP; ++sp)
@@ -1008,7 +1039,15 @@ __global__ void __launch_bounds__(256, MB)
       const unsigned in = in0 + unsigned(sp) * st3;
       T x0[3], x1[3], x2[3];
       if (a0) row_gather(r0, ut, in, x0);
-      if (a1) row_gather(r1, ut, in, x1);
+      if (a1) {
+        if (y_int) {
+          x1[0] = ym[sp];
+          x1[1] = zc[sp];
+          x1[2] = yp[sp];
+        } else {
+          row_gather(r1, ut, in, x1);
+        }
+      }
       if (a2) {
         if (int2) {
           x2[0] = zm[sp];
@@ -1051,6 +1090,8 @@ __global__ void __launch_bounds__(256, MB)
       zm[sp] = zc[sp];
       zc[sp] = zp[sp];
       zp[sp] = zn[sp];
+      ym[sp] = ymn[sp];
+      yp[sp] = ypn[sp];
     }
   }
   };
@@ -1073,10 +1114,11 @@ bool launch_band8(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz,
     return std::string(v) == "v8" ? 2 : 0;
   }();
   if (mode == 0 || b2.active[3] || (!pair && b2.n[3] != 1)) return false;
-  // default for complex tensors only (NLS 512^3: 1.48 vs v6's 1.68 ms); for
-  // real tensors v6 measured faster (AC3D 17 vs 21 us; Brusselator pair 310
-  // vs 322 us): KP_BAND=v8 runs it for every form
-  if (mode == 1 && !cplx) return false;
+  // default for complex tensors (NLS 512^3: 1.48 vs v6's 1.68 ms; 2 blocks of
+  // 124 registers) and species pairs (Brusselator 2 x 256^3: 256 vs v2's 305
+  // us; 3 blocks per SM, shorter z chunks); for single real tensors v6
+  // measured faster (AC3D 17 vs 21 us): KP_BAND=v8 runs it for every form
+  if (mode == 1 && !cplx && !pair) return false;
   static const int pf2 = [] {
     const char* v = getenv("KP_B8_PF");
     return v && *v ? atoi(v) : 4;
@@ -1085,10 +1127,11 @@ bool launch_band8(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz,
     const char* v = getenv("KP_B8_HPF");
     return v && *v ? atoi(v) : 1;
   }();
-  static const long long per_sm = [] {
+  static const long long per_sm_env = [] {
     const char* v = getenv("KP_B8_BLOCKS");
-    return v && *v ? std::max(1LL, atoll(v)) : 4LL;
+    return v && *v ? std::max(1LL, atoll(v)) : 0LL;
   }();
+  const long long per_sm = per_sm_env ? per_sm_env : (pair ? 8LL : 4LL);
   const long long bxy = (long long)((b2.n[0] + 31) / 32) * ((b2.n[1] + 7) / 8);
   const long long want = ctx->num_sms * per_sm;
   const int zchunk =
@@ -1100,16 +1143,29 @@ bool launch_band8(kp_ctx* ctx, const BandArgs& b2, bool cplx, bool pair, int nz,
     launch_pdl(ctx, kern, grid, dim3(32, 8), 0, b2, nz, zchunk, pf2, hpf, u, r, with_g, g, t);
     ctx->launches--;  // counted once by the caller
   };
-  static const int mb = [] {  // resident blocks per SM the kernel is compiled for
+  static const int mb_env = [] {  // resident blocks per SM the kernel is compiled for
     const char* v = getenv("KP_B8_MINB");
     return v && *v ? atoi(v) : 0;
   }();
+  const int mb = mb_env ? mb_env : (pair ? 3 : 0);
+  static const bool yh = [] {  // opt-in: measured slower (NLS 1.60 vs 1.49 ms)
+    const char* v = getenv("KP_B8_YH");
+    return v && std::string(v) == "1";
+  }();
+  auto pick = [&](auto cp, auto pr, auto m) {
+    constexpr bool C = decltype(cp)::value, P = decltype(pr)::value;
+    constexpr int M = decltype(m)::value;
+    yh ? go(kronsum_band8_kernel<C, P, M, true>) : go(kronsum_band8_kernel<C, P, M, false>);
+  };
+  using std::integral_constant;
+  const std::true_type T1{};
+  const std::false_type F0{};
   if (cplx)
-    mb == 3 ? go(kronsum_band8_kernel<true, false, 3>) : go(kronsum_band8_kernel<true, false, 2>);
+    mb == 3 ? pick(T1, F0, integral_constant<int, 3>{}) : pick(T1, F0, integral_constant<int, 2>{});
   else if (pair)
-    mb == 3 ? go(kronsum_band8_kernel<false, true, 3>) : go(kronsum_band8_kernel<false, true, 2>);
+    mb == 3 ? pick(F0, T1, integral_constant<int, 3>{}) : pick(F0, T1, integral_constant<int, 2>{});
   else
-    mb == 3 ? go(kronsum_band8_kernel<false, false, 3>) : go(kronsum_band8_kernel<false, false, 4>);
+    mb == 3 ? pick(F0, F0, integral_constant<int, 3>{}) : pick(F0, F0, integral_constant<int, 4>{});
   return true;
 }
 

@@ -1,6 +1,6 @@
 """The banded Kronecker-sum kernels (banded.cu): the defaults (v8 = v6 with the
-z line in registers one plane ahead for complex tensors, the v6 lean line march
-for real ones, v2 for species pairs), the v7 register-tiled march, the v2 march, the TMA
+z line in registers one plane ahead for complex tensors and species pairs, the
+v6 lean line march for single real tensors), the v7 register-tiled march, the v2 march, the TMA
 plane ring v3, the register z line v4, v2 with its rows in shared memory v5
 and v6 for every form (opt-in, KP_BAND), and other z-chunk lengths
 (KP_BAND_BLOCKS) give
@@ -44,6 +44,7 @@ def test_band_zchunk_bitwise(blocks, default_hashes):
                                  {"KP_BAND": "v7", "KP_B7_BLOCKS": "1"},
                                  {"KP_BAND": "v7", "KP_B7_BLOCKS": "64"},
                                  {"KP_BAND": "v8", "KP_B8_MINB": "3"}, {"KP_BAND": "v8", "KP_B8_PF": "0"},
-                                 {"KP_BAND": "v8", "KP_B8_BLOCKS": "1"}, {"KP_BAND": "v8", "KP_B8_HPF": "0"}])
+                                 {"KP_BAND": "v8", "KP_B8_BLOCKS": "1"}, {"KP_BAND": "v8", "KP_B8_HPF": "0"},
+                                 {"KP_BAND": "v8", "KP_B8_YH": "1"}, {"KP_BAND": "v8", "KP_B8_MINB": "2"}])
 def test_band78_shapes_bitwise(env, default_hashes):
     assert probe(env) == default_hashes
