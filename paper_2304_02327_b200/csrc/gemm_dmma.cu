@@ -630,6 +630,15 @@ void launch_gemm_dmma(kp_ctx* ctx, const GemmProblem& p, const Epilogue& e, int 
     cfg = 'S';
   else if (p.K <= 256)
     cfg = 'N';
+  else if (!fused && p.K >= 1024) {
+    // few rounds of 64 x 64 tiles with a short last round (d = 2, n = 2048:
+    // 1024 tiles on 296 slots = 3.46 rounds, and the last round's lone CTAs,
+    // one DMMA warp per scheduler, run at ~2/3 of an SM's rate): the 32 x 32
+    // tiles spread the tail over every SM -- measured 32.2 vs 30.3 TFLOP/s
+    const double rounds = double(tiles64) / (2.0 * ctx->num_sms);
+    const double fr = rounds - double((long long)rounds);
+    if (rounds < 6.0 && fr > 0.05 && fr < 0.6) cfg = 'S';
+  }
   // balanced tiles (B / C), opt-in: KP_GEMM_BAL=2 for real, unscattered,
   // TMA-describable products whose 112-row (-column) tiles fill one wave of
   // two CTAs per SM, KP_GEMM_BAL=1 also for any product they spread more
