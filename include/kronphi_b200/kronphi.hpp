@@ -14,15 +14,22 @@
 //   (integrators.hpp:24-373).
 // Containers stay host value types; every O(n^3)/O(N n) operation runs on the
 // GPU (upload, DMMA kernels, download).  Differences, by design:
-//   * g is a device nonlinearity from the closed set (kp_gfun: Allen-Cahn,
-//     Brusselator, NLS, zero, square, const, and the reference's own ADR and
-//     Riccati g's) -- a host std::function has no device equivalent and is
-//     rejected (no CPU fallback on the hot path);
-//   * Method::RosenbrockEuler is provided for the Riccati g, whose Jacobian
-//     factors (the reference's ProblemSpec::jacobian_factors callback,
-//     src/problems.cpp:212-250) are rebuilt on the device every step;
-//     rosenbrock_euler_step takes caller-supplied factors like the reference;
-//   * Backend::DenseOracle is not provided;
+//   * g is either a device nonlinearity from the closed set (kp_gfun:
+//     Allen-Cahn, Brusselator, NLS, zero, square, const, and the reference's
+//     own ADR and Riccati g's), evaluated inside the fused GEMM epilogues, or
+//     -- like the reference's GFun -- any host callable Tensor(double, const
+//     Tensor&): the state stays on the GPU and each g evaluation is a host
+//     round trip between the device operations (detail::HostGLoop); real
+//     tensors only;
+//   * Method::RosenbrockEuler: for the device Riccati g the Jacobian factors
+//     (src/problems.cpp:212-250) are rebuilt on the device every step; with a
+//     host ProblemSpec::jacobian_factors callback it is called on the
+//     downloaded state once per step; rosenbrock_euler_step takes
+//     caller-supplied factors like the reference;
+//   * Backend::DenseOracle assembles K (N x N, N <= 8192) and integrates the
+//     one-mode problem on the device (every method, Rosenbrock-Euler with a
+//     host Jacobian callback); phi tables by phiquad, not the reference's
+//     Taylor table (agree to roundoff);
 //   * problems: fd_operator_1d, build_adr, build_riccati (problems.hpp) with
 //     to_problem_spec(); their g's auxiliary fields live on the device and are
 //     kept alive by ProblemSpec::device_data;
@@ -1112,8 +1119,8 @@ IntegrateResultT<T> integrate(const ProblemSpecT<T>& p, const StepperConfig& c) 
   if (c.method == Method::RosenbrockEuler && !p.jacobian_factors && !device_jac)
     throw std::invalid_argument("integrate: Rosenbrock-Euler requires jacobian_factors");
   if (c.backend == Backend::DenseOracle) {
-    if (c.method == Method::RosenbrockEuler)
-      throw std::invalid_argument("DenseOracle: Rosenbrock-Euler is not provided");
+    if (c.method == Method::RosenbrockEuler && !p.jacobian_factors)
+      throw std::invalid_argument("DenseOracle: Rosenbrock-Euler needs a host jacobian_factors");
     if (!p.g.is_host()) {
       const int k = p.g.device().kind;
       if (k == KP_G_BRUSSELATOR || k == KP_G_RICCATI)
@@ -1134,6 +1141,17 @@ IntegrateResultT<T> integrate(const ProblemSpecT<T>& p, const StepperConfig& c) 
       };
     } else {
       q1.g = p.g;
+    }
+    if constexpr (std::is_same_v<T, double>) {
+      if (c.method == Method::RosenbrockEuler) {
+        // inc/integrators.hpp:329-338: the dense Jacobian is the Kronecker sum
+        // of the callback's factors, phi_1(tau J) that of the one-mode problem
+        const auto jf = p.jacobian_factors;
+        q1.jacobian_factors = [jf, shape](const Tensor<T>& u) {
+          return std::vector<Matrix<T>>{
+              assemble_kronsum_dense(KroneckerSum<T>(jf(Tensor<T>(shape, vec(u)))))};
+        };
+      }
     }
     StepperConfig c1 = c;
     c1.backend = Backend::Split;

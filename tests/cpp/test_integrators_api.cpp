@@ -251,6 +251,40 @@ TEST_CASE("rosenbrock with the exact linear Jacobian is exponential Euler") {
   CHECK(diff_norm_inf(integrate(p1, c).final, one) == 0.0);
 }
 
+TEST_CASE("rosenbrock on the dense backend: one step differs from the split one at third order") {
+  // g = 0.3 u with the exact Jacobian: the dense backend applies phi_1(tau J)
+  // of the assembled Kronecker sum (inc/integrators.hpp:329-338), the split
+  // backend the product of the per-direction phi_1's -- equal up to O(tau^3)
+  ProblemSpec p = small_problem();
+  p.g = [](double, const Tensor<double>& u) {
+    Tensor<double> g(u.dims());
+    for (std::size_t i = 0; i < u.size(); ++i) g[i] = 0.3 * u[i];
+    return g;
+  };
+  const auto k = p.K;
+  p.jacobian_factors = [k](const Tensor<double>&) {
+    std::vector<Matrix<double>> j = k.factors;
+    for (int i = 0; i < j[0].rows(); ++i) j[0](i, i) += 0.3;
+    return j;
+  };
+  std::vector<double> taus, diffs;
+  for (int e = 4; e <= 7; ++e) {
+    const double tau = std::ldexp(1.0, -e);
+    p.t_final = tau;
+    StepperConfig c;
+    c.n_steps = 1;
+    c.method = Method::RosenbrockEuler;
+    const auto split = integrate(p, c);
+    c.backend = Backend::DenseOracle;
+    const auto dense = integrate(p, c);
+    CHECK(dense.final.all_finite());
+    taus.push_back(tau);
+    diffs.push_back(rel_fro(split.final, dense.final));
+  }
+  CHECK(slope(taus, diffs) >= 2.7);
+  CHECK(slope(taus, diffs) <= 3.3);
+}
+
 TEST_CASE("shape mismatches are invalid_argument before any device work") {
   ProblemSpec p = small_problem();
   StepperConfig c;
