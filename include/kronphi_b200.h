@@ -306,6 +306,14 @@ int kp_eval_g_f64(kp_ctx* ctx, const kp_gfun* g, double t, const double* u, cons
                   int d, double* gout);
 int kp_eval_g_c128(kp_ctx* ctx, const kp_gfun* g, double t, const double* u, const int* dims,
                    int d, double* gout);
+/* Jacobian factors of the Riccati problem at the n x n state u
+ * (riccati_jacobian_factors, src/problems.cpp:212-250): J = A^T - (U b) b^T;
+ * one factor serves both modes when U is symmetric to 1e-8 (then *nfactors =
+ * 1 and j2 is untouched), else j2 = A^T - (U^T b) b^T and *nfactors = 2.
+ * g: a KP_G_RICCATI descriptor (aux[0] = b); at, u, j1, j2: device, n x n. */
+int kp_riccati_jacobian_factors_f64(kp_ctx* ctx, const kp_gfun* g, const double* u,
+                                    const double* at, int n, double* j1, double* j2,
+                                    int* nfactors);
 /* *all_finite = 1 if every entry is finite (inc/integrators.hpp:101-108) */
 int kp_all_finite_f64(kp_ctx* ctx, size_t n, const double* x, int* all_finite);
 /* Stream-ordered, no host sync: atomicMin(*bad_dev, step) when x (n doubles)

@@ -1489,6 +1489,44 @@ inline RiccatiProblem build_riccati(int n_hat) {
   return pr;
 }
 
+// riccati_rhs / riccati_jacobian_factors / are_residual (inc/problems.hpp,
+// src/problems.cpp:198-256) on the device: A^T U + U A is the Kronecker-sum
+// action with K = {A^T, A^T}, C + U B U the Riccati g, the Jacobian factors
+// come from kp_riccati_jacobian_factors_f64.
+inline Matrix<double> riccati_rhs(const Matrix<double>& u, const RiccatiProblem& p) {
+  const int n = p.a.rows();
+  if (u.rows() != n || u.cols() != n) throw std::invalid_argument("riccati_rhs: size mismatch");
+  const ProblemSpec spec = p.to_problem_spec();
+  const Tensor<double> ut = tensor_from_matrix(u);
+  Tensor<double> r = kronsum_action(ut, spec.K);
+  axpy(1.0, spec.g(0.0, ut), r);
+  return matrix_from_tensor(r);
+}
+
+inline std::vector<Matrix<double>> riccati_jacobian_factors(const Matrix<double>& u,
+                                                            const RiccatiProblem& p) {
+  using namespace detail;
+  const int n = p.a.rows();
+  if (u.rows() != n || u.cols() != n)
+    throw std::invalid_argument("riccati_jacobian_factors: size mismatch");
+  const ProblemSpec spec = p.to_problem_spec();
+  const size_t bytes = bytes_of<double>(u.size());
+  DevBuf du(u.data(), bytes), dat(p.a_t.data(), bytes), j1(bytes), j2(bytes);
+  int nf = 0;
+  check(kp_riccati_jacobian_factors_f64(ctx(), &spec.g.device(), du.d(), dat.d(), n, j1.d(),
+                                        j2.d(), &nf));
+  Matrix<double> m1(n, n);
+  j1.download(m1.data());
+  if (nf == 1) return {m1, m1};
+  Matrix<double> m2(n, n);
+  j2.download(m2.data());
+  return {m1, m2};
+}
+
+inline double are_residual(const Matrix<double>& u, const RiccatiProblem& p) {
+  return riccati_rhs(u, p).norm_fro();
+}
+
 // ---- multi-GPU (new; the reference is single-node CPU): one process per GPU.
 // Rank 0 calls Communicator::unique_id() and ships the 128 bytes to the other
 // ranks by any side channel; every rank then constructs a Communicator

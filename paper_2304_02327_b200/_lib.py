@@ -131,6 +131,7 @@ _SIGS = {
     "kp_add_scaled_f64": (_I, [_CTX, _SZ, _VP, _D, _VP, _VP]),
     "kp_eval_g_f64": (_I, [_CTX, C.POINTER(GFun), _D, _VP, _PI, _I, _VP]),
     "kp_eval_g_c128": (_I, [_CTX, C.POINTER(GFun), _D, _VP, _PI, _I, _VP]),
+    "kp_riccati_jacobian_factors_f64": (_I, [_CTX, C.POINTER(GFun), _VP, _VP, _I, _VP, _VP, _PI]),
     "kp_all_finite_f64": (_I, [_CTX, _SZ, _VP, _PI]),
     "kp_mark_nonfinite_f64": (_I, [_CTX, _SZ, _VP, _VP, _I]),
     "kp_measure_fp64_peak": (_I, [_CTX, _PD]),

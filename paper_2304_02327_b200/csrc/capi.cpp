@@ -808,6 +808,21 @@ int kp_eval_g_f64(kp_ctx* ctx, const kp_gfun* g, double t, const double* u, cons
   });
 }
 
+int kp_riccati_jacobian_factors_f64(kp_ctx* ctx, const kp_gfun* g, const double* u,
+                                    const double* at, int n, double* j1, double* j2,
+                                    int* nfactors) {
+  return guard([&] {
+    need_ctx(ctx);
+    if (!g || g->kind != KP_G_RICCATI || !g->aux[0])
+      throw invalid_argument("riccati_jacobian_factors: needs a Riccati g descriptor");
+    if (n <= 0 || !u || !at || !j1 || !j2 || !nfactors)
+      throw invalid_argument("riccati_jacobian_factors: bad arguments");
+    *nfactors = riccati_jacobians(
+        ctx, *g, u, at, n, static_cast<double*>(ctx->ws.get(50, 2 * size_t(n) * sizeof(double))),
+        j1, j2);
+  });
+}
+
 int kp_eval_g_c128(kp_ctx* ctx, const kp_gfun* g, double t, const double* u, const int* dims,
                    int d, double* gout) {
   return guard([&] {

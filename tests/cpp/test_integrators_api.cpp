@@ -285,6 +285,40 @@ TEST_CASE("rosenbrock on the dense backend: one step differs from the split one 
   CHECK(slope(taus, diffs) <= 3.3);
 }
 
+TEST_CASE("riccati helpers: rhs, Jacobian factors, ARE residual (problems.hpp)") {
+  const RiccatiProblem pr = build_riccati(6);
+  const int n = pr.a.rows();
+  // U = 0: the right-hand side is C, one Jacobian factor A^T serves both modes
+  CHECK(diff_norm_inf(tensor_from_matrix(riccati_rhs(pr.u0, pr)), tensor_from_matrix(pr.c_mat)) == 0.0);
+  CHECK(are_residual(pr.u0, pr) == doctest::Approx(pr.c_mat.norm_fro()).epsilon(1e-15));
+  auto j0 = riccati_jacobian_factors(pr.u0, pr);
+  CHECK(j0.size() == 2);
+  CHECK(diff_norm_inf(tensor_from_matrix(j0[0]), tensor_from_matrix(pr.a_t)) == 0.0);
+  // a symmetric U: J = A^T - (U b) b^T, and rhs = A^T U + U A + C - (U b)(U^T b)^T
+  Matrix<double> u(n, n);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) u(i, j) = 0.01 * std::cos(0.3 * (i + 1)) * std::cos(0.3 * (j + 1)) + (i == j ? 0.02 : 0.0);
+  std::vector<double> w(n, 0.0);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) w[i] += u(i, j) * pr.b[j];
+  const auto js = riccati_jacobian_factors(u, pr);
+  double ejac = 0.0, erhs = 0.0, scale = 0.0;
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i)
+      ejac = std::max(ejac, std::abs(js[0](i, j) - (pr.a_t(i, j) - w[i] * pr.b[j])));
+  CHECK(ejac < 1e-12 * pr.a.norm1());
+  const Matrix<double> rhs = riccati_rhs(u, pr);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      double v = pr.c_mat(i, j) - w[i] * w[j];
+      for (int k = 0; k < n; ++k) v += pr.a_t(i, k) * u(k, j) + u(i, k) * pr.a(k, j);
+      erhs = std::max(erhs, std::abs(rhs(i, j) - v));
+      scale = std::max(scale, std::abs(v));
+    }
+  CHECK(erhs < 1e-12 * scale);
+  CHECK_THROWS_AS(riccati_rhs(Matrix<double>(3, 3), pr), std::invalid_argument);
+}
+
 TEST_CASE("shape mismatches are invalid_argument before any device work") {
   ProblemSpec p = small_problem();
   StepperConfig c;
