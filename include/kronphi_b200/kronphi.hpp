@@ -1374,12 +1374,28 @@ struct ADRProblem {
     scale(e, std::exp(t));
     return e;
   }
+  // Psi(t, .) on the grid: the forcing that makes e^t u0 the solution
+  Tensor<double> source(double t) const {
+    const double et = std::exp(t), e2t = et * et;
+    Tensor<double> out = Tensor<double>::no_init(dims);
+    for (std::size_t r = 0; r < out.size(); ++r)
+      out[r] = et * psi_a[r] - 1.0 / (1.0 + e2t * u0_sq[r]);
+    return out;
+  }
+  // g(t, u) = 1/(1+u^2) + Psi(t, .), evaluated on the device (KP_G_ADR)
+  Tensor<double> g(double t, const Tensor<double>& u) const { return to_problem_spec().g(t, u); }
   ProblemSpec to_problem_spec() const {
     ProblemSpec spec;
     spec.K = KroneckerSum<double>(factors);
     spec.u0 = u0;
     spec.t0 = 0.0;
     spec.t_final = 1.0;
+    const Tensor<double> u0c = u0;
+    spec.exact = [u0c](double t) {
+      Tensor<double> e = u0c;
+      scale(e, std::exp(t));
+      return e;
+    };
     spec.device_data = std::make_shared<DeviceFields>();
     kp_gfun g{KP_G_ADR, {0, 0, 0, 0}};
     g.aux[0] = spec.device_data->add(psi_a.data(), psi_a.size());

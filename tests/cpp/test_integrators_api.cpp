@@ -319,6 +319,27 @@ TEST_CASE("riccati helpers: rhs, Jacobian factors, ARE residual (problems.hpp)")
   CHECK_THROWS_AS(riccati_rhs(Matrix<double>(3, 3), pr), std::invalid_argument);
 }
 
+TEST_CASE("ADR problem: exact, source and g members (problems.hpp)") {
+  const ADRProblem pr = build_adr(6, 7, 8);
+  const ProblemSpec spec = pr.to_problem_spec();
+  REQUIRE(bool(spec.exact));
+  CHECK(diff_norm_inf(spec.exact(0.0), pr.u0) == 0.0);
+  CHECK(diff_norm_inf(spec.exact(0.5), pr.exact(0.5)) == 0.0);
+  // g(t, u) - 1/(1+u^2) = Psi(t, .), and the exact solution satisfies the ODE:
+  // d/dt (e^t u0) = K e^t u0 + g(t, e^t u0) up to the FD truncation (exact for
+  // this polynomial u0 with second-order differences)
+  const double t = 0.3;
+  const Tensor<double> u = pr.exact(t);
+  const Tensor<double> g = pr.g(t, u), psi = pr.source(t);
+  double e1 = 0.0;
+  for (std::size_t r = 0; r < u.size(); ++r)
+    e1 = std::max(e1, std::abs(g[r] - (1.0 / (1.0 + u[r] * u[r]) + psi[r])));
+  CHECK(e1 < 1e-13);
+  Tensor<double> rhs = kronsum_action(u, spec.K);
+  axpy(1.0, g, rhs);
+  CHECK(diff_norm_inf(rhs, u) < 1e-10 * u.norm_inf() + 1e-11);
+}
+
 TEST_CASE("shape mismatches are invalid_argument before any device work") {
   ProblemSpec p = small_problem();
   StepperConfig c;
