@@ -558,6 +558,13 @@ void gemm(int m, int n, int k, T alpha, const T* a, int lda, const T* b, int ldb
   gemm_batch_shared_b(m, n, k, alpha, a, lda, 0, b, ldb, opb, beta, c, ldc, 0, 1, parallel);
 }
 
+// y = A x (inc/matrix.hpp:150-155): the same GEMM with n = 1
+template <typename T>
+void matvec(const Matrix<T>& a, const T* x, T* y, bool parallel = true) {
+  gemm(a.rows(), 1, a.cols(), T(1), a.data(), a.rows(), x, a.cols(), Op::none, T{}, y, a.rows(),
+       parallel);
+}
+
 // ------------------------------------------------------ LU (linsolve.hpp)
 // lu_factor / lu_solve / solve (inc/linsolve.hpp:95-151) on the device blocked
 // LU (64-wide panels, partial pivoting, GEMM trailing updates); double.

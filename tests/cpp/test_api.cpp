@@ -74,6 +74,19 @@ int main() {
     }
     CHECK(ok);
   }
+  {  // matvec (matrix.hpp:150-155) against the plain sum
+    const Matrix<double> a = random_matrix(7, 5);
+    std::vector<double> x(5), y(7, -1.0);
+    for (int j = 0; j < 5; ++j) x[j] = 0.25 * (j + 1);
+    matvec(a, x.data(), y.data());
+    double worst = 0;
+    for (int i = 0; i < 7; ++i) {
+      double want = 0;
+      for (int j = 0; j < 5; ++j) want += a(i, j) * x[j];
+      worst = std::max(worst, std::abs(y[i] - want));
+    }
+    CHECK(worst < 1e-13);
+  }
   {  // tucker in 2d is M1 T M2^T (test_tensor.cpp:159-169)
     const Tensor<double> t = random_tensor({3, 4});
     const Matrix<double> m1 = random_matrix(5, 3), m2 = random_matrix(6, 4);
