@@ -259,3 +259,55 @@ def test_host_tucker_stream_bitwise(kp, dims):
                                             C.cast(outs_p, C.c_void_p)))
     for a, b in zip(outs, want):
         assert np.array_equal(a, b)
+
+
+def _random_banded(r, n, kind):
+    """kind 0: Dirichlet tridiagonal, 1: periodic tridiagonal, 2: bidiagonal (no
+    diagonal), 3: diagonal only -- random values."""
+    a = np.zeros((n, n), order="F")
+    i = np.arange(n)
+    if kind != 2:
+        a[i, i] = r.standard_normal(n)
+    if kind != 3 and n > 1:
+        a[i[1:], i[:-1]] = r.standard_normal(n - 1)
+        a[i[:-1], i[1:]] = r.standard_normal(n - 1)
+    if kind == 1 and n > 2:
+        a[0, n - 1] = r.standard_normal()
+        a[n - 1, 0] = r.standard_normal()
+    return a
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_banded_kronsum_fuzz_bitwise(kp, port, seed):
+    """Random banded factors (every row pattern the stencil canonicalises or
+    routes to its rare path), ragged extents incl. 1-3 and past the KC = 256
+    slice, d = 1..4: bit-identical to the reference's dense kronsum_action."""
+    r = rng(500 + seed)
+    for _ in range(6):
+        d = int(r.integers(1, 5))
+        dims = [int(r.integers(1, 40)) for _ in range(d)]
+        if r.random() < 0.5:
+            dims[int(r.integers(0, d))] = int(r.integers(255, 300))
+        while np.prod(dims) > 2e6:
+            dims[int(np.argmax(dims))] //= 2
+        t = rand(r, dims)
+        As = [_random_banded(r, n, int(r.integers(0, 4))) for n in dims]
+        got = kp.kronsum_action(t, As)
+        want = port.kronsum(t, As)
+        assert np.array_equal(got, want), (dims,)
+
+
+@pytest.mark.parametrize("imag_only", [False, True])
+def test_banded_kronsum_complex_fuzz(kp, port, imag_only):
+    """Complex banded factors: general ones (the generic complex chain) and
+    purely imaginary ones (the stencil's IMAG path: half the FP64 work, every
+    value unchanged), periodic and Dirichlet, with a KC = 256 break."""
+    r = rng(640 + int(imag_only))
+    for dims in [(20, 17, 9), (258, 6, 5), (7, 270, 3), (5, 4, 262), (33, 12)]:
+        t = rand(r, dims, True)
+        As = []
+        for n in dims:
+            re = _random_banded(r, n, int(r.integers(0, 2)))
+            im = _random_banded(r, n, int(r.integers(0, 2)))
+            As.append(np.asfortranarray(1j * im if imag_only else re + 1j * im))
+        assert rel2(kp.kronsum_action(t, As), port.kronsum(t, As)) < 1e-15, (dims,)
