@@ -157,3 +157,22 @@ def test_cluster_lu_panel_bitwise(kp, n, monkeypatch):
     monkeypatch.setenv("KP_LU_PANEL", "simple")
     want = kp.expm(x)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_phi_fuzz(kp, port, seed):
+    """Random sizes 1..130 (every LU panel remainder, odd leading dimensions)
+    and 1-norms 1e-3..300 (every Pade degree and scaling exponent): expm and the
+    phi table against the oracle, same scaling exponent, <= 1e-12."""
+    r = rng(7000 + seed)
+    for _ in range(6):
+        n = int(r.integers(1, 131))
+        target = float(10.0 ** r.uniform(-3, 2.5))
+        x = rand_norm(r, n, target)
+        assert rel1(kp.expm(x), port.expm(x)) < 1e-12, (n, target)
+        ell = int(r.integers(0, 4))
+        tab = kp.phiquad(x, ell)
+        want, s = port.phiquad(x, ell)
+        assert tab.scaling_exponent == s, (n, target)
+        for j in range(ell + 1):
+            assert rel1(tab.phis[j], want[j]) < 1e-12, (n, target, j)
