@@ -190,3 +190,33 @@ def test_tucker_sharded_local(kp, P, mode_d):
         else:            # slab: (n1, n2, n3/P)
             blk = np.asfortranarray(want[:, :, k * n3 // P:(k + 1) * n3 // P])
             assert rel2(flat, blk.reshape(-1, order="F")) < 1e-12
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_native_sharded_fuzz_shapes(kp, seed):
+    """Random ragged slabs: mode extents with odd leading dimensions, P in
+    {2, 3, 4} (modes d-1 and d divisible by P), banded and dense Kronecker
+    sums, all-to-all and fused exchanges -- bitwise equal to one GPU."""
+    from paper_2304_02327_b200 import problems
+    r = rng(4100 + seed)
+    for _ in range(3):
+        P = int(r.integers(2, 5))
+        dims = (int(r.integers(3, 20)), P * int(r.integers(1, 6)), P * int(r.integers(1, 6)))
+        method = ["etd2rk", "exp_euler", "lawson2b", "lawson_euler"][int(r.integers(0, 4))]
+        c = problems.ac3d(n=8, n_steps=int(r.integers(1, 5)))
+        c.method = method
+        c.u0 = np.asfortranarray(0.3 + 0.1 * r.uniform(-1, 1, dims))
+        banded = r.random() < 0.5
+        if banded:
+            c.K = [problems.fd_operator_1d(n, 0.01, 0.05) for n in dims]
+        else:
+            c.K = []
+            for n in dims:
+                a = r.uniform(-1, 1, (n, n))
+                a -= np.abs(a).sum(0).max() * np.eye(n)
+                c.K.append(np.asfortranarray(a))
+        want = kp.integrate_config(c.method, c.u0, c.K, c.g, 0.0, c.t_final, c.n_steps)
+        # (the fused exchange is defined for banded factors and the phi methods)
+        for md in ("alltoall", "fused") if banded else ("alltoall",):
+            got, used, loop = run_native(kp, c, P, md)
+            assert np.array_equal(got, want), (dims, P, method, md, rel2(got, want))
