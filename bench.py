@@ -70,7 +70,10 @@ def config(n, world):
     return {"workload": f"tucker_d3_n{n}", "op": "V x1 L x2 L x3 L",
             "dims": [n, n, n], "factor": "L = phi_1(1e-3 * fd_operator_1d(n, 1.0, 0))",
             "seed": SEED, "parallelism": "replicas" if world > 1 else "single",
-            "l2": "inputs 1 GiB > 126 MB L2 (no flush needed)"}
+            "l2": (f"inputs {8 * n ** 3 / 2 ** 30:.2f} GiB > 126 MB L2 (no flush needed)"
+                   if 8 * n ** 3 > 126e6 else
+                   f"inputs {8 * n ** 3 / 1e6:.0f} MB fit in the 126 MB L2 and are NOT flushed "
+                   "(non-default --n: not a contract number)")}
 
 
 INTEGRATOR_CONFIGS = [  # (tag, builder kwargs) -- BASELINE.json configs 0, 2, 3, 4

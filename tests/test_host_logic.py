@@ -56,3 +56,30 @@ def test_problem_builders_shapes_and_seeds(port):
     assert nl.u0.dtype == np.complex128 and nl.K[0].dtype == np.complex128
     import pyoracle
     assert np.allclose(nl.K[0], 0.5j * pyoracle.periodic_laplacian_1d(8, 2.0))
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference: one JSON line with the contract's keys, timed on
+    the host cores (oracle/_ref when it is built, else the C restatement); under
+    torchrun only rank 0 runs and prints."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+           "--warmup", "1", "--n", "64"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "GFLOP/s" and d["higher_is_better"] is True
+    assert d["metric"].startswith("FP64 Tucker-op GFLOP/s") and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["value"] == d["value"] and d["cpu_baseline"]["sample"]
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
+    env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0 and r.stdout.strip() == ""
