@@ -429,11 +429,34 @@ __global__ void __launch_bounds__(CF::NT, CF::kMinBlocks)
             bv[2 * pj + 1] = b2.y;
           }
         }
+        if constexpr (CPLX == 2 && !B_KCONTIG) {
+          // complex modes >= 1: rows (m, m+1) = (re, im) of a tensor entry,
+          // columns (n, n+1) = (re, im) of a factor entry.  Three products
+          // per complex block instead of four (the 3M form):
+          //   P1 = re re -> acc[even][even], P2 = im im -> acc[odd][odd],
+          //   P3 = (re + im)(re + im) -> acc[even][odd];
+          // the epilogue forms (P1 - P2, P3 - P1 - P2).  acc[odd][even] stays 0.
+          double as[MI / 2], bs[NI / 2];
 #pragma unroll
-        for (int mi = 0; mi < MI; ++mi) {
-          const double a = (mi & 1) ? af[mi >> 1].y : af[mi >> 1].x;
+          for (int pi = 0; pi < MI / 2; ++pi) as[pi] = __dadd_rn(af[pi].x, af[pi].y);
 #pragma unroll
-          for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a, bv[ni]);
+          for (int pj = 0; pj < NI / 2; ++pj) bs[pj] = __dadd_rn(bv[2 * pj], bv[2 * pj + 1]);
+#pragma unroll
+          for (int pi = 0; pi < MI / 2; ++pi)
+#pragma unroll
+            for (int pj = 0; pj < NI / 2; ++pj) {
+              dmma(acc[2 * pi][2 * pj][0], acc[2 * pi][2 * pj][1], af[pi].x, bv[2 * pj]);
+              dmma(acc[2 * pi + 1][2 * pj + 1][0], acc[2 * pi + 1][2 * pj + 1][1], af[pi].y,
+                   bv[2 * pj + 1]);
+              dmma(acc[2 * pi][2 * pj + 1][0], acc[2 * pi][2 * pj + 1][1], as[pi], bs[pj]);
+            }
+        } else {
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi) {
+            const double a = (mi & 1) ? af[mi >> 1].y : af[mi >> 1].x;
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a, bv[ni]);
+          }
         }
       }
       prev = stage;

@@ -305,8 +305,10 @@ __device__ __forceinline__ bool staged_epilogue(const GemmProblem& p, const Epil
         const int e2 = b0 + j * NTH;
         const int pl = e2 % (TM / 2), il = e2 / (TM / 2);
         const double* c0 = cs + 2 * pl + 2 * il * LDS;
-        const double c_rr = c0[0], c_ir = c0[1], c_ri = c0[LDS], c_ii = c0[LDS + 1];
-        double2 v = make_double2(__dsub_rn(c_rr, c_ii), __dadd_rn(c_ri, c_ir));
+        // 3M products staged by the mainloop (gemm_dmma.cu): P1 = re re at
+        // (even, even), P2 = im im at (odd, odd), P3 = (re+im)(re+im) at (even, odd)
+        const double c_rr = c0[0], c_p3 = c0[LDS], c_ii = c0[LDS + 1];
+        double2 v = make_double2(__dsub_rn(c_rr, c_ii), __dsub_rn(__dsub_rn(c_p3, c_rr), c_ii));
         if (!u.one) v = make_double2(al * v.x, al * v.y);
         double2 dv = make_double2(0.0, 0.0);
         const double2 rr = epi_apply_c(e, u, v, in[j], &dv);
